@@ -1,0 +1,167 @@
+/*
+ * pcs_lop.h — C ABI of the B200-native LOP/WLOP operator.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *
+ *   std::pair<PointCloud, LopSummary>
+ *   pcs::lop_project(const PointCloud& data, const PointCloud& initial,
+ *                    const LopParams& params);
+ *       /root/reference/proj/include/pcs/lop.hpp:51-53, src/lop.cpp:10-127
+ *
+ * Plain pointers and sizes only (no C++ or torch types).  The C++ header set
+ * include/pcs/*.hpp re-exposes pcs::lop_project with the reference's structs on
+ * top of this ABI; Python binds it with ctypes (paper_2401_03365_b200/lop.py).
+ *
+ * Error model (mirrors proj/include/pcs/errors.hpp:9-53): every entry point
+ * returns a pcs_status; the message of the last failure on the calling host
+ * thread is available from pcs_last_error().  The reference's validation order
+ * is kept: InvalidParam, then EmptyCloud(data), then an empty initial set
+ * passes through (proj/src/lop.cpp:13-20).
+ *
+ * Threading: every call is synchronous with respect to the host buffers it is
+ * given, re-entrant, and may be issued from any host thread; a plan object is
+ * not thread-safe (one thread at a time per plan).
+ */
+#ifndef PCS_LOP_H
+#define PCS_LOP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PCS_LOP_ABI_VERSION 1
+
+typedef enum pcs_status {
+    PCS_OK = 0,
+    PCS_ERR_INVALID_PARAM = 1,  /* pcs::InvalidParam  (errors.hpp:23-26) */
+    PCS_ERR_EMPTY_CLOUD = 2,    /* pcs::EmptyCloud    (errors.hpp:14-18) */
+    PCS_ERR_NUMERICAL = 3,      /* pcs::NumericalFailure (errors.hpp:48-51) */
+    PCS_ERR_CUDA = 4,           /* device / driver failure (reported as NumericalFailure in C++) */
+    PCS_ERR_NCCL = 5,           /* collective failure */
+    PCS_ERR_NO_DEVICE = 6,      /* no usable sm_100 device: there is no CPU fallback */
+    PCS_ERR_CAPACITY = 7        /* caller buffer too small; required size reported */
+} pcs_status;
+
+/* Repulsion penalty eta.  The reference hard-codes eta = 1/(3 r^3),
+ * |eta'| = 1/r^4 (proj/src/kernels.cpp:17-29).  eta = -r (|eta'| = 1) is the
+ * WLOP convention named by the benchmark configs; it is an extension. */
+typedef enum pcs_eta_kind {
+    PCS_ETA_INV_CUBE = 0,
+    PCS_ETA_NEG_LINEAR = 1
+} pcs_eta_kind;
+
+typedef enum pcs_precision {
+    PCS_PREC_FP64 = 0,  /* reference arithmetic: fp64 storage and math, exact predicate */
+    PCS_PREC_FP32 = 1   /* fp32 storage, fused SFU/FP32 kernel; predicate re-decided in fp64 */
+} pcs_precision;
+
+/* LopParams (proj/include/pcs/lop.hpp:12-27) + KernelParams (kernels.hpp:12-24)
+ * + the B200 extensions.  Initialise with pcs_lop_desc_default(). */
+typedef struct pcs_lop_desc {
+    uint32_t struct_size;      /* sizeof(pcs_lop_desc) — ABI guard */
+    double h;                  /* KernelParams::h (Gaussian bandwidth) */
+    double cutoff_multiple;    /* KernelParams::cutoff_multiple; support = h*cutoff */
+    double mu;                 /* LopParams::mu in [0, 0.5) */
+    int32_t iterations;        /* LopParams::iterations >= 1 */
+    double convergence_tol;    /* LopParams::convergence_tol > 0 */
+    int32_t eta_kind;          /* pcs_eta_kind */
+    int32_t density_weights;   /* 0 = LOP, 1 = WLOP (v_j on data, w_i per sweep) */
+    int32_t precision;         /* pcs_precision */
+    int32_t device;            /* CUDA ordinal; -1 = current device */
+    int32_t lanes_per_point;   /* fp32 kernel tuning: 0 = auto, else 1,2,4,8 */
+    int32_t reserved[7];
+} pcs_lop_desc;
+
+/* LopSummary (proj/include/pcs/lop.hpp:29-35) + measured counters. */
+typedef struct pcs_lop_summary {
+    int32_t iterations_run;
+    int32_t converged;
+    uint64_t isolated_events;    /* per-sweep isolated count, summed over sweeps */
+    uint64_t coincident_pairs;   /* ordered (i,i') pairs with d == 0 seen by repulsion */
+    uint64_t n_isolated;         /* size of the unique ascending isolated index list */
+    uint64_t interactions_attr;  /* evaluated (i,j) pairs with 0 < d <= support, all sweeps */
+    uint64_t interactions_rep;   /* evaluated (i,i') pairs with 0 < d <= support, all sweeps */
+    uint64_t density_pairs;      /* WLOP w_i / v_j pairs evaluated (0 < d <= support) */
+    uint64_t careful_points;     /* points re-evaluated by the exact fp64 path (fp32 mode) */
+    double last_max_disp;        /* max displacement of the last sweep */
+    double setup_ms;             /* device time: upload conversion, data grid, v_j */
+    double sweeps_ms;            /* device time of all sweeps (CUDA events) */
+    double kernel_ms;            /* device time of the fused per-point kernel, all sweeps */
+    double sort_ms;              /* device time of the per-sweep grid rebuild, all sweeps */
+} pcs_lop_summary;
+
+typedef struct pcs_lop_plan pcs_lop_plan;
+
+/* ---- descriptor / errors ------------------------------------------------- */
+void pcs_lop_desc_default(pcs_lop_desc* d);
+const char* pcs_last_error(void);
+int32_t pcs_lop_abi_version(void);
+/* Validates exactly like LopParams::validate() (lop.hpp:18-26). */
+pcs_status pcs_lop_validate(const pcs_lop_desc* d);
+
+/* ---- one-shot drop-in call (replaces pcs::lop_project) ---------------------
+ * P: n points as xyz doubles (PointCloud data), X0: m points (initial),
+ * X_out: m points (the projected cloud).  isolated_out (capacity
+ * isolated_cap, may be NULL) receives LopSummary::isolated_indices; if it is
+ * too small the call still succeeds, summary->n_isolated reports the size and
+ * only the first isolated_cap entries are written. */
+pcs_status pcs_lop_run(const pcs_lop_desc* d, const double* P_xyz, uint64_t n,
+                       const double* X0_xyz, uint64_t m, double* X_out_xyz,
+                       pcs_lop_summary* summary, uint32_t* isolated_out,
+                       uint64_t isolated_cap);
+
+/* ---- plan API: device-resident runs (bench, multi-GPU) --------------------- */
+pcs_status pcs_lop_plan_create(const pcs_lop_desc* d, pcs_lop_plan** out);
+void pcs_lop_plan_destroy(pcs_lop_plan* p);
+/* Uploads P and X0 (host doubles), builds the data grid (and v_j for WLOP). */
+pcs_status pcs_lop_plan_upload(pcs_lop_plan* p, const double* P_xyz, uint64_t n,
+                               const double* X0_xyz, uint64_t m);
+/* Joins an NCCL clique (one process per GPU).  unique_id: 128 bytes from
+ * pcs_nccl_unique_id() on rank 0, broadcast by the caller.  Must precede upload. */
+pcs_status pcs_nccl_unique_id(uint8_t id_out[128]);
+pcs_status pcs_lop_plan_set_comm(pcs_lop_plan* p, const uint8_t id[128], int32_t nranks,
+                                 int32_t rank);
+/* Restores X to X0 and clears the summary (P, grid and v_j are kept). */
+pcs_status pcs_lop_plan_reset(pcs_lop_plan* p);
+/* Runs `sweeps` further Jacobi sweeps (<= 0: the descriptor's iteration count),
+ * stopping early on convergence.  Asynchronous unless sync != 0. */
+pcs_status pcs_lop_plan_run(pcs_lop_plan* p, int32_t sweeps, int32_t sync);
+pcs_status pcs_lop_plan_synchronize(pcs_lop_plan* p);
+/* Device time of the last pcs_lop_plan_run (CUDA events on the plan stream). */
+pcs_status pcs_lop_plan_last_run_ms(pcs_lop_plan* p, double* ms);
+pcs_status pcs_lop_plan_download(pcs_lop_plan* p, double* X_out_xyz, pcs_lop_summary* summary,
+                                 uint32_t* isolated_out, uint64_t isolated_cap);
+/* Number of this process's kernel launches issued by the plan so far. */
+uint64_t pcs_lop_plan_launches(const pcs_lop_plan* p);
+
+/* ---- parity facilities ----------------------------------------------------
+ * SpatialIndex::radius_query (proj/src/spatial.cpp:82-111) for every query, on
+ * the device grid: CSR offsets (m+1) and hit indices ascending per query.
+ * Call with idx == NULL to obtain offsets (total = offsets[m]) first.
+ * Coordinates are rounded to fp32 first when precision == PCS_PREC_FP32
+ * (the predicate is then the fp64 one over the rounded values). */
+pcs_status pcs_radius_query_all(const pcs_lop_desc* d, const double* C_xyz, uint64_t n,
+                                const double* Q_xyz, uint64_t m, double r,
+                                uint64_t* offsets, uint32_t* idx, uint64_t idx_cap);
+/* Grid sort order used by the device hash: sorted positions -> point index,
+ * and the 32-bit cell keys, for a cloud (parity: stable sort by key). */
+pcs_status pcs_grid_sort(const pcs_lop_desc* d, const double* C_xyz, uint64_t n, double support,
+                         uint32_t* keys_out, uint32_t* order_out);
+
+/* ---- host generators (proj/include/pcs/rng.hpp, proj/src/bench.cpp:40-87) -- */
+/* kind: 0 plane, 1 sphere, 2 torus(R=1,r=0.35), 3 gaussian bump */
+pcs_status pcs_generate_surface(int32_t kind, uint64_t n, uint64_t seed, double* xyz);
+pcs_status pcs_add_noise(double* xyz, uint64_t n, double sigma, uint64_t seed);
+/* The benchmark configurations 1..5 (BASELINE.json), scaled by `scale` (1.0 =
+ * full size).  Fills P (n_p points) and X0 (n_x points) — query the sizes with
+ * P_xyz == NULL first.  Seeds: surface 0, noise 1, outliers/subset 2. */
+pcs_status pcs_config_sizes(int32_t config, double scale, uint64_t* n_p, uint64_t* n_x);
+pcs_status pcs_generate_config(int32_t config, double scale, double* P_xyz, double* X0_xyz);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCS_LOP_H */

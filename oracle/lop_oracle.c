@@ -1,0 +1,655 @@
+/*
+ * lop_oracle.c — CPU restatement of the reference LOP/WLOP sweep.
+ *
+ * TEST INFRASTRUCTURE ONLY (see lop_oracle.h).  Compile with
+ * -ffp-contract=off: the reference's bit pattern depends on x86-64 evaluating
+ * a*b + c as two roundings (proj/include/pcs/core.hpp:28).
+ *
+ * Function-by-function map to the reference:
+ *   orc_theta           <- proj/src/kernels.cpp:8-15
+ *   etad()              <- proj/src/kernels.cpp:23-29 (inv-cube); |eta'| = 1 for eta = -r
+ *   grid_query()        <- proj/src/spatial.cpp:82-111 (d2 <= r*r, sqrt(d2), hits by index)
+ *   sweep_point()       <- proj/src/lop.cpp:43-100
+ *   aggregation         <- proj/src/lop.cpp:102-119
+ *   orc_lop_project     <- proj/src/lop.cpp:10-127
+ *   mt19937_64 / rng    <- proj/include/pcs/rng.hpp:16-46 (std::mt19937_64 is fixed by the standard)
+ *   orc_add_noise       <- proj/src/noise.cpp:9-27
+ *   orc_plane/sphere    <- proj/src/bench.cpp:40-60
+ * The neighbour search is a uniform grid instead of the kd-tree; it returns the
+ * same set because both apply the same predicate to the same fp64 values and
+ * both report hits in ascending index order.
+ */
+#include "lop_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* ------------------------------------------------------------------------ */
+/* mt19937_64 and the pinned transforms (proj/include/pcs/rng.hpp)            */
+/* ------------------------------------------------------------------------ */
+
+typedef struct {
+    uint64_t mt[312];
+    int idx;
+} mt64;
+
+static void mt64_seed(mt64* g, uint64_t seed) {
+    g->mt[0] = seed;
+    for (int i = 1; i < 312; ++i)
+        g->mt[i] = 6364136223846793005ULL * (g->mt[i - 1] ^ (g->mt[i - 1] >> 62)) + (uint64_t)i;
+    g->idx = 312;
+}
+
+static uint64_t mt64_next(mt64* g) {
+    if (g->idx >= 312) {
+        for (int i = 0; i < 312; ++i) {
+            uint64_t x = (g->mt[i] & 0xFFFFFFFF80000000ULL) | (g->mt[(i + 1) % 312] & 0x7FFFFFFFULL);
+            uint64_t xa = x >> 1;
+            if (x & 1ULL) xa ^= 0xB5026F5AA96619E9ULL;
+            g->mt[i] = g->mt[(i + 156) % 312] ^ xa;
+        }
+        g->idx = 0;
+    }
+    uint64_t y = g->mt[g->idx++];
+    y ^= (y >> 29) & 0x5555555555555555ULL;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+    y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+    y ^= y >> 43;
+    return y;
+}
+
+static double u01(mt64* g) { return (double)(mt64_next(g) >> 11) * 0x1.0p-53; }
+static double u01_open_low(mt64* g) { return (double)((mt64_next(g) >> 11) + 1) * 0x1.0p-53; }
+
+typedef struct {
+    double spare;
+    int has_spare;
+} normal_t;
+
+static double normal_draw(normal_t* nm, mt64* g) {
+    if (nm->has_spare) {
+        nm->has_spare = 0;
+        return nm->spare;
+    }
+    const double u1 = u01_open_low(g);
+    const double u2 = u01(g);
+    const double radius = sqrt(-2.0 * log(u1));
+    const double angle = 2.0 * 3.141592653589793238462643383279502884 * u2;
+    nm->spare = radius * sin(angle);
+    nm->has_spare = 1;
+    return radius * cos(angle);
+}
+
+void orc_add_noise(double* xyz, size_t n, double sigma, uint64_t seed) {
+    mt64 g;
+    normal_t nm = {0.0, 0};
+    mt64_seed(&g, seed);
+    for (size_t i = 0; i < n; ++i) {
+        const double dx = sigma * normal_draw(&nm, &g);
+        const double dy = sigma * normal_draw(&nm, &g);
+        const double dz = sigma * normal_draw(&nm, &g);
+        xyz[3 * i + 0] = xyz[3 * i + 0] + dx;
+        xyz[3 * i + 1] = xyz[3 * i + 1] + dy;
+        xyz[3 * i + 2] = xyz[3 * i + 2] + dz;
+    }
+}
+
+void orc_plane(double* xyz, size_t n, uint64_t seed) {
+    mt64 g;
+    mt64_seed(&g, seed);
+    for (size_t i = 0; i < n; ++i) {
+        const double x = u01(&g);
+        const double y = u01(&g);
+        xyz[3 * i + 0] = x;
+        xyz[3 * i + 1] = y;
+        xyz[3 * i + 2] = 0.0;
+    }
+}
+
+void orc_sphere(double* xyz, size_t n, uint64_t seed) {
+    mt64 g;
+    mt64_seed(&g, seed);
+    for (size_t i = 0; i < n; ++i) {
+        const double z = 1.0 - 2.0 * u01(&g);
+        const double phi = 2.0 * 3.141592653589793238462643383279502884 * u01(&g);
+        const double t = 1.0 - z * z;
+        const double rxy = sqrt(t > 0.0 ? t : 0.0);
+        xyz[3 * i + 0] = rxy * cos(phi);
+        xyz[3 * i + 1] = rxy * sin(phi);
+        xyz[3 * i + 2] = z;
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* Weight kernels (proj/src/kernels.cpp)                                      */
+/* ------------------------------------------------------------------------ */
+
+double orc_theta(double d, double h, double cutoff) {
+    if (d > h * cutoff)
+        return 0.0;
+    const double s = d / h;
+    return exp(-s * s);
+}
+
+static double etad(double d, int kind) {
+    if (kind == ORC_ETA_NEG_LINEAR)
+        return 1.0;
+    const double d2 = d * d;
+    return 1.0 / (d2 * d2);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Exact radius queries on a uniform grid                                     */
+/* ------------------------------------------------------------------------ */
+
+typedef struct {
+    const double* pts;
+    size_t n;
+    double o[3];
+    double cs, inv;
+    int64_t g[3];
+    uint64_t* start; /* ncells + 1 */
+    uint32_t* order; /* point ids, grouped by cell, ascending id inside a cell */
+} grid_t;
+
+
+static int64_t cell_of(const grid_t* gr, int axis, double x) {
+    const double u = floor((x - gr->o[axis]) * gr->inv);
+    if (!(u >= 0.0)) return 0; /* also catches NaN */
+    if (u >= (double)(gr->g[axis] - 1)) return gr->g[axis] - 1;
+    return (int64_t)u;
+}
+
+static int grid_build(grid_t* gr, const double* pts, size_t n, double r) {
+    memset(gr, 0, sizeof(*gr));
+    gr->pts = pts;
+    gr->n = n;
+    double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    if (n > 0) {
+        for (int a = 0; a < 3; ++a) lo[a] = hi[a] = pts[a];
+        for (size_t i = 1; i < n; ++i)
+            for (int a = 0; a < 3; ++a) {
+                const double v = pts[3 * i + a];
+                if (v < lo[a]) lo[a] = v;
+                if (v > hi[a]) hi[a] = v;
+            }
+    }
+    double cs = r;
+    for (;;) {
+        double cells = 1.0;
+        for (int a = 0; a < 3; ++a) cells *= floor((hi[a] - lo[a]) / cs) + 1.0;
+        if (cells <= (double)(1u << 22)) break;
+        cs *= 1.25;
+    }
+    gr->cs = cs;
+    gr->inv = 1.0 / cs;
+    uint64_t ncells = 1;
+    for (int a = 0; a < 3; ++a) {
+        gr->o[a] = lo[a];
+        gr->g[a] = (int64_t)floor((hi[a] - lo[a]) * gr->inv) + 1;
+        ncells *= (uint64_t)gr->g[a];
+    }
+    gr->start = (uint64_t*)calloc(ncells + 1, sizeof(uint64_t));
+    gr->order = (uint32_t*)malloc((n ? n : 1) * sizeof(uint32_t));
+    uint64_t* cellid = (uint64_t*)malloc((n ? n : 1) * sizeof(uint64_t));
+    if (!gr->start || !gr->order || !cellid) {
+        free(cellid);
+        return ORC_NO_MEMORY;
+    }
+    for (size_t i = 0; i < n; ++i) {
+        const int64_t cx = cell_of(gr, 0, pts[3 * i + 0]);
+        const int64_t cy = cell_of(gr, 1, pts[3 * i + 1]);
+        const int64_t cz = cell_of(gr, 2, pts[3 * i + 2]);
+        cellid[i] = (uint64_t)(cx + gr->g[0] * (cy + gr->g[1] * cz));
+        gr->start[cellid[i] + 1]++;
+    }
+    for (uint64_t c = 0; c < ncells; ++c) gr->start[c + 1] += gr->start[c];
+    uint64_t* fill = (uint64_t*)malloc((ncells + 1) * sizeof(uint64_t));
+    if (!fill) {
+        free(cellid);
+        return ORC_NO_MEMORY;
+    }
+    memcpy(fill, gr->start, (ncells + 1) * sizeof(uint64_t));
+    for (size_t i = 0; i < n; ++i) gr->order[fill[cellid[i]]++] = (uint32_t)i; /* stable */
+    free(fill);
+    free(cellid);
+    return ORC_OK;
+}
+
+static void grid_free(grid_t* gr) {
+    free(gr->start);
+    free(gr->order);
+}
+
+typedef struct {
+    uint32_t* idx;
+    double* d2;
+    uint32_t* tidx;
+    double* td2;
+    size_t n, cap;
+} hits_t;
+
+static void hits_push(hits_t* h, uint32_t i, double d2) {
+    if (h->n == h->cap) {
+        size_t nc = h->cap ? 2 * h->cap : 256;
+        h->idx = (uint32_t*)realloc(h->idx, nc * sizeof(uint32_t));
+        h->d2 = (double*)realloc(h->d2, nc * sizeof(double));
+        h->tidx = (uint32_t*)realloc(h->tidx, nc * sizeof(uint32_t));
+        h->td2 = (double*)realloc(h->td2, nc * sizeof(double));
+        h->cap = nc;
+    }
+    h->idx[h->n] = i;
+    h->d2[h->n] = d2;
+    h->n++;
+}
+
+static void hits_free(hits_t* h) {
+    free(h->idx);
+    free(h->d2);
+    free(h->tidx);
+    free(h->td2);
+}
+
+/* Stable LSD radix sort of the hits by index (spatial.cpp:109-110 sorts by index). */
+static void hits_sort(hits_t* h, size_t n_points) {
+    if (h->n < 2) return;
+    if (h->n <= 32) { /* insertion sort for short lists */
+        for (size_t a = 1; a < h->n; ++a) {
+            uint32_t ki = h->idx[a];
+            double kd = h->d2[a];
+            size_t b = a;
+            while (b > 0 && h->idx[b - 1] > ki) {
+                h->idx[b] = h->idx[b - 1];
+                h->d2[b] = h->d2[b - 1];
+                --b;
+            }
+            h->idx[b] = ki;
+            h->d2[b] = kd;
+        }
+        return;
+    }
+    int passes = 0;
+    for (uint64_t v = n_points > 0 ? (uint64_t)(n_points - 1) : 0; v; v >>= 8) ++passes;
+    for (int p = 0; p < passes; ++p) {
+        size_t cnt[257];
+        memset(cnt, 0, sizeof(cnt));
+        const int sh = 8 * p;
+        for (size_t a = 0; a < h->n; ++a) cnt[((h->idx[a] >> sh) & 0xFF) + 1]++;
+        for (int b = 0; b < 256; ++b) cnt[b + 1] += cnt[b];
+        for (size_t a = 0; a < h->n; ++a) {
+            const size_t dst = cnt[(h->idx[a] >> sh) & 0xFF]++;
+            h->tidx[dst] = h->idx[a];
+            h->td2[dst] = h->d2[a];
+        }
+        uint32_t* ti = h->idx;
+        h->idx = h->tidx;
+        h->tidx = ti;
+        double* td = h->d2;
+        h->d2 = h->td2;
+        h->td2 = td;
+    }
+}
+
+/* radius_query(center, r): every point with norm2(p - c) <= r*r, ascending index. */
+static void grid_query(const grid_t* gr, const double* c, double r, hits_t* out) {
+    out->n = 0;
+    if (gr->n == 0) return;
+    const double r2 = r * r;
+    const double rp = r * (1.0 + 1e-6);
+    int64_t lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = cell_of(gr, a, c[a] - rp);
+        hi[a] = cell_of(gr, a, c[a] + rp);
+    }
+    for (int64_t z = lo[2]; z <= hi[2]; ++z)
+        for (int64_t y = lo[1]; y <= hi[1]; ++y) {
+            const uint64_t row = (uint64_t)(gr->g[0] * (y + gr->g[1] * z));
+            const uint64_t b = gr->start[row + (uint64_t)lo[0]];
+            const uint64_t e = gr->start[row + (uint64_t)hi[0] + 1];
+            for (uint64_t k = b; k < e; ++k) {
+                const uint32_t idx = gr->order[k];
+                const double* p = gr->pts + 3 * (size_t)idx;
+                /* norm2((*cloud_)[idx] - center): (dx*dx + dy*dy) + dz*dz */
+                const double dx = p[0] - c[0];
+                const double dy = p[1] - c[1];
+                const double dz = p[2] - c[2];
+                const double d2 = dx * dx + dy * dy + dz * dz;
+                if (d2 <= r2) hits_push(out, idx, d2);
+            }
+        }
+    hits_sort(out, gr->n);
+}
+
+static int set_threads(int threads) {
+#ifdef _OPENMP
+    if (threads > 0) omp_set_num_threads(threads);
+    return omp_get_max_threads();
+#else
+    (void)threads;
+    return 1;
+#endif
+}
+
+int orc_radius_query_all(const double* C, size_t n, const double* Q, size_t m, double r,
+                         uint64_t* offsets, uint32_t* idx, double* dist, int threads) {
+    if (!(r > 0.0) || !isfinite(r)) return ORC_INVALID_PARAM;
+    grid_t gr;
+    if (grid_build(&gr, C, n, r) != ORC_OK) return ORC_NO_MEMORY;
+    set_threads(threads);
+    if (!idx) {
+        offsets[0] = 0;
+#pragma omp parallel
+        {
+            hits_t h = {0};
+#pragma omp for schedule(dynamic, 64)
+            for (size_t i = 0; i < m; ++i) {
+                grid_query(&gr, Q + 3 * i, r, &h);
+                offsets[i + 1] = h.n;
+            }
+            hits_free(&h);
+        }
+        for (size_t i = 0; i < m; ++i) offsets[i + 1] += offsets[i];
+    } else {
+#pragma omp parallel
+        {
+            hits_t h = {0};
+#pragma omp for schedule(dynamic, 64)
+            for (size_t i = 0; i < m; ++i) {
+                grid_query(&gr, Q + 3 * i, r, &h);
+                const uint64_t o = offsets[i];
+                for (size_t k = 0; k < h.n; ++k) {
+                    idx[o + k] = h.idx[k];
+                    if (dist) dist[o + k] = sqrt(h.d2[k]);
+                }
+            }
+            hits_free(&h);
+        }
+    }
+    grid_free(&gr);
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Density weights (WLOP; not in the reference — pinned here)                 */
+/* ------------------------------------------------------------------------ */
+
+static void density_on_grid(const grid_t* gr, double h, double cutoff, double* v, size_t n) {
+    const double support = h * cutoff;
+#pragma omp parallel
+    {
+        hits_t ht = {0};
+#pragma omp for schedule(dynamic, 64)
+        for (size_t j = 0; j < n; ++j) {
+            grid_query(gr, gr->pts + 3 * j, support, &ht);
+            double acc = 1.0;
+            for (size_t k = 0; k < ht.n; ++k) {
+                if (ht.idx[k] == (uint32_t)j) continue;
+                acc += orc_theta(sqrt(ht.d2[k]), h, cutoff);
+            }
+            v[j] = acc;
+        }
+        hits_free(&ht);
+    }
+}
+
+int orc_density_weights(const double* C, size_t n, double h, double cutoff, double* v_out,
+                        int threads) {
+    if (!(h > 0.0) || !(cutoff > 0.0)) return ORC_INVALID_PARAM;
+    grid_t gr;
+    if (grid_build(&gr, C, n, h * cutoff) != ORC_OK) return ORC_NO_MEMORY;
+    set_threads(threads);
+    density_on_grid(&gr, h, cutoff, v_out, n);
+    grid_free(&gr);
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* The sweep (proj/src/lop.cpp:41-100)                                        */
+/* ------------------------------------------------------------------------ */
+
+static int validate(const orc_params* p) {
+    /* LopParams::validate (proj/include/pcs/lop.hpp:18-26) and KernelParams::validate */
+    if (!(p->h > 0.0)) return ORC_INVALID_PARAM;
+    if (!(p->cutoff_multiple > 0.0)) return ORC_INVALID_PARAM;
+    if (!(p->mu >= 0.0) || !(p->mu < 0.5)) return ORC_INVALID_PARAM;
+    if (p->iterations < 1) return ORC_INVALID_PARAM;
+    if (!(p->convergence_tol > 0.0)) return ORC_INVALID_PARAM;
+    if (p->eta_kind != ORC_ETA_INV_CUBE && p->eta_kind != ORC_ETA_NEG_LINEAR) return ORC_INVALID_PARAM;
+    return ORC_OK;
+}
+
+typedef struct {
+    uint64_t attr, rep;
+} pair_counts;
+
+/* One Jacobi sweep from cur to next. */
+static void sweep(const grid_t* pg, const double* P, const double* v, const grid_t* xg,
+                  const double* cur, const double* w, size_t m, const orc_params* prm,
+                  double* next, uint8_t* isolated, uint32_t* coincident, pair_counts* pc) {
+    const double support = prm->h * prm->cutoff_multiple;
+    const double mu = prm->mu;
+    uint64_t n_attr = 0, n_rep = 0;
+#pragma omp parallel reduction(+ : n_attr, n_rep)
+    {
+        hits_t ht = {0};
+#pragma omp for schedule(static)
+        for (size_t i = 0; i < m; ++i) {
+            const double* x = cur + 3 * i;
+            isolated[i] = 0;
+            coincident[i] = 0;
+            /* Attraction (lop.cpp:49-65) */
+            grid_query(pg, x, support, &ht);
+            double attr_wsum = 0.0;
+            double num[3] = {0.0, 0.0, 0.0};
+            int anchored = 0;
+            double anchor[3] = {0.0, 0.0, 0.0};
+            for (size_t k = 0; k < ht.n; ++k) {
+                const double dist = sqrt(ht.d2[k]);
+                const double* p = P + 3 * (size_t)ht.idx[k];
+                if (dist == 0.0) {
+                    if (!anchored) {
+                        anchored = 1;
+                        anchor[0] = p[0];
+                        anchor[1] = p[1];
+                        anchor[2] = p[2];
+                    }
+                    continue;
+                }
+                double wgt = orc_theta(dist, prm->h, prm->cutoff_multiple) / dist;
+                if (v) wgt = wgt / v[ht.idx[k]];
+                attr_wsum += wgt;
+                num[0] += wgt * p[0];
+                num[1] += wgt * p[1];
+                num[2] += wgt * p[2];
+                ++n_attr;
+            }
+            /* Isolation / anchor (lop.cpp:67-75) */
+            if (!(attr_wsum > 0.0)) {
+                if (anchored) {
+                    next[3 * i + 0] = anchor[0];
+                    next[3 * i + 1] = anchor[1];
+                    next[3 * i + 2] = anchor[2];
+                } else {
+                    isolated[i] = 1;
+                    next[3 * i + 0] = x[0];
+                    next[3 * i + 1] = x[1];
+                    next[3 * i + 2] = x[2];
+                }
+                continue;
+            }
+            /* Weiszfeld quotient (lop.cpp:77) */
+            double upd[3] = {num[0] / attr_wsum, num[1] / attr_wsum, num[2] / attr_wsum};
+            /* Repulsion (lop.cpp:79-97) */
+            if (mu > 0.0) {
+                grid_query(xg, x, support, &ht);
+                double rep_wsum = 0.0;
+                double rn[3] = {0.0, 0.0, 0.0};
+                for (size_t k = 0; k < ht.n; ++k) {
+                    if (ht.idx[k] == (uint32_t)i) continue;
+                    const double dist = sqrt(ht.d2[k]);
+                    if (dist == 0.0) {
+                        ++coincident[i];
+                        continue;
+                    }
+                    const double* xp = cur + 3 * (size_t)ht.idx[k];
+                    double wgt = orc_theta(dist, prm->h, prm->cutoff_multiple) *
+                                 etad(dist, prm->eta_kind) / dist;
+                    if (w) wgt = wgt * w[ht.idx[k]];
+                    rep_wsum += wgt;
+                    rn[0] += wgt * (x[0] - xp[0]);
+                    rn[1] += wgt * (x[1] - xp[1]);
+                    rn[2] += wgt * (x[2] - xp[2]);
+                    ++n_rep;
+                }
+                if (rep_wsum > 0.0) {
+                    upd[0] += mu * (rn[0] / rep_wsum);
+                    upd[1] += mu * (rn[1] / rep_wsum);
+                    upd[2] += mu * (rn[2] / rep_wsum);
+                }
+            }
+            next[3 * i + 0] = upd[0];
+            next[3 * i + 1] = upd[1];
+            next[3 * i + 2] = upd[2];
+        }
+        hits_free(&ht);
+    }
+    if (pc) {
+        pc->attr += n_attr;
+        pc->rep += n_rep;
+    }
+}
+
+static double max_displacement(const double* a, const double* b, size_t m) {
+    double md = 0.0;
+    for (size_t i = 0; i < m; ++i) {
+        const double dx = a[3 * i + 0] - b[3 * i + 0];
+        const double dy = a[3 * i + 1] - b[3 * i + 1];
+        const double dz = a[3 * i + 2] - b[3 * i + 2];
+        const double d = sqrt(dx * dx + dy * dy + dz * dz);
+        md = md > d ? md : d; /* std::max(max_disp, d) keeps the first on ties */
+    }
+    return md;
+}
+
+int orc_lop_sweep(const double* P, size_t n, const double* X, size_t m, const orc_params* prm,
+                  double* Xnext, uint8_t* isolated, uint32_t* coincident, double* max_disp,
+                  int threads) {
+    int rc = validate(prm);
+    if (rc) return rc;
+    if (n == 0) return ORC_EMPTY_CLOUD;
+    if (m == 0) return ORC_OK;
+    set_threads(threads);
+    const double support = prm->h * prm->cutoff_multiple;
+    grid_t pg, xg;
+    if (grid_build(&pg, P, n, support)) return ORC_NO_MEMORY;
+    if (grid_build(&xg, X, m, support)) {
+        grid_free(&pg);
+        return ORC_NO_MEMORY;
+    }
+    double* v = NULL;
+    double* w = NULL;
+    uint8_t* iso = isolated ? isolated : (uint8_t*)malloc(m);
+    uint32_t* co = coincident ? coincident : (uint32_t*)malloc(m * sizeof(uint32_t));
+    if (prm->density_weights) {
+        v = (double*)malloc(n * sizeof(double));
+        w = (double*)malloc(m * sizeof(double));
+        density_on_grid(&pg, prm->h, prm->cutoff_multiple, v, n);
+        density_on_grid(&xg, prm->h, prm->cutoff_multiple, w, m);
+    }
+    sweep(&pg, P, v, &xg, X, w, m, prm, Xnext, iso, co, NULL);
+    if (max_disp) *max_disp = max_displacement(Xnext, X, m);
+    if (!isolated) free(iso);
+    if (!coincident) free(co);
+    free(v);
+    free(w);
+    grid_free(&pg);
+    grid_free(&xg);
+    return ORC_OK;
+}
+
+int orc_lop_project(const double* P, size_t n, const double* X0, size_t m,
+                    const orc_params* prm, double* out, orc_summary* sum,
+                    uint32_t* isolated_out, int threads) {
+    /* Semantics order (lop.cpp:13-20): validate, empty data, empty initial. */
+    int rc = validate(prm);
+    if (rc) return rc;
+    if (n == 0) return ORC_EMPTY_CLOUD;
+    orc_summary s;
+    memset(&s, 0, sizeof(s));
+    if (m == 0) {
+        if (sum) *sum = s;
+        return ORC_OK;
+    }
+    set_threads(threads);
+    const double support = prm->h * prm->cutoff_multiple;
+    grid_t pg;
+    if (grid_build(&pg, P, n, support)) return ORC_NO_MEMORY;
+
+    double* cur = (double*)malloc(3 * m * sizeof(double));
+    double* nxt = (double*)malloc(3 * m * sizeof(double));
+    uint8_t* iso = (uint8_t*)malloc(m);
+    uint8_t* ever = (uint8_t*)calloc(m, 1);
+    uint32_t* co = (uint32_t*)malloc(m * sizeof(uint32_t));
+    double* v = NULL;
+    double* w = NULL;
+    if (prm->density_weights) {
+        v = (double*)malloc(n * sizeof(double));
+        w = (double*)malloc(m * sizeof(double));
+    }
+    if (!cur || !nxt || !iso || !ever || !co || (prm->density_weights && (!v || !w))) {
+        free(cur); free(nxt); free(iso); free(ever); free(co); free(v); free(w);
+        grid_free(&pg);
+        return ORC_NO_MEMORY;
+    }
+    memcpy(cur, X0, 3 * m * sizeof(double));
+    if (v) density_on_grid(&pg, prm->h, prm->cutoff_multiple, v, n);
+    pair_counts pc = {0, 0};
+    for (int it = 1; it <= prm->iterations; ++it) {
+        s.iterations_run = it;
+        grid_t xg;
+        if (grid_build(&xg, cur, m, support)) {
+            rc = ORC_NO_MEMORY;
+            break;
+        }
+        if (w) density_on_grid(&xg, prm->h, prm->cutoff_multiple, w, m);
+        sweep(&pg, P, v, &xg, cur, w, m, prm, nxt, iso, co, &pc);
+        grid_free(&xg);
+        /* Deterministic aggregation in index order (lop.cpp:102-113). */
+        const double md = max_displacement(nxt, cur, m);
+        for (size_t i = 0; i < m; ++i) {
+            if (iso[i]) {
+                s.isolated_events++;
+                ever[i] = 1;
+            }
+            s.coincident_pairs += co[i];
+        }
+        double* t = cur;
+        cur = nxt;
+        nxt = t;
+        s.last_max_disp = md;
+        if (md < prm->convergence_tol) {
+            s.converged = 1;
+            break;
+        }
+    }
+    s.interactions_attr = pc.attr;
+    s.interactions_rep = pc.rep;
+    if (rc == ORC_OK) {
+        memcpy(out, cur, 3 * m * sizeof(double));
+        uint64_t k = 0;
+        for (size_t i = 0; i < m; ++i)
+            if (ever[i]) {
+                if (isolated_out) isolated_out[k] = (uint32_t)i;
+                ++k;
+            }
+        s.n_isolated = k;
+        if (sum) *sum = s;
+    }
+    free(cur); free(nxt); free(iso); free(ever); free(co); free(v); free(w);
+    grid_free(&pg);
+    return rc;
+}

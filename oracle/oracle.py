@@ -1,0 +1,305 @@
+"""ctypes front-end for the CPU oracle (TEST INFRASTRUCTURE ONLY).
+
+Loads ``oracle/liborc.so`` (the C restatement, lop_oracle.c) and, when it was
+built, ``oracle/_ref/libpcs_ref.so`` (the unmodified reference compiled from
+/root/reference by oracle/Makefile).  Only tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs import this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORC_PATH = os.path.join(HERE, "liborc.so")
+REF_PATH = os.path.join(HERE, "_ref", "libpcs_ref.so")
+
+ETA_INV_CUBE = 0
+ETA_NEG_LINEAR = 1
+
+_c_dbl_p = C.POINTER(C.c_double)
+_c_u64_p = C.POINTER(C.c_uint64)
+_c_u32_p = C.POINTER(C.c_uint32)
+_c_u8_p = C.POINTER(C.c_uint8)
+
+
+class OrcParams(C.Structure):
+    _fields_ = [
+        ("h", C.c_double),
+        ("cutoff_multiple", C.c_double),
+        ("mu", C.c_double),
+        ("iterations", C.c_int32),
+        ("convergence_tol", C.c_double),
+        ("eta_kind", C.c_int32),
+        ("density_weights", C.c_int32),
+    ]
+
+
+class OrcSummary(C.Structure):
+    _fields_ = [
+        ("iterations_run", C.c_int32),
+        ("converged", C.c_int32),
+        ("isolated_events", C.c_uint64),
+        ("coincident_pairs", C.c_uint64),
+        ("n_isolated", C.c_uint64),
+        ("interactions_attr", C.c_uint64),
+        ("interactions_rep", C.c_uint64),
+        ("density_pairs_x", C.c_uint64),
+        ("density_pairs_p", C.c_uint64),
+        ("last_max_disp", C.c_double),
+    ]
+
+
+class RefSummary(C.Structure):
+    _fields_ = [
+        ("iterations_run", C.c_int32),
+        ("converged", C.c_int32),
+        ("isolated_events", C.c_uint64),
+        ("coincident_pairs", C.c_uint64),
+        ("n_isolated", C.c_uint64),
+    ]
+
+
+@dataclass
+class Result:
+    points: np.ndarray
+    iterations_run: int
+    converged: bool
+    isolated_events: int
+    coincident_pairs: int
+    isolated_indices: np.ndarray
+    interactions_attr: int = 0
+    interactions_rep: int = 0
+    last_max_disp: float = 0.0
+
+
+def build(reference: bool = True) -> None:
+    """Build liborc.so (and _ref when /root/reference is present)."""
+    targets = ["oracle"]
+    if reference and os.path.isdir("/root/reference/proj/src"):
+        targets.append("ref")
+    subprocess.run(["make", "-s", "-C", HERE, *targets], check=True)
+
+
+_orc = None
+_ref = None
+
+
+def _ptr(a, t):
+    return a.ctypes.data_as(t)
+
+
+def orc():
+    global _orc
+    if _orc is None:
+        if not os.path.exists(ORC_PATH):
+            build(reference=False)
+        lib = C.CDLL(ORC_PATH)
+        lib.orc_lop_project.argtypes = [_c_dbl_p, C.c_size_t, _c_dbl_p, C.c_size_t,
+                                        C.POINTER(OrcParams), _c_dbl_p, C.POINTER(OrcSummary),
+                                        _c_u32_p, C.c_int]
+        lib.orc_lop_sweep.argtypes = [_c_dbl_p, C.c_size_t, _c_dbl_p, C.c_size_t,
+                                      C.POINTER(OrcParams), _c_dbl_p, _c_u8_p, _c_u32_p,
+                                      _c_dbl_p, C.c_int]
+        lib.orc_radius_query_all.argtypes = [_c_dbl_p, C.c_size_t, _c_dbl_p, C.c_size_t,
+                                             C.c_double, _c_u64_p, _c_u32_p, _c_dbl_p, C.c_int]
+        lib.orc_density_weights.argtypes = [_c_dbl_p, C.c_size_t, C.c_double, C.c_double,
+                                            _c_dbl_p, C.c_int]
+        lib.orc_add_noise.argtypes = [_c_dbl_p, C.c_size_t, C.c_double, C.c_uint64]
+        lib.orc_plane.argtypes = [_c_dbl_p, C.c_size_t, C.c_uint64]
+        lib.orc_sphere.argtypes = [_c_dbl_p, C.c_size_t, C.c_uint64]
+        lib.orc_theta.argtypes = [C.c_double, C.c_double, C.c_double]
+        lib.orc_theta.restype = C.c_double
+        _orc = lib
+    return _orc
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_PATH)
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        if not ref_available():
+            raise FileNotFoundError(REF_PATH)
+        lib = C.CDLL(REF_PATH)
+        lib.ref_lop_project.argtypes = [_c_dbl_p, C.c_uint64, _c_dbl_p, C.c_uint64, C.c_double,
+                                        C.c_double, C.c_double, C.c_int, C.c_double, _c_dbl_p,
+                                        C.POINTER(RefSummary), _c_u32_p]
+        lib.ref_radius_query_all.argtypes = [_c_dbl_p, C.c_uint64, _c_dbl_p, C.c_uint64,
+                                             C.c_double, _c_u64_p, _c_u32_p, _c_dbl_p]
+        lib.ref_add_noise.argtypes = [_c_dbl_p, C.c_uint64, C.c_double, C.c_uint64]
+        lib.ref_generate_surface.argtypes = [C.c_int, C.c_uint64, C.c_uint64, _c_dbl_p]
+        lib.ref_theta.argtypes = [C.c_double, C.c_double, C.c_double]
+        lib.ref_theta.restype = C.c_double
+        lib.ref_last_error.restype = C.c_char_p
+        _ref = lib
+    return _ref
+
+
+def _xyz(a) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64).reshape(-1, 3))
+    return a
+
+
+ERRORS = {1: "InvalidParam", 2: "EmptyCloud", 3: "NoMemory"}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, what: str = ""):
+        self.code = code
+        self.kind = ERRORS.get(code, "Error")
+        super().__init__(f"{self.kind}({code}) {what}")
+
+
+def lop_project(P, X0, h, cutoff=3.0, mu=0.4, iterations=30, tol=1e-7,
+                eta=ETA_INV_CUBE, wlop=False, threads=0) -> Result:
+    """orc_lop_project — the C restatement of pcs::lop_project (+eta/WLOP)."""
+    P = _xyz(P)
+    X0 = _xyz(X0)
+    m = X0.shape[0]
+    out = np.empty_like(X0)
+    iso = np.empty(max(m, 1), dtype=np.uint32)
+    prm = OrcParams(h, cutoff, mu, iterations, tol, eta, 1 if wlop else 0)
+    s = OrcSummary()
+    rc = orc().orc_lop_project(_ptr(P, _c_dbl_p), P.shape[0], _ptr(X0, _c_dbl_p), m,
+                               C.byref(prm), _ptr(out, _c_dbl_p), C.byref(s),
+                               _ptr(iso, _c_u32_p), threads)
+    if rc:
+        raise OracleError(rc)
+    return Result(out, s.iterations_run, bool(s.converged), s.isolated_events,
+                  s.coincident_pairs, iso[: s.n_isolated].copy(), s.interactions_attr,
+                  s.interactions_rep, s.last_max_disp)
+
+
+def lop_sweep(P, X, h, cutoff=3.0, mu=0.4, eta=ETA_INV_CUBE, wlop=False, threads=0):
+    """One Jacobi sweep: returns (X_next, isolated[u8], coincident[u32], max_disp)."""
+    P = _xyz(P)
+    X = _xyz(X)
+    m = X.shape[0]
+    nxt = np.empty_like(X)
+    iso = np.zeros(max(m, 1), dtype=np.uint8)
+    co = np.zeros(max(m, 1), dtype=np.uint32)
+    md = C.c_double(0.0)
+    prm = OrcParams(h, cutoff, mu, 1, 1e-7, eta, 1 if wlop else 0)
+    rc = orc().orc_lop_sweep(_ptr(P, _c_dbl_p), P.shape[0], _ptr(X, _c_dbl_p), m, C.byref(prm),
+                             _ptr(nxt, _c_dbl_p), _ptr(iso, _c_u8_p), _ptr(co, _c_u32_p),
+                             C.byref(md), threads)
+    if rc:
+        raise OracleError(rc)
+    return nxt, iso[:m], co[:m], md.value
+
+
+def radius_query_all(C_pts, Q, r, threads=0):
+    """CSR (offsets[m+1], idx, dist) of SpatialIndex::radius_query for every query."""
+    C_pts = _xyz(C_pts)
+    Q = _xyz(Q)
+    m = Q.shape[0]
+    off = np.zeros(m + 1, dtype=np.uint64)
+    lib = orc()
+    rc = lib.orc_radius_query_all(_ptr(C_pts, _c_dbl_p), C_pts.shape[0], _ptr(Q, _c_dbl_p), m,
+                                  r, _ptr(off, _c_u64_p), None, None, threads)
+    if rc:
+        raise OracleError(rc)
+    tot = int(off[-1])
+    idx = np.empty(max(tot, 1), dtype=np.uint32)
+    dist = np.empty(max(tot, 1), dtype=np.float64)
+    rc = lib.orc_radius_query_all(_ptr(C_pts, _c_dbl_p), C_pts.shape[0], _ptr(Q, _c_dbl_p), m,
+                                  r, _ptr(off, _c_u64_p), _ptr(idx, _c_u32_p),
+                                  _ptr(dist, _c_dbl_p), threads)
+    if rc:
+        raise OracleError(rc)
+    return off, idx[:tot], dist[:tot]
+
+
+def density_weights(C_pts, h, cutoff, threads=0):
+    C_pts = _xyz(C_pts)
+    v = np.empty(C_pts.shape[0], dtype=np.float64)
+    rc = orc().orc_density_weights(_ptr(C_pts, _c_dbl_p), C_pts.shape[0], h, cutoff,
+                                   _ptr(v, _c_dbl_p), threads)
+    if rc:
+        raise OracleError(rc)
+    return v
+
+
+def add_noise(xyz, sigma, seed):
+    a = _xyz(xyz).copy()
+    orc().orc_add_noise(_ptr(a, _c_dbl_p), a.shape[0], sigma, seed)
+    return a
+
+
+def plane(n, seed):
+    a = np.empty((n, 3), dtype=np.float64)
+    orc().orc_plane(_ptr(a, _c_dbl_p), n, seed)
+    return a
+
+
+def sphere(n, seed):
+    a = np.empty((n, 3), dtype=np.float64)
+    orc().orc_sphere(_ptr(a, _c_dbl_p), n, seed)
+    return a
+
+
+def theta(d, h, cutoff=3.0):
+    return orc().orc_theta(d, h, cutoff)
+
+
+# --- the unmodified reference (oracle/_ref) ------------------------------------
+
+def ref_lop_project(P, X0, h, cutoff=3.0, mu=0.4, iterations=30, tol=1e-7) -> Result:
+    P = _xyz(P)
+    X0 = _xyz(X0)
+    m = X0.shape[0]
+    out = np.empty_like(X0)
+    iso = np.empty(max(m, 1), dtype=np.uint32)
+    s = RefSummary()
+    lib = ref()
+    rc = lib.ref_lop_project(_ptr(P, _c_dbl_p), P.shape[0], _ptr(X0, _c_dbl_p), m, h, cutoff,
+                             mu, iterations, tol, _ptr(out, _c_dbl_p), C.byref(s),
+                             _ptr(iso, _c_u32_p))
+    if rc:
+        raise OracleError(rc, lib.ref_last_error().decode())
+    return Result(out, s.iterations_run, bool(s.converged), s.isolated_events,
+                  s.coincident_pairs, iso[: s.n_isolated].copy())
+
+
+def ref_radius_query_all(C_pts, Q, r):
+    C_pts = _xyz(C_pts)
+    Q = _xyz(Q)
+    m = Q.shape[0]
+    off = np.zeros(m + 1, dtype=np.uint64)
+    lib = ref()
+    rc = lib.ref_radius_query_all(_ptr(C_pts, _c_dbl_p), C_pts.shape[0], _ptr(Q, _c_dbl_p), m,
+                                  r, _ptr(off, _c_u64_p), None, None)
+    if rc:
+        raise OracleError(rc, lib.ref_last_error().decode())
+    tot = int(off[-1])
+    idx = np.empty(max(tot, 1), dtype=np.uint32)
+    dist = np.empty(max(tot, 1), dtype=np.float64)
+    rc = lib.ref_radius_query_all(_ptr(C_pts, _c_dbl_p), C_pts.shape[0], _ptr(Q, _c_dbl_p), m,
+                                  r, _ptr(off, _c_u64_p), _ptr(idx, _c_u32_p),
+                                  _ptr(dist, _c_dbl_p))
+    if rc:
+        raise OracleError(rc, lib.ref_last_error().decode())
+    return off, idx[:tot], dist[:tot]
+
+
+def ref_generate_surface(kind: int, n: int, seed: int) -> np.ndarray:
+    a = np.empty((n, 3), dtype=np.float64)
+    rc = ref().ref_generate_surface(kind, n, seed, _ptr(a, _c_dbl_p))
+    if rc:
+        raise OracleError(rc)
+    return a
+
+
+def ref_add_noise(xyz, sigma, seed):
+    a = _xyz(xyz).copy()
+    rc = ref().ref_add_noise(_ptr(a, _c_dbl_p), a.shape[0], sigma, seed)
+    if rc:
+        raise OracleError(rc)
+    return a

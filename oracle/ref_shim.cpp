@@ -1,0 +1,161 @@
+// ref_shim.cpp — extern "C" entry points over the UNMODIFIED reference
+// library, compiled together with the reference's own sources where they lie
+// (/root/reference/proj/src/{core,kernels,spatial,lop,noise,bench,io}.cpp) by
+// oracle/Makefile into oracle/_ref/libpcs_ref.so.
+//
+// TEST INFRASTRUCTURE ONLY: loaded by tests/ (to pin oracle/lop_oracle.c) and
+// by bench.py's --impl reference / cpu_baseline legs (the reference's own CPU
+// path, timed on the host cores).  No reference source is copied here; this
+// file only calls the reference's public API:
+//   pcs::lop_project            proj/include/pcs/lop.hpp:51-53
+//   pcs::SpatialIndex           proj/include/pcs/spatial.hpp:19-56
+//   pcs::add_noise              proj/include/pcs/noise.hpp
+//   pcs::generate_surface       proj/include/pcs/bench.hpp
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "pcs/bench.hpp"
+#include "pcs/errors.hpp"
+#include "pcs/lop.hpp"
+#include "pcs/mls.hpp"
+#include "pcs/noise.hpp"
+#include "pcs/parallel.hpp"
+#include "pcs/spatial.hpp"
+
+// bench.cpp references the MLS operators (run_benchmark); they need Eigen
+// (proj/src/wls.cpp), which this image lacks, and they are off the LOP path.
+namespace pcs {
+std::pair<PointCloud, SmoothingSummary> smooth_cloud(const PointCloud&, const MlsParams&) {
+    throw Error("ref_shim: MLS is not built (Eigen absent); off the LOP path");
+}
+std::pair<PointCloud, SmoothingSummary> parallel_smooth(const PointCloud&, const MlsParams&,
+                                                        std::size_t) {
+    throw Error("ref_shim: MLS is not built (Eigen absent); off the LOP path");
+}
+}  // namespace pcs
+
+namespace {
+thread_local std::string g_err;
+
+pcs::PointCloud to_cloud(const double* xyz, std::uint64_t n) {
+    pcs::PointCloud c;
+    c.points.resize(n);
+    for (std::uint64_t i = 0; i < n; ++i) c.points[i] = {xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]};
+    return c;
+}
+
+void from_cloud(const pcs::PointCloud& c, double* xyz) {
+    for (std::size_t i = 0; i < c.size(); ++i) {
+        xyz[3 * i] = c[i].x;
+        xyz[3 * i + 1] = c[i].y;
+        xyz[3 * i + 2] = c[i].z;
+    }
+}
+
+int code_of(const std::exception& e) {
+    g_err = e.what();
+    if (dynamic_cast<const pcs::InvalidParam*>(&e)) return 1;
+    if (dynamic_cast<const pcs::EmptyCloud*>(&e)) return 2;
+    return 9;
+}
+}  // namespace
+
+extern "C" {
+
+struct ref_summary {
+    std::int32_t iterations_run;
+    std::int32_t converged;
+    std::uint64_t isolated_events;
+    std::uint64_t coincident_pairs;
+    std::uint64_t n_isolated;
+};
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_lop_project(const double* P, std::uint64_t n, const double* X0, std::uint64_t m, double h,
+                    double cutoff, double mu, int iterations, double tol, double* out,
+                    ref_summary* sum, std::uint32_t* isolated_out) {
+    try {
+        pcs::LopParams prm;
+        prm.kernel.h = h;
+        prm.kernel.cutoff_multiple = cutoff;
+        prm.mu = mu;
+        prm.iterations = iterations;
+        prm.convergence_tol = tol;
+        const auto data = to_cloud(P, n);
+        const auto init = to_cloud(X0, m);
+        const auto [q, s] = pcs::lop_project(data, init, prm);
+        from_cloud(q, out);
+        if (sum) {
+            sum->iterations_run = s.iterations_run;
+            sum->converged = s.converged ? 1 : 0;
+            sum->isolated_events = s.isolated_events;
+            sum->coincident_pairs = s.coincident_pairs;
+            sum->n_isolated = s.isolated_indices.size();
+        }
+        if (isolated_out)
+            for (std::size_t k = 0; k < s.isolated_indices.size(); ++k)
+                isolated_out[k] = s.isolated_indices[k];
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+// CSR radius queries through the reference kd-tree.  offsets: m+1 entries.
+// Pass idx == nullptr to size the output first.
+int ref_radius_query_all(const double* C, std::uint64_t n, const double* Q, std::uint64_t m,
+                         double r, std::uint64_t* offsets, std::uint32_t* idx, double* dist) {
+    try {
+        const auto cloud = to_cloud(C, n);
+        const pcs::SpatialIndex index(cloud);
+        std::vector<pcs::SpatialIndex::Hit> hits;
+        offsets[0] = 0;
+        for (std::uint64_t i = 0; i < m; ++i) {
+            index.radius_query({Q[3 * i], Q[3 * i + 1], Q[3 * i + 2]}, r, hits);
+            if (idx) {
+                const std::uint64_t o = offsets[i];
+                for (std::size_t k = 0; k < hits.size(); ++k) {
+                    idx[o + k] = static_cast<std::uint32_t>(hits[k].index);
+                    if (dist) dist[o + k] = hits[k].distance;
+                }
+            } else {
+                offsets[i + 1] = offsets[i] + hits.size();
+            }
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+int ref_add_noise(double* xyz, std::uint64_t n, double sigma, std::uint64_t seed) {
+    try {
+        const auto c = pcs::add_noise(to_cloud(xyz, n), {sigma, seed});
+        from_cloud(c, xyz);
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+// kind: 0 plane, 1 sphere, 2 torus, 3 gaussian bump (pcs::SurfaceKind order)
+int ref_generate_surface(int kind, std::uint64_t n, std::uint64_t seed, double* xyz) {
+    try {
+        const auto c = pcs::generate_surface(
+            {static_cast<pcs::SurfaceKind>(kind), static_cast<std::size_t>(n), seed});
+        from_cloud(c, xyz);
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+double ref_theta(double d, double h, double cutoff) {
+    return pcs::theta(d, pcs::KernelParams{h, cutoff});
+}
+
+}  // extern "C"

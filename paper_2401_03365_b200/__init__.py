@@ -1,0 +1,17 @@
+"""B200-native LOP/WLOP (drop-in for pcs::lop_project of arXiv 2401.03365's reference).
+
+The operator runs as hand-written sm_100a CUDA kernels in
+``lib/libpcs_lop_b200.so`` behind the C ABI of ``include/pcs_lop.h``.
+"""
+from .lop import (  # noqa: F401
+    CONFIGS, EmptyCloud, Error, InvalidParam, KernelParams, LopParams, LopPlan, LopSummary,
+    NumericalFailure, DeviceUnavailable, add_noise, config_params, config_sizes, generate_config,
+    generate_surface, grid_sort, lop_project, radius_query_all,
+)
+
+__all__ = [
+    "CONFIGS", "EmptyCloud", "Error", "InvalidParam", "KernelParams", "LopParams", "LopPlan",
+    "LopSummary", "NumericalFailure", "DeviceUnavailable", "add_noise", "config_params",
+    "config_sizes", "generate_config", "generate_surface", "grid_sort", "lop_project",
+    "radius_query_all",
+]

@@ -1,0 +1,195 @@
+// c_api.cpp — the extern "C" boundary (include/pcs_lop.h).
+//
+// Every entry point converts pcsb::Failure / std::exception into a pcs_status
+// and a thread-local message (pcs_last_error), the C rendering of the
+// reference's exception hierarchy (proj/include/pcs/errors.hpp:9-53).
+#include <cstring>
+#include <exception>
+#include <new>
+#include <string>
+
+#include "../../include/pcs_lop.h"
+#include "plan.cuh"
+
+namespace {
+thread_local std::string g_last_error;
+
+template <typename F>
+pcs_status guarded(F&& f) {
+    try {
+        g_last_error.clear();
+        f();
+        return PCS_OK;
+    } catch (const pcsb::Failure& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return PCS_ERR_NUMERICAL;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return PCS_ERR_NUMERICAL;
+    }
+}
+
+const pcs_lop_desc& checked(const pcs_lop_desc* d) {
+    if (!d) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null descriptor");
+    if (d->struct_size != sizeof(pcs_lop_desc))
+        throw pcsb::Failure(PCS_ERR_INVALID_PARAM,
+                            "pcs_lop_desc.struct_size mismatch (initialise with pcs_lop_desc_default)");
+    return *d;
+}
+}  // namespace
+
+extern "C" {
+
+void pcs_lop_desc_default(pcs_lop_desc* d) {
+    if (!d) return;
+    std::memset(d, 0, sizeof(*d));
+    d->struct_size = sizeof(pcs_lop_desc);
+    // defaults of KernelParams / LopParams (kernels.hpp:13-14, lop.hpp:14-17)
+    d->h = 1.0;
+    d->cutoff_multiple = 3.0;
+    d->mu = 0.4;
+    d->iterations = 30;
+    d->convergence_tol = 1e-7;
+    d->eta_kind = PCS_ETA_INV_CUBE;
+    d->density_weights = 0;
+    d->precision = PCS_PREC_FP64;
+    d->device = -1;
+    d->lanes_per_point = 0;
+}
+
+const char* pcs_last_error(void) { return g_last_error.c_str(); }
+
+int32_t pcs_lop_abi_version(void) { return PCS_LOP_ABI_VERSION; }
+
+pcs_status pcs_lop_validate(const pcs_lop_desc* d) {
+    return guarded([&] { pcsb::validate_desc(checked(d)); });
+}
+
+pcs_status pcs_lop_run(const pcs_lop_desc* d, const double* P_xyz, uint64_t n,
+                       const double* X0_xyz, uint64_t m, double* X_out_xyz,
+                       pcs_lop_summary* summary, uint32_t* isolated_out, uint64_t isolated_cap) {
+    return guarded([&] {
+        const pcs_lop_desc& desc = checked(d);
+        // semantics order of proj/src/lop.cpp:13-20
+        pcsb::validate_desc(desc);
+        if (n == 0) throw pcsb::Failure(PCS_ERR_EMPTY_CLOUD, "lop_project: data cloud is empty");
+        if (summary) std::memset(summary, 0, sizeof(*summary));
+        if (m == 0) return;
+        if (!P_xyz || !X0_xyz || !X_out_xyz)
+            throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null point buffer");
+        pcsb::Plan plan(desc);
+        plan.upload(P_xyz, n, X0_xyz, m);
+        plan.run(desc.iterations, true);
+        plan.download(X_out_xyz, summary, isolated_out, isolated_cap);
+    });
+}
+
+pcs_status pcs_lop_plan_create(const pcs_lop_desc* d, pcs_lop_plan** out) {
+    return guarded([&] {
+        if (!out) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null plan pointer");
+        *out = nullptr;
+        auto* p = new pcsb::Plan(checked(d));
+        *out = reinterpret_cast<pcs_lop_plan*>(p);
+    });
+}
+
+void pcs_lop_plan_destroy(pcs_lop_plan* p) { delete reinterpret_cast<pcsb::Plan*>(p); }
+
+#define PLAN(p)                                                                    \
+    if (!(p)) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null plan");             \
+    auto& plan = *reinterpret_cast<pcsb::Plan*>(p)
+
+pcs_status pcs_lop_plan_upload(pcs_lop_plan* p, const double* P_xyz, uint64_t n,
+                               const double* X0_xyz, uint64_t m) {
+    return guarded([&] {
+        PLAN(p);
+        plan.upload(P_xyz, n, X0_xyz, m);
+    });
+}
+
+pcs_status pcs_nccl_unique_id(uint8_t id_out[128]);
+
+pcs_status pcs_lop_plan_set_comm(pcs_lop_plan* p, const uint8_t id[128], int32_t nranks,
+                                 int32_t rank) {
+    return guarded([&] {
+        PLAN(p);
+        plan.set_comm(id, nranks, rank);
+    });
+}
+
+pcs_status pcs_lop_plan_reset(pcs_lop_plan* p) {
+    return guarded([&] {
+        PLAN(p);
+        plan.reset();
+    });
+}
+
+pcs_status pcs_lop_plan_run(pcs_lop_plan* p, int32_t sweeps, int32_t sync) {
+    return guarded([&] {
+        PLAN(p);
+        plan.run(sweeps, sync != 0);
+    });
+}
+
+pcs_status pcs_lop_plan_synchronize(pcs_lop_plan* p) {
+    return guarded([&] {
+        PLAN(p);
+        plan.synchronize();
+    });
+}
+
+pcs_status pcs_lop_plan_last_run_ms(pcs_lop_plan* p, double* ms) {
+    return guarded([&] {
+        PLAN(p);
+        plan.synchronize();
+        if (ms) *ms = plan.last_run_ms();
+    });
+}
+
+pcs_status pcs_lop_plan_download(pcs_lop_plan* p, double* X_out_xyz, pcs_lop_summary* summary,
+                                 uint32_t* isolated_out, uint64_t isolated_cap) {
+    return guarded([&] {
+        PLAN(p);
+        plan.download(X_out_xyz, summary, isolated_out, isolated_cap);
+    });
+}
+
+uint64_t pcs_lop_plan_launches(const pcs_lop_plan* p) {
+    return p ? reinterpret_cast<const pcsb::Plan*>(p)->launches() : 0;
+}
+
+pcs_status pcs_radius_query_all(const pcs_lop_desc* d, const double* C_xyz, uint64_t n,
+                                const double* Q_xyz, uint64_t m, double r, uint64_t* offsets,
+                                uint32_t* idx, uint64_t idx_cap) {
+    return guarded([&] {
+        if (!offsets) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null offsets");
+        pcsb::radius_query_all(checked(d), C_xyz, n, Q_xyz, m, r, offsets, idx, idx_cap);
+    });
+}
+
+pcs_status pcs_grid_sort(const pcs_lop_desc* d, const double* C_xyz, uint64_t n, double support,
+                         uint32_t* keys_out, uint32_t* order_out) {
+    return guarded([&] {
+        pcsb::grid_sort(checked(d), C_xyz, n, support, keys_out, order_out);
+    });
+}
+
+}  // extern "C"
+
+#include "nccl_dl.h"
+
+extern "C" pcs_status pcs_nccl_unique_id(uint8_t id_out[128]) {
+    return guarded([&] {
+        if (!id_out) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null id buffer");
+        std::string err;
+        const pcsb::NcclApi* api = pcsb::nccl_api(&err);
+        if (!api) throw pcsb::Failure(PCS_ERR_NCCL, err);
+        ncclUniqueId uid;
+        const ncclResult_t r = api->GetUniqueId(&uid);
+        if (r != ncclSuccess) throw pcsb::Failure(PCS_ERR_NCCL, api->GetErrorString(r));
+        std::memcpy(id_out, &uid, 128);
+    });
+}

@@ -1,0 +1,338 @@
+// grid_sort.cu — the spatial hash: fp64 cell keys, a hand-written stable LSD
+// radix sort of (key, index), the gather into sorted order and the cell
+// lower-bound table.  Replaces the reference's kd-tree build + radius query
+// (proj/src/spatial.cpp:32-111) with integer work that is HBM/L2-bound.
+#include <cstdio>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace pcsb {
+
+namespace {
+
+constexpr int RS_THREADS = 256;
+constexpr int RS_ITEMS = 8;
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_SCAN_THREADS = 1024;
+
+__device__ __forceinline__ unsigned long long double_to_ordered(double v) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+
+template <typename V, typename T>
+__global__ void convert_xyz_kernel(const double* __restrict__ xyz, V* __restrict__ out, uint64_t n,
+                                   T w) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        V v;
+        v.x = (T)xyz[3 * i];
+        v.y = (T)xyz[3 * i + 1];
+        v.z = (T)xyz[3 * i + 2];
+        v.w = w;
+        out[i] = v;
+    }
+}
+
+template <typename V>
+__global__ void bbox_kernel(const V* __restrict__ pts, uint64_t n, unsigned long long* slots) {
+    double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const V p = pts[i];
+        const double c[3] = {(double)p.x, (double)p.y, (double)p.z};
+        if (!(c[0] == c[0])) continue;  // NaN marks an unused padding slot
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            mn[a] = fmin(mn[a], c[a]);
+            mx[a] = fmax(mx[a], c[a]);
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        for (int o = 16; o; o >>= 1) {
+            mn[a] = fmin(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
+            mx[a] = fmax(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+        }
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            if (mn[a] <= mx[a]) {
+                atomicMin(&slots[a], double_to_ordered(mn[a]));
+                atomicMax(&slots[3 + a], double_to_ordered(mx[a]));
+            }
+        }
+    }
+}
+
+__global__ void init_bbox_kernel(unsigned long long* slots) {
+    if (threadIdx.x < 3) slots[threadIdx.x] = ~0ULL;
+    else if (threadIdx.x < 6) slots[threadIdx.x] = 0ULL;
+}
+
+template <typename V>
+__global__ void keys_kernel(GridGeom g, const V* __restrict__ pts, uint32_t n,
+                            uint32_t* __restrict__ keys, const uint32_t* done) {
+    if (done && *done) return;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const V p = pts[i];
+        const double x = (double)p.x;
+        keys[i] = (x == x) ? point_key(g, x, (double)p.y, (double)p.z) : 0xFFFFFFFFu;
+    }
+}
+
+// ---- radix sort -------------------------------------------------------------
+
+__global__ void __launch_bounds__(RS_THREADS)
+rs_hist_kernel(const uint32_t* __restrict__ keys, uint32_t n, int shift, uint32_t mask,
+               uint32_t* __restrict__ blockhist, uint32_t nblocks, const uint32_t* done) {
+    if (done && *done) return;
+    __shared__ uint32_t h[RS_WARPS][256];
+    for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_THREADS) (&h[0][0])[i] = 0;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5;
+    const uint32_t base = blockIdx.x * RS_TILE;
+#pragma unroll
+    for (int r = 0; r < RS_ITEMS; ++r) {
+        const uint32_t i = base + r * RS_THREADS + threadIdx.x;
+        if (i < n) atomicAdd(&h[warp][(keys[i] >> shift) & mask], 1u);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < 256; d += RS_THREADS) {
+        uint32_t s = 0;
+#pragma unroll
+        for (int w = 0; w < RS_WARPS; ++w) s += h[w][d];
+        blockhist[(size_t)d * nblocks + blockIdx.x] = s;
+    }
+}
+
+// Exclusive scan of `total` entries in one block (digit-major block histograms).
+__global__ void __launch_bounds__(RS_SCAN_THREADS)
+rs_scan_kernel(uint32_t* __restrict__ a, uint32_t total, const uint32_t* done) {
+    if (done && *done) return;
+    __shared__ uint32_t part[RS_SCAN_THREADS];
+    const uint32_t chunk = (total + RS_SCAN_THREADS - 1) / RS_SCAN_THREADS;
+    const uint32_t b = threadIdx.x * chunk;
+    const uint32_t e = min(b + chunk, total);
+    uint32_t s = 0;
+    for (uint32_t i = b; i < e; ++i) s += a[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    // Hillis-Steele inclusive scan over the per-thread sums
+    for (int o = 1; o < RS_SCAN_THREADS; o <<= 1) {
+        const uint32_t v = threadIdx.x >= (unsigned)o ? part[threadIdx.x - o] : 0u;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint32_t run = threadIdx.x ? part[threadIdx.x - 1] : 0u;
+    for (uint32_t i = b; i < e; ++i) {
+        const uint32_t v = a[i];
+        a[i] = run;
+        run += v;
+    }
+}
+
+// Stable scatter: within a tile elements keep their order (round-major,
+// warp-major, lane-minor), ranks inside a warp come from __match_any_sync.
+__global__ void __launch_bounds__(RS_THREADS)
+rs_scatter_kernel(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                  uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, uint32_t n, int shift,
+                  uint32_t mask, const uint32_t* __restrict__ blockoff, uint32_t nblocks,
+                  const uint32_t* done) {
+    if (done && *done) return;
+    __shared__ uint32_t run[256];
+    __shared__ uint32_t wcnt[RS_WARPS][256];
+    __shared__ uint32_t woff[RS_WARPS][256];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int d = threadIdx.x; d < 256; d += RS_THREADS) {
+        run[d] = blockoff[(size_t)d * nblocks + blockIdx.x];
+#pragma unroll
+        for (int w = 0; w < RS_WARPS; ++w) wcnt[w][d] = 0;
+    }
+    __syncthreads();
+    const uint32_t base = blockIdx.x * RS_TILE;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int r = 0; r < RS_ITEMS; ++r) {
+        const uint32_t i = base + r * RS_THREADS + threadIdx.x;
+        const bool valid = i < n;
+        const uint32_t key = valid ? kin[i] : 0u;
+        const uint32_t val = valid ? (vin ? vin[i] : i) : 0u;
+        const uint32_t d = valid ? ((key >> shift) & mask) : 256u;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t rank = __popc(peers & lt);
+        if (valid && (__ffs(peers) - 1) == lane) wcnt[warp][d] = __popc(peers);
+        __syncthreads();
+        for (int dd = threadIdx.x; dd < 256; dd += RS_THREADS) {
+            uint32_t acc = run[dd];
+#pragma unroll
+            for (int w = 0; w < RS_WARPS; ++w) {
+                const uint32_t c = wcnt[w][dd];
+                woff[w][dd] = acc;
+                acc += c;
+                wcnt[w][dd] = 0;
+            }
+            run[dd] = acc;
+        }
+        __syncthreads();
+        if (valid) {
+            const uint32_t pos = woff[warp][d] + rank;
+            kout[pos] = key;
+            vout[pos] = val;
+        }
+    }
+}
+
+template <typename V>
+__global__ void gather_kernel(const V* __restrict__ src, const uint32_t* __restrict__ idx,
+                              uint32_t n, V* __restrict__ dst, const uint32_t* done) {
+    if (done && *done) return;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        dst[i] = src[idx[i]];
+}
+
+constexpr uint32_t kShortGap = 64;
+
+// Thread k (0..n) owns the cells in (cell[k-1], cell[k]]: their lower bound is k.
+__global__ void cell_start_kernel(const uint32_t* __restrict__ skeys, uint32_t n, int sub_shift,
+                                  uint32_t ncells, uint32_t* __restrict__ start,
+                                  uint32_t* __restrict__ gaps, uint32_t* gap_count,
+                                  const uint32_t* done) {
+    if (done && *done) return;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k <= n; k += gridDim.x * blockDim.x) {
+        const int64_t cur = (k < n) ? (int64_t)(skeys[k] >> sub_shift) : (int64_t)ncells;
+        const int64_t prev = (k > 0) ? (int64_t)(skeys[k - 1] >> sub_shift) : -1;
+        const int64_t lo = prev + 1, hi = cur;
+        if (lo > hi) continue;
+        if (hi - lo < (int64_t)kShortGap) {
+            for (int64_t c = lo; c <= hi; ++c) start[c] = k;
+        } else {
+            const uint32_t g = atomicAdd(gap_count, 1u);
+            gaps[3 * g] = (uint32_t)lo;
+            gaps[3 * g + 1] = (uint32_t)hi;
+            gaps[3 * g + 2] = k;
+        }
+    }
+}
+
+__global__ void gap_fill_kernel(uint32_t* __restrict__ start, const uint32_t* __restrict__ gaps,
+                                const uint32_t* gap_count, const uint32_t* done) {
+    if (done && *done) return;
+    const uint32_t ng = *gap_count;
+    for (uint32_t g = blockIdx.x; g < ng; g += gridDim.x) {
+        const uint32_t lo = gaps[3 * g], hi = gaps[3 * g + 1], v = gaps[3 * g + 2];
+        for (uint32_t c = lo + threadIdx.x; c <= hi; c += blockDim.x) start[c] = v;
+    }
+}
+
+int grid_for(uint64_t n, int threads, int max_blocks = 148 * 16) {
+    uint64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > (uint64_t)max_blocks) b = max_blocks;
+    return (int)b;
+}
+
+}  // namespace
+
+double ordered_to_double(unsigned long long v) {
+    const unsigned long long b = (v >> 63) ? (v & 0x7FFFFFFFFFFFFFFFULL) : ~v;
+    double d;
+    memcpy(&d, &b, sizeof(d));
+    return d;
+}
+
+template <typename T>
+void launch_convert_xyz(const double* xyz, typename Vec4<T>::type* out, uint64_t n, T w,
+                        cudaStream_t s) {
+    if (!n) return;
+    convert_xyz_kernel<typename Vec4<T>::type, T><<<grid_for(n, 256), 256, 0, s>>>(xyz, out, n, w);
+}
+
+template <typename T>
+void launch_bbox(const typename Vec4<T>::type* pts, uint64_t n, unsigned long long* slots,
+                 cudaStream_t s) {
+    if (!n) return;
+    bbox_kernel<typename Vec4<T>::type><<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(pts, n, slots);
+}
+
+void init_bbox_slots(unsigned long long* slots, cudaStream_t s) {
+    init_bbox_kernel<<<1, 32, 0, s>>>(slots);
+}
+
+template <typename T>
+void launch_keys(const GridGeom& g, const typename Vec4<T>::type* pts, uint32_t n, uint32_t* keys,
+                 const uint32_t* done, cudaStream_t s) {
+    if (!n) return;
+    keys_kernel<typename Vec4<T>::type><<<grid_for(n, 256), 256, 0, s>>>(g, pts, n, keys, done);
+}
+
+size_t radix_blockhist_entries(uint32_t n) {
+    const size_t nb = (n + RS_TILE - 1) / RS_TILE;
+    return 256 * (nb ? nb : 1);
+}
+
+int radix_sort(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
+               uint32_t* vals_out, uint32_t n, int key_bits, RadixScratch& scr,
+               const uint32_t* done, cudaStream_t s) {
+    if (n == 0) return 0;
+    const uint32_t nblocks = (n + RS_TILE - 1) / RS_TILE;
+    const int passes = key_bits <= 0 ? 1 : (key_bits + 7) / 8;
+    // ping-pong so that the last pass writes keys_out/vals_out
+    const uint32_t* kin = keys_in;
+    const uint32_t* vin = vals_in;
+    int launches = 0;
+    for (int p = 0; p < passes; ++p) {
+        const int shift = 8 * p;
+        const int bits = (key_bits - shift) < 8 ? (key_bits - shift) : 8;
+        const uint32_t mask = bits <= 0 ? 0u : ((1u << bits) - 1u);
+        const bool last = (p == passes - 1);
+        // pass parity: the final pass targets *_out
+        const bool to_out = ((passes - 1 - p) % 2) == 0;
+        uint32_t* ko = to_out ? keys_out : scr.keys_alt;
+        uint32_t* vo = to_out ? vals_out : scr.vals_alt;
+        rs_hist_kernel<<<nblocks, RS_THREADS, 0, s>>>(kin, n, shift, mask, scr.blockhist, nblocks,
+                                                      done);
+        rs_scan_kernel<<<1, RS_SCAN_THREADS, 0, s>>>(scr.blockhist, 256 * nblocks, done);
+        rs_scatter_kernel<<<nblocks, RS_THREADS, 0, s>>>(kin, vin, ko, vo, n, shift, mask,
+                                                         scr.blockhist, nblocks, done);
+        launches += 3;
+        kin = ko;
+        vin = vo;
+        (void)last;
+    }
+    return launches;
+}
+
+template <typename T>
+void launch_gather(const typename Vec4<T>::type* src, const uint32_t* idx, uint32_t n,
+                   typename Vec4<T>::type* dst, const uint32_t* done, cudaStream_t s) {
+    if (!n) return;
+    gather_kernel<typename Vec4<T>::type><<<grid_for(n, 256), 256, 0, s>>>(src, idx, n, dst, done);
+}
+
+int build_cell_start(const uint32_t* sorted_keys, uint32_t n, int sub_shift, uint32_t ncells,
+                     uint32_t* cell_start, uint32_t* gap_list, uint32_t* gap_count,
+                     const uint32_t* done, cudaStream_t s) {
+    cudaMemsetAsync(gap_count, 0, sizeof(uint32_t), s);
+    cell_start_kernel<<<grid_for((uint64_t)n + 1, 256), 256, 0, s>>>(
+        sorted_keys, n, sub_shift, ncells, cell_start, gap_list, gap_count, done);
+    gap_fill_kernel<<<148 * 2, 256, 0, s>>>(cell_start, gap_list, gap_count, done);
+    return 2;
+}
+
+template void launch_convert_xyz<float>(const double*, float4*, uint64_t, float, cudaStream_t);
+template void launch_convert_xyz<double>(const double*, double4*, uint64_t, double, cudaStream_t);
+template void launch_bbox<float>(const float4*, uint64_t, unsigned long long*, cudaStream_t);
+template void launch_bbox<double>(const double4*, uint64_t, unsigned long long*, cudaStream_t);
+template void launch_keys<float>(const GridGeom&, const float4*, uint32_t, uint32_t*,
+                                 const uint32_t*, cudaStream_t);
+template void launch_keys<double>(const GridGeom&, const double4*, uint32_t, uint32_t*,
+                                  const uint32_t*, cudaStream_t);
+template void launch_gather<float>(const float4*, const uint32_t*, uint32_t, float4*,
+                                   const uint32_t*, cudaStream_t);
+template void launch_gather<double>(const double4*, const uint32_t*, uint32_t, double4*,
+                                    const uint32_t*, cudaStream_t);
+
+}  // namespace pcsb

@@ -1,0 +1,157 @@
+// kernels.cuh — launcher declarations for the sm_100a kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace pcsb {
+
+// ---- grid / sort (grid_sort.cu) ---------------------------------------------
+template <typename T>
+void launch_convert_xyz(const double* xyz, typename Vec4<T>::type* out, uint64_t n, T w,
+                        cudaStream_t s);
+// bbox accumulated into 6 ordered-uint64 slots: min xyz, max xyz
+template <typename T>
+void launch_bbox(const typename Vec4<T>::type* pts, uint64_t n, unsigned long long* slots,
+                 cudaStream_t s);
+void init_bbox_slots(unsigned long long* slots, cudaStream_t s);
+double ordered_to_double(unsigned long long v);
+
+template <typename T>
+void launch_keys(const GridGeom& g, const typename Vec4<T>::type* pts, uint32_t n,
+                 uint32_t* keys, const uint32_t* done, cudaStream_t s);
+
+struct RadixScratch {
+    uint32_t* keys_alt = nullptr;
+    uint32_t* vals_alt = nullptr;
+    uint32_t* blockhist = nullptr;  // 256 * nblocks
+    uint32_t capacity = 0;
+};
+size_t radix_blockhist_entries(uint32_t n);
+// Stable LSD sort of (keys, values = 0..n-1 when vals_in == nullptr) on the low
+// key_bits bits.  Results land in keys_out / vals_out.  Returns kernel count.
+int radix_sort(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
+               uint32_t* vals_out, uint32_t n, int key_bits, RadixScratch& scr,
+               const uint32_t* done, cudaStream_t s);
+
+template <typename T>
+void launch_gather(const typename Vec4<T>::type* src, const uint32_t* idx, uint32_t n,
+                   typename Vec4<T>::type* dst, const uint32_t* done, cudaStream_t s);
+
+// cell_start[c] = first sorted position whose cell >= c, c in [0, ncells]
+int build_cell_start(const uint32_t* sorted_keys, uint32_t n, int sub_shift, uint32_t ncells,
+                     uint32_t* cell_start, uint32_t* gap_list, uint32_t* gap_count,
+                     const uint32_t* done, cudaStream_t s);
+
+// ---- fused fp32 kernels (lop_fast.cu) ---------------------------------------
+struct FastArgs {
+    const float4* P;          // data, sorted; .w = 1/v_j (WLOP) or 1
+    const uint32_t* Pstart;   // cell table of P
+    const float4* Xs;         // projected set, sorted; .w = w_i (WLOP)
+    const uint32_t* Xstart;   // cell table of X
+    const uint32_t* Xs_idx;   // sorted slot -> internal index
+    const uint32_t* qlist;    // queries (sorted slots); nullptr = 0..nq-1
+    uint32_t nq;
+    GridGeom g;
+    double s_pad;             // support with margin (cell ranges)
+    float scull2;             // (support*(1+2^-10))^2: candidate vs group box
+    float kneg;               // -log2(e)/h^2
+    float K0;                 // log2(e) * r2f / h^2  (hit <=> fma(d2,kneg,K0) >= 0)
+    float band;               // |arg| <= band -> borderline, re-decided in fp64
+    float support;            // s (fp32), repulsion scale
+    float mu;
+    float4* Xnext;            // internal index order
+    uint32_t* careful_list;   // deferred queries (sorted slots)
+    uint8_t* ever_isolated;   // internal index
+    RunState* st;
+    SweepSlot* slot;
+    const uint32_t* done;
+};
+
+// mode: 0 = attraction only (mu == 0), 1 = inv-cube repulsion, 2 = neg-linear
+void launch_fast(const FastArgs& a, int lanes_per_point, bool wlop, bool check_zero,
+                 int rep_mode, int grid_blocks, cudaStream_t s);
+int fast_blocks_per_sm(int lanes_per_point, bool wlop, bool check_zero, int rep_mode);
+
+struct DensityArgs {
+    const float4* C;          // cloud, sorted (queries and candidates)
+    const uint32_t* Cstart;
+    const uint32_t* qlist;    // queries (sorted slots), nullptr = 0..nq-1
+    uint32_t nq;
+    GridGeom g;
+    double s_pad;
+    float scull2, kneg, K0;
+    float inv_scale;          // 2^-K0 (undo the theta scaling)
+    int invert;               // 1: write 1/(density) (data v_j), 0: write density (w_i)
+    float4* out_sorted;       // if non-null: .w of this sorted array
+    float4* out_internal;     // else: .w of this internal-order array, index via idx
+    const uint32_t* idx;      // sorted slot -> internal index
+    RunState* st;
+    uint32_t* counter;
+    const uint32_t* done;
+};
+void launch_density(const DensityArgs& a, int grid_blocks, cudaStream_t s);
+
+// ---- exact fp64 path (lop_exact.cu) -----------------------------------------
+template <typename T>
+struct ExactArgs {
+    using V = typename Vec4<T>::type;
+    const V* P;               // sorted data; .w = v_j (fp64) or 1/v_j (fp32), 1 if LOP
+    const uint32_t* Porder;   // sorted -> original data index (anchor tie-break)
+    const uint32_t* Pstart;
+    const V* Xs;              // sorted projected set; .w = w_i (WLOP)
+    const uint32_t* Xstart;
+    const uint32_t* Xs_idx;   // sorted slot -> internal index
+    const uint32_t* qlist;    // queries (sorted slots); nullptr = 0..nq-1
+    const uint32_t* nq_dev;   // if non-null, the query count lives on the device
+    uint32_t nq;
+    GridGeom g;
+    double s_pad, r2, support, h, mu;
+    int eta_kind;             // 0 inv-cube, 1 neg-linear
+    int wlop;
+    V* Xnext;
+    uint8_t* ever_isolated;
+    RunState* st;
+    SweepSlot* slot;
+    const uint32_t* done;
+    int count_careful;        // add processed queries to st->careful_points
+};
+template <typename T>
+void launch_exact(const ExactArgs<T>& a, int grid_blocks, cudaStream_t s);
+
+// Exact (fp64) density weights over a sorted cloud: v = 1 + sum theta (j' != j).
+template <typename T>
+void launch_exact_density(const typename Vec4<T>::type* C, const uint32_t* Cstart,
+                          const uint32_t* qlist, uint32_t nq, const GridGeom& g, double s_pad,
+                          double r2, double support, double h, int invert,
+                          typename Vec4<T>::type* out_sorted, typename Vec4<T>::type* out_internal,
+                          const uint32_t* idx, RunState* st, const uint32_t* done,
+                          cudaStream_t s);
+
+// Radius queries (parity facility): count (idx == nullptr) or fill CSR (unsorted).
+template <typename T>
+void launch_radius_dump(const typename Vec4<T>::type* C, const uint32_t* Corder,
+                        const uint32_t* Cstart, const GridGeom& g, const double* Q, uint32_t m,
+                        double r, double s_pad, uint64_t* offsets_or_counts, uint32_t* idx,
+                        cudaStream_t s);
+
+// ---- sweep bookkeeping --------------------------------------------------------
+void launch_finalize_sweep(RunState* st, SweepSlot* slot, int sweep, double tol, cudaStream_t s);
+template <typename T>
+void launch_unpermute(const typename Vec4<T>::type* X, const uint32_t* orig_of_internal,
+                      uint32_t mpad, double* out_xyz, cudaStream_t s);
+void launch_iso_to_orig(const uint8_t* ever_iso, const uint32_t* orig_of_internal, uint32_t mpad,
+                        uint8_t* iso_orig, cudaStream_t s);
+// owned-query compaction key: 0 for internal index in [lo, hi), 1 otherwise
+void launch_owner_keys(const uint32_t* sorted_idx, uint32_t n, uint32_t lo, uint32_t hi,
+                       uint32_t* keys, const uint32_t* done, cudaStream_t s);
+template <typename T>
+void launch_scatter_init(const typename Vec4<T>::type* X0, const uint32_t* internal_of_orig,
+                         uint32_t m, typename Vec4<T>::type* X, cudaStream_t s);
+template <typename T>
+void launch_fill_invalid(typename Vec4<T>::type* X, uint32_t mpad, const uint32_t* orig_of_internal,
+                         cudaStream_t s);
+
+}  // namespace pcsb

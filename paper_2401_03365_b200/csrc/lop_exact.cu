@@ -1,0 +1,460 @@
+// lop_exact.cu — the exact-arithmetic path (fp64 math, reference predicate).
+//
+// One warp per query; lanes stride over the candidates of the cell rows that
+// can hold a point within the support.  Every decision follows the reference
+// literally:
+//   membership   d2 = (dx*dx + dy*dy) + dz*dz <= r*r, no FMA  (spatial.cpp:89,100-101, core.hpp:28)
+//   distance     sqrt(d2)                                       (spatial.cpp:102)
+//   theta        d > support ? 0 : exp(-(d/h)^2)               (kernels.cpp:8-15)
+//   |eta'|       1/(d^2)^2 (inv-cube) | 1 (neg-linear)          (kernels.cpp:23-29)
+//   attraction   d == 0 -> anchor candidate (smallest index), else w = theta/d  (lop.cpp:54-65)
+//   isolation    !(sum w > 0): anchored -> anchor, else held + flagged         (lop.cpp:67-75)
+//   repulsion    skip self, d == 0 -> coincident++, w = theta*|eta'|/d         (lop.cpp:79-97)
+// Only the summation order differs from the reference (lane-strided partial sums
+// combined by a fixed xor tree — deterministic, but not index order), so the
+// result agrees to a few ulp rather than bit-for-bit.
+//
+// It is the whole computation in PCS_PREC_FP64 mode and the deferred-query path
+// of the fp32 fused kernel.
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace pcsb {
+
+namespace {
+
+constexpr int EX_WARPS = 4;
+constexpr int EX_THREADS = EX_WARPS * 32;
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ unsigned long long warp_sum_u(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ unsigned long long warp_min_u(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w < v ? w : v;
+    }
+    return v;
+}
+
+__device__ __forceinline__ double theta_ref(double d, double support, double h) {
+    if (d > support) return 0.0;
+    const double s = d / h;
+    return exp(-s * s);
+}
+
+__device__ __forceinline__ double etad_ref(double d, int kind) {
+    if (kind == 1) return 1.0;
+    const double d2 = __dmul_rn(d, d);
+    return 1.0 / __dmul_rn(d2, d2);
+}
+
+struct Rows {
+    int lox, hix, loy, ny, loz, nrows;
+};
+
+__device__ __forceinline__ Rows rows_around(const GridGeom& g, double x, double y, double z,
+                                            double s_pad) {
+    Rows r;
+    r.lox = cell_coord(x - s_pad, g.ox, g.inv_cs, g.gx);
+    r.hix = cell_coord(x + s_pad, g.ox, g.inv_cs, g.gx);
+    r.loy = cell_coord(y - s_pad, g.oy, g.inv_cs, g.gy);
+    const int hiy = cell_coord(y + s_pad, g.oy, g.inv_cs, g.gy);
+    r.loz = cell_coord(z - s_pad, g.oz, g.inv_cs, g.gz);
+    const int hiz = cell_coord(z + s_pad, g.oz, g.inv_cs, g.gz);
+    r.ny = hiy - r.loy + 1;
+    r.nrows = r.ny * (hiz - r.loz + 1);
+    return r;
+}
+
+// Calls f(k) for every sorted position k of the rows, lane-strided.
+template <typename F>
+__device__ __forceinline__ void for_each_candidate(const uint32_t* __restrict__ start,
+                                                   const GridGeom& g, const Rows& rw, int lane,
+                                                   F&& f) {
+    for (int r = 0; r < rw.nrows; ++r) {
+        const int yy = rw.loy + r % rw.ny;
+        const int zz = rw.loz + r / rw.ny;
+        const uint32_t base = ((uint32_t)zz * (uint32_t)g.gy + (uint32_t)yy) * (uint32_t)g.gx;
+        const uint32_t b = __ldg(&start[base + rw.lox]);
+        const uint32_t e = __ldg(&start[base + rw.hix + 1]);
+        for (uint32_t k = b + lane; k < e; k += 32) f(k);
+    }
+}
+
+template <typename T, bool kWlop>
+__global__ void __launch_bounds__(EX_THREADS) exact_kernel(const ExactArgs<T> a) {
+    using V = typename Vec4<T>::type;
+    if (a.done && *a.done) return;
+    const int lane = threadIdx.x & 31;
+    const uint32_t nq = a.nq_dev ? *a.nq_dev : a.nq;
+    uint32_t* counter = &a.slot->exact_counter;
+    for (;;) {
+        uint32_t qn = 0;
+        if (lane == 0) qn = atomicAdd(counter, 1u);
+        qn = __shfl_sync(0xffffffffu, qn, 0);
+        if (qn >= nq) break;
+        const uint32_t qslot = a.qlist ? a.qlist[qn] : qn;
+        const V qv = a.Xs[qslot];
+        const uint32_t q_int = a.Xs_idx[qslot];
+        const double x = (double)qv.x, y = (double)qv.y, z = (double)qv.z;
+        const Rows rw = rows_around(a.g, x, y, z, a.s_pad);
+
+        // ---- attraction over the data (lop.cpp:49-65) ----
+        double sw = 0.0, nx = 0.0, ny = 0.0, nz = 0.0;
+        unsigned long long cnt = 0;
+        unsigned long long anchor = ~0ull;  // (original index << 32) | sorted position
+        for_each_candidate(a.Pstart, a.g, rw, lane, [&](uint32_t k) {
+            const V p = a.P[k];
+            const double px = (double)p.x, py = (double)p.y, pz = (double)p.z;
+            const double d2 = exact_d2(px, py, pz, x, y, z);
+            if (!(d2 <= a.r2)) return;
+            const double d = __dsqrt_rn(d2);
+            if (d == 0.0) {
+                const unsigned long long key =
+                    ((unsigned long long)a.Porder[k] << 32) | (unsigned long long)k;
+                anchor = key < anchor ? key : anchor;
+                return;
+            }
+            double w = theta_ref(d, a.support, a.h) / d;
+            if (kWlop) w = (sizeof(T) == 8) ? w / (double)p.w : w * (double)p.w;
+            sw += w;
+            nx += w * px;
+            ny += w * py;
+            nz += w * pz;
+            ++cnt;
+        });
+        sw = warp_sum_d(sw);
+        nx = warp_sum_d(nx);
+        ny = warp_sum_d(ny);
+        nz = warp_sum_d(nz);
+        cnt = warp_sum_u(cnt);
+        anchor = warp_min_u(anchor);
+
+        double ux, uy, uz;
+        bool isolated = false, attracted = sw > 0.0;
+        unsigned long long rcnt = 0, coinc = 0;
+        if (!attracted) {
+            if (anchor != ~0ull) {
+                const V p = a.P[(uint32_t)(anchor & 0xFFFFFFFFull)];
+                ux = (double)p.x;
+                uy = (double)p.y;
+                uz = (double)p.z;
+            } else {
+                isolated = true;
+                ux = x;
+                uy = y;
+                uz = z;
+            }
+        } else {
+            ux = nx / sw;
+            uy = ny / sw;
+            uz = nz / sw;
+            // ---- repulsion over the projected set (lop.cpp:79-97) ----
+            if (a.mu > 0.0) {
+                double rs = 0.0, rx = 0.0, ry = 0.0, rz = 0.0;
+                for_each_candidate(a.Xstart, a.g, rw, lane, [&](uint32_t k) {
+                    if (a.Xs_idx[k] == q_int) return;
+                    const V c = a.Xs[k];
+                    const double cx = (double)c.x, cy = (double)c.y, cz = (double)c.z;
+                    const double d2 = exact_d2(cx, cy, cz, x, y, z);
+                    if (!(d2 <= a.r2)) return;
+                    const double d = __dsqrt_rn(d2);
+                    if (d == 0.0) {
+                        ++coinc;
+                        return;
+                    }
+                    double w = theta_ref(d, a.support, a.h) * etad_ref(d, a.eta_kind) / d;
+                    if (kWlop) w = w * (double)c.w;
+                    rs += w;
+                    rx += w * (x - cx);
+                    ry += w * (y - cy);
+                    rz += w * (z - cz);
+                    ++rcnt;
+                });
+                rs = warp_sum_d(rs);
+                rx = warp_sum_d(rx);
+                ry = warp_sum_d(ry);
+                rz = warp_sum_d(rz);
+                rcnt = warp_sum_u(rcnt);
+                coinc = warp_sum_u(coinc);
+                if (rs > 0.0) {
+                    ux += a.mu * (rx / rs);
+                    uy += a.mu * (ry / rs);
+                    uz += a.mu * (rz / rs);
+                }
+            }
+        }
+        if (lane == 0) {
+            V out;
+            out.x = (T)ux;
+            out.y = (T)uy;
+            out.z = (T)uz;
+            out.w = (T)0;
+            a.Xnext[q_int] = out;
+            const double dx = (double)out.x - x, dy = (double)out.y - y, dz = (double)out.z - z;
+            const double disp = sqrt(dx * dx + dy * dy + dz * dz);
+            if (disp > 0.0) atomic_max_nonneg_double(&a.slot->max_disp_bits, disp);
+            if (isolated) {
+                a.ever_isolated[q_int] = 1;
+                atomicAdd(&a.st->isolated_events, 1ull);
+            }
+            if (attracted) {
+                if (cnt) atomicAdd(&a.st->interactions_attr, cnt);
+                if (rcnt) atomicAdd(&a.st->interactions_rep, rcnt);
+                if (coinc) atomicAdd(&a.st->coincident_pairs, coinc);
+            }
+            if (a.count_careful) atomicAdd(&a.st->careful_points, 1ull);
+        }
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(EX_THREADS)
+exact_density_kernel(const typename Vec4<T>::type* __restrict__ C, const uint32_t* __restrict__ Cstart,
+                     const uint32_t* __restrict__ qlist, uint32_t nq, GridGeom g, double s_pad,
+                     double r2, double support, double h, int invert,
+                     typename Vec4<T>::type* out_sorted, typename Vec4<T>::type* out_internal,
+                     const uint32_t* __restrict__ idx, RunState* st, const uint32_t* done) {
+    using V = typename Vec4<T>::type;
+    if (done && *done) return;
+    const int lane = threadIdx.x & 31;
+    const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t qn = wid; qn < nq; qn += nw) {
+        const uint32_t qslot = qlist ? qlist[qn] : qn;
+        const V qv = C[qslot];
+        const double x = (double)qv.x, y = (double)qv.y, z = (double)qv.z;
+        const Rows rw = rows_around(g, x, y, z, s_pad);
+        double acc = 0.0;
+        unsigned long long pairs = 0;
+        for_each_candidate(Cstart, g, rw, lane, [&](uint32_t k) {
+            if (k == qslot) return;
+            const V c = C[k];
+            const double d2 = exact_d2((double)c.x, (double)c.y, (double)c.z, x, y, z);
+            if (!(d2 <= r2)) return;
+            const double d = __dsqrt_rn(d2);
+            acc += theta_ref(d, support, h);
+            if (d > 0.0) ++pairs;
+        });
+        acc = warp_sum_d(acc);
+        pairs = warp_sum_u(pairs);
+        if (lane == 0) {
+            const double dens = 1.0 + acc;
+            const T val = invert ? (T)(1.0 / dens) : (T)dens;
+            if (out_sorted) out_sorted[qslot].w = val;
+            else out_internal[idx[qslot]].w = val;
+            if (pairs) atomicAdd(&st->density_pairs, pairs);
+        }
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(EX_THREADS)
+radius_dump_kernel(const typename Vec4<T>::type* __restrict__ C, const uint32_t* __restrict__ Corder,
+                   const uint32_t* __restrict__ Cstart, GridGeom g, const double* __restrict__ Q,
+                   uint32_t m, double r2, double s_pad, uint64_t* offsets_or_counts,
+                   uint32_t* idx) {
+    using V = typename Vec4<T>::type;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t qn = wid; qn < m; qn += nw) {
+        // queries are rounded exactly like the cloud (fp32 mode compares fp32 values)
+        const double x = (double)(T)Q[3 * (size_t)qn], y = (double)(T)Q[3 * (size_t)qn + 1],
+                     z = (double)(T)Q[3 * (size_t)qn + 2];
+        const Rows rw = rows_around(g, x, y, z, s_pad);
+        uint64_t pos = idx ? offsets_or_counts[qn] : 0;
+        for (int rr = 0; rr < rw.nrows; ++rr) {
+            const int yy = rw.loy + rr % rw.ny;
+            const int zz = rw.loz + rr / rw.ny;
+            const uint32_t base = ((uint32_t)zz * (uint32_t)g.gy + (uint32_t)yy) * (uint32_t)g.gx;
+            const uint32_t b = Cstart[base + rw.lox];
+            const uint32_t e = Cstart[base + rw.hix + 1];
+            for (uint32_t k0 = b; k0 < e; k0 += 32) {
+                const uint32_t k = k0 + lane;
+                bool hit = false;
+                if (k < e) {
+                    const V c = C[k];
+                    hit = exact_d2((double)c.x, (double)c.y, (double)c.z, x, y, z) <= r2;
+                }
+                const unsigned msk = __ballot_sync(0xffffffffu, hit);
+                if (idx && hit) idx[pos + __popc(msk & lt)] = Corder[k];
+                pos += __popc(msk);
+            }
+        }
+        if (!idx && lane == 0) offsets_or_counts[qn] = pos;
+    }
+}
+
+__global__ void finalize_kernel(RunState* st, SweepSlot* slot, int sweep, double tol) {
+    if (st->done) return;
+    const unsigned long long b = slot->max_disp_bits;
+    const double md = __longlong_as_double((long long)b);
+    st->iterations_run = sweep;
+    st->last_max_disp = md;
+    if (md < tol) {  // lop.cpp:116-119
+        st->converged = 1;
+        st->done = 1;
+    }
+}
+
+template <typename V>
+__global__ void unpermute_kernel(const V* __restrict__ X, const uint32_t* __restrict__ orig,
+                                 uint32_t mpad, double* __restrict__ out) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < mpad; i += gridDim.x * blockDim.x) {
+        const uint32_t o = orig ? orig[i] : i;
+        if (o == 0xFFFFFFFFu) continue;
+        const V v = X[i];
+        out[3 * (size_t)o] = (double)v.x;
+        out[3 * (size_t)o + 1] = (double)v.y;
+        out[3 * (size_t)o + 2] = (double)v.z;
+    }
+}
+
+__global__ void iso_to_orig_kernel(const uint8_t* __restrict__ ever, const uint32_t* __restrict__ orig,
+                                   uint32_t mpad, uint8_t* __restrict__ out) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < mpad; i += gridDim.x * blockDim.x) {
+        const uint32_t o = orig ? orig[i] : i;
+        if (o == 0xFFFFFFFFu) continue;
+        out[o] = ever[i];
+    }
+}
+
+__global__ void owner_keys_kernel(const uint32_t* __restrict__ sidx, uint32_t n, uint32_t lo,
+                                  uint32_t hi, uint32_t* __restrict__ keys, const uint32_t* done) {
+    if (done && *done) return;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t v = sidx[i];
+        keys[i] = (v >= lo && v < hi) ? 0u : 1u;
+    }
+}
+
+template <typename V>
+__global__ void scatter_init_kernel(const V* __restrict__ X0, const uint32_t* __restrict__ iof,
+                                    uint32_t m, V* __restrict__ X) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+        X[iof ? iof[i] : i] = X0[i];
+}
+
+template <typename V, typename T>
+__global__ void fill_invalid_kernel(V* __restrict__ X, uint32_t mpad, const uint32_t* __restrict__ orig) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < mpad; i += gridDim.x * blockDim.x) {
+        if (orig[i] == 0xFFFFFFFFu) {
+            V v;
+            v.x = (T)NAN;
+            v.y = (T)NAN;
+            v.z = (T)NAN;
+            v.w = (T)0;
+            X[i] = v;
+        }
+    }
+}
+
+int blocks_for(uint64_t n, int threads) {
+    uint64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > 148 * 16) b = 148 * 16;
+    return (int)b;
+}
+
+}  // namespace
+
+template <typename T>
+void launch_exact(const ExactArgs<T>& a, int grid_blocks, cudaStream_t s) {
+    if (a.wlop) exact_kernel<T, true><<<grid_blocks, EX_THREADS, 0, s>>>(a);
+    else exact_kernel<T, false><<<grid_blocks, EX_THREADS, 0, s>>>(a);
+}
+
+template <typename T>
+void launch_exact_density(const typename Vec4<T>::type* C, const uint32_t* Cstart,
+                          const uint32_t* qlist, uint32_t nq, const GridGeom& g, double s_pad,
+                          double r2, double support, double h, int invert,
+                          typename Vec4<T>::type* out_sorted, typename Vec4<T>::type* out_internal,
+                          const uint32_t* idx, RunState* st, const uint32_t* done,
+                          cudaStream_t s) {
+    if (!nq) return;
+    exact_density_kernel<T><<<blocks_for((uint64_t)nq * 32, EX_THREADS), EX_THREADS, 0, s>>>(
+        C, Cstart, qlist, nq, g, s_pad, r2, support, h, invert, out_sorted, out_internal, idx, st,
+        done);
+}
+
+template <typename T>
+void launch_radius_dump(const typename Vec4<T>::type* C, const uint32_t* Corder,
+                        const uint32_t* Cstart, const GridGeom& g, const double* Q, uint32_t m,
+                        double r, double s_pad, uint64_t* offsets_or_counts, uint32_t* idx,
+                        cudaStream_t s) {
+    if (!m) return;
+    const double r2 = r * r;
+    radius_dump_kernel<T><<<blocks_for((uint64_t)m * 32, EX_THREADS), EX_THREADS, 0, s>>>(
+        C, Corder, Cstart, g, Q, m, r2, s_pad, offsets_or_counts, idx);
+}
+
+void launch_finalize_sweep(RunState* st, SweepSlot* slot, int sweep, double tol, cudaStream_t s) {
+    finalize_kernel<<<1, 1, 0, s>>>(st, slot, sweep, tol);
+}
+
+template <typename T>
+void launch_unpermute(const typename Vec4<T>::type* X, const uint32_t* orig, uint32_t mpad,
+                      double* out, cudaStream_t s) {
+    if (!mpad) return;
+    unpermute_kernel<typename Vec4<T>::type><<<blocks_for(mpad, 256), 256, 0, s>>>(X, orig, mpad, out);
+}
+
+void launch_iso_to_orig(const uint8_t* ever, const uint32_t* orig, uint32_t mpad, uint8_t* out,
+                        cudaStream_t s) {
+    if (!mpad) return;
+    iso_to_orig_kernel<<<blocks_for(mpad, 256), 256, 0, s>>>(ever, orig, mpad, out);
+}
+
+void launch_owner_keys(const uint32_t* sidx, uint32_t n, uint32_t lo, uint32_t hi, uint32_t* keys,
+                       const uint32_t* done, cudaStream_t s) {
+    if (!n) return;
+    owner_keys_kernel<<<blocks_for(n, 256), 256, 0, s>>>(sidx, n, lo, hi, keys, done);
+}
+
+template <typename T>
+void launch_scatter_init(const typename Vec4<T>::type* X0, const uint32_t* iof, uint32_t m,
+                         typename Vec4<T>::type* X, cudaStream_t s) {
+    if (!m) return;
+    scatter_init_kernel<typename Vec4<T>::type><<<blocks_for(m, 256), 256, 0, s>>>(X0, iof, m, X);
+}
+
+template <typename T>
+void launch_fill_invalid(typename Vec4<T>::type* X, uint32_t mpad, const uint32_t* orig,
+                         cudaStream_t s) {
+    if (!mpad) return;
+    fill_invalid_kernel<typename Vec4<T>::type, T><<<blocks_for(mpad, 256), 256, 0, s>>>(X, mpad, orig);
+}
+
+#define PCSB_INST(T)                                                                              \
+    template void launch_exact<T>(const ExactArgs<T>&, int, cudaStream_t);                       \
+    template void launch_exact_density<T>(const Vec4<T>::type*, const uint32_t*, const uint32_t*, \
+                                          uint32_t, const GridGeom&, double, double, double,      \
+                                          double, int, Vec4<T>::type*, Vec4<T>::type*,            \
+                                          const uint32_t*, RunState*, const uint32_t*,            \
+                                          cudaStream_t);                                          \
+    template void launch_radius_dump<T>(const Vec4<T>::type*, const uint32_t*, const uint32_t*,   \
+                                        const GridGeom&, const double*, uint32_t, double, double, \
+                                        uint64_t*, uint32_t*, cudaStream_t);                      \
+    template void launch_unpermute<T>(const Vec4<T>::type*, const uint32_t*, uint32_t, double*,   \
+                                      cudaStream_t);                                              \
+    template void launch_scatter_init<T>(const Vec4<T>::type*, const uint32_t*, uint32_t,         \
+                                         Vec4<T>::type*, cudaStream_t);                           \
+    template void launch_fill_invalid<T>(Vec4<T>::type*, uint32_t, const uint32_t*, cudaStream_t);
+PCSB_INST(float)
+PCSB_INST(double)
+#undef PCSB_INST
+
+}  // namespace pcsb

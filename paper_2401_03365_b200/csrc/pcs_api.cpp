@@ -1,0 +1,145 @@
+// pcs_api.cpp — the reference's C++ API (include/pcs/*.hpp) over the C ABI.
+//
+// pcs::lop_project keeps the declaration, structs, validation order and
+// exception types of proj/include/pcs/lop.hpp:51-53 / proj/src/lop.cpp:13-20,
+// so the reference's own proj/tests/test_lop.cpp compiles and runs against
+// this library unchanged (tests/test_dropin.py).
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "../../include/pcs/bench.hpp"
+#include "../../include/pcs/kernels.hpp"
+#include "../../include/pcs/lop.hpp"
+#include "../../include/pcs/lop_ex.hpp"
+#include "../../include/pcs/noise.hpp"
+#include "../../include/pcs_lop.h"
+
+namespace pcs {
+
+namespace {
+
+[[noreturn]] void raise(pcs_status st) {
+    const std::string msg = pcs_last_error();
+    switch (st) {
+        case PCS_ERR_INVALID_PARAM: throw InvalidParam(msg);
+        case PCS_ERR_EMPTY_CLOUD: throw EmptyCloud(msg);
+        default: throw NumericalFailure(msg);
+    }
+}
+
+const double* xyz(const PointCloud& c) { return c.empty() ? nullptr : &c.points[0].x; }
+
+}  // namespace
+
+bool PointCloud::all_finite() const {
+    for (const Point3& p : points)
+        if (!is_finite(p)) return false;
+    return true;
+}
+
+Aabb bounding_box(const PointCloud& cloud) {
+    if (cloud.empty()) throw EmptyCloud("bounding_box: empty cloud");
+    Aabb b{cloud[0], cloud[0]};
+    for (const Point3& p : cloud) {
+        b.min.x = std::fmin(b.min.x, p.x);
+        b.min.y = std::fmin(b.min.y, p.y);
+        b.min.z = std::fmin(b.min.z, p.z);
+        b.max.x = std::fmax(b.max.x, p.x);
+        b.max.y = std::fmax(b.max.y, p.y);
+        b.max.z = std::fmax(b.max.z, p.z);
+    }
+    return b;
+}
+
+double theta(double d, const KernelParams& params) {
+    params.validate();
+    if (d > params.support()) return 0.0;
+    const double s = d / params.h;
+    return std::exp(-s * s);
+}
+
+double eta(double d) {
+    if (!(d > 0.0)) throw InvalidParam("eta requires d > 0");
+    return 1.0 / (3.0 * d * d * d);
+}
+
+double eta_derivative_magnitude(double d) {
+    if (!(d > 0.0)) throw InvalidParam("eta_derivative_magnitude requires d > 0");
+    const double d2 = d * d;
+    return 1.0 / (d2 * d2);
+}
+
+std::pair<PointCloud, LopSummary> lop_project_ex(const PointCloud& data, const PointCloud& initial,
+                                                 const LopParams& params, const LopOptions& options,
+                                                 LopStats* stats) {
+    params.validate();  // InvalidParam first (lop.cpp:13)
+    if (data.empty()) throw EmptyCloud("lop_project: data cloud is empty");
+    LopSummary summary;
+    PointCloud out = initial;
+    if (initial.empty()) return {out, summary};
+
+    pcs_lop_desc d;
+    pcs_lop_desc_default(&d);
+    d.h = params.kernel.h;
+    d.cutoff_multiple = params.kernel.cutoff_multiple;
+    d.mu = params.mu;
+    d.iterations = params.iterations;
+    d.convergence_tol = params.convergence_tol;
+    d.eta_kind = options.eta == EtaKind::NegLinear ? PCS_ETA_NEG_LINEAR : PCS_ETA_INV_CUBE;
+    d.density_weights = options.density_weights ? 1 : 0;
+    d.precision = options.precision == Precision::Fp32 ? PCS_PREC_FP32 : PCS_PREC_FP64;
+    d.device = options.device;
+
+    pcs_lop_summary s;
+    std::vector<std::uint32_t> iso(initial.size());
+    const pcs_status st = pcs_lop_run(&d, xyz(data), data.size(), xyz(initial), initial.size(),
+                                      &out.points[0].x, &s, iso.data(), iso.size());
+    if (st != PCS_OK) raise(st);
+    summary.iterations_run = s.iterations_run;
+    summary.converged = s.converged != 0;
+    summary.isolated_events = s.isolated_events;
+    summary.coincident_pairs = s.coincident_pairs;
+    iso.resize(s.n_isolated);
+    summary.isolated_indices = std::move(iso);
+    if (stats) {
+        stats->interactions_attr = s.interactions_attr;
+        stats->interactions_rep = s.interactions_rep;
+        stats->density_pairs = s.density_pairs;
+        stats->careful_points = s.careful_points;
+        stats->setup_ms = s.setup_ms;
+        stats->sweeps_ms = s.sweeps_ms;
+        stats->kernel_ms = s.kernel_ms;
+        stats->sort_ms = s.sort_ms;
+        stats->last_max_disp = s.last_max_disp;
+    }
+    return {out, summary};
+}
+
+std::pair<PointCloud, LopSummary> lop_project(const PointCloud& data, const PointCloud& initial,
+                                              const LopParams& params) {
+    return lop_project_ex(data, initial, params, LopOptions{});
+}
+
+PointCloud add_noise(const PointCloud& cloud, const NoiseParams& params) {
+    if (!(params.sigma >= 0.0) || !std::isfinite(params.sigma))
+        throw InvalidParam("add_noise: sigma must be finite and >= 0");
+    PointCloud out = cloud;
+    if (!out.empty()) {
+        const pcs_status st = pcs_add_noise(&out.points[0].x, out.size(), params.sigma, params.seed);
+        if (st != PCS_OK) raise(st);
+    }
+    return out;
+}
+
+PointCloud generate_surface(const SyntheticSurface& surface) {
+    if (surface.n < 1) throw InvalidParam("generate_surface: n must be >= 1");
+    PointCloud c;
+    c.points.resize(surface.n);
+    const pcs_status st =
+        pcs_generate_surface(static_cast<int32_t>(surface.kind), surface.n, surface.seed, &c.points[0].x);
+    if (st != PCS_OK) throw InvalidParam("generate_surface: invalid surface kind");
+    return c;
+}
+
+}  // namespace pcs

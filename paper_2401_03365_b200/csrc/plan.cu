@@ -1,0 +1,857 @@
+// plan.cu — host orchestration (see plan.cuh).  Mirrors the control flow of
+// pcs::lop_project (proj/src/lop.cpp:10-127): validate, build the data index
+// once (:24), then per sweep rebuild the index over the moving set (:39),
+// update every point (:41-100), aggregate (:102-113) and stop early (:116-119).
+#include "plan.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "nccl_dl.h"
+
+namespace pcsb {
+
+namespace {
+constexpr int kSlotCap = 4096;
+
+const NcclApi& nccl() {
+    std::string err;
+    const NcclApi* api = nccl_api(&err);
+    if (!api) throw Failure(PCS_ERR_NCCL, err);
+    return *api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        throw Failure(PCS_ERR_NCCL, std::string(what) + ": " + nccl().GetErrorString(r));
+}
+
+int bit_width_u64(uint64_t v) {
+    int b = 0;
+    while (v) {
+        ++b;
+        v >>= 1;
+    }
+    return b;
+}
+
+double cells_for(const double lo[3], const double hi[3], double cs) {
+    double c = 1.0;
+    for (int a = 0; a < 3; ++a) c *= std::floor((hi[a] - lo[a]) / cs) + 3.0;
+    return c;
+}
+}  // namespace
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw Failure(PCS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+GridGeom make_grid(const double lo_in[3], const double hi_in[3], double support) {
+    double lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = lo_in[a];
+        hi[a] = hi_in[a];
+        if (!(lo[a] <= hi[a])) lo[a] = hi[a] = 0.0;  // empty / non-finite
+    }
+    GridGeom g{};
+    double cs;
+    int sb;
+    if (cells_for(lo, hi, support * 0.5) <= (double)(1u << 24)) {
+        cs = support * 0.5;
+        sb = 1;
+    } else {
+        cs = support;
+        sb = cells_for(lo, hi, cs) <= (double)(1u << 25) ? 2 : 1;
+        while (cells_for(lo, hi, cs) > (double)(1u << 27)) cs *= 1.25;
+    }
+    g.cs = cs;
+    g.inv_cs = 1.0 / cs;
+    g.ox = lo[0] - cs;
+    g.oy = lo[1] - cs;
+    g.oz = lo[2] - cs;
+    g.gx = (int32_t)std::floor((hi[0] - g.ox) * g.inv_cs) + 2;
+    g.gy = (int32_t)std::floor((hi[1] - g.oy) * g.inv_cs) + 2;
+    g.gz = (int32_t)std::floor((hi[2] - g.oz) * g.inv_cs) + 2;
+    g.sub_bits = sb;
+    g.ncells = (uint32_t)g.gx * (uint32_t)g.gy * (uint32_t)g.gz;
+    g.key_bits = bit_width_u64((uint64_t)g.ncells << (3 * sb));
+    return g;
+}
+
+void validate_desc(const pcs_lop_desc& d) {
+    // LopParams::validate + KernelParams::validate (proj/include/pcs/lop.hpp:18-26,
+    // proj/include/pcs/kernels.hpp:18-23), same messages.
+    if (!(d.h > 0.0)) throw Failure(PCS_ERR_INVALID_PARAM, "kernel bandwidth h must be positive");
+    if (!(d.cutoff_multiple > 0.0))
+        throw Failure(PCS_ERR_INVALID_PARAM, "kernel cutoff_multiple must be positive");
+    if (!(d.mu >= 0.0) || !(d.mu < 0.5))
+        throw Failure(PCS_ERR_INVALID_PARAM, "LopParams: mu must be in [0, 0.5)");
+    if (d.iterations < 1)
+        throw Failure(PCS_ERR_INVALID_PARAM, "LopParams: iterations must be >= 1");
+    if (!(d.convergence_tol > 0.0))
+        throw Failure(PCS_ERR_INVALID_PARAM, "LopParams: convergence_tol must be positive");
+    if (d.eta_kind != PCS_ETA_INV_CUBE && d.eta_kind != PCS_ETA_NEG_LINEAR)
+        throw Failure(PCS_ERR_INVALID_PARAM, "eta_kind must be PCS_ETA_INV_CUBE or PCS_ETA_NEG_LINEAR");
+    if (d.precision != PCS_PREC_FP64 && d.precision != PCS_PREC_FP32)
+        throw Failure(PCS_ERR_INVALID_PARAM, "precision must be PCS_PREC_FP64 or PCS_PREC_FP32");
+    if (d.lanes_per_point != 0 && d.lanes_per_point != 1 && d.lanes_per_point != 2 &&
+        d.lanes_per_point != 4 && d.lanes_per_point != 8)
+        throw Failure(PCS_ERR_INVALID_PARAM, "lanes_per_point must be 0, 1, 2, 4 or 8");
+    const double s = d.h * d.cutoff_multiple;
+    if (!std::isfinite(s)) throw Failure(PCS_ERR_INVALID_PARAM, "support h*cutoff_multiple must be finite");
+    if (d.precision == PCS_PREC_FP32) {
+        // theta is evaluated as 2^(log2e*(r^2 - d^2)/h^2) in [1, e^(cutoff^2)]
+        if (d.cutoff_multiple * d.cutoff_multiple > 80.0)
+            throw Failure(PCS_ERR_INVALID_PARAM, "fp32 precision requires cutoff_multiple <= 8.9");
+        if (!(s * s >= 1e-30 && s * s <= 1e30))
+            throw Failure(PCS_ERR_INVALID_PARAM, "fp32 precision requires 1e-15 <= support <= 1e15");
+    }
+}
+
+int select_device(int requested) {
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        throw Failure(PCS_ERR_NO_DEVICE,
+                      "no CUDA device available: the B200 LOP path has no CPU fallback");
+    }
+    int dev = requested;
+    if (dev < 0) PCSB_CUDA(cudaGetDevice(&dev));
+    if (dev >= n) throw Failure(PCS_ERR_INVALID_PARAM, "device ordinal out of range");
+    cudaDeviceProp prop;
+    PCSB_CUDA(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10)
+        throw Failure(PCS_ERR_NO_DEVICE, std::string("device ") + prop.name +
+                                             " is not sm_100 (B200); kernels are built for sm_100a only");
+    PCSB_CUDA(cudaSetDevice(dev));
+    return dev;
+}
+
+// ---------------------------------------------------------------------------
+
+Plan::Plan(const pcs_lop_desc& d) : d_(d) {
+    validate_desc(d_);
+    fp32_ = d_.precision == PCS_PREC_FP32;
+    vec_bytes_ = fp32_ ? sizeof(float4) : sizeof(double4);
+    lanes_ = d_.lanes_per_point ? d_.lanes_per_point : 4;
+    device_ = select_device(d_.device);
+    PCSB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    PCSB_CUDA(cudaEventCreate(&run_ev_[0]));
+    PCSB_CUDA(cudaEventCreate(&run_ev_[1]));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_);
+    fast_grid_ = sms * fast_blocks_per_sm(lanes_, d_.density_weights != 0, false, 2);
+    density_grid_ = fast_grid_;
+    exact_grid_ = sms * 8;
+    support_ = d_.h * d_.cutoff_multiple;
+    r2_ = support_ * support_;
+}
+
+Plan::~Plan() {
+    if (stream_) cudaStreamSynchronize(stream_);
+    free_all();
+    for (auto& se : event_pool_)
+        for (auto e : se.e) cudaEventDestroy(e);
+    for (auto& se : pending_)
+        for (auto e : se.e) cudaEventDestroy(e);
+    if (run_ev_[0]) cudaEventDestroy(run_ev_[0]);
+    if (run_ev_[1]) cudaEventDestroy(run_ev_[1]);
+    if (comm_) {
+        std::string err;
+        if (const NcclApi* api = nccl_api(&err)) api->CommDestroy((ncclComm_t)comm_);
+    }
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+void* Plan::dalloc(size_t bytes) {
+    void* p = nullptr;
+    PCSB_CUDA(cudaMalloc(&p, bytes ? bytes : 16));
+    allocs_.push_back(p);
+    return p;
+}
+
+void Plan::free_all() {
+    for (void* p : allocs_) cudaFree(p);
+    allocs_.clear();
+}
+
+void Plan::set_comm(const uint8_t id[128], int nranks, int rank) {
+    if (uploaded_) throw Failure(PCS_ERR_INVALID_PARAM, "set_comm must precede upload");
+    if (nranks < 1 || rank < 0 || rank >= nranks)
+        throw Failure(PCS_ERR_INVALID_PARAM, "invalid rank / nranks");
+    nranks_ = nranks;
+    rank_ = rank;
+    if (nranks == 1) return;
+    ncclUniqueId uid;
+    static_assert(sizeof(uid) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(&uid, id, 128);
+    ncclComm_t c;
+    nccl_check(nccl().CommInitRank(&c, nranks, uid, rank), "ncclCommInitRank");
+    comm_ = c;
+}
+
+void Plan::upload(const double* P, uint64_t n, const double* X0, uint64_t m) {
+    if (n == 0) throw Failure(PCS_ERR_EMPTY_CLOUD, "lop_project: data cloud is empty");
+    if (n >= 0xFFFFFFF0ull || m >= 0xFFFFFFF0ull)
+        throw Failure(PCS_ERR_INVALID_PARAM, "clouds are limited to 2^32-16 points");
+    PCSB_CUDA(cudaSetDevice(device_));
+    if (fp32_) upload_t<float>(P, n, X0, m);
+    else upload_t<double>(P, n, X0, m);
+    uploaded_ = true;
+    reset();
+}
+
+template <typename T>
+void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
+    using V = typename Vec4<T>::type;
+    free_all();
+    n_ = n;
+    m_ = m;
+    cudaEvent_t e0, e1;
+    PCSB_CUDA(cudaEventCreate(&e0));
+    PCSB_CUDA(cudaEventCreate(&e1));
+    PCSB_CUDA(cudaEventRecord(e0, stream_));
+
+    // temporaries
+    double *dP = nullptr, *dX0 = nullptr;
+    V *Pv = nullptr, *X0v = nullptr;
+    uint32_t *tk = nullptr, *tsk = nullptr;
+    PCSB_CUDA(cudaMalloc(&dP, n * 3 * sizeof(double)));
+    PCSB_CUDA(cudaMalloc(&dX0, (m ? m : 1) * 3 * sizeof(double)));
+    PCSB_CUDA(cudaMalloc(&Pv, n * sizeof(V)));
+    PCSB_CUDA(cudaMalloc(&X0v, (m ? m : 1) * sizeof(V)));
+    PCSB_CUDA(cudaMemcpyAsync(dP, P, n * 3 * sizeof(double), cudaMemcpyHostToDevice, stream_));
+    if (m) PCSB_CUDA(cudaMemcpyAsync(dX0, X0, m * 3 * sizeof(double), cudaMemcpyHostToDevice, stream_));
+    launch_convert_xyz<T>(dP, Pv, n, (T)1, stream_);
+    launch_convert_xyz<T>(dX0, X0v, m, (T)0, stream_);
+    launches_ += 2;
+
+    bbox_slots_ = (unsigned long long*)dalloc(8 * sizeof(unsigned long long));
+    init_bbox_slots(bbox_slots_, stream_);
+    launch_bbox<T>(Pv, n, bbox_slots_, stream_);
+    launch_bbox<T>(X0v, m, bbox_slots_, stream_);
+    launches_ += 3;
+    unsigned long long hb[6];
+    PCSB_CUDA(cudaMemcpyAsync(hb, bbox_slots_, sizeof(hb), cudaMemcpyDeviceToHost, stream_));
+    PCSB_CUDA(cudaStreamSynchronize(stream_));
+    double lo[3], hi[3], maxabs = 0.0;
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = ordered_to_double(hb[a]);
+        hi[a] = ordered_to_double(hb[3 + a]);
+        if (!std::isfinite(lo[a]) || !std::isfinite(hi[a]))
+            throw Failure(PCS_ERR_INVALID_PARAM, "clouds must have finite coordinates");
+        maxabs = std::max(maxabs, std::max(std::fabs(lo[a]), std::fabs(hi[a])));
+    }
+    g_ = make_grid(lo, hi, support_);
+    s_pad_ = support_ * (1.0 + std::ldexp(1.0, -10)) + 1e-12 * maxabs;
+
+    // ---- data grid (built once, lop.cpp:24) ----
+    const uint32_t nn = (uint32_t)n;
+    if (nranks_ > 1) {
+        chunk_ = (uint32_t)((m + nranks_ - 1) / nranks_);
+        mpad_ = chunk_ * nranks_;
+    } else {
+        chunk_ = (uint32_t)m;
+        mpad_ = (uint32_t)m;
+    }
+    const uint32_t sort_cap = std::max<uint32_t>(nn, std::max<uint32_t>(mpad_, 1));
+    rs_.keys_alt = (uint32_t*)dalloc(sort_cap * sizeof(uint32_t));
+    rs_.vals_alt = (uint32_t*)dalloc(sort_cap * sizeof(uint32_t));
+    rs_.blockhist = (uint32_t*)dalloc(radix_blockhist_entries(sort_cap) * sizeof(uint32_t));
+    rs_.capacity = sort_cap;
+    gap_list_ = (uint32_t*)dalloc(3 * ((size_t)sort_cap + 2) * sizeof(uint32_t));
+    gap_count_ = (uint32_t*)dalloc(sizeof(uint32_t));
+    st_ = (RunState*)dalloc(sizeof(RunState));
+    PCSB_CUDA(cudaMemsetAsync(st_, 0, sizeof(RunState), stream_));
+
+    PCSB_CUDA(cudaMalloc(&tk, sort_cap * sizeof(uint32_t)));
+    PCSB_CUDA(cudaMalloc(&tsk, sort_cap * sizeof(uint32_t)));
+    P_order_ = (uint32_t*)dalloc(nn * sizeof(uint32_t));
+    P_sorted_ = dalloc((size_t)nn * sizeof(V));
+    P_start_ = (uint32_t*)dalloc(((size_t)g_.ncells + 1) * sizeof(uint32_t));
+    launch_keys<T>(g_, Pv, nn, tk, nullptr, stream_);
+    launches_ += 1;
+    launches_ += radix_sort(tk, nullptr, tsk, P_order_, nn, g_.key_bits, rs_, nullptr, stream_);
+    launch_gather<T>(Pv, P_order_, nn, (V*)P_sorted_, nullptr, stream_);
+    launches_ += 1;
+    launches_ += build_cell_start(tsk, nn, 3 * g_.sub_bits, g_.ncells, P_start_, gap_list_,
+                                  gap_count_, nullptr, stream_);
+
+    // ---- WLOP data density v_j (once) ----
+    uint32_t* counter = (uint32_t*)dalloc(sizeof(uint32_t));
+    if (d_.density_weights) {
+        if (fp32_) {
+            PCSB_CUDA(cudaMemsetAsync(counter, 0, sizeof(uint32_t), stream_));
+            DensityArgs da{};
+            da.C = (const float4*)P_sorted_;
+            da.Cstart = P_start_;
+            da.qlist = nullptr;
+            da.nq = nn;
+            da.g = g_;
+            da.s_pad = s_pad_;
+            const double sc = support_ * (1.0 + std::ldexp(1.0, -10));
+            da.scull2 = (float)(sc * sc);
+            const float kneg = (float)(-M_LOG2E / (d_.h * d_.h));
+            da.kneg = kneg;
+            da.K0 = (float)(-(double)kneg * (double)(float)r2_);
+            da.inv_scale = (float)std::exp2(-(double)da.K0);
+            da.invert = 1;
+            da.out_sorted = (float4*)P_sorted_;
+            da.st = st_;
+            da.counter = counter;
+            da.done = nullptr;
+            launch_density(da, density_grid_, stream_);
+        } else {
+            launch_exact_density<T>((const V*)P_sorted_, P_start_, nullptr, nn, g_, s_pad_, r2_,
+                                    support_, d_.h, 0, (V*)P_sorted_, nullptr, nullptr, st_,
+                                    nullptr, stream_);
+        }
+        launches_ += 1;
+    }
+
+    // ---- projected set layout ----
+    X_init_ = dalloc((size_t)std::max<uint32_t>(mpad_, 1) * sizeof(V));
+    if (nranks_ > 1) {
+        // ownership: equal contiguous ranges of the initial cell-sorted order
+        std::vector<uint32_t> sidx(m);
+        if (m) {
+            launch_keys<T>(g_, X0v, (uint32_t)m, tk, nullptr, stream_);
+            launches_ += 1;
+            uint32_t* order = (uint32_t*)dalloc(m * sizeof(uint32_t));
+            launches_ += radix_sort(tk, nullptr, tsk, order, (uint32_t)m, g_.key_bits, rs_, nullptr,
+                                    stream_);
+            PCSB_CUDA(cudaMemcpyAsync(sidx.data(), order, m * sizeof(uint32_t),
+                                      cudaMemcpyDeviceToHost, stream_));
+            PCSB_CUDA(cudaStreamSynchronize(stream_));
+        }
+        std::vector<uint32_t> ooi(mpad_, 0xFFFFFFFFu), ioo(m);
+        for (int r = 0; r < nranks_; ++r) {
+            const uint64_t lo_p = (uint64_t)m * r / nranks_, hi_p = (uint64_t)m * (r + 1) / nranks_;
+            if (r == rank_) {
+                own_lo_ = (uint32_t)r * chunk_;
+                own_cnt_ = (uint32_t)(hi_p - lo_p);
+            }
+            for (uint64_t p = lo_p; p < hi_p; ++p) {
+                const uint32_t slot = (uint32_t)r * chunk_ + (uint32_t)(p - lo_p);
+                ooi[slot] = sidx[p];
+                ioo[sidx[p]] = slot;
+            }
+        }
+        orig_of_internal_ = (uint32_t*)dalloc((size_t)mpad_ * sizeof(uint32_t));
+        uint32_t* iof = nullptr;
+        PCSB_CUDA(cudaMalloc(&iof, (m ? m : 1) * sizeof(uint32_t)));
+        PCSB_CUDA(cudaMemcpyAsync(orig_of_internal_, ooi.data(), (size_t)mpad_ * sizeof(uint32_t),
+                                  cudaMemcpyHostToDevice, stream_));
+        if (m)
+            PCSB_CUDA(cudaMemcpyAsync(iof, ioo.data(), m * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                      stream_));
+        launch_fill_invalid<T>((V*)X_init_, mpad_, orig_of_internal_, stream_);
+        launch_scatter_init<T>(X0v, iof, (uint32_t)m, (V*)X_init_, stream_);
+        launches_ += 2;
+        PCSB_CUDA(cudaStreamSynchronize(stream_));
+        cudaFree(iof);
+        q_keys_ = (uint32_t*)dalloc((size_t)mpad_ * sizeof(uint32_t));
+        q_skeys_ = (uint32_t*)dalloc((size_t)mpad_ * sizeof(uint32_t));
+        q_list_ = (uint32_t*)dalloc((size_t)mpad_ * sizeof(uint32_t));
+    } else {
+        own_lo_ = 0;
+        own_cnt_ = (uint32_t)m;
+        if (m)
+            PCSB_CUDA(cudaMemcpyAsync(X_init_, X0v, m * sizeof(V), cudaMemcpyDeviceToDevice, stream_));
+    }
+    const size_t mp = std::max<uint32_t>(mpad_, 1);
+    X_[0] = dalloc(mp * sizeof(V));
+    X_[1] = dalloc(mp * sizeof(V));
+    X_sorted_ = dalloc(mp * sizeof(V));
+    X_keys_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
+    X_skeys_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
+    X_sidx_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
+    X_start_ = (uint32_t*)dalloc(((size_t)g_.ncells + 1) * sizeof(uint32_t));
+    careful_list_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
+    ever_iso_ = (uint8_t*)dalloc(mp);
+    slots_ = (SweepSlot*)dalloc(kSlotCap * sizeof(SweepSlot));
+    slot_cap_ = kSlotCap;
+
+    PCSB_CUDA(cudaEventRecord(e1, stream_));
+    PCSB_CUDA(cudaStreamSynchronize(stream_));
+    float ms = 0.f;
+    PCSB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    setup_ms_ = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    RunState hs;
+    PCSB_CUDA(cudaMemcpy(&hs, st_, sizeof(hs), cudaMemcpyDeviceToHost));
+    setup_density_pairs_ = hs.density_pairs;
+    cudaFree(dP);
+    cudaFree(dX0);
+    cudaFree(Pv);
+    cudaFree(X0v);
+    cudaFree(tk);
+    cudaFree(tsk);
+}
+
+void Plan::reset() {
+    if (!n_) throw Failure(PCS_ERR_INVALID_PARAM, "plan has no data (upload first)");
+    PCSB_CUDA(cudaSetDevice(device_));
+    synchronize();
+    const size_t xb = (size_t)std::max<uint32_t>(mpad_, 1) * vec_bytes_;
+    PCSB_CUDA(cudaMemcpyAsync(X_[0], X_init_, xb, cudaMemcpyDeviceToDevice, stream_));
+    PCSB_CUDA(cudaMemcpyAsync(X_[1], X_init_, xb, cudaMemcpyDeviceToDevice, stream_));
+    PCSB_CUDA(cudaMemsetAsync(st_, 0, sizeof(RunState), stream_));
+    PCSB_CUDA(cudaMemsetAsync(slots_, 0, (size_t)slot_cap_ * sizeof(SweepSlot), stream_));
+    PCSB_CUDA(cudaMemsetAsync(ever_iso_, 0, std::max<uint32_t>(mpad_, 1), stream_));
+    PCSB_CUDA(cudaStreamSynchronize(stream_));
+    sweeps_issued_ = 0;
+    sweeps_ms_ = kernel_ms_ = sort_ms_ = 0.0;
+}
+
+void Plan::run(int sweeps, bool sync) {
+    if (!uploaded_) throw Failure(PCS_ERR_INVALID_PARAM, "plan has no data (upload first)");
+    if (sweeps <= 0) sweeps = d_.iterations;
+    if (sweeps_issued_ + sweeps > slot_cap_)
+        throw Failure(PCS_ERR_INVALID_PARAM, "too many sweeps for one plan run (reset the plan)");
+    PCSB_CUDA(cudaSetDevice(device_));
+    synchronize();
+    PCSB_CUDA(cudaEventRecord(run_ev_[0], stream_));
+    for (int i = 0; i < sweeps; ++i) {
+        const int k = ++sweeps_issued_;
+        if (fp32_) enqueue_sweep<float>(k);
+        else enqueue_sweep<double>(k);
+    }
+    PCSB_CUDA(cudaEventRecord(run_ev_[1], stream_));
+    run_pending_ = true;
+    if (sync) synchronize();
+}
+
+void Plan::synchronize() {
+    PCSB_CUDA(cudaStreamSynchronize(stream_));
+    PCSB_CUDA(cudaGetLastError());
+    if (run_pending_) {
+        float ms = 0.f;
+        PCSB_CUDA(cudaEventElapsedTime(&ms, run_ev_[0], run_ev_[1]));
+        last_run_ms_ = ms;
+        sweeps_ms_ += ms;
+        run_pending_ = false;
+    }
+    for (auto& se : pending_) {
+        float a = 0.f, b = 0.f;
+        PCSB_CUDA(cudaEventElapsedTime(&a, se.e[0], se.e[1]));
+        PCSB_CUDA(cudaEventElapsedTime(&b, se.e[1], se.e[2]));
+        sort_ms_ += a;
+        kernel_ms_ += b;
+        event_pool_.push_back(se);
+    }
+    pending_.clear();
+}
+
+template <typename T>
+void Plan::grid_rebuild(const void* Xcur) {
+    using V = typename Vec4<T>::type;
+    const uint32_t* done = &st_->done;
+    launch_keys<T>(g_, (const V*)Xcur, mpad_, X_keys_, done, stream_);
+    launches_ += 1;
+    launches_ += radix_sort(X_keys_, nullptr, X_skeys_, X_sidx_, mpad_, g_.key_bits, rs_, done,
+                            stream_);
+    launch_gather<T>((const V*)Xcur, X_sidx_, (uint32_t)m_, (V*)X_sorted_, done, stream_);
+    launches_ += 1;
+    launches_ += build_cell_start(X_skeys_, (uint32_t)m_, 3 * g_.sub_bits, g_.ncells, X_start_,
+                                  gap_list_, gap_count_, done, stream_);
+}
+
+void Plan::allgather_x(void* X, bool f32) {
+    const NcclApi& api = nccl();
+    const size_t elems = (size_t)chunk_ * 4;
+    char* base = (char*)X;
+    const size_t esz = f32 ? sizeof(float) : sizeof(double);
+    nccl_check(api.AllGather(base + (size_t)rank_ * elems * esz, base, elems,
+                             f32 ? ncclFloat : ncclDouble, (ncclComm_t)comm_, stream_),
+               "ncclAllGather");
+}
+
+template <typename T>
+void Plan::density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur) {
+    using V = typename Vec4<T>::type;
+    const bool multi = nranks_ > 1;
+    SweepSlot* slot = slots_ + (sweeps_issued_ - 1);
+    if (fp32_) {
+        DensityArgs da{};
+        da.C = (const float4*)X_sorted_;
+        da.Cstart = X_start_;
+        da.qlist = qlist;
+        da.nq = nq;
+        da.g = g_;
+        da.s_pad = s_pad_;
+        const double sc = support_ * (1.0 + std::ldexp(1.0, -10));
+        da.scull2 = (float)(sc * sc);
+        const float kneg = (float)(-M_LOG2E / (d_.h * d_.h));
+        da.kneg = kneg;
+        da.K0 = (float)(-(double)kneg * (double)(float)r2_);
+        da.inv_scale = (float)std::exp2(-(double)da.K0);
+        da.invert = 0;
+        da.out_sorted = multi ? nullptr : (float4*)X_sorted_;
+        da.out_internal = multi ? (float4*)Xcur : nullptr;
+        da.idx = X_sidx_;
+        da.st = st_;
+        da.counter = &slot->density_counter;
+        da.done = &st_->done;
+        launch_density(da, density_grid_, stream_);
+    } else {
+        launch_exact_density<T>((const V*)X_sorted_, X_start_, qlist, nq, g_, s_pad_, r2_, support_,
+                                d_.h, 0, multi ? nullptr : (V*)X_sorted_, multi ? (V*)Xcur : nullptr,
+                                X_sidx_, st_, &st_->done, stream_);
+    }
+    launches_ += 1;
+    if (multi) {
+        allgather_x(Xcur, fp32_);
+        launch_gather<T>((const V*)Xcur, X_sidx_, (uint32_t)m_, (V*)X_sorted_, &st_->done, stream_);
+        launches_ += 1;
+    }
+}
+
+template <typename T>
+void Plan::enqueue_sweep(int k) {
+    using V = typename Vec4<T>::type;
+    SweepSlot* slot = slots_ + (k - 1);
+    void* cur = X_[(k - 1) & 1];
+    void* nxt = X_[k & 1];
+    const uint32_t* done = &st_->done;
+    const bool multi = nranks_ > 1;
+
+    SweepEvents se;
+    if (!event_pool_.empty()) {
+        se = event_pool_.back();
+        event_pool_.pop_back();
+    } else {
+        for (auto& e : se.e) PCSB_CUDA(cudaEventCreate(&e));
+    }
+    PCSB_CUDA(cudaEventRecord(se.e[0], stream_));
+
+    // (1) index over the moving set (lop.cpp:39)
+    grid_rebuild<T>(cur);
+    const uint32_t* qlist = nullptr;
+    uint32_t nq = (uint32_t)m_;
+    if (multi) {
+        launch_owner_keys(X_sidx_, (uint32_t)m_, own_lo_, own_lo_ + own_cnt_, q_keys_, done, stream_);
+        launches_ += 1;
+        launches_ += radix_sort(q_keys_, nullptr, q_skeys_, q_list_, (uint32_t)m_, 1, rs_, done,
+                                stream_);
+        // q_list_ holds sorted slots? no: values are positions in X_sidx_ order == sorted slots
+        qlist = q_list_;
+        nq = own_cnt_;
+    }
+    // (2) WLOP density of the projected set on X^k
+    if (d_.density_weights) density_pass_x<T>(qlist, nq, cur);
+    PCSB_CUDA(cudaEventRecord(se.e[1], stream_));
+
+    // (3) per-point update (lop.cpp:41-100)
+    if (fp32_) {
+        FastArgs a{};
+        a.P = (const float4*)P_sorted_;
+        a.Pstart = P_start_;
+        a.Xs = (const float4*)X_sorted_;
+        a.Xstart = X_start_;
+        a.Xs_idx = X_sidx_;
+        a.qlist = qlist;
+        a.nq = nq;
+        a.g = g_;
+        a.s_pad = s_pad_;
+        const double sc = support_ * (1.0 + std::ldexp(1.0, -10));
+        a.scull2 = (float)(sc * sc);
+        const float kneg = (float)(-M_LOG2E / (d_.h * d_.h));
+        a.kneg = kneg;
+        a.K0 = (float)(-(double)kneg * (double)(float)r2_);
+        a.band = a.K0 * (float)std::ldexp(1.0, -18);
+        a.support = (float)support_;
+        a.mu = (float)d_.mu;
+        a.Xnext = (float4*)nxt;
+        a.careful_list = careful_list_;
+        a.ever_isolated = ever_iso_;
+        a.st = st_;
+        a.slot = slot;
+        a.done = done;
+        const int rep = d_.mu > 0.0 ? (d_.eta_kind == PCS_ETA_INV_CUBE ? 1 : 2) : 0;
+        launch_fast(a, lanes_, d_.density_weights != 0, k == 1, rep, fast_grid_, stream_);
+        launches_ += 1;
+    }
+    PCSB_CUDA(cudaEventRecord(se.e[2], stream_));
+    {
+        ExactArgs<T> e{};
+        e.P = (const V*)P_sorted_;
+        e.Porder = P_order_;
+        e.Pstart = P_start_;
+        e.Xs = (const V*)X_sorted_;
+        e.Xstart = X_start_;
+        e.Xs_idx = X_sidx_;
+        e.g = g_;
+        e.s_pad = s_pad_;
+        e.r2 = r2_;
+        e.support = support_;
+        e.h = d_.h;
+        e.mu = d_.mu;
+        e.eta_kind = d_.eta_kind;
+        e.wlop = d_.density_weights;
+        e.Xnext = (V*)nxt;
+        e.ever_isolated = ever_iso_;
+        e.st = st_;
+        e.slot = slot;
+        e.done = done;
+        if (fp32_) {
+            e.qlist = careful_list_;
+            e.nq_dev = &slot->careful_count;
+            e.count_careful = 1;
+            launch_exact<T>(e, 148 * 2, stream_);
+        } else {
+            e.qlist = qlist;
+            e.nq = nq;
+            e.count_careful = 0;
+            launch_exact<T>(e, exact_grid_, stream_);
+        }
+        launches_ += 1;
+    }
+    // (4) exchange + aggregation (lop.cpp:102-119)
+    if (multi) {
+        const NcclApi& api = nccl();
+        nccl_check(api.GroupStart(), "ncclGroupStart");
+        allgather_x(nxt, fp32_);
+        nccl_check(api.AllReduce(&slot->max_disp_bits, &slot->max_disp_bits, 1, ncclUint64, ncclMax,
+                                 (ncclComm_t)comm_, stream_),
+                   "ncclAllReduce");
+        nccl_check(api.GroupEnd(), "ncclGroupEnd");
+    }
+    launch_finalize_sweep(st_, slot, k, d_.convergence_tol, stream_);
+    launches_ += 1;
+    PCSB_CUDA(cudaEventRecord(se.e[3], stream_));
+    pending_.push_back(se);
+}
+
+void Plan::download(double* X_out, pcs_lop_summary* s, uint32_t* iso, uint64_t cap) {
+    PCSB_CUDA(cudaSetDevice(device_));
+    synchronize();
+    RunState hs;
+    PCSB_CUDA(cudaMemcpy(&hs, st_, sizeof(hs), cudaMemcpyDeviceToHost));
+    const bool multi = nranks_ > 1;
+    if (multi) {
+        // per-rank counters -> job totals
+        unsigned long long* tmp = nullptr;
+        PCSB_CUDA(cudaMalloc(&tmp, 6 * sizeof(unsigned long long)));
+        unsigned long long hv[6] = {hs.isolated_events, hs.coincident_pairs, hs.interactions_attr,
+                                    hs.interactions_rep, hs.density_pairs, hs.careful_points};
+        PCSB_CUDA(cudaMemcpy(tmp, hv, sizeof(hv), cudaMemcpyHostToDevice));
+        nccl_check(nccl().AllReduce(tmp, tmp, 6, ncclUint64, ncclSum, (ncclComm_t)comm_, stream_),
+                   "ncclAllReduce");
+        PCSB_CUDA(cudaMemcpyAsync(hv, tmp, sizeof(hv), cudaMemcpyDeviceToHost, stream_));
+        PCSB_CUDA(cudaStreamSynchronize(stream_));
+        cudaFree(tmp);
+        hs.isolated_events = hv[0];
+        hs.coincident_pairs = hv[1];
+        hs.interactions_attr = hv[2];
+        hs.interactions_rep = hv[3];
+        hs.density_pairs = hv[4] + setup_density_pairs_;
+        hs.careful_points = hv[5];
+    } else {
+        hs.density_pairs += setup_density_pairs_;
+    }
+    const int iters = hs.iterations_run;
+    void* fin = X_[iters & 1];
+    double* dout = nullptr;
+    uint8_t* diso = nullptr;
+    PCSB_CUDA(cudaMalloc(&dout, (m_ ? m_ : 1) * 3 * sizeof(double)));
+    PCSB_CUDA(cudaMalloc(&diso, m_ ? m_ : 1));
+    PCSB_CUDA(cudaMemsetAsync(diso, 0, m_ ? m_ : 1, stream_));
+    if (fp32_) launch_unpermute<float>((const float4*)fin, orig_of_internal_, mpad_, dout, stream_);
+    else launch_unpermute<double>((const double4*)fin, orig_of_internal_, mpad_, dout, stream_);
+    launch_iso_to_orig(ever_iso_, orig_of_internal_, mpad_, diso, stream_);
+    launches_ += 2;
+    if (multi && m_)
+        nccl_check(nccl().AllReduce(diso, diso, m_, ncclUint8, ncclMax, (ncclComm_t)comm_, stream_),
+                   "ncclAllReduce");
+    std::vector<uint8_t> hiso(m_);
+    if (X_out && m_)
+        PCSB_CUDA(cudaMemcpyAsync(X_out, dout, m_ * 3 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    if (m_) PCSB_CUDA(cudaMemcpyAsync(hiso.data(), diso, m_, cudaMemcpyDeviceToHost, stream_));
+    PCSB_CUDA(cudaStreamSynchronize(stream_));
+    cudaFree(dout);
+    cudaFree(diso);
+    uint64_t k = 0;
+    for (uint64_t i = 0; i < m_; ++i)
+        if (hiso[i]) {
+            if (iso && k < cap) iso[k] = (uint32_t)i;
+            ++k;
+        }
+    if (s) {
+        std::memset(s, 0, sizeof(*s));
+        s->iterations_run = hs.iterations_run;
+        s->converged = (int32_t)hs.converged;
+        s->isolated_events = hs.isolated_events;
+        s->coincident_pairs = hs.coincident_pairs;
+        s->n_isolated = k;
+        s->interactions_attr = hs.interactions_attr;
+        s->interactions_rep = hs.interactions_rep;
+        s->density_pairs = hs.density_pairs;
+        s->careful_points = hs.careful_points;
+        s->last_max_disp = hs.last_max_disp;
+        s->setup_ms = setup_ms_;
+        s->sweeps_ms = sweeps_ms_;
+        s->kernel_ms = kernel_ms_;
+        s->sort_ms = sort_ms_;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Parity facilities
+// ---------------------------------------------------------------------------
+
+namespace {
+
+template <typename T>
+struct TmpGrid {
+    using V = typename Vec4<T>::type;
+    GridGeom g{};
+    V* sorted = nullptr;
+    uint32_t* order = nullptr;
+    uint32_t* start = nullptr;
+    uint32_t* skeys = nullptr;
+    double s_pad = 0;
+    std::vector<void*> allocs;
+    ~TmpGrid() {
+        for (void* p : allocs) cudaFree(p);
+    }
+    void* alloc(size_t b) {
+        void* p = nullptr;
+        PCSB_CUDA(cudaMalloc(&p, b ? b : 16));
+        allocs.push_back(p);
+        return p;
+    }
+    // builds the grid of C over bbox(C u Q)
+    void build(const double* C, uint64_t n, const double* dQ_or_null, const double* Q, uint64_t m,
+               double support, cudaStream_t s) {
+        const uint32_t nn = (uint32_t)n;
+        double* dC = (double*)alloc(n * 3 * sizeof(double));
+        PCSB_CUDA(cudaMemcpyAsync(dC, C, n * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+        V* Cv = (V*)alloc(n * sizeof(V));
+        launch_convert_xyz<T>(dC, Cv, n, (T)1, s);
+        unsigned long long* slots = (unsigned long long*)alloc(8 * sizeof(unsigned long long));
+        init_bbox_slots(slots, s);
+        launch_bbox<T>(Cv, n, slots, s);
+        if (m) {
+            V* Qv = (V*)alloc(m * sizeof(V));
+            launch_convert_xyz<T>(dQ_or_null, Qv, m, (T)0, s);
+            launch_bbox<T>(Qv, m, slots, s);
+        }
+        (void)Q;
+        unsigned long long hb[6];
+        PCSB_CUDA(cudaMemcpyAsync(hb, slots, sizeof(hb), cudaMemcpyDeviceToHost, s));
+        PCSB_CUDA(cudaStreamSynchronize(s));
+        double lo[3], hi[3], maxabs = 0;
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = ordered_to_double(hb[a]);
+            hi[a] = ordered_to_double(hb[3 + a]);
+            if (!std::isfinite(lo[a]) || !std::isfinite(hi[a]))
+                throw Failure(PCS_ERR_INVALID_PARAM, "clouds must have finite coordinates");
+            maxabs = std::max(maxabs, std::max(std::fabs(lo[a]), std::fabs(hi[a])));
+        }
+        g = make_grid(lo, hi, support);
+        s_pad = support * (1.0 + std::ldexp(1.0, -10)) + 1e-12 * maxabs;
+        uint32_t* keys = (uint32_t*)alloc(nn * sizeof(uint32_t));
+        skeys = (uint32_t*)alloc(nn * sizeof(uint32_t));
+        order = (uint32_t*)alloc(nn * sizeof(uint32_t));
+        sorted = (V*)alloc(nn * sizeof(V));
+        start = (uint32_t*)alloc(((size_t)g.ncells + 1) * sizeof(uint32_t));
+        RadixScratch rs;
+        rs.keys_alt = (uint32_t*)alloc(nn * sizeof(uint32_t));
+        rs.vals_alt = (uint32_t*)alloc(nn * sizeof(uint32_t));
+        rs.blockhist = (uint32_t*)alloc(radix_blockhist_entries(nn) * sizeof(uint32_t));
+        rs.capacity = nn;
+        uint32_t* gaps = (uint32_t*)alloc(3 * ((size_t)nn + 2) * sizeof(uint32_t));
+        uint32_t* gc = (uint32_t*)alloc(sizeof(uint32_t));
+        launch_keys<T>(g, Cv, nn, keys, nullptr, s);
+        radix_sort(keys, nullptr, skeys, order, nn, g.key_bits, rs, nullptr, s);
+        launch_gather<T>(Cv, order, nn, sorted, nullptr, s);
+        build_cell_start(skeys, nn, 3 * g.sub_bits, g.ncells, start, gaps, gc, nullptr, s);
+    }
+};
+
+template <typename T>
+void radius_query_t(const double* C, uint64_t n, const double* Q, uint64_t m, double r,
+                    uint64_t* offsets, uint32_t* idx, uint64_t cap, cudaStream_t s) {
+    TmpGrid<T> tg;
+    double* dQ = (double*)tg.alloc((m ? m : 1) * 3 * sizeof(double));
+    if (m) PCSB_CUDA(cudaMemcpyAsync(dQ, Q, m * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+    tg.build(C, n, dQ, Q, m, r, s);
+    uint64_t* dcnt = (uint64_t*)tg.alloc((m + 1) * sizeof(uint64_t));
+    launch_radius_dump<T>(tg.sorted, tg.order, tg.start, tg.g, dQ, (uint32_t)m, r, tg.s_pad, dcnt,
+                          nullptr, s);
+    std::vector<uint64_t> cnt(m);
+    if (m) PCSB_CUDA(cudaMemcpyAsync(cnt.data(), dcnt, m * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    PCSB_CUDA(cudaStreamSynchronize(s));
+    offsets[0] = 0;
+    for (uint64_t i = 0; i < m; ++i) offsets[i + 1] = offsets[i] + cnt[i];
+    if (!idx) return;
+    const uint64_t total = offsets[m];
+    if (total > cap) throw Failure(PCS_ERR_CAPACITY, "idx buffer too small");
+    uint32_t* didx = (uint32_t*)tg.alloc((total ? total : 1) * sizeof(uint32_t));
+    PCSB_CUDA(cudaMemcpyAsync(dcnt, offsets, m * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    launch_radius_dump<T>(tg.sorted, tg.order, tg.start, tg.g, dQ, (uint32_t)m, r, tg.s_pad, dcnt,
+                          didx, s);
+    if (total)
+        PCSB_CUDA(cudaMemcpyAsync(idx, didx, total * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    PCSB_CUDA(cudaStreamSynchronize(s));
+    PCSB_CUDA(cudaGetLastError());
+    // hits ascending by index (proj/src/spatial.cpp:109-110)
+    for (uint64_t i = 0; i < m; ++i) std::sort(idx + offsets[i], idx + offsets[i + 1]);
+}
+
+template <typename T>
+void grid_sort_t(const double* C, uint64_t n, double support, uint32_t* keys_out,
+                 uint32_t* order_out, cudaStream_t s) {
+    TmpGrid<T> tg;
+    tg.build(C, n, nullptr, nullptr, 0, support, s);
+    PCSB_CUDA(cudaMemcpyAsync(keys_out, tg.skeys, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    PCSB_CUDA(cudaMemcpyAsync(order_out, tg.order, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    PCSB_CUDA(cudaStreamSynchronize(s));
+    PCSB_CUDA(cudaGetLastError());
+}
+
+struct StreamGuard {
+    cudaStream_t s = nullptr;
+    StreamGuard() { PCSB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+    ~StreamGuard() {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+    }
+};
+
+}  // namespace
+
+void radius_query_all(const pcs_lop_desc& d, const double* C, uint64_t n, const double* Q,
+                      uint64_t m, double r, uint64_t* offsets, uint32_t* idx, uint64_t cap) {
+    if (!(r > 0.0) || !std::isfinite(r))
+        throw Failure(PCS_ERR_INVALID_PARAM, "radius_query requires finite r > 0");
+    offsets[0] = 0;
+    if (n == 0) {
+        for (uint64_t i = 0; i < m; ++i) offsets[i + 1] = 0;
+        return;
+    }
+    select_device(d.device);
+    StreamGuard sg;
+    if (d.precision == PCS_PREC_FP32) radius_query_t<float>(C, n, Q, m, r, offsets, idx, cap, sg.s);
+    else radius_query_t<double>(C, n, Q, m, r, offsets, idx, cap, sg.s);
+}
+
+void grid_sort(const pcs_lop_desc& d, const double* C, uint64_t n, double support,
+               uint32_t* keys_out, uint32_t* order_out) {
+    if (!(support > 0.0)) throw Failure(PCS_ERR_INVALID_PARAM, "support must be positive");
+    if (n == 0) return;
+    select_device(d.device);
+    StreamGuard sg;
+    if (d.precision == PCS_PREC_FP32) grid_sort_t<float>(C, n, support, keys_out, order_out, sg.s);
+    else grid_sort_t<double>(C, n, support, keys_out, order_out, sg.s);
+}
+
+}  // namespace pcsb

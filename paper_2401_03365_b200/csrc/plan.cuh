@@ -1,0 +1,125 @@
+// plan.cuh — host-side orchestration of one LOP/WLOP run on one GPU (one rank).
+//
+// The plan owns every device buffer of a run, the stream it is issued on and
+// (for multi-GPU) the NCCL communicator.  A sweep is a fixed sequence of
+// launches (keys -> radix sort -> gather -> cell table -> [w_i] -> fused
+// kernel -> deferred exact queries -> [all-gather X] -> finalize); all of them
+// read a device "done" flag so sweeps after convergence cost a launch only.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pcs_lop.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace pcsb {
+
+// Error carrying a pcs_status; converted at the C boundary.
+struct Failure : std::runtime_error {
+    pcs_status code;
+    Failure(pcs_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what);
+#define PCSB_CUDA(x) ::pcsb::cuda_check((x), #x)
+
+// Derives the shared grid for a bounding box and a support radius.
+GridGeom make_grid(const double lo[3], const double hi[3], double support);
+
+void validate_desc(const pcs_lop_desc& d);  // throws Failure(INVALID_PARAM)
+int select_device(int requested);           // throws Failure(NO_DEVICE)
+
+class Plan {
+public:
+    explicit Plan(const pcs_lop_desc& d);
+    ~Plan();
+    Plan(const Plan&) = delete;
+    Plan& operator=(const Plan&) = delete;
+
+    void set_comm(const uint8_t id[128], int nranks, int rank);
+    void upload(const double* P, uint64_t n, const double* X0, uint64_t m);
+    void reset();
+    void run(int sweeps, bool sync);
+    void synchronize();
+    double last_run_ms() const { return last_run_ms_; }
+    void download(double* X_out, pcs_lop_summary* s, uint32_t* iso, uint64_t cap);
+    uint64_t launches() const { return launches_; }
+
+private:
+    template <typename T> void upload_t(const double* P, uint64_t n, const double* X0, uint64_t m);
+    template <typename T> void enqueue_sweep(int k);
+    template <typename T> void density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur);
+    template <typename T> void grid_rebuild(const void* Xcur);
+    void allgather_x(void* X, bool fp32);
+    void free_all();
+    void* dalloc(size_t bytes);
+
+    pcs_lop_desc d_;
+    bool fp32_;
+    int device_ = 0;
+    cudaStream_t stream_ = nullptr;
+    int nranks_ = 1, rank_ = 0;
+    void* comm_ = nullptr;  // ncclComm_t
+
+    uint64_t n_ = 0, m_ = 0;
+    uint32_t mpad_ = 0, chunk_ = 0, own_lo_ = 0, own_cnt_ = 0;
+    GridGeom g_{};
+    double support_ = 0, r2_ = 0, s_pad_ = 0;
+    int lanes_ = 4;
+    int fast_grid_ = 0, exact_grid_ = 0, density_grid_ = 0;
+
+    std::vector<void*> allocs_;
+    size_t vec_bytes_ = 16;
+    // data
+    void* P_sorted_ = nullptr;
+    uint32_t* P_order_ = nullptr;
+    uint32_t* P_start_ = nullptr;
+    // projected set
+    void* X_[2] = {nullptr, nullptr};
+    void* X_init_ = nullptr;
+    void* X_sorted_ = nullptr;
+    uint32_t* X_keys_ = nullptr;
+    uint32_t* X_skeys_ = nullptr;
+    uint32_t* X_sidx_ = nullptr;
+    uint32_t* X_start_ = nullptr;
+    uint32_t* gap_list_ = nullptr;
+    uint32_t* gap_count_ = nullptr;
+    uint32_t* q_keys_ = nullptr;
+    uint32_t* q_skeys_ = nullptr;
+    uint32_t* q_list_ = nullptr;
+    uint32_t* careful_list_ = nullptr;
+    uint8_t* ever_iso_ = nullptr;
+    uint32_t* orig_of_internal_ = nullptr;  // multi-GPU only
+    RadixScratch rs_{};
+    RunState* st_ = nullptr;
+    SweepSlot* slots_ = nullptr;
+    int slot_cap_ = 0;
+    unsigned long long* bbox_slots_ = nullptr;
+
+    int sweeps_issued_ = 0;
+    bool uploaded_ = false;
+    bool run_pending_ = false;
+    unsigned long long setup_density_pairs_ = 0;
+    uint64_t launches_ = 0;
+    double setup_ms_ = 0, last_run_ms_ = 0, sweeps_ms_ = 0, kernel_ms_ = 0, sort_ms_ = 0;
+    cudaEvent_t run_ev_[2] = {nullptr, nullptr};
+    struct SweepEvents {
+        cudaEvent_t e[4];
+    };
+    std::vector<SweepEvents> pending_;  // per issued sweep in the current run
+    std::vector<SweepEvents> event_pool_;
+};
+
+// Parity facilities (stateless).
+void radius_query_all(const pcs_lop_desc& d, const double* C, uint64_t n, const double* Q,
+                      uint64_t m, double r, uint64_t* offsets, uint32_t* idx, uint64_t cap);
+void grid_sort(const pcs_lop_desc& d, const double* C, uint64_t n, double support,
+               uint32_t* keys_out, uint32_t* order_out);
+
+}  // namespace pcsb
