@@ -9,7 +9,7 @@
  *       /root/reference/proj/include/pcs/lop.hpp:51-53, src/lop.cpp:10-127
  *
  * Plain pointers and sizes only (no C++ or torch types).  The C++ header set
- * include/pcs/*.hpp re-exposes pcs::lop_project with the reference's structs on
+ * include/pcs/ (*.hpp) re-exposes pcs::lop_project with the reference's structs on
  * top of this ABI; Python binds it with ctypes (paper_2401_03365_b200/lop.py).
  *
  * Error model (mirrors proj/include/pcs/errors.hpp:9-53): every entry point
@@ -146,6 +146,11 @@ uint64_t pcs_lop_plan_launches(const pcs_lop_plan* p);
 pcs_status pcs_radius_query_all(const pcs_lop_desc* d, const double* C_xyz, uint64_t n,
                                 const double* Q_xyz, uint64_t m, double r,
                                 uint64_t* offsets, uint32_t* idx, uint64_t idx_cap);
+/* WLOP density weights over one cloud, v_j = 1 + sum_{j' != j, d <= support}
+ * theta(d) (original order), evaluated exactly like the run does (fp32 fused
+ * kernel or fp64 exact kernel per d->precision). */
+pcs_status pcs_density_weights(const pcs_lop_desc* d, const double* C_xyz, uint64_t n,
+                               double* v_out);
 /* Grid sort order used by the device hash: sorted positions -> point index,
  * and the 32-bit cell keys, for a cloud (parity: stable sort by key). */
 pcs_status pcs_grid_sort(const pcs_lop_desc* d, const double* C_xyz, uint64_t n, double support,

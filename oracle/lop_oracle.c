@@ -617,6 +617,8 @@ int orc_lop_project(const double* P, size_t n, const double* X0, size_t m,
         }
         if (w) density_on_grid(&xg, prm->h, prm->cutoff_multiple, w, m);
         sweep(&pg, P, v, &xg, cur, w, m, prm, nxt, iso, co, &pc);
+        if (prm->store_f32)
+            for (size_t i = 0; i < 3 * m; ++i) nxt[i] = (double)(float)nxt[i];
         grid_free(&xg);
         /* Deterministic aggregation in index order (lop.cpp:102-113). */
         const double md = max_displacement(nxt, cur, m);

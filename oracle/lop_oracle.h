@@ -46,6 +46,9 @@ typedef struct orc_params {
     double convergence_tol;  /* LopParams::convergence_tol > 0 */
     int32_t eta_kind;        /* ORC_ETA_* */
     int32_t density_weights; /* 0 = LOP, 1 = WLOP */
+    int32_t store_f32;       /* 1: round the iterate to fp32 after every sweep and the
+                                data density weights to fp32 (mirrors the fp32 storage of
+                                the B200 fp32 mode; 0 = the reference's fp64 storage) */
 } orc_params;
 
 typedef struct orc_summary {

@@ -36,6 +36,7 @@ class OrcParams(C.Structure):
         ("convergence_tol", C.c_double),
         ("eta_kind", C.c_int32),
         ("density_weights", C.c_int32),
+        ("store_f32", C.c_int32),
     ]
 
 
@@ -158,14 +159,14 @@ class OracleError(RuntimeError):
 
 
 def lop_project(P, X0, h, cutoff=3.0, mu=0.4, iterations=30, tol=1e-7,
-                eta=ETA_INV_CUBE, wlop=False, threads=0) -> Result:
+                eta=ETA_INV_CUBE, wlop=False, threads=0, store_f32=False) -> Result:
     """orc_lop_project — the C restatement of pcs::lop_project (+eta/WLOP)."""
     P = _xyz(P)
     X0 = _xyz(X0)
     m = X0.shape[0]
     out = np.empty_like(X0)
     iso = np.empty(max(m, 1), dtype=np.uint32)
-    prm = OrcParams(h, cutoff, mu, iterations, tol, eta, 1 if wlop else 0)
+    prm = OrcParams(h, cutoff, mu, iterations, tol, eta, 1 if wlop else 0, 1 if store_f32 else 0)
     s = OrcSummary()
     rc = orc().orc_lop_project(_ptr(P, _c_dbl_p), P.shape[0], _ptr(X0, _c_dbl_p), m,
                                C.byref(prm), _ptr(out, _c_dbl_p), C.byref(s),
@@ -186,7 +187,7 @@ def lop_sweep(P, X, h, cutoff=3.0, mu=0.4, eta=ETA_INV_CUBE, wlop=False, threads
     iso = np.zeros(max(m, 1), dtype=np.uint8)
     co = np.zeros(max(m, 1), dtype=np.uint32)
     md = C.c_double(0.0)
-    prm = OrcParams(h, cutoff, mu, 1, 1e-7, eta, 1 if wlop else 0)
+    prm = OrcParams(h, cutoff, mu, 1, 1e-7, eta, 1 if wlop else 0, 0)
     rc = orc().orc_lop_sweep(_ptr(P, _c_dbl_p), P.shape[0], _ptr(X, _c_dbl_p), m, C.byref(prm),
                              _ptr(nxt, _c_dbl_p), _ptr(iso, _c_u8_p), _ptr(co, _c_u32_p),
                              C.byref(md), threads)

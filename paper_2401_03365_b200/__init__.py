@@ -5,13 +5,13 @@ The operator runs as hand-written sm_100a CUDA kernels in
 """
 from .lop import (  # noqa: F401
     CONFIGS, EmptyCloud, Error, InvalidParam, KernelParams, LopParams, LopPlan, LopSummary,
-    NumericalFailure, DeviceUnavailable, add_noise, config_params, config_sizes, generate_config,
+    NumericalFailure, DeviceUnavailable, add_noise, config_params, config_sizes, density_weights, generate_config,
     generate_surface, grid_sort, lop_project, radius_query_all,
 )
 
 __all__ = [
     "CONFIGS", "EmptyCloud", "Error", "InvalidParam", "KernelParams", "LopParams", "LopPlan",
     "LopSummary", "NumericalFailure", "DeviceUnavailable", "add_noise", "config_params",
-    "config_sizes", "generate_config", "generate_surface", "grid_sort", "lop_project",
+    "config_sizes", "density_weights", "generate_config", "generate_surface", "grid_sort", "lop_project",
     "radius_query_all",
 ]

@@ -33,7 +33,7 @@ EXPORTED = [
     "pcs_lop_run", "pcs_lop_plan_create", "pcs_lop_plan_destroy", "pcs_lop_plan_upload",
     "pcs_nccl_unique_id", "pcs_lop_plan_set_comm", "pcs_lop_plan_reset", "pcs_lop_plan_run",
     "pcs_lop_plan_synchronize", "pcs_lop_plan_last_run_ms", "pcs_lop_plan_download",
-    "pcs_lop_plan_launches", "pcs_radius_query_all", "pcs_grid_sort", "pcs_generate_surface",
+    "pcs_lop_plan_launches", "pcs_radius_query_all", "pcs_density_weights", "pcs_grid_sort", "pcs_generate_surface",
     "pcs_add_noise", "pcs_config_sizes", "pcs_generate_config",
 ]
 
@@ -118,6 +118,7 @@ def lib():
         L.pcs_lop_plan_launches.restype = C.c_uint64
         L.pcs_radius_query_all.argtypes = [C.POINTER(LopDesc), _dp, C.c_uint64, _dp, C.c_uint64,
                                            C.c_double, _u64p, _u32p, C.c_uint64]
+        L.pcs_density_weights.argtypes = [C.POINTER(LopDesc), _dp, C.c_uint64, _dp]
         L.pcs_grid_sort.argtypes = [C.POINTER(LopDesc), _dp, C.c_uint64, C.c_double, _u32p, _u32p]
         L.pcs_generate_surface.argtypes = [C.c_int32, C.c_uint64, C.c_uint64, _dp]
         L.pcs_add_noise.argtypes = [_dp, C.c_uint64, C.c_double, C.c_uint64]

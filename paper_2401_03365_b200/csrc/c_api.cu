@@ -170,6 +170,11 @@ pcs_status pcs_radius_query_all(const pcs_lop_desc* d, const double* C_xyz, uint
     });
 }
 
+pcs_status pcs_density_weights(const pcs_lop_desc* d, const double* C_xyz, uint64_t n,
+                               double* v_out) {
+    return guarded([&] { pcsb::density_weights(checked(d), C_xyz, n, v_out); });
+}
+
 pcs_status pcs_grid_sort(const pcs_lop_desc* d, const double* C_xyz, uint64_t n, double support,
                          uint32_t* keys_out, uint32_t* order_out) {
     return guarded([&] {

@@ -89,15 +89,19 @@ __device__ __forceinline__ uint32_t point_key(const GridGeom& g, double x, doubl
     return (cell << (3 * g.sub_bits)) | m;
 }
 
+// MUFU.EX2 / MUFU.RSQ, flush-to-zero forms (one SFU op each, no range fix-up).
+// Hits have arg >= -band (ex2 >= ~1) and d2 >= FLT_MIN unless the pair is
+// (nearly) coincident, which surfaces as a non-finite sum and is deferred to
+// the exact fp64 path.
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
-    asm("ex2.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
 
 __device__ __forceinline__ float rsqrt_approx(float x) {
     float y;
-    asm("rsqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
 

@@ -52,10 +52,12 @@ struct FastArgs {
     const float4* Xs;         // projected set, sorted; .w = w_i (WLOP)
     const uint32_t* Xstart;   // cell table of X
     const uint32_t* Xs_idx;   // sorted slot -> internal index
+    const uint32_t* Xskeys;   // sorted slot -> grid key (query grouping)
     const uint32_t* qlist;    // queries (sorted slots); nullptr = 0..nq-1
     uint32_t nq;
     GridGeom g;
     double s_pad;             // support with margin (cell ranges)
+    double r2;                // support^2 in fp64: exact re-decision of borderline pairs
     float scull2;             // (support*(1+2^-10))^2: candidate vs group box
     float kneg;               // -log2(e)/h^2
     float K0;                 // log2(e) * r2f / h^2  (hit <=> fma(d2,kneg,K0) >= 0)
@@ -78,11 +80,12 @@ int fast_blocks_per_sm(int lanes_per_point, bool wlop, bool check_zero, int rep_
 struct DensityArgs {
     const float4* C;          // cloud, sorted (queries and candidates)
     const uint32_t* Cstart;
+    const uint32_t* Cskeys;   // sorted slot -> grid key (query grouping)
     const uint32_t* qlist;    // queries (sorted slots), nullptr = 0..nq-1
     uint32_t nq;
     GridGeom g;
-    double s_pad;
-    float scull2, kneg, K0;
+    double s_pad, r2;
+    float scull2, kneg, K0, band;
     float inv_scale;          // 2^-K0 (undo the theta scaling)
     int invert;               // 1: write 1/(density) (data v_j), 0: write density (w_i)
     float4* out_sorted;       // if non-null: .w of this sorted array

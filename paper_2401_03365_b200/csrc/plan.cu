@@ -37,6 +37,27 @@ int bit_width_u64(uint64_t v) {
     return b;
 }
 
+// fp32 kernel constants.  theta(d) = 2^(kneg*d2) with kneg = -log2(e)/h^2; the
+// kernels evaluate arg = fma(d2, kneg, K0), K0 = -kneg*r2f, so arg >= 0 <=> d2 <= r2
+// in fp32 and 2^arg = theta * 2^K0 (the constant scale cancels in every ratio).
+// |arg| <= band flags |d2 - r2| <~ 2^-19 r2: the fp32 decision could disagree
+// with the reference's fp64 one only for |d2 - r2| <= ~14 ulp(r2) (2^-20.2 r2),
+// so those pairs are re-decided exactly in fp64 (lop_fast.cu load_cands).
+struct F32Consts {
+    float kneg, K0, band, scull2, inv_scale;
+};
+
+F32Consts fp32_consts(double h, double r2, double support) {
+    F32Consts c;
+    c.kneg = (float)(-M_LOG2E / (h * h));
+    c.K0 = (float)(-(double)c.kneg * (double)(float)r2);
+    c.band = (float)((double)c.K0 * std::ldexp(1.0, -19));
+    const double sc = support * (1.0 + std::ldexp(1.0, -10));  // candidate-vs-box cull
+    c.scull2 = (float)(sc * sc);
+    c.inv_scale = (float)std::exp2(-(double)c.K0);
+    return c;
+}
+
 double cells_for(const double lo[3], const double hi[3], double cs) {
     double c = 1.0;
     for (int a = 0; a < 3; ++a) c *= std::floor((hi[a] - lo[a]) / cs) + 3.0;
@@ -63,7 +84,7 @@ GridGeom make_grid(const double lo_in[3], const double hi_in[3], double support)
     int sb;
     if (cells_for(lo, hi, support * 0.5) <= (double)(1u << 24)) {
         cs = support * 0.5;
-        sb = 1;
+        sb = 2;  // 4x4x4 Z-order inside a cell: groups of 8 queries span ~s/8
     } else {
         cs = support;
         sb = cells_for(lo, hi, cs) <= (double)(1u << 25) ? 2 : 1;
@@ -291,16 +312,18 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
             DensityArgs da{};
             da.C = (const float4*)P_sorted_;
             da.Cstart = P_start_;
+            da.Cskeys = tsk;
             da.qlist = nullptr;
             da.nq = nn;
             da.g = g_;
             da.s_pad = s_pad_;
-            const double sc = support_ * (1.0 + std::ldexp(1.0, -10));
-            da.scull2 = (float)(sc * sc);
-            const float kneg = (float)(-M_LOG2E / (d_.h * d_.h));
-            da.kneg = kneg;
-            da.K0 = (float)(-(double)kneg * (double)(float)r2_);
-            da.inv_scale = (float)std::exp2(-(double)da.K0);
+            da.r2 = r2_;
+            const F32Consts fc = fp32_consts(d_.h, r2_, support_);
+            da.scull2 = fc.scull2;
+            da.kneg = fc.kneg;
+            da.K0 = fc.K0;
+            da.band = fc.band;
+            da.inv_scale = fc.inv_scale;
             da.invert = 1;
             da.out_sorted = (float4*)P_sorted_;
             da.st = st_;
@@ -483,16 +506,18 @@ void Plan::density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur) {
         DensityArgs da{};
         da.C = (const float4*)X_sorted_;
         da.Cstart = X_start_;
+        da.Cskeys = X_skeys_;
         da.qlist = qlist;
         da.nq = nq;
         da.g = g_;
         da.s_pad = s_pad_;
-        const double sc = support_ * (1.0 + std::ldexp(1.0, -10));
-        da.scull2 = (float)(sc * sc);
-        const float kneg = (float)(-M_LOG2E / (d_.h * d_.h));
-        da.kneg = kneg;
-        da.K0 = (float)(-(double)kneg * (double)(float)r2_);
-        da.inv_scale = (float)std::exp2(-(double)da.K0);
+        da.r2 = r2_;
+        const F32Consts fc = fp32_consts(d_.h, r2_, support_);
+        da.scull2 = fc.scull2;
+        da.kneg = fc.kneg;
+        da.K0 = fc.K0;
+        da.band = fc.band;
+        da.inv_scale = fc.inv_scale;
         da.invert = 0;
         da.out_sorted = multi ? nullptr : (float4*)X_sorted_;
         da.out_internal = multi ? (float4*)Xcur : nullptr;
@@ -557,16 +582,17 @@ void Plan::enqueue_sweep(int k) {
         a.Xs = (const float4*)X_sorted_;
         a.Xstart = X_start_;
         a.Xs_idx = X_sidx_;
+        a.Xskeys = X_skeys_;
         a.qlist = qlist;
         a.nq = nq;
         a.g = g_;
         a.s_pad = s_pad_;
-        const double sc = support_ * (1.0 + std::ldexp(1.0, -10));
-        a.scull2 = (float)(sc * sc);
-        const float kneg = (float)(-M_LOG2E / (d_.h * d_.h));
-        a.kneg = kneg;
-        a.K0 = (float)(-(double)kneg * (double)(float)r2_);
-        a.band = a.K0 * (float)std::ldexp(1.0, -18);
+        a.r2 = r2_;
+        const F32Consts fc = fp32_consts(d_.h, r2_, support_);
+        a.scull2 = fc.scull2;
+        a.kneg = fc.kneg;
+        a.K0 = fc.K0;
+        a.band = fc.band;
         a.support = (float)support_;
         a.mu = (float)d_.mu;
         a.Xnext = (float4*)nxt;
@@ -714,6 +740,7 @@ struct TmpGrid {
     using V = typename Vec4<T>::type;
     GridGeom g{};
     V* sorted = nullptr;
+    V* unsorted = nullptr;
     uint32_t* order = nullptr;
     uint32_t* start = nullptr;
     uint32_t* skeys = nullptr;
@@ -735,6 +762,7 @@ struct TmpGrid {
         double* dC = (double*)alloc(n * 3 * sizeof(double));
         PCSB_CUDA(cudaMemcpyAsync(dC, C, n * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
         V* Cv = (V*)alloc(n * sizeof(V));
+        unsorted = Cv;
         launch_convert_xyz<T>(dC, Cv, n, (T)1, s);
         unsigned long long* slots = (unsigned long long*)alloc(8 * sizeof(unsigned long long));
         init_bbox_slots(slots, s);
@@ -842,6 +870,64 @@ void radius_query_all(const pcs_lop_desc& d, const double* C, uint64_t n, const 
     StreamGuard sg;
     if (d.precision == PCS_PREC_FP32) radius_query_t<float>(C, n, Q, m, r, offsets, idx, cap, sg.s);
     else radius_query_t<double>(C, n, Q, m, r, offsets, idx, cap, sg.s);
+}
+
+namespace {
+template <typename T>
+void density_weights_t(const pcs_lop_desc& d, const double* C, uint64_t n, double* v_out,
+                       cudaStream_t s) {
+    using V = typename Vec4<T>::type;
+    const double support = d.h * d.cutoff_multiple;
+    const double r2 = support * support;
+    TmpGrid<T> tg;
+    tg.build(C, n, nullptr, nullptr, 0, support, s);
+    RunState* st = (RunState*)tg.alloc(sizeof(RunState));
+    uint32_t* counter = (uint32_t*)tg.alloc(sizeof(uint32_t));
+    PCSB_CUDA(cudaMemsetAsync(st, 0, sizeof(RunState), s));
+    PCSB_CUDA(cudaMemsetAsync(counter, 0, sizeof(uint32_t), s));
+    if (sizeof(T) == 4) {
+        DensityArgs da{};
+        da.C = (const float4*)tg.sorted;
+        da.Cstart = tg.start;
+        da.Cskeys = tg.skeys;
+        da.nq = (uint32_t)n;
+        da.g = tg.g;
+        da.s_pad = tg.s_pad;
+        da.r2 = r2;
+        const F32Consts fc = fp32_consts(d.h, r2, support);
+        da.scull2 = fc.scull2;
+        da.kneg = fc.kneg;
+        da.K0 = fc.K0;
+        da.band = fc.band;
+        da.inv_scale = fc.inv_scale;
+        da.invert = 0;
+        da.out_internal = (float4*)tg.unsorted;
+        da.idx = tg.order;
+        da.st = st;
+        da.counter = counter;
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        launch_density(da, sms * fast_blocks_per_sm(4, true, false, 0), s);
+    } else {
+        launch_exact_density<T>(tg.sorted, tg.start, nullptr, (uint32_t)n, tg.g, tg.s_pad, r2,
+                                support, d.h, 0, nullptr, tg.unsorted, tg.order, st, nullptr, s);
+    }
+    std::vector<V> h(n);
+    PCSB_CUDA(cudaMemcpyAsync(h.data(), tg.unsorted, n * sizeof(V), cudaMemcpyDeviceToHost, s));
+    PCSB_CUDA(cudaStreamSynchronize(s));
+    PCSB_CUDA(cudaGetLastError());
+    for (uint64_t i = 0; i < n; ++i) v_out[i] = (double)h[i].w;
+}
+}  // namespace
+
+void density_weights(const pcs_lop_desc& d, const double* C, uint64_t n, double* v_out) {
+    validate_desc(d);
+    if (n == 0) return;
+    select_device(d.device);
+    StreamGuard sg;
+    if (d.precision == PCS_PREC_FP32) density_weights_t<float>(d, C, n, v_out, sg.s);
+    else density_weights_t<double>(d, C, n, v_out, sg.s);
 }
 
 void grid_sort(const pcs_lop_desc& d, const double* C, uint64_t n, double support,

@@ -119,6 +119,7 @@ private:
 // Parity facilities (stateless).
 void radius_query_all(const pcs_lop_desc& d, const double* C, uint64_t n, const double* Q,
                       uint64_t m, double r, uint64_t* offsets, uint32_t* idx, uint64_t cap);
+void density_weights(const pcs_lop_desc& d, const double* C, uint64_t n, double* v_out);
 void grid_sort(const pcs_lop_desc& d, const double* C, uint64_t n, double support,
                uint32_t* keys_out, uint32_t* order_out);
 

@@ -255,6 +255,17 @@ def radius_query_all(cloud, queries, r: float, precision: str = "fp64", device: 
     return off, idx[:tot]
 
 
+def density_weights(cloud, h: float, cutoff_multiple: float = 3.0, precision: str = "fp64",
+                    device: int = -1) -> np.ndarray:
+    """WLOP density weights v_j = 1 + sum_{j' != j, d <= support} theta(d)."""
+    Cc = _cloud(cloud)
+    v = np.zeros(max(Cc.shape[0], 1), dtype=np.float64)
+    d = make_desc(LopParams(kernel=KernelParams(h, cutoff_multiple)), precision=precision,
+                  device=device)
+    _check(L.lib().pcs_density_weights(C.byref(d), _ptr(Cc), Cc.shape[0], _ptr(v)))
+    return v[: Cc.shape[0]]
+
+
 def grid_sort(cloud, support: float, precision: str = "fp64", device: int = -1):
     """(sorted keys, order) of the device hash for a cloud."""
     Cc = _cloud(cloud)

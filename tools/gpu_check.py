@@ -67,7 +67,7 @@ for cfg, scale in ((3, 0.01), (2, 0.02), (4, 0.01)):
     t1 = time.time() - t
     t = time.time()
     r = O.lop_project(P, X0, prm.kernel.h, 4.0, prm.mu, prm.iterations,
-                      eta=O.ETA_NEG_LINEAR if c["eta"] == "neg_linear" else O.ETA_INV_CUBE,
+                      eta=O.ETA_NEG_LINEAR if c["eta"] == "neg_linear" else O.ETA_INV_CUBE, store_f32=True,
                       wlop=c["wlop"])
     t2 = time.time() - t
     err = np.abs(out - r.points).max()
