@@ -1,0 +1,395 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 LOP/WLOP hot path (BASELINE.json metric).
+
+Workload (default): BASELINE.json configs[2] — LOP on the bumpy height field,
+P = 10,000,000 data points, X0 = 1,000,000 (seeded subset), h = 0.02 (support),
+mu = 0.4, eta(r) = -r, fp32 — the north star's "10M-point config", sharded over
+1/2/4/8 GPUs (strong scaling).  A step is one LOP sweep (grid rebuild + fused
+per-point kernel + deferred exact queries + [all-gather] + convergence).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
+
+For N > 1 the driver launches one process per GPU with torch.distributed.run;
+the plan joins an NCCL clique and all-gathers X every sweep.
+
+The timed region (value) runs K sweeps with P and X0 already resident in HBM,
+bracketed by a barrier and a device synchronize, timed with CUDA events on the
+plan's stream, max over ranks.  `e2e` is the same metric through the public
+API with host buffers (upload, data grid, K sweeps, download) — wall clock.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+WORKLOADS = {
+    1: "config1: LOP noisy unit sphere, P=20k, X0=2k, h=0.1, mu=0.45, eta=1/(3r^3), fp64",
+    2: "config2: WLOP torus R=1 r=0.3 + 5% outliers, P=1M, X0=100k, h=0.05, mu=0.45, eta=-r, fp32",
+    3: "config3: LOP height field z=0.1 sin8x cos8y, P=10M, X0=1M, h=0.02, mu=0.4, eta=-r, fp32",
+    4: "config4: WLOP density sphere ~e^{3.9z}, P=4M, X0=400k, h=0.03, mu=0.45, eta=-r, fp32",
+    5: "config5: LOP 8 ellipsoids, P=50M, X0=5M, h=0.02, mu=0.45, eta=1/(3r^3), fp32",
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------------------
+# clocks during the timed region (NVML sampled from a thread)
+# ------------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index: int, period_s: float = 0.005):
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self.period = period_s
+        self._stop = threading.Event()
+        self._thr = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover - no NVML
+            log("NVML unavailable:", e)
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def start(self):
+        if self.nv:
+            self._thr = threading.Thread(target=self._run, daemon=True)
+            self._thr.start()
+
+    def stop(self) -> dict:
+        if not self._thr:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml_unavailable"]}
+        self._stop.set()
+        self._thr.join()
+        reasons = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "samples": len(self.samples), "reasons": reasons}
+
+
+# ------------------------------------------------------------------------------
+# roofline denominators
+# ------------------------------------------------------------------------------
+def sfu_peak(sm_mhz: float, sms: int = 148) -> dict:
+    """Interactions/s bound of the fused kernel.
+
+    Per interaction the kernel needs 2 MUFU ops (ex2 for theta, rsqrt for 1/d);
+    sm_100 issues 16 MUFU results per SM per clock, so the bound is
+    8 interactions / SM / clock.  profiles/pipe_peaks.json, when
+    present, holds the MUFU rate measured on this pool's B200s.
+    """
+    per_sm_clk = 8.0
+    src = "derived: 16 MUFU/SM/clk (sm_100) / 2 MUFU per interaction x 148 SMs x clock"
+    p = os.path.join(HERE, "profiles", "pipe_peaks.json")
+    if os.path.exists(p):
+        try:
+            pk = json.load(open(p))
+            per_sm_clk = pk["mufu_per_sm_clk"] / 2.0
+            src = f"measured MUFU rate {pk['mufu_per_sm_clk']:.2f}/SM/clk (profiles/pipe_peaks.json) / 2"
+        except Exception:
+            pass
+    return {"per_sm_clk": per_sm_clk, "peak": per_sm_clk * sms * sm_mhz * 1e6, "source": src}
+
+
+# ------------------------------------------------------------------------------
+# CPU baseline: the reference's own lop_project on the host cores
+# ------------------------------------------------------------------------------
+def cpu_baseline(cfg: int, P: np.ndarray, X0: np.ndarray, params, c: dict, budget_s: float = 20.0,
+                 steps: int = 1) -> dict:
+    from oracle import oracle as O
+
+    nthreads = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(nthreads))
+    rng = np.random.default_rng(12345)
+    frac = 0.01 if X0.shape[0] >= 100000 else 1.0
+    nsub = max(1, int(X0.shape[0] * frac))
+    sub = np.sort(rng.choice(X0.shape[0], nsub, replace=False))
+    Xs = X0[sub]
+    h, cut, mu = params.kernel.h, params.kernel.cutoff_multiple, params.mu
+    # exact interaction count of one sweep of this sample (the port counts; counting is not timed)
+    eta_kind = O.ETA_NEG_LINEAR if c["eta"] == "neg_linear" else O.ETA_INV_CUBE
+    cnt = O.lop_project(P, Xs, h, cut, mu, 1, eta=eta_kind, wlop=c["wlop"])
+    inter = cnt.interactions_attr + cnt.interactions_rep
+    use_ref = O.ref_available() and not c["wlop"]
+    times = []
+    build_ms = 0.0
+    if use_ref:
+        build_ms = O.ref_index_build_ms(P)
+        for _ in range(steps):
+            t = time.perf_counter()
+            O.ref_lop_project(P, Xs, h, cut, mu, 1)
+            times.append(time.perf_counter() - t)
+        kind = "reference"
+        what = (f"reference pcs::lop_project (oracle/_ref, built from /root/reference), 1 sweep of a "
+                f"seeded {nsub}-point subset of X0 against the full P ({P.shape[0]} pts); the "
+                f"data kd-tree build ({build_ms/1e3:.2f} s, timed separately) is subtracted")
+        if c["eta"] != "inv_cube":
+            what += "; eta=1/(3r^3) (the only eta the reference implements; same neighbour work)"
+    else:
+        for _ in range(steps):
+            t = time.perf_counter()
+            O.lop_project(P, Xs, h, cut, mu, 1, eta=eta_kind, wlop=c["wlop"])
+            times.append(time.perf_counter() - t)
+        kind = "port"
+        what = (f"oracle port (oracle/lop_oracle.c, OpenMP), 1 sweep of a seeded {nsub}-point "
+                f"subset of X0 against the full P ({P.shape[0]} pts)")
+    t_sweep = max(1e-9, statistics.median(times) - build_ms / 1e3)
+    return {"value": inter / t_sweep, "unit": "interactions/s", "cores": int(os.environ.get(
+        "OMP_NUM_THREADS", nthreads)), "kind": kind, "sample": what,
+        "sample_interactions": int(inter), "sample_seconds": t_sweep,
+        "raw_call_seconds": statistics.median(times), "index_build_seconds": build_ms / 1e3}
+
+
+# ------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=15)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--lanes", type=int, default=0)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        log(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}; using WORLD_SIZE")
+    ngpu = world
+
+    import paper_2401_03365_b200 as pb
+
+    cfg = args.config
+    params, c = pb.config_params(cfg)
+    precision = c["precision"]
+
+    # ---------------- reference arm ----------------
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        P, X0 = pb.generate_config(cfg)
+        if precision == "fp32":
+            P = P.astype(np.float32).astype(np.float64)
+            X0 = X0.astype(np.float32).astype(np.float64)
+        cb = cpu_baseline(cfg, P, X0, params, c, steps=max(1, args.steps))
+        line = {
+            "impl": "reference", "metric": "neighbour interactions/sec (LOP sweep)",
+            "value": cb["value"], "unit": "interactions/s", "n_gpus": ngpu, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": cb["sample_seconds"] * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded host generator, BASELINE.md §4)",
+            "config": {"workload": WORKLOADS[cfg], "sample": cb["sample"]},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": "interactions/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return 0
+
+    # ---------------- B200 arm ----------------
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    else:
+        torch.cuda.set_device(0)
+    dev = local_rank if world > 1 else 0
+
+    t0 = time.time()
+    P, X0 = pb.generate_config(cfg)
+    log(f"[rank {rank}] generated config {cfg}: P={P.shape[0]} X0={X0.shape[0]} "
+        f"in {time.time() - t0:.1f}s")
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(v: float) -> float:
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def make_plan():
+        plan = pb.LopPlan(params, eta=c["eta"], density_weights=c["wlop"], precision=precision,
+                          device=dev, lanes_per_point=args.lanes)
+        if world > 1:
+            uid = [pb.LopPlan.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            plan.set_comm(uid[0], world, rank)
+        return plan
+
+    plan = make_plan()
+    t = time.time()
+    plan.upload(P, X0)
+    log(f"[rank {rank}] upload + data grid {time.time() - t:.2f}s")
+
+    # warm-up sweeps, then restart from X0 so the timed sweeps are sweeps 1..K
+    if args.warmup > 0:
+        plan.run(args.warmup)
+    plan.reset()
+    _, s0 = plan.download()
+    launches0 = plan.launches()
+    sampler = ClockSampler(dev)
+    barrier()
+    sampler.start()
+    plan.run(args.steps, sync=True)
+    barrier()
+    clocks = sampler.stop()
+    ms_local = plan.last_run_ms()
+    launches = plan.launches() - launches0
+    _, s = plan.download()
+    ms = max_over_ranks(ms_local)
+    inter = (s.interactions_attr + s.interactions_rep) - (s0.interactions_attr + s0.interactions_rep)
+    # summaries are job totals already (all-reduced inside the plan)
+    kernel_ms = max_over_ranks(s.kernel_ms - s0.kernel_ms)
+    sort_ms = max_over_ranks(s.sort_ms - s0.sort_ms)
+    sweeps = s.iterations_run
+    value = inter / (ms / 1e3)
+    log(f"[rank {rank}] {args.steps} sweeps: {ms:.2f} ms, {value:.3e} interactions/s, "
+        f"kernel {kernel_ms:.2f} ms, grid {sort_ms:.2f} ms, careful {s.careful_points}")
+
+    # ---------------- roofline of the fused kernel ----------------
+    sm_mhz = clocks.get("sm_mhz") or 1965.0
+    pk = sfu_peak(1965.0)
+    # per-GPU rate of the dominant kernel: this GPU's share of the interactions over
+    # the kernel's own device time (slowest rank)
+    kernel_rate = (inter / world) / (kernel_ms / 1e3) if kernel_ms > 0 else 0.0
+    roofline = {
+        "bound": "sfu", "unit": "interactions/s",
+        "achieved": kernel_rate,
+        "peak": pk["peak"],
+        "frac": kernel_rate / pk["peak"],
+        "kernel": "fast_kernel (fused attraction+repulsion, lop_fast.cu)",
+        "kernel_share_of_step": kernel_ms / ms if ms > 0 else None,
+        "peak_source": pk["source"] + " at sm_max 1965 MHz",
+        "frac_at_measured_clock": kernel_rate / (pk["per_sm_clk"] * 148 * sm_mhz * 1e6),
+        "traffic": None,
+    }
+    prof = os.path.join(HERE, "profiles", "fast_kernel_ncu.json")
+    if os.path.exists(prof):
+        try:
+            roofline["traffic"] = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+
+    # ---------------- e2e through the public API ----------------
+    e2e = None
+    if not args.no_e2e:
+        barrier()
+        t = time.perf_counter()
+        if world == 1:
+            prm2 = pb.LopParams(kernel=params.kernel, mu=params.mu, iterations=args.steps,
+                                convergence_tol=params.convergence_tol)
+            out, se = pb.lop_project(P, X0, prm2, eta=c["eta"], density_weights=c["wlop"],
+                                     precision=precision, device=dev, lanes_per_point=args.lanes)
+        else:
+            p2 = make_plan()
+            p2.upload(P, X0)
+            p2.run(args.steps)
+            out, se = p2.download()
+            p2.close()
+        wall = time.perf_counter() - t
+        wall = max_over_ranks(wall)
+        inter_e = se.interactions_attr + se.interactions_rep
+        e2e = {"value": inter_e / wall, "unit": "interactions/s",
+               "h2d_bytes_per_step": int((P.nbytes + X0.nbytes) / max(1, args.steps)),
+               "d2h_bytes_per_step": int(out.nbytes / max(1, args.steps)),
+               "h2d_bytes_total": int(P.nbytes + X0.nbytes), "d2h_bytes_total": int(out.nbytes),
+               "wall_s": wall, "api": "pcs_lop_run (C ABI) with host buffers" if world == 1
+               else "pcs_lop_plan_{create,set_comm,upload,run,download} with host buffers"}
+
+    # ---------------- CPU baseline (rank 0, N = 1 only) ----------------
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        Pb, Xb = P, X0
+        if precision == "fp32":
+            Pb = P.astype(np.float32).astype(np.float64)
+            Xb = X0.astype(np.float32).astype(np.float64)
+        try:
+            cbr = cpu_baseline(cfg, Pb, Xb, params, c)
+            cb = {k: cbr[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # pragma: no cover
+            cb = {"value": None, "unit": "interactions/s", "cores": os.cpu_count(),
+                  "kind": "unavailable", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": "neighbour interactions/sec (LOP sweep)",
+            "value": value, "unit": "interactions/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / max(1, args.steps),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32" if precision == "fp32" else "f64",
+            "data": "synthetic (seeded host generator, BASELINE.md §4)",
+            "config": {"workload": WORKLOADS[cfg], "sweeps_timed": args.steps,
+                       "sweeps_run": sweeps, "l2": "inputs larger than L2 (P = "
+                       f"{P.shape[0] * 16 / 1e6:.0f} MB fp32 on device > 126 MB)",
+                       "parallelism": f"dp{world}: P replicated, X sharded by cell-sorted ranges,"
+                                      " NCCL all-gather of X per sweep" if world > 1 else "1 GPU"},
+            "sweeps_per_s": args.steps / (ms / 1e3),
+            "interactions_per_sweep": inter / max(1, args.steps),
+            "kernel_ms_per_sweep": kernel_ms / max(1, args.steps),
+            "grid_ms_per_sweep": sort_ms / max(1, args.steps),
+            "careful_points": s.careful_points,
+            "roofline": roofline,
+            "cpu_baseline": cb,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -71,7 +71,7 @@ typedef struct pcs_lop_desc {
     int32_t density_weights;   /* 0 = LOP, 1 = WLOP (v_j on data, w_i per sweep) */
     int32_t precision;         /* pcs_precision */
     int32_t device;            /* CUDA ordinal; -1 = current device */
-    int32_t lanes_per_point;   /* fp32 kernel tuning: 0 = auto, else 1,2,4,8 */
+    int32_t lanes_per_point;   /* fp32 kernel tuning: 0 = auto, else 2, 4, 8 */
     int32_t reserved[7];
 } pcs_lop_desc;
 
@@ -91,6 +91,7 @@ typedef struct pcs_lop_summary {
     double sweeps_ms;            /* device time of all sweeps (CUDA events) */
     double kernel_ms;            /* device time of the fused per-point kernel, all sweeps */
     double sort_ms;              /* device time of the per-sweep grid rebuild, all sweeps */
+    uint64_t lane_candidates;    /* (point, candidate) evaluations of the fused kernel */
 } pcs_lop_summary;
 
 typedef struct pcs_lop_plan pcs_lop_plan;

@@ -138,6 +138,8 @@ def ref():
         lib.ref_generate_surface.argtypes = [C.c_int, C.c_uint64, C.c_uint64, _c_dbl_p]
         lib.ref_theta.argtypes = [C.c_double, C.c_double, C.c_double]
         lib.ref_theta.restype = C.c_double
+        lib.ref_index_build_ms.argtypes = [_c_dbl_p, C.c_uint64]
+        lib.ref_index_build_ms.restype = C.c_double
         lib.ref_last_error.restype = C.c_char_p
         _ref = lib
     return _ref
@@ -304,3 +306,8 @@ def ref_add_noise(xyz, sigma, seed):
     if rc:
         raise OracleError(rc)
     return a
+
+
+def ref_index_build_ms(P) -> float:
+    P = _xyz(P)
+    return float(ref().ref_index_build_ms(_ptr(P, _c_dbl_p), P.shape[0]))

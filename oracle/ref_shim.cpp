@@ -11,6 +11,7 @@
 //   pcs::SpatialIndex           proj/include/pcs/spatial.hpp:19-56
 //   pcs::add_noise              proj/include/pcs/noise.hpp
 //   pcs::generate_surface       proj/include/pcs/bench.hpp
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -152,6 +153,17 @@ int ref_generate_surface(int kind, std::uint64_t n, std::uint64_t seed, double* 
     } catch (const std::exception& e) {
         return code_of(e);
     }
+}
+
+// Wall time (ms) of the reference's one-time data index build
+// (SpatialIndex(data), proj/src/lop.cpp:24), so a timed lop_project sample can
+// report the sweep alone.
+double ref_index_build_ms(const double* P, std::uint64_t n) {
+    const auto cloud = to_cloud(P, n);
+    const auto t0 = std::chrono::steady_clock::now();
+    const pcs::SpatialIndex index(cloud);
+    const auto t1 = std::chrono::steady_clock::now();
+    return std::chrono::duration<double, std::milli>(t1 - t0).count() + 0.0 * index.size();
 }
 
 double ref_theta(double d, double h, double cutoff) {

@@ -11,7 +11,7 @@ import os
 import subprocess
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "lib", "libpcs_lop_b200.so")
+LIB_PATH = os.environ.get("PCS_LOP_LIB") or os.path.join(PKG_DIR, "lib", "libpcs_lop_b200.so")
 
 PCS_OK = 0
 PCS_ERR_INVALID_PARAM = 1
@@ -71,6 +71,7 @@ class LopSummaryC(C.Structure):
         ("sweeps_ms", C.c_double),
         ("kernel_ms", C.c_double),
         ("sort_ms", C.c_double),
+        ("lane_candidates", C.c_uint64),
     ]
 
 

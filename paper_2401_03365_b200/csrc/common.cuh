@@ -40,6 +40,7 @@ struct RunState {
     unsigned long long interactions_rep;
     unsigned long long density_pairs;
     unsigned long long careful_points;
+    unsigned long long lane_candidates;  // (query, buffered candidate) evaluations, fused kernel
     double last_max_disp;
 };
 

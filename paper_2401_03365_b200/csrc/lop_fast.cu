@@ -36,10 +36,16 @@ namespace pcsb {
 
 namespace {
 
+#ifndef PCSB_FAST_MINB
+#define PCSB_FAST_MINB 6
+#endif
 constexpr int FAST_WARPS = 4;
 constexpr int FAST_THREADS = FAST_WARPS * 32;
 constexpr int BUF = 256;     // staged candidates per warp (float4)
-constexpr int UNROLL = 4;
+constexpr int RING = 4;      // cp.async pipeline depth: 32-candidate chunks in flight per warp
+// Unrolled pairs per lane step: L*UNROLL = 16 pairs, so the bank swizzle of the
+// staging layout (bit 3 of the pair index) is a compile-time constant per step.
+template <int L> struct Unroll { static constexpr int value = 16 / L; };
 constexpr float kFar = 1.0e18f;
 
 struct Box {
@@ -128,6 +134,32 @@ __device__ __forceinline__ Group<L> load_group(uint32_t grp, uint32_t nq, const 
     return G;
 }
 
+// Staging layout (per warp, BUF candidates): PAIR-INTERLEAVED so that one lane
+// evaluates two candidates with packed fp32x2 instructions, and BANK-SWIZZLED so
+// that the scalar stores of 32 consecutive candidates hit 32 distinct banks:
+//   AX = float4[BUF/2]: pair j = (x0 x1 y0 y1), BZ = float4[BUF/2]: (z0 z1 w0 w1),
+//   with the two halves swapped when bit 3 of j is set.
+__device__ __forceinline__ int stage_word(int k, int comp) {
+    const int j = k >> 1;
+    return j * 4 + 2 * (comp ^ ((j >> 3) & 1)) + (k & 1);
+}
+
+__device__ __forceinline__ void stage_store(float4* buf, int k, const float4& c) {
+    float* ax = reinterpret_cast<float*>(buf);
+    float* bz = reinterpret_cast<float*>(buf + BUF / 2);
+    ax[stage_word(k, 0)] = c.x;
+    ax[stage_word(k, 1)] = c.y;
+    bz[stage_word(k, 0)] = c.z;
+    bz[stage_word(k, 1)] = c.w;
+}
+
+__device__ __forceinline__ float4 stage_load(const float4* buf, int k) {
+    const float* ax = reinterpret_cast<const float*>(buf);
+    const float* bz = reinterpret_cast<const float*>(buf + BUF / 2);
+    return make_float4(ax[stage_word(k, 0)], ax[stage_word(k, 1)], bz[stage_word(k, 0)],
+                       bz[stage_word(k, 1)]);
+}
+
 // Streams every candidate of the rows covered by `cr`, culls it against the
 // box and hands full buffers to `eval(count)`.  Warp-uniform control flow.
 // The next 32-candidate chunk of a row is loaded before the current one is
@@ -137,7 +169,7 @@ __device__ __forceinline__ void stream_candidates(const float4* __restrict__ src
                                                   const uint32_t* __restrict__ start,
                                                   const GridGeom& g, const CellRange& cr,
                                                   const Box& b, float scull2, float4* buf,
-                                                  int lane, Eval&& eval) {
+                                                  float4* /*ring*/, int lane, Eval&& eval) {
     const int ny = cr.hiy - cr.loy + 1;
     const int nrows = ny * (cr.hiz - cr.loz + 1);
     const unsigned lt = (1u << lane) - 1u;
@@ -167,7 +199,7 @@ __device__ __forceinline__ void stream_candidates(const float4* __restrict__ src
                 const float ez = fmaxf(fmaxf(b.mnz - c.z, c.z - b.mxz), 0.f);
                 const bool keep = fmaf(ez, ez, fmaf(ey, ey, ex * ex)) <= scull2;
                 const unsigned m = __ballot_sync(0xffffffffu, keep);
-                if (keep) buf[count + __popc(m & lt)] = c;
+                if (keep) stage_store(buf, count + __popc(m & lt), c);
                 count += __popc(m);
                 if (count > BUF - 32) {
                     __syncwarp();
@@ -186,125 +218,203 @@ __device__ __forceinline__ void stream_candidates(const float4* __restrict__ src
     }
 }
 
-// Pads the buffer to a multiple of L*UNROLL with far-away dummies.
-template <int L>
-__device__ __forceinline__ int pad_buffer(float4* buf, int count, int lane) {
-    constexpr int STEP = L * UNROLL;
-    const int padded = (count + STEP - 1) / STEP * STEP;
-    for (int i = count + lane; i < padded; i += 32) buf[i] = make_float4(kFar, kFar, kFar, 0.f);
-    __syncwarp();
-    return padded;
-}
+// ---------------------------------------------------------------------------
+// Evaluation of a staged buffer.  Candidates sit in PAIR-INTERLEAVED layout
+// (pair j = 32 bytes: x0 x1 y0 y1 | z0 z1 w0 w1) so that one lane evaluates two
+// candidates per iteration with packed fp32x2 instructions (FADD2/FMUL2/FFMA2:
+// half the issue slots of scalar FP32).  Per pair: 2 LDS.128, 3+3 packed ops
+// for d2, 1 FFMA2 for the exponent, 4 MUFU (2x EX2, 2x RSQ), 2 FSETP + 2 FSEL
+// for the hit mask, 1 FMUL2 and 4 packed accumulations.
+// ---------------------------------------------------------------------------
+enum : int { K_ATTR = 0, K_REP_INVCUBE = 1, K_REP_NEGLIN = 2, K_DENSITY = 3 };
 
-// Accumulators of one query (per lane partial sums).
 struct Acc {
-    float s, n, x, y, z;  // sum w, #hits, sum w*(c - q)
-    float nr;             // candidates with d2 <= r2 (incl. zero distance)
+    float2 s, x, y, z;  // sum w, sum w*(c - q), per candidate parity
+    float2 n2;          // hits, per candidate parity
+    float n, nr;        // hits (after reduction), candidates in range (incl. zero distance)
 };
 
-// The kernel of every pass: the in-range decision is made in fp32 on
-// arg = fma(d2, kneg, K0) >= 0.  `bmin` tracks min |arg| so that, once per
-// buffer, pairs inside the guard band can be re-decided exactly in fp64 (rare).
-template <int L, typename Weight>
-__device__ __forceinline__ void eval_buffer(const float4* buf, int padded, int sub,
-                                            const float4& q, float kneg, float K0,
-                                            bool count_range, Acc& A, float& bmin, Weight&& wfn) {
-    for (int k = sub; k < padded; k += L * UNROLL) {
+__device__ __forceinline__ Acc acc_zero() {
+    Acc A;
+    A.s = A.x = A.y = A.z = A.n2 = make_float2(0.f, 0.f);
+    A.n = A.nr = 0.f;
+    return A;
+}
+
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+struct EvalConsts {
+    float2 nqx, nqy, nqz;  // -q
+    float2 kneg, K0;
+    float support;
+};
+
+// Pads the buffer (count candidates) to a multiple of 32 (16 pairs) with far
+// dummies; returns the number of pairs.
+__device__ __forceinline__ int pad_pairs(float4* buf, int count, int lane) {
+    const int padded = (count + 31) & ~31;
+    if (count + lane < padded) stage_store(buf, count + lane, make_float4(kFar, kFar, kFar, 0.f));
+    __syncwarp();
+    return padded >> 1;
+}
+
+// weight of one candidate given its hit predicate (kind-specific); vectorised over a pair
+template <int KIND, bool kWlop, bool kZero>
+__device__ __forceinline__ float2 pair_weight(const float2& d2, const float2& arg, bool px, bool py,
+                                              const float4& B, const EvalConsts& ec) {
+    float2 w;
+    if (KIND == K_DENSITY) {
+        w = f2(px ? ex2_approx(arg.x) : 0.f, py ? ex2_approx(arg.y) : 0.f);
+        return w;
+    }
+    // kZero: zero-distance candidates are masked out, so keep their rsqrt finite
+    // (0 * inf would poison the sums); otherwise a zero distance is a hit whose
+    // infinite weight surfaces as a non-finite sum and defers the query
+    const float2 d2s = kZero ? f2(fmaxf(d2.x, 1e-37f), fmaxf(d2.y, 1e-37f)) : d2;
+    const float2 rs = f2(rsqrt_approx(d2s.x), rsqrt_approx(d2s.y));
+    if (KIND == K_REP_INVCUBE) {
+        // theta/d^5 scaled by s^5 = theta * (s/d)^5 (no fp32 overflow)
+        const float2 a2 = __fmul2_rn(d2, ec.kneg);
+        const float2 th = f2(px ? ex2_approx(a2.x) : 0.f, py ? ex2_approx(a2.y) : 0.f);
+        const float2 u = __fmul2_rn(rs, f2(ec.support, ec.support));
+        const float2 u2 = __fmul2_rn(u, u);
+        w = __fmul2_rn(__fmul2_rn(__fmul2_rn(th, u2), u2), u);
+    } else {
+        // alpha = theta/d (attraction) or beta = theta*1/d (eta = -r), theta scaled by 2^K0
+        const float2 th = f2(px ? ex2_approx(arg.x) : 0.f, py ? ex2_approx(arg.y) : 0.f);
+        w = __fmul2_rn(th, rs);
+    }
+    if (kWlop) w = __fmul2_rn(w, f2(B.z, B.w));  // 1/v_j (attraction) | w_i' (repulsion)
+    return w;
+}
+
+// kZero: exclude d2 == 0 from the hits (and count in-range candidates in nr).
+template <int L, int KIND, bool kWlop, bool kZero>
+__device__ __forceinline__ void eval_pairs(const float4* __restrict__ pb, int npairs, int sub,
+                                           const EvalConsts& ec, Acc& A, float& bmin) {
+    constexpr int U = Unroll<L>::value;
+    const float4* ax = pb;
+    const float4* bz = pb + BUF / 2;
+    for (int j0 = sub; j0 < npairs; j0 += L * U) {
 #pragma unroll
-        for (int u = 0; u < UNROLL; ++u) {
-            const float4 c = buf[k + u * L];
-            const float dx = c.x - q.x, dy = c.y - q.y, dz = c.z - q.z;
-            const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-            const float arg = fmaf(d2, kneg, K0);
-            bmin = fminf(bmin, fabsf(arg));
-            const float w = wfn(c, d2, arg);
-            if (arg >= 0.f) {
-                if (count_range) A.nr += 1.f;
-                if (!count_range || d2 > 0.f) {
-                    A.s += w;
-                    A.n += 1.f;
-                    A.x = fmaf(w, dx, A.x);
-                    A.y = fmaf(w, dy, A.y);
-                    A.z = fmaf(w, dz, A.z);
-                }
+        for (int u = 0; u < U; ++u) {
+            const int j = j0 + u * L;
+            // j0 = sub + 16 t with sub < L, so bit 3 of j is that of u*L: a constant
+            constexpr bool kSw = false;
+            const bool sw = kSw || (((u * L) >> 3) & 1);
+            const float4 Ar = ax[j], Br = bz[j];
+            const float4 Apos = sw ? make_float4(Ar.z, Ar.w, Ar.x, Ar.y) : Ar;
+            const float4 B = sw ? make_float4(Br.z, Br.w, Br.x, Br.y) : Br;
+            const float2 dx = __fadd2_rn(f2(Apos.x, Apos.y), ec.nqx);
+            const float2 dy = __fadd2_rn(f2(Apos.z, Apos.w), ec.nqy);
+            const float2 dz = __fadd2_rn(f2(B.x, B.y), ec.nqz);
+            float2 d2 = __fmul2_rn(dx, dx);
+            d2 = __ffma2_rn(dy, dy, d2);
+            d2 = __ffma2_rn(dz, dz, d2);
+            const float2 arg = __ffma2_rn(d2, ec.kneg, ec.K0);  // >= 0 <=> d2 <= r2 (fp32)
+            bmin = fminf(bmin, fminf(fabsf(arg.x), fabsf(arg.y)));
+            bool px = arg.x >= 0.f, py = arg.y >= 0.f;
+            if (kZero) {
+                A.nr += (px ? 1.f : 0.f) + (py ? 1.f : 0.f);
+                px = px && d2.x > 0.f;
+                py = py && d2.y > 0.f;
+            }
+            const float2 w = pair_weight<KIND, kWlop, kZero>(d2, arg, px, py, B, ec);
+            A.n2 = __fadd2_rn(A.n2, f2(px ? 1.f : 0.f, py ? 1.f : 0.f));
+            A.s = __fadd2_rn(A.s, w);
+            if (KIND != K_DENSITY) {
+                A.x = __ffma2_rn(w, dx, A.x);
+                A.y = __ffma2_rn(w, dy, A.y);
+                A.z = __ffma2_rn(w, dz, A.z);
             }
         }
     }
 }
 
-// Exact fp64 re-decision of the guard-band pairs of one buffer: a pair whose
-// fp32 decision differs from the reference predicate (d2 <= r*r in fp64,
-// proj/src/spatial.cpp:89,101) has its contribution added or removed.
-template <int L, typename Weight>
-__device__ __forceinline__ void fix_band(const float4* buf, int padded, int sub, const float4& q,
-                                         float kneg, float K0, float band, double r2,
-                                         bool count_range, Acc& A, Weight&& wfn) {
-    for (int k = sub; k < padded; k += L) {
-        const float4 c = buf[k];
-        const float dx = c.x - q.x, dy = c.y - q.y, dz = c.z - q.z;
+// Exact fp64 re-decision of the guard-band pairs of one buffer: a candidate
+// whose fp32 decision differs from the reference predicate (d2 <= r*r in fp64,
+// proj/src/spatial.cpp:89,101) has its contribution added or removed.  The
+// weights are recomputed with the very same fp32 operations as eval_pairs.
+template <int L, int KIND, bool kWlop, bool kZero>
+__device__ __forceinline__ void fix_band(const float4* buf, int npairs, int sub, const float4& q,
+                                         const EvalConsts& ec, float band, double r2, Acc& A) {
+    // candidate k sits in pair k/2, evaluated by lane sub == (k/2) % L
+    for (int j = sub; j < npairs; j += L)
+        for (int h = 0; h < 2; ++h) {
+        const float4 cc = stage_load(buf, 2 * j + h);
+        const float cx = cc.x, cy = cc.y, cz = cc.z, cw = cc.w;
+        const float dx = cx - q.x, dy = cy - q.y, dz = cz - q.z;
         const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-        const float arg = fmaf(d2, kneg, K0);
+        const float arg = fmaf(d2, ec.kneg.x, ec.K0.x);
         if (!(fabsf(arg) <= band)) continue;
-        const bool exact = exact_d2(c.x, c.y, c.z, q.x, q.y, q.z) <= r2;
+        const bool exact = exact_d2(cx, cy, cz, q.x, q.y, q.z) <= r2;
         const bool fp32 = arg >= 0.f;
         if (exact == fp32) continue;
+        // (the accumulators are per candidate parity h; any slot of the lane works)
         const float sgn = exact ? 1.f : -1.f;
-        const float w = wfn(c, d2, arg) * sgn;
-        if (count_range) A.nr += sgn;
-        if (!count_range || d2 > 0.f) {
-            A.s += w;
-            A.n += sgn;
-            A.x = fmaf(w, dx, A.x);
-            A.y = fmaf(w, dy, A.y);
-            A.z = fmaf(w, dz, A.z);
+        const float4 B = make_float4(cz, cz, cw, cw);
+        const float2 w2 = pair_weight<KIND, kWlop, kZero>(f2(d2, d2), f2(arg, arg), true, true, B, ec);
+        if (kZero) A.nr += sgn;
+        if (!kZero || d2 > 0.f) {
+            const float w = w2.x * sgn;
+            A.n2.x += sgn;
+            A.s.x += w;
+            if (KIND != K_DENSITY) {
+                A.x.x = fmaf(w, dx, A.x.x);
+                A.y.x = fmaf(w, dy, A.y.x);
+                A.z.x = fmaf(w, dz, A.z.x);
+            }
         }
-    }
+        }
+}
+
+// One buffer: pad, evaluate, re-decide the band if any lane saw a band pair.
+template <int L, int KIND, bool kWlop, bool kZero>
+__device__ __forceinline__ int eval_buffer(float4* buf, int count, int lane, int sub,
+                                           const float4& q, const EvalConsts& ec, float band,
+                                           double r2, Acc& A) {
+    const int npairs = pad_pairs(buf, count, lane);
+    float bmin = INFINITY;
+    eval_pairs<L, KIND, kWlop, kZero>(buf, npairs, sub, ec, A, bmin);
+    if (__any_sync(0xffffffffu, bmin <= band))
+        fix_band<L, KIND, kWlop, kZero>(buf, npairs, sub, q, ec, band, r2, A);
+    return 2 * npairs;
 }
 
 template <int L>
 __device__ __forceinline__ void group_reduce(Acc& A, bool with_nr) {
-    A.s = group_sum<L>(A.s);
-    A.n = group_sum<L>(A.n);
-    A.x = group_sum<L>(A.x);
-    A.y = group_sum<L>(A.y);
-    A.z = group_sum<L>(A.z);
+    A.s.x = group_sum<L>(A.s.x + A.s.y);
+    A.x.x = group_sum<L>(A.x.x + A.x.y);
+    A.y.x = group_sum<L>(A.y.x + A.y.y);
+    A.z.x = group_sum<L>(A.z.x + A.z.y);
+    A.n = group_sum<L>(A.n2.x + A.n2.y);
     if (with_nr) A.nr = group_sum<L>(A.nr);
 }
 
+__device__ __forceinline__ EvalConsts make_consts(const float4& q, float kneg, float K0,
+                                                  float support) {
+    EvalConsts ec;
+    ec.nqx = f2(-q.x, -q.x);
+    ec.nqy = f2(-q.y, -q.y);
+    ec.nqz = f2(-q.z, -q.z);
+    ec.kneg = f2(kneg, kneg);
+    ec.K0 = f2(K0, K0);
+    ec.support = support;
+    return ec;
+}
+
 template <int L, bool kWlop, bool kCheckZero, int kRep>
-__global__ void __launch_bounds__(FAST_THREADS)
+__global__ void __launch_bounds__(FAST_THREADS, PCSB_FAST_MINB)
 fast_kernel(const FastArgs a) {
     constexpr int Q = 32 / L;
-    __shared__ float4 smem[FAST_WARPS * BUF];
+    constexpr int KREP = kRep == 1 ? K_REP_INVCUBE : K_REP_NEGLIN;
+    __shared__ float4 smem[FAST_WARPS * (BUF + RING * 32)];
     if (*a.done) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float4* buf = smem + warp * BUF;
+    float4* buf = smem + warp * (BUF + RING * 32);
+    float4* ring = buf + BUF;
     const int sub = lane % L;
     const uint32_t ngroups = (a.nq + Q - 1) / Q;
-    const float kneg = a.kneg, K0 = a.K0;
-
-    // alpha = theta/d (scaled by 2^K0), x (1/v_j) for WLOP     (lop.cpp:62)
-    auto w_attr = [&](const float4& c, float d2, float arg) {
-        float w = ex2_approx(arg) * rsqrt_approx(d2);
-        if (kWlop) w *= c.w;
-        return w;
-    };
-    // beta = theta |eta'| / d, x w_i' for WLOP                   (lop.cpp:90-91)
-    auto w_rep = [&](const float4& c, float d2, float arg) {
-        const float rs = rsqrt_approx(d2);
-        float w;
-        if (kRep == 1) {
-            // theta/d^5, scaled by s^5: theta * (s/d)^5 (no fp32 overflow)
-            const float th = ex2_approx(d2 * kneg);
-            const float u1 = rs * a.support;
-            const float u2 = u1 * u1;
-            w = th * u2 * u2 * u1;
-        } else {
-            w = ex2_approx(arg) * rs;  // theta/d, scaled by 2^K0
-        }
-        if (kWlop) w *= c.w;
-        return w;
-    };
 
     for (;;) {
         uint32_t grp = 0;
@@ -313,31 +423,27 @@ fast_kernel(const FastArgs a) {
         if (grp >= ngroups) break;
         const Group<L> G = load_group<L>(grp, a.nq, a.qlist, a.Xs, a.Xskeys, a.g, lane);
         const float4 q = G.q;
+        const EvalConsts ec = make_consts(q, a.kneg, a.K0, a.support);
 
         for (int sg = 0; sg < G.nseg; ++sg) {
             const bool member = G.qvalid && G.seg == sg;
             const Box box = member_box(q, member);
             const CellRange cr = cell_range(a.g, box, a.s_pad);
 
-            // ---------------- attraction: data candidates ----------------
-            Acc at{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            stream_candidates(a.P, a.Pstart, a.g, cr, box, a.scull2, buf, lane, [&](int count) {
-                const int padded = pad_buffer<L>(buf, count, lane);
-                float bmin = INFINITY;
-                eval_buffer<L>(buf, padded, sub, q, kneg, K0, kCheckZero, at, bmin, w_attr);
-                if (__any_sync(0xffffffffu, bmin <= a.band))
-                    fix_band<L>(buf, padded, sub, q, kneg, K0, a.band, a.r2, kCheckZero, at, w_attr);
+            // ---------------- attraction: data candidates (lop.cpp:49-65) ----------------
+            Acc at = acc_zero();
+            uint32_t evals = 0;  // buffered candidates evaluated by this segment (x Q queries)
+            stream_candidates(a.P, a.Pstart, a.g, cr, box, a.scull2, buf, ring, lane, [&](int count) {
+                evals += eval_buffer<L, K_ATTR, kWlop, kCheckZero>(buf, count, lane, sub, q, ec,
+                                                                   a.band, a.r2, at);
             });
 
-            // ---------------- repulsion: projected-set candidates ----------------
-            Acc rp{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            // ---------------- repulsion: projected-set candidates (lop.cpp:79-97) ----------------
+            Acc rp = acc_zero();
             if (kRep != 0) {
-                stream_candidates(a.Xs, a.Xstart, a.g, cr, box, a.scull2, buf, lane, [&](int count) {
-                    const int padded = pad_buffer<L>(buf, count, lane);
-                    float bmin = INFINITY;
-                    eval_buffer<L>(buf, padded, sub, q, kneg, K0, true, rp, bmin, w_rep);
-                    if (__any_sync(0xffffffffu, bmin <= a.band))
-                        fix_band<L>(buf, padded, sub, q, kneg, K0, a.band, a.r2, true, rp, w_rep);
+                stream_candidates(a.Xs, a.Xstart, a.g, cr, box, a.scull2, buf, ring, lane, [&](int count) {
+                    evals += eval_buffer<L, KREP, kWlop, true>(buf, count, lane, sub, q, ec, a.band,
+                                                               a.r2, rp);
                 });
             }
 
@@ -350,20 +456,22 @@ fast_kernel(const FastArgs a) {
             unsigned long long n_attr = 0, n_rep = 0;
             if (member && sub == 0) {
                 const uint32_t qi_int = __ldg(&a.Xs_idx[G.qslot]);
-                bool bad = !isfinite(at.s) || !isfinite(at.x) || !isfinite(at.y) || !isfinite(at.z);
+                const float sa = at.s.x;
+                bool bad = !isfinite(sa) || !isfinite(at.x.x) || !isfinite(at.y.x) ||
+                           !isfinite(at.z.x);
                 const float zeros = kCheckZero ? (at.nr - at.n) : 0.f;
                 if (kCheckZero && zeros > 0.f) {
                     // an fp32 d2 of 0 could hide a distinct pair only for tiny coordinates
-                    const float tiny = 0x1p-50f;
+                    const float tiny = 0x1p-40f;
                     if (fabsf(q.x) < tiny || fabsf(q.y) < tiny || fabsf(q.z) < tiny) bad = true;
                 }
-                const bool attracted = at.s > 0.f;
+                const bool attracted = sa > 0.f;
                 if (kRep != 0 && attracted) {
                     // exactly one zero-distance candidate must remain: the query itself;
                     // any other is a coincident pair, counted by the exact path
                     const float z = rp.nr - rp.n;
-                    bad = bad || !isfinite(rp.s) || !isfinite(rp.x) || !isfinite(rp.y) ||
-                          !isfinite(rp.z) || z > 1.5f || z < 0.5f;
+                    bad = bad || !isfinite(rp.s.x) || !isfinite(rp.x.x) || !isfinite(rp.y.x) ||
+                          !isfinite(rp.z.x) || z > 1.5f || z < 0.5f;
                 }
                 if (bad) {
                     const uint32_t pos = atomicAdd(&a.slot->careful_count, 1u);
@@ -376,18 +484,18 @@ fast_kernel(const FastArgs a) {
                         // (lop.cpp:67-69); otherwise isolated and held (lop.cpp:70-73)
                         isolated = !(kCheckZero && zeros > 0.f);
                     } else {
-                        const float inv = 1.0f / at.s;  // Weiszfeld quotient (lop.cpp:77)
-                        nx = q.x + at.x * inv;
-                        ny = q.y + at.y * inv;
-                        nz = q.z + at.z * inv;
+                        const float inv = 1.0f / sa;  // Weiszfeld quotient (lop.cpp:77)
+                        nx = q.x + at.x.x * inv;
+                        ny = q.y + at.y.x * inv;
+                        nz = q.z + at.z.x * inv;
                         n_attr = (unsigned long long)at.n;
                         if (kRep != 0) {
                             n_rep = (unsigned long long)rp.n;
-                            if (rp.s > 0.f) {  // lop.cpp:95-96, x - x' = -(c - q)
-                                const float f = a.mu / rp.s;
-                                nx = fmaf(-f, rp.x, nx);
-                                ny = fmaf(-f, rp.y, ny);
-                                nz = fmaf(-f, rp.z, nz);
+                            if (rp.s.x > 0.f) {  // lop.cpp:95-96, x - x' = -(c - q)
+                                const float f = a.mu / rp.s.x;
+                                nx = fmaf(-f, rp.x.x, nx);
+                                ny = fmaf(-f, rp.y.x, ny);
+                                nz = fmaf(-f, rp.z.x, nz);
                             }
                         }
                     }
@@ -412,6 +520,7 @@ fast_kernel(const FastArgs a) {
                 if (md > 0.f) atomic_max_nonneg_double(&a.slot->max_disp_bits, (double)md);
                 if (n_attr) atomicAdd(&a.st->interactions_attr, n_attr);
                 if (n_rep) atomicAdd(&a.st->interactions_rep, n_rep);
+                atomicAdd(&a.st->lane_candidates, (unsigned long long)evals * Q);
             }
         }
     }
@@ -425,14 +534,14 @@ constexpr int DL = 4;  // lanes per point
 
 __global__ void __launch_bounds__(FAST_THREADS)
 density_kernel(const DensityArgs a) {
-    __shared__ float4 smem[FAST_WARPS * BUF];
+    __shared__ float4 smem[FAST_WARPS * (BUF + RING * 32)];
     constexpr int Q = 32 / DL;
     if (a.done && *a.done) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float4* buf = smem + warp * BUF;
+    float4* buf = smem + warp * (BUF + RING * 32);
+    float4* ring = buf + BUF;
     const int sub = lane % DL;
     const uint32_t ngroups = (a.nq + Q - 1) / Q;
-    auto w_theta = [&](const float4&, float, float arg) { return ex2_approx(arg); };
     for (;;) {
         uint32_t grp = 0;
         if (lane == 0) grp = atomicAdd(a.counter, 1u);
@@ -440,25 +549,22 @@ density_kernel(const DensityArgs a) {
         if (grp >= ngroups) break;
         const Group<DL> G = load_group<DL>(grp, a.nq, a.qlist, a.C, a.Cskeys, a.g, lane);
         const float4 q = G.q;
+        const EvalConsts ec = make_consts(q, a.kneg, a.K0, 0.f);
         for (int sg = 0; sg < G.nseg; ++sg) {
             const bool member = G.qvalid && G.seg == sg;
             const Box box = member_box(q, member);
             const CellRange cr = cell_range(a.g, box, a.s_pad);
-            Acc A{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            stream_candidates(a.C, a.Cstart, a.g, cr, box, a.scull2, buf, lane, [&](int count) {
-                const int padded = pad_buffer<DL>(buf, count, lane);
-                float bmin = INFINITY;
-                eval_buffer<DL>(buf, padded, sub, q, a.kneg, a.K0, true, A, bmin, w_theta);
-                if (__any_sync(0xffffffffu, bmin <= a.band))
-                    fix_band<DL>(buf, padded, sub, q, a.kneg, a.K0, a.band, a.r2, true, A, w_theta);
+            Acc A = acc_zero();
+            stream_candidates(a.C, a.Cstart, a.g, cr, box, a.scull2, buf, ring, lane, [&](int count) {
+                eval_buffer<DL, K_DENSITY, false, true>(buf, count, lane, sub, q, ec, a.band, a.r2, A);
             });
-            A.s = group_sum<DL>(A.s);
-            A.n = group_sum<DL>(A.n);
+            A.s.x = group_sum<DL>(A.s.x + A.s.y);
+            A.n = group_sum<DL>(A.n2.x + A.n2.y);
             A.nr = group_sum<DL>(A.nr);
             unsigned long long pairs = 0;
             if (member && sub == 0) {
                 // theta(0) = 1 for coincident duplicates; minus one for the point itself
-                const float dens = 1.0f + A.s * a.inv_scale + (A.nr - A.n - 1.0f);
+                const float dens = 1.0f + A.s.x * a.inv_scale + (A.nr - A.n - 1.0f);
                 const float val = a.invert ? 1.0f / dens : dens;
                 if (a.out_sorted) a.out_sorted[G.qslot].w = val;
                 else a.out_internal[__ldg(&a.idx[G.qslot])].w = val;
@@ -501,7 +607,6 @@ void launch_l(const FastArgs& a, bool wlop, bool cz, int rep, int grid, cudaStre
 void launch_fast(const FastArgs& a, int lanes_per_point, bool wlop, bool check_zero, int rep_mode,
                  int grid_blocks, cudaStream_t s) {
     switch (lanes_per_point) {
-        case 1: return launch_l<1>(a, wlop, check_zero, rep_mode, grid_blocks, s);
         case 2: return launch_l<2>(a, wlop, check_zero, rep_mode, grid_blocks, s);
         case 8: return launch_l<8>(a, wlop, check_zero, rep_mode, grid_blocks, s);
         default: return launch_l<4>(a, wlop, check_zero, rep_mode, grid_blocks, s);

@@ -120,9 +120,9 @@ void validate_desc(const pcs_lop_desc& d) {
         throw Failure(PCS_ERR_INVALID_PARAM, "eta_kind must be PCS_ETA_INV_CUBE or PCS_ETA_NEG_LINEAR");
     if (d.precision != PCS_PREC_FP64 && d.precision != PCS_PREC_FP32)
         throw Failure(PCS_ERR_INVALID_PARAM, "precision must be PCS_PREC_FP64 or PCS_PREC_FP32");
-    if (d.lanes_per_point != 0 && d.lanes_per_point != 1 && d.lanes_per_point != 2 &&
-        d.lanes_per_point != 4 && d.lanes_per_point != 8)
-        throw Failure(PCS_ERR_INVALID_PARAM, "lanes_per_point must be 0, 1, 2, 4 or 8");
+    if (d.lanes_per_point != 0 && d.lanes_per_point != 2 && d.lanes_per_point != 4 &&
+        d.lanes_per_point != 8)
+        throw Failure(PCS_ERR_INVALID_PARAM, "lanes_per_point must be 0, 2, 4 or 8");
     const double s = d.h * d.cutoff_multiple;
     if (!std::isfinite(s)) throw Failure(PCS_ERR_INVALID_PARAM, "support h*cutoff_multiple must be finite");
     if (d.precision == PCS_PREC_FP32) {
@@ -665,11 +665,12 @@ void Plan::download(double* X_out, pcs_lop_summary* s, uint32_t* iso, uint64_t c
     if (multi) {
         // per-rank counters -> job totals
         unsigned long long* tmp = nullptr;
-        PCSB_CUDA(cudaMalloc(&tmp, 6 * sizeof(unsigned long long)));
-        unsigned long long hv[6] = {hs.isolated_events, hs.coincident_pairs, hs.interactions_attr,
-                                    hs.interactions_rep, hs.density_pairs, hs.careful_points};
+        PCSB_CUDA(cudaMalloc(&tmp, 7 * sizeof(unsigned long long)));
+        unsigned long long hv[7] = {hs.isolated_events, hs.coincident_pairs, hs.interactions_attr,
+                                    hs.interactions_rep, hs.density_pairs, hs.careful_points,
+                                    hs.lane_candidates};
         PCSB_CUDA(cudaMemcpy(tmp, hv, sizeof(hv), cudaMemcpyHostToDevice));
-        nccl_check(nccl().AllReduce(tmp, tmp, 6, ncclUint64, ncclSum, (ncclComm_t)comm_, stream_),
+        nccl_check(nccl().AllReduce(tmp, tmp, 7, ncclUint64, ncclSum, (ncclComm_t)comm_, stream_),
                    "ncclAllReduce");
         PCSB_CUDA(cudaMemcpyAsync(hv, tmp, sizeof(hv), cudaMemcpyDeviceToHost, stream_));
         PCSB_CUDA(cudaStreamSynchronize(stream_));
@@ -680,6 +681,7 @@ void Plan::download(double* X_out, pcs_lop_summary* s, uint32_t* iso, uint64_t c
         hs.interactions_rep = hv[3];
         hs.density_pairs = hv[4] + setup_density_pairs_;
         hs.careful_points = hv[5];
+        hs.lane_candidates = hv[6];
     } else {
         hs.density_pairs += setup_density_pairs_;
     }
@@ -721,6 +723,7 @@ void Plan::download(double* X_out, pcs_lop_summary* s, uint32_t* iso, uint64_t c
         s->interactions_rep = hs.interactions_rep;
         s->density_pairs = hs.density_pairs;
         s->careful_points = hs.careful_points;
+        s->lane_candidates = hs.lane_candidates;
         s->last_max_disp = hs.last_max_disp;
         s->setup_ms = setup_ms_;
         s->sweeps_ms = sweeps_ms_;

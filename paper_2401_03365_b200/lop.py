@@ -103,6 +103,7 @@ class LopSummary:
     sweeps_ms: float = 0.0
     kernel_ms: float = 0.0
     sort_ms: float = 0.0
+    lane_candidates: int = 0
 
 
 ETA = {"inv_cube": L.PCS_ETA_INV_CUBE, "neg_linear": L.PCS_ETA_NEG_LINEAR}
@@ -149,7 +150,8 @@ def _summary(s: L.LopSummaryC, iso: np.ndarray) -> LopSummary:
         interactions_attr=int(s.interactions_attr), interactions_rep=int(s.interactions_rep),
         density_pairs=int(s.density_pairs), careful_points=int(s.careful_points),
         last_max_disp=float(s.last_max_disp), setup_ms=float(s.setup_ms),
-        sweeps_ms=float(s.sweeps_ms), kernel_ms=float(s.kernel_ms), sort_ms=float(s.sort_ms))
+        sweeps_ms=float(s.sweeps_ms), kernel_ms=float(s.kernel_ms), sort_ms=float(s.sort_ms),
+        lane_candidates=int(s.lane_candidates))
 
 
 def lop_project(data, initial, params: LopParams, *, eta: str = "inv_cube",

@@ -29,5 +29,5 @@ for L in args.lanes:
     print(f"cfg{args.config} L={L} upload {up:.2f}s  {args.sweeps} sweeps {ms:.2f} ms -> "
           f"{inter / (ms / 1e3):.3e} int/s {args.sweeps / (ms / 1e3):.1f} sweeps/s kernel_ms "
           f"{s.kernel_ms:.2f} sort_ms {s.sort_ms:.2f} careful {s.careful_points} "
-          f"int/sweep {inter / args.sweeps:.3e} dens {s.density_pairs}", flush=True)
+          f"int/sweep {inter / args.sweeps:.3e} dens {s.density_pairs} lc/int {s.lane_candidates / max(1, inter):.3f}", flush=True)
     plan.close()
