@@ -157,6 +157,14 @@ pcs_status pcs_density_weights(const pcs_lop_desc* d, const double* C_xyz, uint6
 pcs_status pcs_grid_sort(const pcs_lop_desc* d, const double* C_xyz, uint64_t n, double support,
                          uint32_t* keys_out, uint32_t* order_out);
 
+/* Multi-GPU ownership layout (host only, no device needed): shard r owns the
+ * r-th contiguous range of `sorted_order` (the initial grid order of X0) and
+ * occupies internal slots [r*chunk, r*chunk + counts[r]).  orig_of_internal
+ * has nranks*chunk entries (0xFFFFFFFF for padding), internal_of_orig m. */
+pcs_status pcs_shard_layout(const uint32_t* sorted_order, uint64_t m, int32_t nranks,
+                            uint32_t* orig_of_internal, uint32_t* internal_of_orig,
+                            uint32_t* chunk, uint32_t* counts);
+
 /* ---- host generators (proj/include/pcs/rng.hpp, proj/src/bench.cpp:40-87) -- */
 /* kind: 0 plane, 1 sphere, 2 torus(R=1,r=0.35), 3 gaussian bump */
 pcs_status pcs_generate_surface(int32_t kind, uint64_t n, uint64_t seed, double* xyz);

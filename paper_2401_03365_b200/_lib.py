@@ -34,7 +34,7 @@ EXPORTED = [
     "pcs_nccl_unique_id", "pcs_lop_plan_set_comm", "pcs_lop_plan_reset", "pcs_lop_plan_run",
     "pcs_lop_plan_synchronize", "pcs_lop_plan_last_run_ms", "pcs_lop_plan_download",
     "pcs_lop_plan_launches", "pcs_radius_query_all", "pcs_density_weights", "pcs_grid_sort", "pcs_generate_surface",
-    "pcs_add_noise", "pcs_config_sizes", "pcs_generate_config",
+    "pcs_add_noise", "pcs_config_sizes", "pcs_generate_config", "pcs_shard_layout",
 ]
 
 
@@ -125,6 +125,7 @@ def lib():
         L.pcs_add_noise.argtypes = [_dp, C.c_uint64, C.c_double, C.c_uint64]
         L.pcs_config_sizes.argtypes = [C.c_int32, C.c_double, _u64p, _u64p]
         L.pcs_generate_config.argtypes = [C.c_int32, C.c_double, _dp, _dp]
+        L.pcs_shard_layout.argtypes = [_u32p, C.c_uint64, C.c_int32, _u32p, _u32p, _u32p, _u32p]
         for name in EXPORTED:
             fn = getattr(L, name)
             if fn.restype is C.c_int:  # default restype -> pcs_status

@@ -353,19 +353,13 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
                                       cudaMemcpyDeviceToHost, stream_));
             PCSB_CUDA(cudaStreamSynchronize(stream_));
         }
-        std::vector<uint32_t> ooi(mpad_, 0xFFFFFFFFu), ioo(m);
-        for (int r = 0; r < nranks_; ++r) {
-            const uint64_t lo_p = (uint64_t)m * r / nranks_, hi_p = (uint64_t)m * (r + 1) / nranks_;
-            if (r == rank_) {
-                own_lo_ = (uint32_t)r * chunk_;
-                own_cnt_ = (uint32_t)(hi_p - lo_p);
-            }
-            for (uint64_t p = lo_p; p < hi_p; ++p) {
-                const uint32_t slot = (uint32_t)r * chunk_ + (uint32_t)(p - lo_p);
-                ooi[slot] = sidx[p];
-                ioo[sidx[p]] = slot;
-            }
-        }
+        std::vector<uint32_t> ooi(mpad_), ioo(m ? m : 1), counts(nranks_);
+        uint32_t chunk = 0;
+        if (pcs_shard_layout(sidx.data(), m, nranks_, ooi.data(), ioo.data(), &chunk,
+                             counts.data()) != PCS_OK || chunk != chunk_)
+            throw Failure(PCS_ERR_NUMERICAL, "shard layout failed");
+        own_lo_ = (uint32_t)rank_ * chunk_;
+        own_cnt_ = counts[rank_];
         orig_of_internal_ = (uint32_t*)dalloc((size_t)mpad_ * sizeof(uint32_t));
         uint32_t* iof = nullptr;
         PCSB_CUDA(cudaMalloc(&iof, (m ? m : 1) * sizeof(uint32_t)));

@@ -280,6 +280,22 @@ def grid_sort(cloud, support: float, precision: str = "fp64", device: int = -1):
     return keys[:n], order[:n]
 
 
+def shard_layout(sorted_order, nranks: int):
+    """Multi-GPU ownership layout (pcs_shard_layout): returns (chunk, counts,
+    orig_of_internal[nranks*chunk], internal_of_orig[m])."""
+    so = np.ascontiguousarray(np.asarray(sorted_order, dtype=np.uint32))
+    m = so.size
+    chunk = C.c_uint32()
+    counts = np.zeros(nranks, dtype=np.uint32)
+    cap = max(1, (m + nranks - 1) // nranks * nranks)
+    ooi = np.zeros(cap, dtype=np.uint32)
+    ioo = np.zeros(max(m, 1), dtype=np.uint32)
+    _check(L.lib().pcs_shard_layout(_ptr(so, L._u32p), m, nranks, ooi.ctypes.data_as(L._u32p),
+                                    ioo.ctypes.data_as(L._u32p), C.byref(chunk),
+                                    counts.ctypes.data_as(L._u32p)))
+    return chunk.value, counts, ooi[: chunk.value * nranks], ioo[:m]
+
+
 # ---- host generators (rng.hpp / bench.cpp / noise.cpp semantics) ------------------
 SURFACE = {"plane": 0, "sphere": 1, "torus": 2, "bump": 3}
 
