@@ -15,7 +15,6 @@ constexpr int RS_THREADS = 256;
 constexpr int RS_ITEMS = 8;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
 constexpr int RS_WARPS = RS_THREADS / 32;
-constexpr int RS_SCAN_THREADS = 1024;
 
 __device__ __forceinline__ unsigned long long double_to_ordered(double v) {
     const unsigned long long b = (unsigned long long)__double_as_longlong(v);
@@ -108,31 +107,68 @@ rs_hist_kernel(const uint32_t* __restrict__ keys, uint32_t n, int shift, uint32_
     }
 }
 
-// Exclusive scan of `total` entries in one block (digit-major block histograms).
-__global__ void __launch_bounds__(RS_SCAN_THREADS)
-rs_scan_kernel(uint32_t* __restrict__ a, uint32_t total, const uint32_t* done) {
-    if (done && *done) return;
-    __shared__ uint32_t part[RS_SCAN_THREADS];
-    const uint32_t chunk = (total + RS_SCAN_THREADS - 1) / RS_SCAN_THREADS;
-    const uint32_t b = threadIdx.x * chunk;
-    const uint32_t e = min(b + chunk, total);
-    uint32_t s = 0;
-    for (uint32_t i = b; i < e; ++i) s += a[i];
-    part[threadIdx.x] = s;
-    __syncthreads();
-    // Hillis-Steele inclusive scan over the per-thread sums
-    for (int o = 1; o < RS_SCAN_THREADS; o <<= 1) {
-        const uint32_t v = threadIdx.x >= (unsigned)o ? part[threadIdx.x - o] : 0u;
-        __syncthreads();
-        part[threadIdx.x] += v;
-        __syncthreads();
+// Exclusive scan of the digit-major block histograms, one block per digit row
+// (row d = the counts of digit d in every tile); the row totals land in
+// `totals` and are scanned by rs_scan_totals_kernel.
+constexpr int RS_ROW_THREADS = 256;
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* sh, uint32_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
     }
-    uint32_t run = threadIdx.x ? part[threadIdx.x - 1] : 0u;
+    if (lane == 31) sh[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0u;
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += t;
+        }
+        if (lane < (int)(blockDim.x >> 5)) sh[lane] = wi - w;
+        if (lane == 31) sh[32] = wi;
+    }
+    __syncthreads();
+    const uint32_t r = sh[warp] + incl - v;
+    if (total) *total = sh[32];
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(RS_ROW_THREADS)
+rs_scan_rows_kernel(uint32_t* __restrict__ a, uint32_t nblocks, uint32_t* __restrict__ totals,
+                    const uint32_t* done) {
+    if (done && *done) return;
+    __shared__ uint32_t sh[33];
+    uint32_t* row = a + (size_t)blockIdx.x * nblocks;
+    const uint32_t chunk = (nblocks + RS_ROW_THREADS - 1) / RS_ROW_THREADS;
+    const uint32_t b = threadIdx.x * chunk;
+    const uint32_t e = min(b + chunk, nblocks);
+    uint32_t s = 0;
+    for (uint32_t i = b; i < e; ++i) s += row[i];
+    uint32_t tot = 0;
+    uint32_t run = block_exclusive_scan(s, sh, &tot);
     for (uint32_t i = b; i < e; ++i) {
-        const uint32_t v = a[i];
-        a[i] = run;
+        const uint32_t v = row[i];
+        row[i] = run;
         run += v;
     }
+    if (threadIdx.x == 0) totals[blockIdx.x] = tot;
+}
+
+// Exclusive scan of the 256 digit totals -> digit bases (in place).
+__global__ void __launch_bounds__(256) rs_scan_totals_kernel(uint32_t* __restrict__ totals,
+                                                            const uint32_t* done) {
+    if (done && *done) return;
+    __shared__ uint32_t sh[33];
+    const uint32_t v = totals[threadIdx.x];
+    const uint32_t ex = block_exclusive_scan(v, sh, nullptr);
+    totals[threadIdx.x] = ex;
 }
 
 // Stable scatter: within a tile elements keep their order (round-major,
@@ -141,14 +177,14 @@ __global__ void __launch_bounds__(RS_THREADS)
 rs_scatter_kernel(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                   uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, uint32_t n, int shift,
                   uint32_t mask, const uint32_t* __restrict__ blockoff, uint32_t nblocks,
-                  const uint32_t* done) {
+                  const uint32_t* __restrict__ digit_base, const uint32_t* done) {
     if (done && *done) return;
     __shared__ uint32_t run[256];
     __shared__ uint32_t wcnt[RS_WARPS][256];
     __shared__ uint32_t woff[RS_WARPS][256];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int d = threadIdx.x; d < 256; d += RS_THREADS) {
-        run[d] = blockoff[(size_t)d * nblocks + blockIdx.x];
+        run[d] = digit_base[d] + blockoff[(size_t)d * nblocks + blockIdx.x];
 #pragma unroll
         for (int w = 0; w < RS_WARPS; ++w) wcnt[w][d] = 0;
     }
@@ -270,7 +306,7 @@ void launch_keys(const GridGeom& g, const typename Vec4<T>::type* pts, uint32_t 
 
 size_t radix_blockhist_entries(uint32_t n) {
     const size_t nb = (n + RS_TILE - 1) / RS_TILE;
-    return 256 * (nb ? nb : 1);
+    return 256 * (nb ? nb : 1) + 256;  // + the digit totals / bases
 }
 
 int radix_sort(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
@@ -294,10 +330,12 @@ int radix_sort(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_
         uint32_t* vo = to_out ? vals_out : scr.vals_alt;
         rs_hist_kernel<<<nblocks, RS_THREADS, 0, s>>>(kin, n, shift, mask, scr.blockhist, nblocks,
                                                       done);
-        rs_scan_kernel<<<1, RS_SCAN_THREADS, 0, s>>>(scr.blockhist, 256 * nblocks, done);
+        uint32_t* totals = scr.blockhist + 256 * (size_t)nblocks;
+        rs_scan_rows_kernel<<<256, RS_ROW_THREADS, 0, s>>>(scr.blockhist, nblocks, totals, done);
+        rs_scan_totals_kernel<<<1, 256, 0, s>>>(totals, done);
         rs_scatter_kernel<<<nblocks, RS_THREADS, 0, s>>>(kin, vin, ko, vo, n, shift, mask,
-                                                         scr.blockhist, nblocks, done);
-        launches += 3;
+                                                         scr.blockhist, nblocks, totals, done);
+        launches += 4;
         kin = ko;
         vin = vo;
         (void)last;
