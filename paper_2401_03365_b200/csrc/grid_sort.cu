@@ -2,7 +2,10 @@
 // radix sort of (key, index), the gather into sorted order and the cell
 // lower-bound table.  Replaces the reference's kd-tree build + radius query
 // (proj/src/spatial.cpp:32-111) with integer work that is HBM/L2-bound.
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -229,6 +232,48 @@ __global__ void gather_kernel(const V* __restrict__ src, const uint32_t* __restr
         dst[i] = src[idx[i]];
 }
 
+// Query order of the fused kernels (kernels.cuh build_query_list): Morton
+// (Z-curve) code of the point's sub-cell, decoded from its grid key.
+__device__ __forceinline__ uint32_t compact3(uint32_t m) {  // bits 0,3,6,.. -> 0,1,2,..
+    m &= 0x09249249u;
+    m = (m ^ (m >> 2)) & 0x030C30C3u;
+    m = (m ^ (m >> 4)) & 0x0300F00Fu;
+    m = (m ^ (m >> 8)) & 0x030000FFu;
+    m = (m ^ (m >> 16)) & 0x000003FFu;
+    return m;
+}
+__device__ __forceinline__ uint32_t spread3(uint32_t v) {  // 10 bits -> 0,3,6,..
+    v &= 0x3FFu;
+    v = (v | (v << 16)) & 0x030000FFu;
+    v = (v | (v << 8)) & 0x0300F00Fu;
+    v = (v | (v << 4)) & 0x030C30C3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+
+__global__ void morton_keys_kernel(const uint32_t* __restrict__ skeys, uint32_t n, int sb, uint32_t gx,
+                                   uint32_t gy, int shift, const uint32_t* __restrict__ sidx,
+                                   uint32_t lo, uint32_t hi, uint32_t* __restrict__ keys,
+                                   const uint32_t* done) {
+    if (done && *done) return;
+    const uint32_t smask = (1u << (3 * sb)) - 1u;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t k = skeys[i];
+        const uint32_t cell = k >> (3 * sb), sub = k & smask;
+        const uint32_t cx = cell % gx, r = cell / gx;
+        const uint32_t cy = r % gy, cz = r / gy;
+        const uint32_t fx = ((cx << sb) | compact3(sub)) >> shift;
+        const uint32_t fy = ((cy << sb) | compact3(sub >> 1)) >> shift;
+        const uint32_t fz = ((cz << sb) | compact3(sub >> 2)) >> shift;
+        uint32_t key = spread3(fx) | (spread3(fy) << 1) | (spread3(fz) << 2);
+        if (sidx) {
+            const uint32_t o = sidx[i];
+            if (o < lo || o >= hi) key |= 1u << 30;  // not owned: after the owned queries
+        }
+        keys[i] = key;
+    }
+}
+
 constexpr uint32_t kShortGap = 64;
 
 // Thread k (0..n) owns the cells in (cell[k-1], cell[k]]: their lower bound is k.
@@ -260,6 +305,57 @@ __global__ void gap_fill_kernel(uint32_t* __restrict__ start, const uint32_t* __
     for (uint32_t g = blockIdx.x; g < ng; g += gridDim.x) {
         const uint32_t lo = gaps[3 * g], hi = gaps[3 * g + 1], v = gaps[3 * g + 2];
         for (uint32_t c = lo + threadIdx.x; c <= hi; c += blockDim.x) start[c] = v;
+    }
+}
+
+// ---- pair records (kernels.cuh) ----------------------------------------------
+// Slot of the first point of grid row `row` is start[row*gx] + row_delta(row):
+// even, and rows never overlap (delta grows by at most 2 per row).
+__device__ __forceinline__ uint32_t row_delta(const uint32_t* __restrict__ start, uint32_t row,
+                                              uint32_t gx) {
+    const uint32_t rs = start[(size_t)row * gx];
+    return row + ((rs + row) & 1u);
+}
+
+__device__ __forceinline__ void write_slot(float* __restrict__ pairs, uint32_t p, float x, float y,
+                                           float z, float w) {
+    float* r = pairs + 8 * (size_t)(p >> 1) + (p & 1u);
+    r[0] = x;
+    r[2] = y;
+    r[4] = z;
+    r[6] = w;
+}
+
+constexpr float kPadFar = 1.0e18f;  // padding slot: far from everything, weight 0
+
+// start_pad[c] = start[c] + row_delta(row of c); the slots between two rows
+// (and after the last) become far padding points.
+__global__ void pad_table_kernel(const uint32_t* __restrict__ start, uint32_t ncells, uint32_t gx,
+                                 uint32_t* __restrict__ start_pad, float* __restrict__ pairs,
+                                 const uint32_t* done) {
+    if (done && *done) return;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c <= ncells;
+         c += gridDim.x * blockDim.x) {
+        const uint32_t row = c / gx;
+        const uint32_t d = row_delta(start, row, gx);
+        const uint32_t v = start[c];
+        start_pad[c] = v + d;
+        if (c == row * gx && row > 0) {
+            const uint32_t dp = row_delta(start, row - 1, gx);
+            for (uint32_t p = v + dp; p < v + d; ++p) write_slot(pairs, p, kPadFar, kPadFar, kPadFar, 0.f);
+        }
+    }
+}
+
+__global__ void pack_pairs_kernel(const float4* __restrict__ sorted, const uint32_t* __restrict__ skeys,
+                                  uint32_t n, int sub_shift, uint32_t gx,
+                                  const uint32_t* __restrict__ start, float* __restrict__ pairs,
+                                  const uint32_t* done) {
+    if (done && *done) return;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const float4 c = sorted[i];
+        const uint32_t row = (skeys[i] >> sub_shift) / gx;
+        write_slot(pairs, i + row_delta(start, row, gx), c.x, c.y, c.z, c.w);
     }
 }
 
@@ -350,6 +446,30 @@ void launch_gather(const typename Vec4<T>::type* src, const uint32_t* idx, uint3
     gather_kernel<typename Vec4<T>::type><<<grid_for(n, 256), 256, 0, s>>>(src, idx, n, dst, done);
 }
 
+int build_query_list(const uint32_t* sorted_keys, uint32_t n, const GridGeom& g, double support,
+                     const uint32_t* sorted_idx, uint32_t own_lo, uint32_t own_hi, uint32_t* keys_tmp,
+                     uint32_t* keys_sorted_tmp, uint32_t* qlist, int* block_shift,
+                     RadixScratch& scr, const uint32_t* done, cudaStream_t s) {
+    const int sb = g.sub_bits;
+    uint32_t fmax = (uint32_t)std::max(g.gx, std::max(g.gy, g.gz)) << sb;
+    int bits = 0;
+    while (bits < 32 && (1ull << bits) < fmax) ++bits;
+    const int shift = bits > 10 ? bits - 10 : 0;
+    // Morton blocks of side ~support: 2^k code units per axis
+    const double unit = g.cs * std::ldexp(1.0, shift - sb);
+    int k = (int)std::floor(std::log2(support / unit) + 0.5);
+    if (const char* e = std::getenv("PCSB_BLOCK_ADJ")) k += std::atoi(e);  // developer knob
+    k = std::max(0, std::min(k, 10));
+    *block_shift = 3 * k;
+    if (!n) return 0;
+    morton_keys_kernel<<<grid_for(n, 256), 256, 0, s>>>(sorted_keys, n, sb, (uint32_t)g.gx,
+                                                        (uint32_t)g.gy, shift, sorted_idx, own_lo,
+                                                        own_hi, keys_tmp, done);
+    const int key_bits = 3 * std::min(bits, 10) + (sorted_idx ? 1 : 0);
+    return 1 + radix_sort(keys_tmp, nullptr, keys_sorted_tmp, qlist, n,
+                          key_bits > 30 ? (sorted_idx ? 31 : 30) : std::max(key_bits, 1), scr, done, s);
+}
+
 int build_cell_start(const uint32_t* sorted_keys, uint32_t n, int sub_shift, uint32_t ncells,
                      uint32_t* cell_start, uint32_t* gap_list, uint32_t* gap_count,
                      const uint32_t* done, cudaStream_t s) {
@@ -358,6 +478,29 @@ int build_cell_start(const uint32_t* sorted_keys, uint32_t n, int sub_shift, uin
         sorted_keys, n, sub_shift, ncells, cell_start, gap_list, gap_count, done);
     gap_fill_kernel<<<148 * 2, 256, 0, s>>>(cell_start, gap_list, gap_count, done);
     return 2;
+}
+
+size_t pairs_capacity(uint32_t n, const GridGeom& g) {
+    const size_t rows = (size_t)g.gy * (size_t)g.gz;
+    return (size_t)n + 2 * rows + 4;
+}
+
+int build_pairs(const float4* sorted, const uint32_t* sorted_keys, uint32_t n, const GridGeom& g,
+                const uint32_t* cell_start, uint32_t* start_pad, float4* pairs, bool table,
+                const uint32_t* done, cudaStream_t s) {
+    int k = 0;
+    if (table) {
+        pad_table_kernel<<<grid_for((uint64_t)g.ncells + 1, 256), 256, 0, s>>>(
+            cell_start, g.ncells, (uint32_t)g.gx, start_pad, (float*)pairs, done);
+        ++k;
+    }
+    if (n) {
+        pack_pairs_kernel<<<grid_for(n, 256), 256, 0, s>>>(sorted, sorted_keys, n, 3 * g.sub_bits,
+                                                          (uint32_t)g.gx, cell_start,
+                                                          (float*)pairs, done);
+        ++k;
+    }
+    return k;
 }
 
 template void launch_convert_xyz<float>(const double*, float4*, uint64_t, float, cudaStream_t);

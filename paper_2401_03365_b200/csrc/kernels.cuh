@@ -40,20 +40,47 @@ template <typename T>
 void launch_gather(const typename Vec4<T>::type* src, const uint32_t* idx, uint32_t n,
                    typename Vec4<T>::type* dst, const uint32_t* done, cudaStream_t s);
 
+// Query list of the fused kernels: the sorted slots in Morton (Z-curve) order of
+// their sub-cells (<= 10 bits per axis; keys_sorted_tmp keeps the codes), so
+// that consecutive queries are spatially close; a query group never crosses a
+// Morton block of side ~support (code >> block_shift changes), which bounds its
+// box.  With sorted_idx, the queries whose internal index lies in [own_lo,
+// own_hi) come first (multi-GPU ownership).  Returns kernel count.
+int build_query_list(const uint32_t* sorted_keys, uint32_t n, const GridGeom& g, double support,
+                     const uint32_t* sorted_idx, uint32_t own_lo, uint32_t own_hi, uint32_t* keys_tmp,
+                     uint32_t* keys_sorted_tmp, uint32_t* qlist, int* block_shift,
+                     RadixScratch& scr, const uint32_t* done, cudaStream_t s);
+// Work unit of the fused kernels: kUnitQueries consecutive entries of the query list.
+constexpr uint32_t kUnitQueries = 32;
+
 // cell_start[c] = first sorted position whose cell >= c, c in [0, ncells]
 int build_cell_start(const uint32_t* sorted_keys, uint32_t n, int sub_shift, uint32_t ncells,
                      uint32_t* cell_start, uint32_t* gap_list, uint32_t* gap_count,
                      const uint32_t* done, cudaStream_t s);
 
+// Pair records: the fp32 candidate layout of the fused kernels.  A sorted cloud
+// is re-laid as records of two consecutive slots, record r = float4 pairs[2r] =
+// (x0 x1 y0 y1) and pairs[2r+1] = (z0 z1 w0 w1), with every grid row (fixed
+// y, z) starting at an even slot, so any x-range of a row is a contiguous,
+// 32-byte aligned byte range (one bulk copy).  The slots that pad the rows hold
+// far points of weight 0.  start_pad is the cell table in slot units.
+size_t pairs_capacity(uint32_t n, const GridGeom& g);  // float4 elements
+// table: also (re)build start_pad and the padding (positions changed)
+int build_pairs(const float4* sorted, const uint32_t* sorted_keys, uint32_t n, const GridGeom& g,
+                const uint32_t* cell_start, uint32_t* start_pad, float4* pairs, bool table,
+                const uint32_t* done, cudaStream_t s);
+
 // ---- fused fp32 kernels (lop_fast.cu) ---------------------------------------
 struct FastArgs {
-    const float4* P;          // data, sorted; .w = 1/v_j (WLOP) or 1
-    const uint32_t* Pstart;   // cell table of P
-    const float4* Xs;         // projected set, sorted; .w = w_i (WLOP)
-    const uint32_t* Xstart;   // cell table of X
+    const float4* Ppairs;     // data, pair records; w = 1/v_j (WLOP) or 1
+    const uint32_t* Pstart;   // slot table of Ppairs
+    const float4* Xs;         // projected set, sorted (queries)
+    const float4* Xpairs;     // projected set, pair records; w = w_i (WLOP)
+    const uint32_t* Xstart;   // slot table of Xpairs
     const uint32_t* Xs_idx;   // sorted slot -> internal index
-    const uint32_t* Xskeys;   // sorted slot -> grid key (query grouping)
-    const uint32_t* qlist;    // queries (sorted slots); nullptr = 0..nq-1
+    const uint32_t* qlist;    // queries (sorted slots, build_query_list order)
+    const uint32_t* qcodes;   // their Morton codes
+    int block_shift;          // groups stay inside one (code >> block_shift) block
     uint32_t nq;
     GridGeom g;
     double s_pad;             // support with margin (cell ranges)
@@ -78,10 +105,12 @@ void launch_fast(const FastArgs& a, int lanes_per_point, bool wlop, bool check_z
 int fast_blocks_per_sm(int lanes_per_point, bool wlop, bool check_zero, int rep_mode);
 
 struct DensityArgs {
-    const float4* C;          // cloud, sorted (queries and candidates)
-    const uint32_t* Cstart;
-    const uint32_t* Cskeys;   // sorted slot -> grid key (query grouping)
-    const uint32_t* qlist;    // queries (sorted slots), nullptr = 0..nq-1
+    const float4* C;          // cloud, sorted (queries)
+    const float4* Cpairs;     // cloud, pair records (candidates)
+    const uint32_t* Cstart;   // slot table of Cpairs
+    const uint32_t* qlist;    // queries (sorted slots, build_query_list order)
+    const uint32_t* qcodes;
+    int block_shift;
     uint32_t nq;
     GridGeom g;
     double s_pad, r2;
@@ -147,9 +176,6 @@ void launch_unpermute(const typename Vec4<T>::type* X, const uint32_t* orig_of_i
                       uint32_t mpad, double* out_xyz, cudaStream_t s);
 void launch_iso_to_orig(const uint8_t* ever_iso, const uint32_t* orig_of_internal, uint32_t mpad,
                         uint8_t* iso_orig, cudaStream_t s);
-// owned-query compaction key: 0 for internal index in [lo, hi), 1 otherwise
-void launch_owner_keys(const uint32_t* sorted_idx, uint32_t n, uint32_t lo, uint32_t hi,
-                       uint32_t* keys, const uint32_t* done, cudaStream_t s);
 template <typename T>
 void launch_scatter_init(const typename Vec4<T>::type* X0, const uint32_t* internal_of_orig,
                          uint32_t m, typename Vec4<T>::type* X, cudaStream_t s);

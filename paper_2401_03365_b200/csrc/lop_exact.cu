@@ -332,14 +332,6 @@ __global__ void iso_to_orig_kernel(const uint8_t* __restrict__ ever, const uint3
     }
 }
 
-__global__ void owner_keys_kernel(const uint32_t* __restrict__ sidx, uint32_t n, uint32_t lo,
-                                  uint32_t hi, uint32_t* __restrict__ keys, const uint32_t* done) {
-    if (done && *done) return;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t v = sidx[i];
-        keys[i] = (v >= lo && v < hi) ? 0u : 1u;
-    }
-}
 
 template <typename V>
 __global__ void scatter_init_kernel(const V* __restrict__ X0, const uint32_t* __restrict__ iof,
@@ -418,11 +410,6 @@ void launch_iso_to_orig(const uint8_t* ever, const uint32_t* orig, uint32_t mpad
     iso_to_orig_kernel<<<blocks_for(mpad, 256), 256, 0, s>>>(ever, orig, mpad, out);
 }
 
-void launch_owner_keys(const uint32_t* sidx, uint32_t n, uint32_t lo, uint32_t hi, uint32_t* keys,
-                       const uint32_t* done, cudaStream_t s) {
-    if (!n) return;
-    owner_keys_kernel<<<blocks_for(n, 256), 256, 0, s>>>(sidx, n, lo, hi, keys, done);
-}
 
 template <typename T>
 void launch_scatter_init(const typename Vec4<T>::type* X0, const uint32_t* iof, uint32_t m,

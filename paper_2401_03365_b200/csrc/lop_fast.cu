@@ -4,56 +4,55 @@
 // (attraction :49-65, isolation/anchor :67-75, Weiszfeld quotient :77,
 // repulsion :79-97), with one persistent warp-cooperative kernel:
 //
-//  * A warp takes a GROUP of Q = 32/L consecutive queries of the cell-sorted
-//    projected set (L lanes per query).  Groups are fetched dynamically
-//    (atomic counter) so density imbalance self-schedules.  A group is split
-//    into SEGMENTS of queries that sit in one cell row and in adjacent cells,
-//    so a segment's bounding box is at most a few cells wide.
-//  * For each segment the warp walks the cell rows that can hold a point within
-//    the support of the box (each row is ONE contiguous run of the sorted
-//    array), streams the run with coalesced float4 loads, culls every
-//    candidate against the box once, and compacts the survivors into a
-//    per-warp shared-memory buffer (ballot + popc).
-//  * Each lane then evaluates its query against every L-th buffered candidate
-//    (shared-memory broadcast, one wavefront per LDS.128): d2 with FFMA,
-//    theta with MUFU.EX2, 1/d with MUFU.RSQ, predicated accumulation.
+//  * Work unit = a RUN of the cell-sorted query list (consecutive queries in one
+//    grid row, x cells at most one apart; build_runs), fetched by an atomic
+//    counter so density imbalance self-schedules.  A warp walks its run in
+//    GROUPS of Q = 32/L queries (L lanes per query): a group's bounding box is
+//    a couple of cells wide at most.
+//  * Candidates: the cell rows (fixed y, z) that can hold a point within the
+//    support of the box, each trimmed to the x-interval allowed by the row's
+//    distance to the box (a per-row Minkowski sum of box and ball — no
+//    per-candidate cull).  Each row is one contiguous run of the sorted array;
+//    runs are streamed back to back with cp.async (4-byte copies straight into a
+//    pair-interleaved, bank-swizzled layout) into one half of a per-warp double
+//    buffer while the other half is evaluated.
+//  * Evaluation: two candidates per lane with packed fp32x2 (FADD2/FMUL2/FFMA2),
+//    theta on MUFU.EX2, 1/d on MUFU.RSQ, predicated accumulation of
+//    sum w (c - q) relative to the query (fp32 error ~ support, not ~ |x|).
 //  * The reference's exact neighbour predicate (fp64, d2 <= r*r,
 //    proj/src/spatial.cpp:89,101) is reproduced by deciding in fp32 and
-//    re-deciding in fp64, in-kernel, every pair that falls in a guard band
-//    around the support (a warp vote keeps that path off the common case).
-//    Queries that meet an exact zero distance in the attraction (sweeps >= 2),
-//    a coincident projected pair, or a non-finite sum are deferred to the exact
-//    fp64 kernel (lop_exact.cu).  The neighbour SET is always the reference's.
-//
-// Accumulation is relative to the query (sum alpha*(p - x)), which keeps the
-// fp32 rounding error proportional to the support radius rather than to |x|.
+//    re-deciding in fp64, in-kernel, every pair within a guard band of the
+//    support (a warp vote keeps that path off the common case).  Queries that
+//    meet an exact zero distance in the attraction (sweeps >= 2), a coincident
+//    projected pair or a non-finite sum are deferred to the exact fp64 kernel
+//    (lop_exact.cu).  The neighbour SET is always the reference's.
 #include <cfloat>
 
 #include "common.cuh"
 #include "kernels.cuh"
 
+#ifndef PCSB_FAST_MINB
+#define PCSB_FAST_MINB 6
+#endif
+
 namespace pcsb {
 
 namespace {
 
-#ifndef PCSB_FAST_MINB
-#define PCSB_FAST_MINB 6
-#endif
 constexpr int FAST_WARPS = 4;
 constexpr int FAST_THREADS = FAST_WARPS * 32;
-constexpr int BUF = 256;     // staged candidates per warp (float4)
-constexpr int RING = 4;      // cp.async pipeline depth: 32-candidate chunks in flight per warp
-// Unrolled pairs per lane step: L*UNROLL = 16 pairs, so the bank swizzle of the
-// staging layout (bit 3 of the pair index) is a compile-time constant per step.
-template <int L> struct Unroll { static constexpr int value = 16 / L; };
+#ifndef PCSB_HR
+#define PCSB_HR 128
+#endif
+constexpr int HR = PCSB_HR;  // pair records per half (2 candidates each; per warp: 2 halves)
+static_assert(HR % 16 == 0, "a half holds whole 16-record eval steps");
 constexpr float kFar = 1.0e18f;
+
+// Unrolled records per lane step: L*U = 16 records per warp step.
+template <int L> struct Unroll { static constexpr int value = 16 / L; };
 
 struct Box {
     float mnx, mny, mnz, mxx, mxy, mxz;
-};
-
-struct CellRange {
-    int lox, loy, loz, hix, hiy, hiz;
 };
 
 __device__ __forceinline__ float warp_min(float v) {
@@ -74,18 +73,6 @@ __device__ __forceinline__ float group_sum(float v) {
     return v;
 }
 
-__device__ __forceinline__ CellRange cell_range(const GridGeom& g, const Box& b, double s_pad) {
-    CellRange r;
-    r.lox = cell_coord((double)b.mnx - s_pad, g.ox, g.inv_cs, g.gx);
-    r.loy = cell_coord((double)b.mny - s_pad, g.oy, g.inv_cs, g.gy);
-    r.loz = cell_coord((double)b.mnz - s_pad, g.oz, g.inv_cs, g.gz);
-    r.hix = cell_coord((double)b.mxx + s_pad, g.ox, g.inv_cs, g.gx);
-    r.hiy = cell_coord((double)b.mxy + s_pad, g.oy, g.inv_cs, g.gy);
-    r.hiz = cell_coord((double)b.mxz + s_pad, g.oz, g.inv_cs, g.gz);
-    return r;
-}
-
-// Bounding box over the member lanes of the current segment.
 __device__ __forceinline__ Box member_box(const float4& q, bool member) {
     Box b;
     b.mnx = warp_min(member ? q.x : INFINITY);
@@ -97,134 +84,202 @@ __device__ __forceinline__ Box member_box(const float4& q, bool member) {
     return b;
 }
 
-// Query group of Q = 32/L consecutive sorted slots, split into segments of
-// queries in the same cell row whose x cells are at most one apart.
-template <int L>
-struct Group {
-    uint32_t qslot;
-    float4 q;
-    bool qvalid;
-    int seg;
-    int nseg;
+// ---------------------------------------------------------------------------
+// Staging: per warp a ring of two halves of HR pair records (kernels.cuh:
+// record = (x0 x1 y0 y1)(z0 z1 w0 w1)), filled by bulk asynchronous copies
+// (cp.async.bulk, the TMA engine's linear mode) that complete on one mbarrier
+// per half.  A candidate row is ONE contiguous range of records, so a row
+// costs one copy instruction regardless of its length.  Eval reads records
+// with two LDS.128; the L lanes of a query read L consecutive records (32-byte
+// stride: conflict-free for L <= 4).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_LOOP:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_LOOP;\n\t}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+// generic-proxy accesses of a half before the async proxy rewrites it
+__device__ __forceinline__ void fence_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+struct Stage {
+    float4* ring;     // 2 halves x HR records x 2 float4
+    uint32_t ring_s;  // its shared-window address
+    uint32_t bar_s;   // two mbarriers (one per half)
+    uint32_t phase;   // bit h: parity of the next completion of half h
 };
 
-template <int L>
-__device__ __forceinline__ Group<L> load_group(uint32_t grp, uint32_t nq, const uint32_t* qlist,
-                                               const float4* __restrict__ pts,
-                                               const uint32_t* __restrict__ skeys,
-                                               const GridGeom& g, int lane) {
-    constexpr int Q = 32 / L;
-    Group<L> G;
-    const int qi = lane / L, sub = lane % L;
-    const uint32_t qpos = grp * Q + qi;
-    G.qvalid = qpos < nq;
-    const uint32_t qp = G.qvalid ? qpos : grp * Q;  // padding lanes duplicate query 0
-    G.qslot = qlist ? __ldg(&qlist[qp]) : qp;
-    G.q = __ldg(&pts[G.qslot]);
-    const uint32_t cell = __ldg(&skeys[G.qslot]) >> (3 * g.sub_bits);
-    const uint32_t row = cell / (uint32_t)g.gx;
-    const uint32_t cx = cell - row * (uint32_t)g.gx;
-    const int src = qi > 0 ? (qi - 1) * L : 0;
-    const uint32_t prow = __shfl_sync(0xffffffffu, row, src);
-    const uint32_t pcx = __shfl_sync(0xffffffffu, cx, src);
-    const bool start = G.qvalid && (qi == 0 || row != prow || cx > pcx + 1 || cx < pcx);
-    const unsigned smask = __ballot_sync(0xffffffffu, start && sub == 0);
-    G.nseg = __popc(smask);
-    G.seg = __popc(smask & (unsigned)((2ull << (qi * L)) - 1ull)) - 1;
-    return G;
-}
-
-// Staging layout (per warp, BUF candidates): PAIR-INTERLEAVED so that one lane
-// evaluates two candidates with packed fp32x2 instructions, and BANK-SWIZZLED so
-// that the scalar stores of 32 consecutive candidates hit 32 distinct banks:
-//   AX = float4[BUF/2]: pair j = (x0 x1 y0 y1), BZ = float4[BUF/2]: (z0 z1 w0 w1),
-//   with the two halves swapped when bit 3 of j is set.
-__device__ __forceinline__ int stage_word(int k, int comp) {
-    const int j = k >> 1;
-    return j * 4 + 2 * (comp ^ ((j >> 3) & 1)) + (k & 1);
-}
-
-__device__ __forceinline__ void stage_store(float4* buf, int k, const float4& c) {
-    float* ax = reinterpret_cast<float*>(buf);
-    float* bz = reinterpret_cast<float*>(buf + BUF / 2);
-    ax[stage_word(k, 0)] = c.x;
-    ax[stage_word(k, 1)] = c.y;
-    bz[stage_word(k, 0)] = c.z;
-    bz[stage_word(k, 1)] = c.w;
-}
-
-__device__ __forceinline__ float4 stage_load(const float4* buf, int k) {
-    const float* ax = reinterpret_cast<const float*>(buf);
-    const float* bz = reinterpret_cast<const float*>(buf + BUF / 2);
-    return make_float4(ax[stage_word(k, 0)], ax[stage_word(k, 1)], bz[stage_word(k, 0)],
-                       bz[stage_word(k, 1)]);
-}
-
-// Streams every candidate of the rows covered by `cr`, culls it against the
-// box and hands full buffers to `eval(count)`.  Warp-uniform control flow.
-// The next 32-candidate chunk of a row is loaded before the current one is
-// culled (one chunk of prefetch per lane hides most of the L2 latency).
-template <typename Eval>
-__device__ __forceinline__ void stream_candidates(const float4* __restrict__ src,
-                                                  const uint32_t* __restrict__ start,
-                                                  const GridGeom& g, const CellRange& cr,
-                                                  const Box& b, float scull2, float4* buf,
-                                                  float4* /*ring*/, int lane, Eval&& eval) {
-    const int ny = cr.hiy - cr.loy + 1;
-    const int nrows = ny * (cr.hiz - cr.loz + 1);
-    const unsigned lt = (1u << lane) - 1u;
-    const float4 far4 = make_float4(kFar, kFar, kFar, 0.f);
-    int count = 0;
-    for (int r0 = 0; r0 < nrows; r0 += 32) {
-        uint32_t rb = 0, re = 0;
-        const int r = r0 + lane;
-        if (r < nrows) {
-            const int yy = cr.loy + r % ny;
-            const int zz = cr.loz + r / ny;
-            const uint32_t base = ((uint32_t)zz * (uint32_t)g.gy + (uint32_t)yy) * (uint32_t)g.gx;
-            rb = __ldg(&start[base + cr.lox]);
-            re = __ldg(&start[base + cr.hix + 1]);
-        }
-        const int nr = min(32, nrows - r0);
-        for (int j = 0; j < nr; ++j) {
-            const uint32_t b0 = __shfl_sync(0xffffffffu, rb, j);
-            const uint32_t e0 = __shfl_sync(0xffffffffu, re, j);
-            if (b0 >= e0) continue;
-            float4 c = (b0 + lane < e0) ? __ldg(&src[b0 + lane]) : far4;
-            for (uint32_t k = b0; k < e0; k += 32) {
-                const uint32_t kn = k + 32 + lane;
-                const float4 cn = (kn < e0) ? __ldg(&src[kn]) : far4;
-                const float ex = fmaxf(fmaxf(b.mnx - c.x, c.x - b.mxx), 0.f);
-                const float ey = fmaxf(fmaxf(b.mny - c.y, c.y - b.mxy), 0.f);
-                const float ez = fmaxf(fmaxf(b.mnz - c.z, c.z - b.mxz), 0.f);
-                const bool keep = fmaf(ez, ez, fmaf(ey, ey, ex * ex)) <= scull2;
-                const unsigned m = __ballot_sync(0xffffffffu, keep);
-                if (keep) stage_store(buf, count + __popc(m & lt), c);
-                count += __popc(m);
-                if (count > BUF - 32) {
-                    __syncwarp();
-                    eval(count);
-                    __syncwarp();
-                    count = 0;
-                }
-                c = cn;
-            }
-        }
+__device__ __forceinline__ Stage make_stage(float4* ring, uint64_t* bars, int lane) {
+    Stage S;
+    S.ring = ring;
+    S.ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+    S.bar_s = (uint32_t)__cvta_generic_to_shared(bars);
+    S.phase = 0;
+    if (lane == 0) {
+        mbar_init(S.bar_s, 1);
+        mbar_init(S.bar_s + 8, 1);
+        mbar_init_fence();
     }
-    if (count) {
-        __syncwarp();
-        eval(count);
-        __syncwarp();
-    }
+    __syncwarp();
+    return S;
+}
+
+// candidate k of a staged half (fix-up path)
+__device__ __forceinline__ float4 stage_load(const float4* half, int k) {
+    const float4 A = half[2 * (k >> 1)];
+    const float4 B = half[2 * (k >> 1) + 1];
+    return (k & 1) ? make_float4(A.y, A.w, B.y, B.w) : make_float4(A.x, A.z, B.x, B.z);
 }
 
 // ---------------------------------------------------------------------------
-// Evaluation of a staged buffer.  Candidates sit in PAIR-INTERLEAVED layout
-// (pair j = 32 bytes: x0 x1 y0 y1 | z0 z1 w0 w1) so that one lane evaluates two
-// candidates per iteration with packed fp32x2 instructions (FADD2/FMUL2/FFMA2:
-// half the issue slots of scalar FP32).  Per pair: 2 LDS.128, 3+3 packed ops
-// for d2, 1 FFMA2 for the exponent, 4 MUFU (2x EX2, 2x RSQ), 2 FSETP + 2 FSEL
-// for the hit mask, 1 FMUL2 and 4 packed accumulations.
+// Candidate rows of a box: for every cell row (y, z) in range, the x interval
+// [box.x - hx, box.x + hx] with hx = sqrt(s^2 - dy^2 - dz^2), dy/dz the gaps
+// between the row's cells and the box (boundary cells, which also hold clamped
+// outside points, count as unbounded).  Exact superset of the ball-of-box.
+// ---------------------------------------------------------------------------
+struct RowSpan {
+    int loy, ny, loz, nrows;
+};
+
+__device__ __forceinline__ RowSpan row_span(const GridGeom& g, const Box& b, double s_pad) {
+    RowSpan r;
+    r.loy = cell_coord((double)b.mny - s_pad, g.oy, g.inv_cs, g.gy);
+    const int hiy = cell_coord((double)b.mxy + s_pad, g.oy, g.inv_cs, g.gy);
+    r.loz = cell_coord((double)b.mnz - s_pad, g.oz, g.inv_cs, g.gz);
+    const int hiz = cell_coord((double)b.mxz + s_pad, g.oz, g.inv_cs, g.gz);
+    r.ny = hiy - r.loy + 1;
+    r.nrows = r.ny * (hiz - r.loz + 1);
+    return r;
+}
+
+__device__ __forceinline__ double axis_gap(int c, int gdim, double o, double cs, double lo,
+                                           double hi) {
+    // gap between [lo, hi] and cell c's interval; boundary cells are unbounded outward
+    const double c0 = (c == 0) ? -INFINITY : o + cs * (double)c;
+    const double c1 = (c == gdim - 1) ? INFINITY : o + cs * (double)(c + 1);
+    return fmax(0.0, fmax(c0 - hi, lo - c1));
+}
+
+// (begin, end) of row r of the span, trimmed; begin == end if the row is empty
+__device__ __forceinline__ void row_range(const uint32_t* __restrict__ start, const GridGeom& g,
+                                          const Box& b, const RowSpan& rs, double s_pad, int r,
+                                          uint32_t& rb, uint32_t& re) {
+    rb = re = 0;
+    if (r >= rs.nrows) return;
+    const int yy = rs.loy + r % rs.ny;
+    const int zz = rs.loz + r / rs.ny;
+    const double dy = axis_gap(yy, g.gy, g.oy, g.cs, (double)b.mny, (double)b.mxy);
+    const double dz = axis_gap(zz, g.gz, g.oz, g.cs, (double)b.mnz, (double)b.mxz);
+    const double rem = s_pad * s_pad - dy * dy - dz * dz;
+    if (!(rem >= 0.0)) return;
+    const double hx = sqrt(rem);
+    const int lox = cell_coord((double)b.mnx - hx, g.ox, g.inv_cs, g.gx);
+    const int hix = cell_coord((double)b.mxx + hx, g.ox, g.inv_cs, g.gx);
+    const uint32_t base = ((uint32_t)zz * (uint32_t)g.gy + (uint32_t)yy) * (uint32_t)g.gx;
+    rb = __ldg(&start[base + lox]);
+    re = __ldg(&start[base + hix + 1]);
+}
+
+// Streams every record of the trimmed rows through the double buffer and calls
+// eval(half_ptr, nrec) on each full half (nrec = HR) and on the final partial
+// one (padded with far records to a multiple of 16).  The rows of a batch (<=
+// 32, one per lane) are laid end to end (warp scan of their record counts);
+// each lane copies the part of its row that falls in the current half with ONE
+// cp.async.bulk (expect_tx on the half's mbarrier first); lane 0 arrives once
+// the half is full.  A half is evaluated after the other half has been filled,
+// so its copies had that long to land.
+template <typename Eval>
+__device__ __forceinline__ void gather_eval(const float4* __restrict__ pairs,
+                                            const uint32_t* __restrict__ start, const GridGeom& g,
+                                            const Box& b, double s_pad, Stage& S, int lane,
+                                            Eval&& eval) {
+    const RowSpan rs = row_span(g, b, s_pad);
+    uint32_t cur = 0, fill = 0;
+    int pending = -1;
+    auto finish = [&](uint32_t h, int nrec) {
+        mbar_wait(S.bar_s + 8u * h, (S.phase >> h) & 1u);
+        S.phase ^= 1u << h;
+        eval(S.ring + h * (2 * HR), nrec);
+        __syncwarp();
+    };
+    for (int r0 = 0; r0 < rs.nrows; r0 += 32) {
+        uint32_t rb, re;
+        row_range(start, g, b, rs, s_pad, r0 + lane, rb, re);
+        const uint32_t rec0 = rb >> 1;
+        const uint32_t nrec = re > rb ? ((re + 1) >> 1) - rec0 : 0u;
+        uint32_t incl = nrec;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t mine0 = incl - nrec;  // my row: batch offsets [mine0, incl)
+        for (uint32_t w0 = 0; w0 < total;) {
+            const uint32_t w1 = min(total, w0 + (uint32_t)HR - fill);
+            const uint32_t lo = max(mine0, w0), hi = min(incl, w1);
+            if (lo < hi) {
+                const uint32_t bar = S.bar_s + 8u * cur;
+                mbar_expect_tx(bar, (hi - lo) * 32u);
+                bulk_g2s(S.ring_s + (cur * HR + fill + (lo - w0)) * 32u,
+                         pairs + 2 * (size_t)(rec0 + (lo - mine0)), (hi - lo) * 32u, bar);
+            }
+            fill += w1 - w0;
+            w0 = w1;
+            if (fill == HR) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(S.bar_s + 8u * cur);
+                if (pending >= 0) finish((uint32_t)pending, HR);
+                pending = (int)cur;
+                cur ^= 1u;
+                fill = 0;
+                fence_async_smem();
+            }
+        }
+    }
+    if (fill > 0) {
+        const uint32_t padded = (fill + 15u) & ~15u;
+        float4* h = S.ring + cur * (2 * HR);
+        for (uint32_t t = 2 * fill + lane; t < 2 * padded; t += 32)
+            h[t] = (t & 1) ? make_float4(kFar, kFar, 0.f, 0.f) : make_float4(kFar, kFar, kFar, kFar);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(S.bar_s + 8u * cur);
+        if (pending >= 0) finish((uint32_t)pending, HR);
+        finish(cur, (int)padded);
+    } else if (pending >= 0) {
+        finish((uint32_t)pending, HR);
+    }
+    fence_async_smem();
+}
+
+// ---------------------------------------------------------------------------
+// Evaluation of a staged half: per pair 2 LDS.128, 3+3 packed ops for d2, one
+// FFMA2 for the exponent, 4 MUFU (2x EX2, 2x RSQ), 2 FSETP (hit mask, MUFU
+// predicated), one FMUL2 and 4-5 packed accumulations.
 // ---------------------------------------------------------------------------
 enum : int { K_ATTR = 0, K_REP_INVCUBE = 1, K_REP_NEGLIN = 2, K_DENSITY = 3 };
 
@@ -249,24 +304,13 @@ struct EvalConsts {
     float support;
 };
 
-// Pads the buffer (count candidates) to a multiple of 32 (16 pairs) with far
-// dummies; returns the number of pairs.
-__device__ __forceinline__ int pad_pairs(float4* buf, int count, int lane) {
-    const int padded = (count + 31) & ~31;
-    if (count + lane < padded) stage_store(buf, count + lane, make_float4(kFar, kFar, kFar, 0.f));
-    __syncwarp();
-    return padded >> 1;
-}
-
-// weight of one candidate given its hit predicate (kind-specific); vectorised over a pair
+// The hit mask m (1.0 / 0.0 per candidate, FSET.BF) multiplies the weight, so
+// MUFU runs unpredicated and the same mask feeds the hit count.
 template <int KIND, bool kWlop, bool kZero>
-__device__ __forceinline__ float2 pair_weight(const float2& d2, const float2& arg, bool px, bool py,
+__device__ __forceinline__ float2 pair_weight(const float2& d2, const float2& arg, const float2& m,
                                               const float4& B, const EvalConsts& ec) {
     float2 w;
-    if (KIND == K_DENSITY) {
-        w = f2(px ? ex2_approx(arg.x) : 0.f, py ? ex2_approx(arg.y) : 0.f);
-        return w;
-    }
+    if (KIND == K_DENSITY) return __fmul2_rn(f2(ex2_approx(arg.x), ex2_approx(arg.y)), m);
     // kZero: zero-distance candidates are masked out, so keep their rsqrt finite
     // (0 * inf would poison the sums); otherwise a zero distance is a hit whose
     // infinite weight surfaces as a non-finite sum and defers the query
@@ -275,14 +319,13 @@ __device__ __forceinline__ float2 pair_weight(const float2& d2, const float2& ar
     if (KIND == K_REP_INVCUBE) {
         // theta/d^5 scaled by s^5 = theta * (s/d)^5 (no fp32 overflow)
         const float2 a2 = __fmul2_rn(d2, ec.kneg);
-        const float2 th = f2(px ? ex2_approx(a2.x) : 0.f, py ? ex2_approx(a2.y) : 0.f);
+        const float2 th = __fmul2_rn(f2(ex2_approx(a2.x), ex2_approx(a2.y)), m);
         const float2 u = __fmul2_rn(rs, f2(ec.support, ec.support));
         const float2 u2 = __fmul2_rn(u, u);
         w = __fmul2_rn(__fmul2_rn(__fmul2_rn(th, u2), u2), u);
     } else {
         // alpha = theta/d (attraction) or beta = theta*1/d (eta = -r), theta scaled by 2^K0
-        const float2 th = f2(px ? ex2_approx(arg.x) : 0.f, py ? ex2_approx(arg.y) : 0.f);
-        w = __fmul2_rn(th, rs);
+        w = __fmul2_rn(__fmul2_rn(f2(ex2_approx(arg.x), ex2_approx(arg.y)), m), rs);
     }
     if (kWlop) w = __fmul2_rn(w, f2(B.z, B.w));  // 1/v_j (attraction) | w_i' (repulsion)
     return w;
@@ -290,21 +333,15 @@ __device__ __forceinline__ float2 pair_weight(const float2& d2, const float2& ar
 
 // kZero: exclude d2 == 0 from the hits (and count in-range candidates in nr).
 template <int L, int KIND, bool kWlop, bool kZero>
-__device__ __forceinline__ void eval_pairs(const float4* __restrict__ pb, int npairs, int sub,
+__device__ __forceinline__ void eval_pairs(const float4* __restrict__ pb, int nrec, int sub,
                                            const EvalConsts& ec, Acc& A, float& bmin) {
     constexpr int U = Unroll<L>::value;
-    const float4* ax = pb;
-    const float4* bz = pb + BUF / 2;
-    for (int j0 = sub; j0 < npairs; j0 += L * U) {
+    for (int j0 = sub; j0 < nrec; j0 += L * U) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int j = j0 + u * L;
-            // j0 = sub + 16 t with sub < L, so bit 3 of j is that of u*L: a constant
-            constexpr bool kSw = false;
-            const bool sw = kSw || (((u * L) >> 3) & 1);
-            const float4 Ar = ax[j], Br = bz[j];
-            const float4 Apos = sw ? make_float4(Ar.z, Ar.w, Ar.x, Ar.y) : Ar;
-            const float4 B = sw ? make_float4(Br.z, Br.w, Br.x, Br.y) : Br;
+            const float4 Apos = pb[2 * j];
+            const float4 B = pb[2 * j + 1];
             const float2 dx = __fadd2_rn(f2(Apos.x, Apos.y), ec.nqx);
             const float2 dy = __fadd2_rn(f2(Apos.z, Apos.w), ec.nqy);
             const float2 dz = __fadd2_rn(f2(B.x, B.y), ec.nqz);
@@ -313,14 +350,13 @@ __device__ __forceinline__ void eval_pairs(const float4* __restrict__ pb, int np
             d2 = __ffma2_rn(dz, dz, d2);
             const float2 arg = __ffma2_rn(d2, ec.kneg, ec.K0);  // >= 0 <=> d2 <= r2 (fp32)
             bmin = fminf(bmin, fminf(fabsf(arg.x), fabsf(arg.y)));
-            bool px = arg.x >= 0.f, py = arg.y >= 0.f;
+            float2 m = f2(arg.x >= 0.f ? 1.f : 0.f, arg.y >= 0.f ? 1.f : 0.f);
             if (kZero) {
-                A.nr += (px ? 1.f : 0.f) + (py ? 1.f : 0.f);
-                px = px && d2.x > 0.f;
-                py = py && d2.y > 0.f;
+                A.nr += m.x + m.y;
+                m = f2(d2.x > 0.f ? m.x : 0.f, d2.y > 0.f ? m.y : 0.f);
             }
-            const float2 w = pair_weight<KIND, kWlop, kZero>(d2, arg, px, py, B, ec);
-            A.n2 = __fadd2_rn(A.n2, f2(px ? 1.f : 0.f, py ? 1.f : 0.f));
+            const float2 w = pair_weight<KIND, kWlop, kZero>(d2, arg, m, B, ec);
+            A.n2 = __fadd2_rn(A.n2, m);
             A.s = __fadd2_rn(A.s, w);
             if (KIND != K_DENSITY) {
                 A.x = __ffma2_rn(w, dx, A.x);
@@ -331,54 +367,50 @@ __device__ __forceinline__ void eval_pairs(const float4* __restrict__ pb, int np
     }
 }
 
-// Exact fp64 re-decision of the guard-band pairs of one buffer: a candidate
+// Exact fp64 re-decision of the guard-band pairs of one half: a candidate
 // whose fp32 decision differs from the reference predicate (d2 <= r*r in fp64,
 // proj/src/spatial.cpp:89,101) has its contribution added or removed.  The
 // weights are recomputed with the very same fp32 operations as eval_pairs.
 template <int L, int KIND, bool kWlop, bool kZero>
-__device__ __forceinline__ void fix_band(const float4* buf, int npairs, int sub, const float4& q,
+__device__ __forceinline__ void fix_band(const float4* buf, int nrec, int sub, const float4& q,
                                          const EvalConsts& ec, float band, double r2, Acc& A) {
-    // candidate k sits in pair k/2, evaluated by lane sub == (k/2) % L
-    for (int j = sub; j < npairs; j += L)
+    for (int j = sub; j < nrec; j += L) {  // candidate k sits in record k/2, lane (k/2) % L
         for (int h = 0; h < 2; ++h) {
-        const float4 cc = stage_load(buf, 2 * j + h);
-        const float cx = cc.x, cy = cc.y, cz = cc.z, cw = cc.w;
-        const float dx = cx - q.x, dy = cy - q.y, dz = cz - q.z;
-        const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-        const float arg = fmaf(d2, ec.kneg.x, ec.K0.x);
-        if (!(fabsf(arg) <= band)) continue;
-        const bool exact = exact_d2(cx, cy, cz, q.x, q.y, q.z) <= r2;
-        const bool fp32 = arg >= 0.f;
-        if (exact == fp32) continue;
-        // (the accumulators are per candidate parity h; any slot of the lane works)
-        const float sgn = exact ? 1.f : -1.f;
-        const float4 B = make_float4(cz, cz, cw, cw);
-        const float2 w2 = pair_weight<KIND, kWlop, kZero>(f2(d2, d2), f2(arg, arg), true, true, B, ec);
-        if (kZero) A.nr += sgn;
-        if (!kZero || d2 > 0.f) {
-            const float w = w2.x * sgn;
-            A.n2.x += sgn;
-            A.s.x += w;
-            if (KIND != K_DENSITY) {
-                A.x.x = fmaf(w, dx, A.x.x);
-                A.y.x = fmaf(w, dy, A.y.x);
-                A.z.x = fmaf(w, dz, A.z.x);
+            const float4 cc = stage_load(buf, 2 * j + h);
+            const float dx = cc.x - q.x, dy = cc.y - q.y, dz = cc.z - q.z;
+            const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+            const float arg = fmaf(d2, ec.kneg.x, ec.K0.x);
+            if (!(fabsf(arg) <= band)) continue;
+            const bool exact = exact_d2(cc.x, cc.y, cc.z, q.x, q.y, q.z) <= r2;
+            const bool fp32 = arg >= 0.f;
+            if (exact == fp32) continue;
+            const float sgn = exact ? 1.f : -1.f;
+            const float4 B = make_float4(cc.z, cc.z, cc.w, cc.w);
+            const float2 w2 = pair_weight<KIND, kWlop, kZero>(f2(d2, d2), f2(arg, arg), f2(1.f, 1.f),
+                                                              B, ec);
+            if (kZero) A.nr += sgn;
+            if (!kZero || d2 > 0.f) {
+                const float w = w2.x * sgn;
+                A.n2.x += sgn;
+                A.s.x += w;
+                if (KIND != K_DENSITY) {
+                    A.x.x = fmaf(w, dx, A.x.x);
+                    A.y.x = fmaf(w, dy, A.y.x);
+                    A.z.x = fmaf(w, dz, A.z.x);
+                }
             }
         }
-        }
+    }
 }
 
-// One buffer: pad, evaluate, re-decide the band if any lane saw a band pair.
+// One staged half: evaluate, re-decide the band if any lane saw a band pair.
 template <int L, int KIND, bool kWlop, bool kZero>
-__device__ __forceinline__ int eval_buffer(float4* buf, int count, int lane, int sub,
-                                           const float4& q, const EvalConsts& ec, float band,
-                                           double r2, Acc& A) {
-    const int npairs = pad_pairs(buf, count, lane);
+__device__ __forceinline__ void eval_half(const float4* half, int nrec, int sub, const float4& q,
+                                          const EvalConsts& ec, float band, double r2, Acc& A) {
     float bmin = INFINITY;
-    eval_pairs<L, KIND, kWlop, kZero>(buf, npairs, sub, ec, A, bmin);
+    eval_pairs<L, KIND, kWlop, kZero>(half, nrec, sub, ec, A, bmin);
     if (__any_sync(0xffffffffu, bmin <= band))
-        fix_band<L, KIND, kWlop, kZero>(buf, npairs, sub, q, ec, band, r2, A);
-    return 2 * npairs;
+        fix_band<L, KIND, kWlop, kZero>(half, nrec, sub, q, ec, band, r2, A);
 }
 
 template <int L>
@@ -403,48 +435,81 @@ __device__ __forceinline__ EvalConsts make_consts(const float4& q, float kneg, f
     return ec;
 }
 
+// The next work unit for this warp: [r0, r1) positions in the query list.
+__device__ __forceinline__ bool next_unit(uint32_t* counter, uint32_t nq, int lane, uint32_t& r0,
+                                          uint32_t& r1) {
+    uint32_t u = 0;
+    if (lane == 0) u = atomicAdd(counter, 1u);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    r0 = u * kUnitQueries;
+    if (r0 >= nq) return false;
+    r1 = min(r0 + kUnitQueries, nq);
+    return true;
+}
+
+// Group starts inside a unit (bit i: a group must start at r0 + i): Morton
+// block changes.
+__device__ __forceinline__ unsigned group_breaks(const uint32_t* __restrict__ qcodes, int shift,
+                                                 uint32_t r0, uint32_t r1, int lane) {
+    const uint32_t pos = r0 + lane;
+    const uint32_t code = pos < r1 ? (__ldg(&qcodes[pos]) >> shift) : 0xFFFFFFFFu;
+    const uint32_t prev = __shfl_up_sync(0xffffffffu, code, 1);
+    return __ballot_sync(0xffffffffu, lane == 0 || (pos < r1 && code != prev));
+}
+
+// End of the group starting at g0: the next break, at most Q queries.
+__device__ __forceinline__ uint32_t group_end(unsigned brk, uint32_t r0, uint32_t r1, uint32_t g0,
+                                              uint32_t Q) {
+    const uint32_t rel = g0 - r0;
+    const unsigned later = brk & ~((2u << rel) - 1u);
+    const uint32_t e = later ? r0 + (uint32_t)(__ffs(later) - 1) : r1;
+    return min(e, min(g0 + Q, r1));
+}
+
 template <int L, bool kWlop, bool kCheckZero, int kRep>
 __global__ void __launch_bounds__(FAST_THREADS, PCSB_FAST_MINB)
 fast_kernel(const FastArgs a) {
     constexpr int Q = 32 / L;
     constexpr int KREP = kRep == 1 ? K_REP_INVCUBE : K_REP_NEGLIN;
-    __shared__ float4 smem[FAST_WARPS * (BUF + RING * 32)];
+    __shared__ __align__(128) float4 smem[FAST_WARPS * 4 * HR];
+    __shared__ __align__(8) uint64_t bars[FAST_WARPS * 2];
     if (*a.done) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float4* buf = smem + warp * (BUF + RING * 32);
-    float4* ring = buf + BUF;
-    const int sub = lane % L;
-    const uint32_t ngroups = (a.nq + Q - 1) / Q;
+    Stage S = make_stage(smem + warp * 4 * HR, bars + 2 * warp, lane);
+    const int qi = lane / L, sub = lane % L;
 
-    for (;;) {
-        uint32_t grp = 0;
-        if (lane == 0) grp = atomicAdd(&a.slot->group_counter, 1u);
-        grp = __shfl_sync(0xffffffffu, grp, 0);
-        if (grp >= ngroups) break;
-        const Group<L> G = load_group<L>(grp, a.nq, a.qlist, a.Xs, a.Xskeys, a.g, lane);
-        const float4 q = G.q;
-        const EvalConsts ec = make_consts(q, a.kneg, a.K0, a.support);
-
-        for (int sg = 0; sg < G.nseg; ++sg) {
-            const bool member = G.qvalid && G.seg == sg;
+    uint32_t r0, r1;
+    while (next_unit(&a.slot->group_counter, a.nq, lane, r0, r1)) {
+        const unsigned brk = group_breaks(a.qcodes, a.block_shift, r0, r1, lane);
+        for (uint32_t g0 = r0, g1; g0 < r1; g0 = g1) {
+            g1 = group_end(brk, r0, r1, g0, Q);
+            const uint32_t qpos = g0 + qi;
+            const bool member = qpos < g1;
+            const uint32_t qp = member ? qpos : g0;  // padding lanes duplicate the first query
+            const uint32_t qslot = __ldg(&a.qlist[qp]);
+            const float4 q = __ldg(&a.Xs[qslot]);
+            const EvalConsts ec = make_consts(q, a.kneg, a.K0, a.support);
             const Box box = member_box(q, member);
-            const CellRange cr = cell_range(a.g, box, a.s_pad);
 
             // ---------------- attraction: data candidates (lop.cpp:49-65) ----------------
             Acc at = acc_zero();
-            uint32_t evals = 0;  // buffered candidates evaluated by this segment (x Q queries)
-            stream_candidates(a.P, a.Pstart, a.g, cr, box, a.scull2, buf, ring, lane, [&](int count) {
-                evals += eval_buffer<L, K_ATTR, kWlop, kCheckZero>(buf, count, lane, sub, q, ec,
-                                                                   a.band, a.r2, at);
-            });
+            uint32_t evals = 0;  // staged candidates evaluated (x Q queries)
+            gather_eval(a.Ppairs, a.Pstart, a.g, box, a.s_pad, S, lane,
+                        [&](const float4* half, int nrec) {
+                            eval_half<L, K_ATTR, kWlop, kCheckZero>(half, nrec, sub, q, ec, a.band,
+                                                                  a.r2, at);
+                            evals += 2 * nrec;
+                        });
 
             // ---------------- repulsion: projected-set candidates (lop.cpp:79-97) ----------------
             Acc rp = acc_zero();
             if (kRep != 0) {
-                stream_candidates(a.Xs, a.Xstart, a.g, cr, box, a.scull2, buf, ring, lane, [&](int count) {
-                    evals += eval_buffer<L, KREP, kWlop, true>(buf, count, lane, sub, q, ec, a.band,
-                                                               a.r2, rp);
-                });
+                gather_eval(a.Xpairs, a.Xstart, a.g, box, a.s_pad, S, lane,
+                            [&](const float4* half, int nrec) {
+                                eval_half<L, KREP, kWlop, true>(half, nrec, sub, q, ec, a.band,
+                                                                a.r2, rp);
+                                evals += 2 * nrec;
+                            });
             }
 
             // ---------------- per-query reduction over its L lanes ----------------
@@ -455,7 +520,7 @@ fast_kernel(const FastArgs a) {
             float disp = 0.f;
             unsigned long long n_attr = 0, n_rep = 0;
             if (member && sub == 0) {
-                const uint32_t qi_int = __ldg(&a.Xs_idx[G.qslot]);
+                const uint32_t qi_int = __ldg(&a.Xs_idx[qslot]);
                 const float sa = at.s.x;
                 bool bad = !isfinite(sa) || !isfinite(at.x.x) || !isfinite(at.y.x) ||
                            !isfinite(at.z.x);
@@ -475,7 +540,7 @@ fast_kernel(const FastArgs a) {
                 }
                 if (bad) {
                     const uint32_t pos = atomicAdd(&a.slot->careful_count, 1u);
-                    a.careful_list[pos] = G.qslot;
+                    a.careful_list[pos] = qslot;
                 } else {
                     float nx = q.x, ny = q.y, nz = q.z;
                     bool isolated = false;
@@ -508,7 +573,7 @@ fast_kernel(const FastArgs a) {
                     }
                 }
             }
-            // warp aggregation of the per-segment statistics
+            // warp aggregation of the per-group statistics
             float md = disp;
 #pragma unroll
             for (int o = 16; o; o >>= 1) {
@@ -520,7 +585,12 @@ fast_kernel(const FastArgs a) {
                 if (md > 0.f) atomic_max_nonneg_double(&a.slot->max_disp_bits, (double)md);
                 if (n_attr) atomicAdd(&a.st->interactions_attr, n_attr);
                 if (n_rep) atomicAdd(&a.st->interactions_rep, n_rep);
+#ifdef PCSB_COUNT_MEMBERS
+                atomicAdd(&a.st->lane_candidates,
+                          (unsigned long long)evals * (unsigned long long)(g1 - g0));
+#else
                 atomicAdd(&a.st->lane_candidates, (unsigned long long)evals * Q);
+#endif
             }
         }
     }
@@ -532,32 +602,33 @@ fast_kernel(const FastArgs a) {
 // ---------------------------------------------------------------------------
 constexpr int DL = 4;  // lanes per point
 
-__global__ void __launch_bounds__(FAST_THREADS)
+__global__ void __launch_bounds__(FAST_THREADS, PCSB_FAST_MINB)
 density_kernel(const DensityArgs a) {
-    __shared__ float4 smem[FAST_WARPS * (BUF + RING * 32)];
     constexpr int Q = 32 / DL;
+    __shared__ __align__(128) float4 smem[FAST_WARPS * 4 * HR];
+    __shared__ __align__(8) uint64_t bars[FAST_WARPS * 2];
     if (a.done && *a.done) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float4* buf = smem + warp * (BUF + RING * 32);
-    float4* ring = buf + BUF;
-    const int sub = lane % DL;
-    const uint32_t ngroups = (a.nq + Q - 1) / Q;
-    for (;;) {
-        uint32_t grp = 0;
-        if (lane == 0) grp = atomicAdd(a.counter, 1u);
-        grp = __shfl_sync(0xffffffffu, grp, 0);
-        if (grp >= ngroups) break;
-        const Group<DL> G = load_group<DL>(grp, a.nq, a.qlist, a.C, a.Cskeys, a.g, lane);
-        const float4 q = G.q;
-        const EvalConsts ec = make_consts(q, a.kneg, a.K0, 0.f);
-        for (int sg = 0; sg < G.nseg; ++sg) {
-            const bool member = G.qvalid && G.seg == sg;
+    Stage S = make_stage(smem + warp * 4 * HR, bars + 2 * warp, lane);
+    const int qi = lane / DL, sub = lane % DL;
+    uint32_t r0, r1;
+    while (next_unit(a.counter, a.nq, lane, r0, r1)) {
+        const unsigned brk = group_breaks(a.qcodes, a.block_shift, r0, r1, lane);
+        for (uint32_t g0 = r0, g1; g0 < r1; g0 = g1) {
+            g1 = group_end(brk, r0, r1, g0, Q);
+            const uint32_t qpos = g0 + qi;
+            const bool member = qpos < g1;
+            const uint32_t qp = member ? qpos : g0;
+            const uint32_t qslot = __ldg(&a.qlist[qp]);
+            const float4 q = __ldg(&a.C[qslot]);
+            const EvalConsts ec = make_consts(q, a.kneg, a.K0, 0.f);
             const Box box = member_box(q, member);
-            const CellRange cr = cell_range(a.g, box, a.s_pad);
             Acc A = acc_zero();
-            stream_candidates(a.C, a.Cstart, a.g, cr, box, a.scull2, buf, ring, lane, [&](int count) {
-                eval_buffer<DL, K_DENSITY, false, true>(buf, count, lane, sub, q, ec, a.band, a.r2, A);
-            });
+            gather_eval(a.Cpairs, a.Cstart, a.g, box, a.s_pad, S, lane,
+                        [&](const float4* half, int nrec) {
+                            eval_half<DL, K_DENSITY, false, true>(half, nrec, sub, q, ec, a.band,
+                                                                 a.r2, A);
+                        });
             A.s.x = group_sum<DL>(A.s.x + A.s.y);
             A.n = group_sum<DL>(A.n2.x + A.n2.y);
             A.nr = group_sum<DL>(A.nr);
@@ -566,8 +637,8 @@ density_kernel(const DensityArgs a) {
                 // theta(0) = 1 for coincident duplicates; minus one for the point itself
                 const float dens = 1.0f + A.s.x * a.inv_scale + (A.nr - A.n - 1.0f);
                 const float val = a.invert ? 1.0f / dens : dens;
-                if (a.out_sorted) a.out_sorted[G.qslot].w = val;
-                else a.out_internal[__ldg(&a.idx[G.qslot])].w = val;
+                if (a.out_sorted) a.out_sorted[qslot].w = val;
+                else a.out_internal[__ldg(&a.idx[qslot])].w = val;
                 pairs = (unsigned long long)A.n;
             }
 #pragma unroll
@@ -576,7 +647,6 @@ density_kernel(const DensityArgs a) {
         }
     }
 }
-
 
 template <int L, bool W, bool Z, int R>
 void launch_one(const FastArgs& a, int grid, cudaStream_t s) {

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -82,14 +83,24 @@ GridGeom make_grid(const double lo_in[3], const double hi_in[3], double support)
     GridGeom g{};
     double cs;
     int sb;
-    if (cells_for(lo, hi, support * 0.5) <= (double)(1u << 24)) {
+    if (cells_for(lo, hi, support * 0.25) <= (double)(1u << 25)) {
+        cs = support * 0.25;  // rows trimmed at s/4 granularity hug the ball-of-box
+        sb = 1;
+    } else if (cells_for(lo, hi, support * 0.5) <= (double)(1u << 25)) {
         cs = support * 0.5;
-        sb = 2;  // 4x4x4 Z-order inside a cell: groups of 8 queries span ~s/8
+        sb = 1;
     } else {
         cs = support;
         sb = cells_for(lo, hi, cs) <= (double)(1u << 25) ? 2 : 1;
         while (cells_for(lo, hi, cs) > (double)(1u << 27)) cs *= 1.25;
     }
+    // developer knobs (grid experiments): PCSB_CELL_FRAC = cell side / support,
+    // PCSB_SUB_BITS = morton bits per axis inside a cell
+    if (const char* e = std::getenv("PCSB_CELL_FRAC")) {
+        const double f = std::atof(e);
+        if (f > 0.0 && cells_for(lo, hi, support * f) <= (double)(1u << 25)) cs = support * f;
+    }
+    if (const char* e = std::getenv("PCSB_SUB_BITS")) sb = std::atoi(e);
     g.cs = cs;
     g.inv_cs = 1.0 / cs;
     g.ox = lo[0] - cs;
@@ -303,6 +314,12 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     launches_ += 1;
     launches_ += build_cell_start(tsk, nn, 3 * g_.sub_bits, g_.ncells, P_start_, gap_list_,
                                   gap_count_, nullptr, stream_);
+    if (fp32_) {
+        P_pairs_ = (float4*)dalloc(pairs_capacity(nn, g_) * sizeof(float4));
+        P_start_pad_ = (uint32_t*)dalloc(((size_t)g_.ncells + 1) * sizeof(uint32_t));
+        launches_ += build_pairs((const float4*)P_sorted_, tsk, nn, g_, P_start_, P_start_pad_,
+                                 P_pairs_, true, nullptr, stream_);
+    }
 
     // ---- WLOP data density v_j (once) ----
     uint32_t* counter = (uint32_t*)dalloc(sizeof(uint32_t));
@@ -310,10 +327,19 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
         if (fp32_) {
             PCSB_CUDA(cudaMemsetAsync(counter, 0, sizeof(uint32_t), stream_));
             DensityArgs da{};
+            uint32_t *pf = nullptr, *pfs = nullptr, *pq = nullptr;
+            PCSB_CUDA(cudaMalloc(&pf, (size_t)nn * sizeof(uint32_t)));
+            PCSB_CUDA(cudaMalloc(&pfs, (size_t)nn * sizeof(uint32_t)));
+            PCSB_CUDA(cudaMalloc(&pq, (size_t)nn * sizeof(uint32_t)));
+            int bsh = 0;
+            launches_ += build_query_list(tsk, nn, g_, support_, nullptr, 0, 0, pf, pfs, pq, &bsh,
+                                          rs_, nullptr, stream_);
             da.C = (const float4*)P_sorted_;
-            da.Cstart = P_start_;
-            da.Cskeys = tsk;
-            da.qlist = nullptr;
+            da.Cpairs = P_pairs_;
+            da.Cstart = P_start_pad_;
+            da.qlist = pq;
+            da.qcodes = pfs;
+            da.block_shift = bsh;
             da.nq = nn;
             da.g = g_;
             da.s_pad = s_pad_;
@@ -330,6 +356,13 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
             da.counter = counter;
             da.done = nullptr;
             launch_density(da, density_grid_, stream_);
+            // the records carry 1/v_j too
+            launches_ += 1 + build_pairs((const float4*)P_sorted_, tsk, nn, g_, P_start_,
+                                         P_start_pad_, P_pairs_, false, nullptr, stream_);
+            PCSB_CUDA(cudaStreamSynchronize(stream_));
+            cudaFree(pf);
+            cudaFree(pfs);
+            cudaFree(pq);
         } else {
             launch_exact_density<T>((const V*)P_sorted_, P_start_, nullptr, nn, g_, s_pad_, r2_,
                                     support_, d_.h, 0, (V*)P_sorted_, nullptr, nullptr, st_,
@@ -373,9 +406,6 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
         launches_ += 2;
         PCSB_CUDA(cudaStreamSynchronize(stream_));
         cudaFree(iof);
-        q_keys_ = (uint32_t*)dalloc((size_t)mpad_ * sizeof(uint32_t));
-        q_skeys_ = (uint32_t*)dalloc((size_t)mpad_ * sizeof(uint32_t));
-        q_list_ = (uint32_t*)dalloc((size_t)mpad_ * sizeof(uint32_t));
     } else {
         own_lo_ = 0;
         own_cnt_ = (uint32_t)m;
@@ -390,7 +420,14 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     X_skeys_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
     X_sidx_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
     X_start_ = (uint32_t*)dalloc(((size_t)g_.ncells + 1) * sizeof(uint32_t));
+    if (fp32_) {
+        X_pairs_ = (float4*)dalloc(pairs_capacity((uint32_t)mp, g_) * sizeof(float4));
+        X_start_pad_ = (uint32_t*)dalloc(((size_t)g_.ncells + 1) * sizeof(uint32_t));
+    }
     careful_list_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
+    q_keys_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
+    q_skeys_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
+    q_list_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
     ever_iso_ = (uint8_t*)dalloc(mp);
     slots_ = (SweepSlot*)dalloc(kSlotCap * sizeof(SweepSlot));
     slot_cap_ = kSlotCap;
@@ -479,6 +516,9 @@ void Plan::grid_rebuild(const void* Xcur) {
     launches_ += 1;
     launches_ += build_cell_start(X_skeys_, (uint32_t)m_, 3 * g_.sub_bits, g_.ncells, X_start_,
                                   gap_list_, gap_count_, done, stream_);
+    if (fp32_)
+        launches_ += build_pairs((const float4*)X_sorted_, X_skeys_, (uint32_t)m_, g_, X_start_,
+                                 X_start_pad_, X_pairs_, true, done, stream_);
 }
 
 void Plan::allgather_x(void* X, bool f32) {
@@ -499,9 +539,11 @@ void Plan::density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur) {
     if (fp32_) {
         DensityArgs da{};
         da.C = (const float4*)X_sorted_;
-        da.Cstart = X_start_;
-        da.Cskeys = X_skeys_;
+        da.Cpairs = X_pairs_;
+        da.Cstart = X_start_pad_;
         da.qlist = qlist;
+        da.qcodes = q_skeys_;
+        da.block_shift = block_shift_;
         da.nq = nq;
         da.g = g_;
         da.s_pad = s_pad_;
@@ -531,6 +573,10 @@ void Plan::density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur) {
         launch_gather<T>((const V*)Xcur, X_sidx_, (uint32_t)m_, (V*)X_sorted_, &st_->done, stream_);
         launches_ += 1;
     }
+    // the records carry w_i too
+    if (fp32_)
+        launches_ += build_pairs((const float4*)X_sorted_, X_skeys_, (uint32_t)m_, g_, X_start_,
+                                 X_start_pad_, X_pairs_, false, &st_->done, stream_);
 }
 
 template <typename T>
@@ -553,17 +599,12 @@ void Plan::enqueue_sweep(int k) {
 
     // (1) index over the moving set (lop.cpp:39)
     grid_rebuild<T>(cur);
-    const uint32_t* qlist = nullptr;
-    uint32_t nq = (uint32_t)m_;
-    if (multi) {
-        launch_owner_keys(X_sidx_, (uint32_t)m_, own_lo_, own_lo_ + own_cnt_, q_keys_, done, stream_);
-        launches_ += 1;
-        launches_ += radix_sort(q_keys_, nullptr, q_skeys_, q_list_, (uint32_t)m_, 1, rs_, done,
-                                stream_);
-        // q_list_ holds sorted slots? no: values are positions in X_sidx_ order == sorted slots
-        qlist = q_list_;
-        nq = own_cnt_;
-    }
+    // query order (Morton; owned queries first when sharded)
+    launches_ += build_query_list(X_skeys_, (uint32_t)m_, g_, support_, multi ? X_sidx_ : nullptr,
+                                  own_lo_, own_lo_ + own_cnt_, q_keys_, q_skeys_, q_list_,
+                                  &block_shift_, rs_, done, stream_);
+    const uint32_t* qlist = q_list_;
+    const uint32_t nq = multi ? own_cnt_ : (uint32_t)m_;
     // (2) WLOP density of the projected set on X^k
     if (d_.density_weights) density_pass_x<T>(qlist, nq, cur);
     PCSB_CUDA(cudaEventRecord(se.e[1], stream_));
@@ -571,13 +612,15 @@ void Plan::enqueue_sweep(int k) {
     // (3) per-point update (lop.cpp:41-100)
     if (fp32_) {
         FastArgs a{};
-        a.P = (const float4*)P_sorted_;
-        a.Pstart = P_start_;
+        a.Ppairs = P_pairs_;
+        a.Pstart = P_start_pad_;
         a.Xs = (const float4*)X_sorted_;
-        a.Xstart = X_start_;
+        a.Xpairs = X_pairs_;
+        a.Xstart = X_start_pad_;
         a.Xs_idx = X_sidx_;
-        a.Xskeys = X_skeys_;
         a.qlist = qlist;
+        a.qcodes = q_skeys_;
+        a.block_shift = block_shift_;
         a.nq = nq;
         a.g = g_;
         a.s_pad = s_pad_;
@@ -884,9 +927,27 @@ void density_weights_t(const pcs_lop_desc& d, const double* C, uint64_t n, doubl
     PCSB_CUDA(cudaMemsetAsync(counter, 0, sizeof(uint32_t), s));
     if (sizeof(T) == 4) {
         DensityArgs da{};
+        uint32_t* pf = (uint32_t*)tg.alloc(n * sizeof(uint32_t));
+        uint32_t* pfs = (uint32_t*)tg.alloc(n * sizeof(uint32_t));
+        uint32_t* pq = (uint32_t*)tg.alloc(n * sizeof(uint32_t));
+        RadixScratch rs;
+        rs.keys_alt = (uint32_t*)tg.alloc(n * sizeof(uint32_t));
+        rs.vals_alt = (uint32_t*)tg.alloc(n * sizeof(uint32_t));
+        rs.blockhist = (uint32_t*)tg.alloc(radix_blockhist_entries((uint32_t)n) * sizeof(uint32_t));
+        rs.capacity = (uint32_t)n;
+        int bsh = 0;
+        build_query_list(tg.skeys, (uint32_t)n, tg.g, support, nullptr, 0, 0, pf, pfs, pq, &bsh, rs,
+                         nullptr, s);
+        float4* cp = (float4*)tg.alloc(pairs_capacity((uint32_t)n, tg.g) * sizeof(float4));
+        uint32_t* cps = (uint32_t*)tg.alloc(((size_t)tg.g.ncells + 1) * sizeof(uint32_t));
+        build_pairs((const float4*)tg.sorted, tg.skeys, (uint32_t)n, tg.g, tg.start, cps, cp, true,
+                    nullptr, s);
         da.C = (const float4*)tg.sorted;
-        da.Cstart = tg.start;
-        da.Cskeys = tg.skeys;
+        da.Cpairs = cp;
+        da.Cstart = cps;
+        da.qlist = pq;
+        da.qcodes = pfs;
+        da.block_shift = bsh;
         da.nq = (uint32_t)n;
         da.g = tg.g;
         da.s_pad = tg.s_pad;

@@ -80,6 +80,8 @@ private:
     void* P_sorted_ = nullptr;
     uint32_t* P_order_ = nullptr;
     uint32_t* P_start_ = nullptr;
+    float4* P_pairs_ = nullptr;      // fp32 candidate records (kernels.cuh)
+    uint32_t* P_start_pad_ = nullptr;
     // projected set
     void* X_[2] = {nullptr, nullptr};
     void* X_init_ = nullptr;
@@ -88,9 +90,12 @@ private:
     uint32_t* X_skeys_ = nullptr;
     uint32_t* X_sidx_ = nullptr;
     uint32_t* X_start_ = nullptr;
+    float4* X_pairs_ = nullptr;
+    uint32_t* X_start_pad_ = nullptr;
     uint32_t* gap_list_ = nullptr;
     uint32_t* gap_count_ = nullptr;
-    uint32_t* q_keys_ = nullptr;
+    uint32_t* q_keys_ = nullptr;      // Morton codes of the query order (build_query_list)
+    int block_shift_ = 0;
     uint32_t* q_skeys_ = nullptr;
     uint32_t* q_list_ = nullptr;
     uint32_t* careful_list_ = nullptr;
