@@ -43,7 +43,7 @@ void launch_gather(const typename Vec4<T>::type* src, const uint32_t* idx, uint3
 // Query list of the fused kernels: the sorted slots in Morton (Z-curve) order of
 // their sub-cells (<= 10 bits per axis; keys_sorted_tmp keeps the codes), so
 // that consecutive queries are spatially close; a query group never crosses a
-// Morton block of side ~support (code >> block_shift changes), which bounds its
+// Morton block of side ~2 support (code >> block_shift changes), which bounds its
 // box.  With sorted_idx, the queries whose internal index lies in [own_lo,
 // own_hi) come first (multi-GPU ownership).  Returns kernel count.
 int build_query_list(const uint32_t* sorted_keys, uint32_t n, const GridGeom& g, double support,
@@ -85,7 +85,7 @@ struct FastArgs {
     GridGeom g;
     double s_pad;             // support with margin (cell ranges)
     double r2;                // support^2 in fp64: exact re-decision of borderline pairs
-    float scull2;             // (support*(1+2^-10))^2: candidate vs group box
+    float scull2;             // row trimming radius^2 (s_pad + fp32 slack)
     float kneg;               // -log2(e)/h^2
     float K0;                 // log2(e) * r2f / h^2  (hit <=> fma(d2,kneg,K0) >= 0)
     float band;               // |arg| <= band -> borderline, re-decided in fp64

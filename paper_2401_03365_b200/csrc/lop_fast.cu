@@ -156,10 +156,9 @@ __device__ __forceinline__ float4 stage_load(const float4* half, int k) {
 }
 
 // ---------------------------------------------------------------------------
-// Candidate rows of a box: for every cell row (y, z) in range, the x interval
-// [box.x - hx, box.x + hx] with hx = sqrt(s^2 - dy^2 - dz^2), dy/dz the gaps
-// between the row's cells and the box (boundary cells, which also hold clamped
-// outside points, count as unbounded).  Exact superset of the ball-of-box.
+// Candidate rows of a group: every cell row (y, z) within the support of the
+// group's box, each trimmed in x to the union of its queries' ball chords
+// (row_range).  A superset of the union of the queries' neighbourhoods.
 // ---------------------------------------------------------------------------
 struct RowSpan {
     int loy, ny, loz, nrows;
@@ -176,29 +175,45 @@ __device__ __forceinline__ RowSpan row_span(const GridGeom& g, const Box& b, dou
     return r;
 }
 
-__device__ __forceinline__ double axis_gap(int c, int gdim, double o, double cs, double lo,
-                                           double hi) {
-    // gap between [lo, hi] and cell c's interval; boundary cells are unbounded outward
-    const double c0 = (c == 0) ? -INFINITY : o + cs * (double)c;
-    const double c1 = (c == gdim - 1) ? INFINITY : o + cs * (double)(c + 1);
-    return fmax(0.0, fmax(c0 - hi, lo - c1));
-}
+// The queries of the current group (shared memory) and the squared radius the
+// rows are trimmed with: (s_pad + 16 ulp(max |coord|))^2, so that the fp32
+// interval arithmetic below stays a superset of the exact neighbourhoods.
+struct GroupQ {
+    const float4* q;
+    int n;
+    float cull2;
+};
 
-// (begin, end) of row r of the span, trimmed; begin == end if the row is empty
+// (begin, end) of row r of the span, in slot units; begin == end if the row is
+// empty.  The row's x range is the union over the group's queries of the chord
+// of each query's ball through the row (gaps to the row's y/z cell intervals;
+// boundary cells, which also hold clamped outside points, are unbounded).
 __device__ __forceinline__ void row_range(const uint32_t* __restrict__ start, const GridGeom& g,
-                                          const Box& b, const RowSpan& rs, double s_pad, int r,
-                                          uint32_t& rb, uint32_t& re) {
+                                          const GroupQ& G, const RowSpan& rs, int r, uint32_t& rb,
+                                          uint32_t& re) {
     rb = re = 0;
     if (r >= rs.nrows) return;
     const int yy = rs.loy + r % rs.ny;
     const int zz = rs.loz + r / rs.ny;
-    const double dy = axis_gap(yy, g.gy, g.oy, g.cs, (double)b.mny, (double)b.mxy);
-    const double dz = axis_gap(zz, g.gz, g.oz, g.cs, (double)b.mnz, (double)b.mxz);
-    const double rem = s_pad * s_pad - dy * dy - dz * dz;
-    if (!(rem >= 0.0)) return;
-    const double hx = sqrt(rem);
-    const int lox = cell_coord((double)b.mnx - hx, g.ox, g.inv_cs, g.gx);
-    const int hix = cell_coord((double)b.mxx + hx, g.ox, g.inv_cs, g.gx);
+    const float y0 = yy == 0 ? -INFINITY : (float)(g.oy + g.cs * (double)yy);
+    const float y1 = yy == g.gy - 1 ? INFINITY : (float)(g.oy + g.cs * (double)(yy + 1));
+    const float z0 = zz == 0 ? -INFINITY : (float)(g.oz + g.cs * (double)zz);
+    const float z1 = zz == g.gz - 1 ? INFINITY : (float)(g.oz + g.cs * (double)(zz + 1));
+    float lo = INFINITY, hi = -INFINITY;
+    for (int k = 0; k < G.n; ++k) {
+        const float4 q = G.q[k];
+        const float gy = fmaxf(0.f, fmaxf(y0 - q.y, q.y - y1));
+        const float gz = fmaxf(0.f, fmaxf(z0 - q.z, q.z - z1));
+        const float rem = fmaf(-gz, gz, fmaf(-gy, gy, G.cull2));
+        if (rem >= 0.f) {
+            const float hx = rem > 0.f ? rem * rsqrt_approx(rem) : 0.f;
+            lo = fminf(lo, q.x - hx);
+            hi = fmaxf(hi, q.x + hx);
+        }
+    }
+    if (!(lo <= hi)) return;
+    const int lox = cell_coord((double)lo, g.ox, g.inv_cs, g.gx);
+    const int hix = cell_coord((double)hi, g.ox, g.inv_cs, g.gx);
     const uint32_t base = ((uint32_t)zz * (uint32_t)g.gy + (uint32_t)yy) * (uint32_t)g.gx;
     rb = __ldg(&start[base + lox]);
     re = __ldg(&start[base + hix + 1]);
@@ -215,8 +230,8 @@ __device__ __forceinline__ void row_range(const uint32_t* __restrict__ start, co
 template <typename Eval>
 __device__ __forceinline__ void gather_eval(const float4* __restrict__ pairs,
                                             const uint32_t* __restrict__ start, const GridGeom& g,
-                                            const Box& b, double s_pad, Stage& S, int lane,
-                                            Eval&& eval) {
+                                            const Box& b, double s_pad, const GroupQ& G, Stage& S,
+                                            int lane, Eval&& eval) {
     const RowSpan rs = row_span(g, b, s_pad);
     uint32_t cur = 0, fill = 0;
     int pending = -1;
@@ -228,7 +243,7 @@ __device__ __forceinline__ void gather_eval(const float4* __restrict__ pairs,
     };
     for (int r0 = 0; r0 < rs.nrows; r0 += 32) {
         uint32_t rb, re;
-        row_range(start, g, b, rs, s_pad, r0 + lane, rb, re);
+        row_range(start, g, G, rs, r0 + lane, rb, re);
         const uint32_t rec0 = rb >> 1;
         const uint32_t nrec = re > rb ? ((re + 1) >> 1) - rec0 : 0u;
         uint32_t incl = nrec;
@@ -473,6 +488,7 @@ fast_kernel(const FastArgs a) {
     constexpr int KREP = kRep == 1 ? K_REP_INVCUBE : K_REP_NEGLIN;
     __shared__ __align__(128) float4 smem[FAST_WARPS * 4 * HR];
     __shared__ __align__(8) uint64_t bars[FAST_WARPS * 2];
+    __shared__ float4 qsh[FAST_WARPS][Q];
     if (*a.done) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     Stage S = make_stage(smem + warp * 4 * HR, bars + 2 * warp, lane);
@@ -490,11 +506,14 @@ fast_kernel(const FastArgs a) {
             const float4 q = __ldg(&a.Xs[qslot]);
             const EvalConsts ec = make_consts(q, a.kneg, a.K0, a.support);
             const Box box = member_box(q, member);
+            if (member && sub == 0) qsh[warp][qi] = q;
+            __syncwarp();
+            const GroupQ G{qsh[warp], (int)(g1 - g0), a.scull2};
 
             // ---------------- attraction: data candidates (lop.cpp:49-65) ----------------
             Acc at = acc_zero();
             uint32_t evals = 0;  // staged candidates evaluated (x Q queries)
-            gather_eval(a.Ppairs, a.Pstart, a.g, box, a.s_pad, S, lane,
+            gather_eval(a.Ppairs, a.Pstart, a.g, box, a.s_pad, G, S, lane,
                         [&](const float4* half, int nrec) {
                             eval_half<L, K_ATTR, kWlop, kCheckZero>(half, nrec, sub, q, ec, a.band,
                                                                   a.r2, at);
@@ -504,7 +523,7 @@ fast_kernel(const FastArgs a) {
             // ---------------- repulsion: projected-set candidates (lop.cpp:79-97) ----------------
             Acc rp = acc_zero();
             if (kRep != 0) {
-                gather_eval(a.Xpairs, a.Xstart, a.g, box, a.s_pad, S, lane,
+                gather_eval(a.Xpairs, a.Xstart, a.g, box, a.s_pad, G, S, lane,
                             [&](const float4* half, int nrec) {
                                 eval_half<L, KREP, kWlop, true>(half, nrec, sub, q, ec, a.band,
                                                                 a.r2, rp);
@@ -607,6 +626,7 @@ density_kernel(const DensityArgs a) {
     constexpr int Q = 32 / DL;
     __shared__ __align__(128) float4 smem[FAST_WARPS * 4 * HR];
     __shared__ __align__(8) uint64_t bars[FAST_WARPS * 2];
+    __shared__ float4 qsh[FAST_WARPS][Q];
     if (a.done && *a.done) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     Stage S = make_stage(smem + warp * 4 * HR, bars + 2 * warp, lane);
@@ -623,8 +643,11 @@ density_kernel(const DensityArgs a) {
             const float4 q = __ldg(&a.C[qslot]);
             const EvalConsts ec = make_consts(q, a.kneg, a.K0, 0.f);
             const Box box = member_box(q, member);
+            if (member && sub == 0) qsh[warp][qi] = q;
+            __syncwarp();
+            const GroupQ G{qsh[warp], (int)(g1 - g0), a.scull2};
             Acc A = acc_zero();
-            gather_eval(a.Cpairs, a.Cstart, a.g, box, a.s_pad, S, lane,
+            gather_eval(a.Cpairs, a.Cstart, a.g, box, a.s_pad, G, S, lane,
                         [&](const float4* half, int nrec) {
                             eval_half<DL, K_DENSITY, false, true>(half, nrec, sub, q, ec, a.band,
                                                                  a.r2, A);

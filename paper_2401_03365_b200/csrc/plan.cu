@@ -48,13 +48,16 @@ struct F32Consts {
     float kneg, K0, band, scull2, inv_scale;
 };
 
-F32Consts fp32_consts(double h, double r2, double support) {
+// maxabs: largest |coordinate| of the clouds (fp32 rounding scale)
+F32Consts fp32_consts(double h, double r2, double s_pad, double maxabs) {
     F32Consts c;
     c.kneg = (float)(-M_LOG2E / (h * h));
     c.K0 = (float)(-(double)c.kneg * (double)(float)r2);
     c.band = (float)((double)c.K0 * std::ldexp(1.0, -19));
-    const double sc = support * (1.0 + std::ldexp(1.0, -10));  // candidate-vs-box cull
-    c.scull2 = (float)(sc * sc);
+    // row trimming radius (fp32 interval math, lop_fast.cu row_range): s_pad plus
+    // 32 ulps of the coordinate scale, rounded up
+    const double sc = s_pad + std::ldexp(maxabs + s_pad, -18);
+    c.scull2 = std::nextafter((float)(sc * sc), INFINITY);
     c.inv_scale = (float)std::exp2(-(double)c.K0);
     return c;
 }
@@ -282,6 +285,7 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     }
     g_ = make_grid(lo, hi, support_);
     s_pad_ = support_ * (1.0 + std::ldexp(1.0, -10)) + 1e-12 * maxabs;
+    maxabs_ = maxabs;
 
     // ---- data grid (built once, lop.cpp:24) ----
     const uint32_t nn = (uint32_t)n;
@@ -344,7 +348,7 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
             da.g = g_;
             da.s_pad = s_pad_;
             da.r2 = r2_;
-            const F32Consts fc = fp32_consts(d_.h, r2_, support_);
+            const F32Consts fc = fp32_consts(d_.h, r2_, s_pad_, maxabs_);
             da.scull2 = fc.scull2;
             da.kneg = fc.kneg;
             da.K0 = fc.K0;
@@ -548,7 +552,7 @@ void Plan::density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur) {
         da.g = g_;
         da.s_pad = s_pad_;
         da.r2 = r2_;
-        const F32Consts fc = fp32_consts(d_.h, r2_, support_);
+        const F32Consts fc = fp32_consts(d_.h, r2_, s_pad_, maxabs_);
         da.scull2 = fc.scull2;
         da.kneg = fc.kneg;
         da.K0 = fc.K0;
@@ -625,7 +629,7 @@ void Plan::enqueue_sweep(int k) {
         a.g = g_;
         a.s_pad = s_pad_;
         a.r2 = r2_;
-        const F32Consts fc = fp32_consts(d_.h, r2_, support_);
+        const F32Consts fc = fp32_consts(d_.h, r2_, s_pad_, maxabs_);
         a.scull2 = fc.scull2;
         a.kneg = fc.kneg;
         a.K0 = fc.K0;
@@ -785,6 +789,7 @@ struct TmpGrid {
     uint32_t* start = nullptr;
     uint32_t* skeys = nullptr;
     double s_pad = 0;
+    double maxabs = 0;
     std::vector<void*> allocs;
     ~TmpGrid() {
         for (void* p : allocs) cudaFree(p);
@@ -826,6 +831,7 @@ struct TmpGrid {
         }
         g = make_grid(lo, hi, support);
         s_pad = support * (1.0 + std::ldexp(1.0, -10)) + 1e-12 * maxabs;
+        this->maxabs = maxabs;
         uint32_t* keys = (uint32_t*)alloc(nn * sizeof(uint32_t));
         skeys = (uint32_t*)alloc(nn * sizeof(uint32_t));
         order = (uint32_t*)alloc(nn * sizeof(uint32_t));
@@ -952,7 +958,7 @@ void density_weights_t(const pcs_lop_desc& d, const double* C, uint64_t n, doubl
         da.g = tg.g;
         da.s_pad = tg.s_pad;
         da.r2 = r2;
-        const F32Consts fc = fp32_consts(d.h, r2, support);
+        const F32Consts fc = fp32_consts(d.h, r2, tg.s_pad, tg.maxabs);
         da.scull2 = fc.scull2;
         da.kneg = fc.kneg;
         da.K0 = fc.K0;

@@ -71,6 +71,7 @@ private:
     uint32_t mpad_ = 0, chunk_ = 0, own_lo_ = 0, own_cnt_ = 0;
     GridGeom g_{};
     double support_ = 0, r2_ = 0, s_pad_ = 0;
+    double maxabs_ = 0;               // largest |coordinate| at upload (fp32 rounding scale)
     int lanes_ = 4;
     int fast_grid_ = 0, exact_grid_ = 0, density_grid_ = 0;
 
