@@ -45,11 +45,16 @@ constexpr int FAST_THREADS = FAST_WARPS * 32;
 #define PCSB_HR 128
 #endif
 constexpr int HR = PCSB_HR;  // pair records per half (2 candidates each; per warp: 2 halves)
-static_assert(HR % 16 == 0, "a half holds whole 16-record eval steps");
+
 constexpr float kFar = 1.0e18f;
 
-// Unrolled records per lane step: L*U = 16 records per warp step.
-template <int L> struct Unroll { static constexpr int value = 16 / L; };
+// Unrolled records per lane step: L*U = STEP records per warp step.
+#ifndef PCSB_STEP
+#define PCSB_STEP 16
+#endif
+constexpr int STEP = PCSB_STEP;
+static_assert(HR % STEP == 0, "a half holds whole eval steps");
+template <int L> struct Unroll { static constexpr int value = STEP / L; };
 
 struct Box {
     float mnx, mny, mnz, mxx, mxy, mxz;
@@ -221,7 +226,7 @@ __device__ __forceinline__ void row_range(const uint32_t* __restrict__ start, co
 
 // Streams every record of the trimmed rows through the double buffer and calls
 // eval(half_ptr, nrec) on each full half (nrec = HR) and on the final partial
-// one (padded with far records to a multiple of 16).  The rows of a batch (<=
+// one (padded with far records to a multiple of STEP).  The rows of a batch (<=
 // 32, one per lane) are laid end to end (warp scan of their record counts);
 // each lane copies the part of its row that falls in the current half with ONE
 // cp.async.bulk (expect_tx on the half's mbarrier first); lane 0 arrives once
@@ -277,7 +282,7 @@ __device__ __forceinline__ void gather_eval(const float4* __restrict__ pairs,
         }
     }
     if (fill > 0) {
-        const uint32_t padded = (fill + 15u) & ~15u;
+        const uint32_t padded = (fill + STEP - 1) / STEP * STEP;
         float4* h = S.ring + cur * (2 * HR);
         for (uint32_t t = 2 * fill + lane; t < 2 * padded; t += 32)
             h[t] = (t & 1) ? make_float4(kFar, kFar, 0.f, 0.f) : make_float4(kFar, kFar, kFar, kFar);
@@ -292,26 +297,33 @@ __device__ __forceinline__ void gather_eval(const float4* __restrict__ pairs,
 }
 
 // ---------------------------------------------------------------------------
-// Evaluation of a staged half: per pair 2 LDS.128, 3+3 packed ops for d2, one
-// FFMA2 for the exponent, 4 MUFU (2x EX2, 2x RSQ), 2 FSETP (hit mask, MUFU
-// predicated), one FMUL2 and 4-5 packed accumulations.
+// Evaluation of a staged half.  Per record (two candidates, one query): 2 LDS,
+// 3+3 packed ops for d2, one FFMA2 for the exponent, 4 MUFU (2x EX2, 2x RSQ),
+// one FMUL2 for the weight and 4 packed accumulations — 12 FMA-pipe ops; the
+// hit masks, their count and the guard-band minimum run on the integer/ALU
+// pipe (FSET, LOP3, IADD3, FMNMX3), which the packed-FMA/MUFU mix leaves idle
+// (tools/mix_bench.cu: each packed op removed from the mix is ~0.4 ns/record).
 // ---------------------------------------------------------------------------
 enum : int { K_ATTR = 0, K_REP_INVCUBE = 1, K_REP_NEGLIN = 2, K_DENSITY = 3 };
 
 struct Acc {
     float2 s, x, y, z;  // sum w, sum w*(c - q), per candidate parity
-    float2 n2;          // hits, per candidate parity
-    float n, nr;        // hits (after reduction), candidates in range (incl. zero distance)
+    int hneg;           // -(hits)
+    int rneg;           // -(candidates in range, incl. zero distance) (kZero)
 };
 
 __device__ __forceinline__ Acc acc_zero() {
     Acc A;
-    A.s = A.x = A.y = A.z = A.n2 = make_float2(0.f, 0.f);
-    A.n = A.nr = 0.f;
+    A.s = A.x = A.y = A.z = make_float2(0.f, 0.f);
+    A.hneg = A.rneg = 0;
     return A;
 }
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+__device__ __forceinline__ float2 and2(const float2& v, const uint2& m) {
+    return f2(__uint_as_float(__float_as_uint(v.x) & m.x), __uint_as_float(__float_as_uint(v.y) & m.y));
+}
 
 struct EvalConsts {
     float2 nqx, nqy, nqz;  // -q
@@ -319,13 +331,13 @@ struct EvalConsts {
     float support;
 };
 
-// The hit mask m (1.0 / 0.0 per candidate, FSET.BF) multiplies the weight, so
-// MUFU runs unpredicated and the same mask feeds the hit count.
+// The hit mask m (all-ones / zero per candidate) clears theta's bits, so MUFU
+// runs unpredicated and a miss contributes exactly +0.
 template <int KIND, bool kWlop, bool kZero>
-__device__ __forceinline__ float2 pair_weight(const float2& d2, const float2& arg, const float2& m,
+__device__ __forceinline__ float2 pair_weight(const float2& d2, const float2& arg, const uint2& m,
                                               const float4& B, const EvalConsts& ec) {
     float2 w;
-    if (KIND == K_DENSITY) return __fmul2_rn(f2(ex2_approx(arg.x), ex2_approx(arg.y)), m);
+    if (KIND == K_DENSITY) return and2(f2(ex2_approx(arg.x), ex2_approx(arg.y)), m);
     // kZero: zero-distance candidates are masked out, so keep their rsqrt finite
     // (0 * inf would poison the sums); otherwise a zero distance is a hit whose
     // infinite weight surfaces as a non-finite sum and defers the query
@@ -334,19 +346,31 @@ __device__ __forceinline__ float2 pair_weight(const float2& d2, const float2& ar
     if (KIND == K_REP_INVCUBE) {
         // theta/d^5 scaled by s^5 = theta * (s/d)^5 (no fp32 overflow)
         const float2 a2 = __fmul2_rn(d2, ec.kneg);
-        const float2 th = __fmul2_rn(f2(ex2_approx(a2.x), ex2_approx(a2.y)), m);
+        const float2 th = and2(f2(ex2_approx(a2.x), ex2_approx(a2.y)), m);
         const float2 u = __fmul2_rn(rs, f2(ec.support, ec.support));
         const float2 u2 = __fmul2_rn(u, u);
         w = __fmul2_rn(__fmul2_rn(__fmul2_rn(th, u2), u2), u);
     } else {
         // alpha = theta/d (attraction) or beta = theta*1/d (eta = -r), theta scaled by 2^K0
-        w = __fmul2_rn(__fmul2_rn(f2(ex2_approx(arg.x), ex2_approx(arg.y)), m), rs);
+        w = __fmul2_rn(and2(f2(ex2_approx(arg.x), ex2_approx(arg.y)), m), rs);
     }
     if (kWlop) w = __fmul2_rn(w, f2(B.z, B.w));  // 1/v_j (attraction) | w_i' (repulsion)
     return w;
 }
 
-// kZero: exclude d2 == 0 from the hits (and count in-range candidates in nr).
+// all-ones if v >= 0 (FSET: an integer mask, kept off the predicate/select path)
+__device__ __forceinline__ uint32_t ge0_mask(float v) {
+    uint32_t m;
+    asm("set.ge.u32.f32 %0, %1, 0f00000000;" : "=r"(m) : "f"(v));
+    return m;
+}
+__device__ __forceinline__ uint32_t gt0_mask(float v) {
+    uint32_t m;
+    asm("set.gt.u32.f32 %0, %1, 0f00000000;" : "=r"(m) : "f"(v));
+    return m;
+}
+
+// kZero: exclude d2 == 0 from the hits (and count in-range candidates in rneg).
 template <int L, int KIND, bool kWlop, bool kZero>
 __device__ __forceinline__ void eval_pairs(const float4* __restrict__ pb, int nrec, int sub,
                                            const EvalConsts& ec, Acc& A, float& bmin) {
@@ -365,13 +389,14 @@ __device__ __forceinline__ void eval_pairs(const float4* __restrict__ pb, int nr
             d2 = __ffma2_rn(dz, dz, d2);
             const float2 arg = __ffma2_rn(d2, ec.kneg, ec.K0);  // >= 0 <=> d2 <= r2 (fp32)
             bmin = fminf(bmin, fminf(fabsf(arg.x), fabsf(arg.y)));
-            float2 m = f2(arg.x >= 0.f ? 1.f : 0.f, arg.y >= 0.f ? 1.f : 0.f);
+            uint2 m = make_uint2(ge0_mask(arg.x), ge0_mask(arg.y));
             if (kZero) {
-                A.nr += m.x + m.y;
-                m = f2(d2.x > 0.f ? m.x : 0.f, d2.y > 0.f ? m.y : 0.f);
+                A.rneg += (int)m.x + (int)m.y;
+                m.x &= gt0_mask(d2.x);
+                m.y &= gt0_mask(d2.y);
             }
             const float2 w = pair_weight<KIND, kWlop, kZero>(d2, arg, m, B, ec);
-            A.n2 = __fadd2_rn(A.n2, m);
+            A.hneg += (int)m.x + (int)m.y;
             A.s = __fadd2_rn(A.s, w);
             if (KIND != K_DENSITY) {
                 A.x = __ffma2_rn(w, dx, A.x);
@@ -399,14 +424,14 @@ __device__ __forceinline__ void fix_band(const float4* buf, int nrec, int sub, c
             const bool exact = exact_d2(cc.x, cc.y, cc.z, q.x, q.y, q.z) <= r2;
             const bool fp32 = arg >= 0.f;
             if (exact == fp32) continue;
-            const float sgn = exact ? 1.f : -1.f;
+            const int sgn = exact ? 1 : -1;
             const float4 B = make_float4(cc.z, cc.z, cc.w, cc.w);
-            const float2 w2 = pair_weight<KIND, kWlop, kZero>(f2(d2, d2), f2(arg, arg), f2(1.f, 1.f),
-                                                              B, ec);
-            if (kZero) A.nr += sgn;
+            const float2 w2 = pair_weight<KIND, kWlop, kZero>(f2(d2, d2), f2(arg, arg),
+                                                              make_uint2(~0u, ~0u), B, ec);
+            if (kZero) A.rneg -= sgn;
             if (!kZero || d2 > 0.f) {
-                const float w = w2.x * sgn;
-                A.n2.x += sgn;
+                const float w = w2.x * (float)sgn;
+                A.hneg -= sgn;
                 A.s.x += w;
                 if (KIND != K_DENSITY) {
                     A.x.x = fmaf(w, dx, A.x.x);
@@ -429,13 +454,21 @@ __device__ __forceinline__ void eval_half(const float4* half, int nrec, int sub,
 }
 
 template <int L>
+__device__ __forceinline__ int group_isum(int v) {
+#pragma unroll
+    for (int o = 1; o < L; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Per-query totals over its L lanes; afterwards hneg/rneg hold the positive counts.
+template <int L>
 __device__ __forceinline__ void group_reduce(Acc& A, bool with_nr) {
     A.s.x = group_sum<L>(A.s.x + A.s.y);
     A.x.x = group_sum<L>(A.x.x + A.x.y);
     A.y.x = group_sum<L>(A.y.x + A.y.y);
     A.z.x = group_sum<L>(A.z.x + A.z.y);
-    A.n = group_sum<L>(A.n2.x + A.n2.y);
-    if (with_nr) A.nr = group_sum<L>(A.nr);
+    A.hneg = -group_isum<L>(A.hneg);
+    if (with_nr) A.rneg = -group_isum<L>(A.rneg);
 }
 
 __device__ __forceinline__ EvalConsts make_consts(const float4& q, float kneg, float K0,
@@ -543,8 +576,8 @@ fast_kernel(const FastArgs a) {
                 const float sa = at.s.x;
                 bool bad = !isfinite(sa) || !isfinite(at.x.x) || !isfinite(at.y.x) ||
                            !isfinite(at.z.x);
-                const float zeros = kCheckZero ? (at.nr - at.n) : 0.f;
-                if (kCheckZero && zeros > 0.f) {
+                const int zeros = kCheckZero ? (at.rneg - at.hneg) : 0;
+                if (kCheckZero && zeros > 0) {
                     // an fp32 d2 of 0 could hide a distinct pair only for tiny coordinates
                     const float tiny = 0x1p-40f;
                     if (fabsf(q.x) < tiny || fabsf(q.y) < tiny || fabsf(q.z) < tiny) bad = true;
@@ -553,9 +586,9 @@ fast_kernel(const FastArgs a) {
                 if (kRep != 0 && attracted) {
                     // exactly one zero-distance candidate must remain: the query itself;
                     // any other is a coincident pair, counted by the exact path
-                    const float z = rp.nr - rp.n;
+                    const int z = rp.rneg - rp.hneg;
                     bad = bad || !isfinite(rp.s.x) || !isfinite(rp.x.x) || !isfinite(rp.y.x) ||
-                          !isfinite(rp.z.x) || z > 1.5f || z < 0.5f;
+                          !isfinite(rp.z.x) || z != 1;
                 }
                 if (bad) {
                     const uint32_t pos = atomicAdd(&a.slot->careful_count, 1u);
@@ -566,15 +599,15 @@ fast_kernel(const FastArgs a) {
                     if (!attracted) {
                         // zeros > 0: anchored at the coincident sample, which IS q
                         // (lop.cpp:67-69); otherwise isolated and held (lop.cpp:70-73)
-                        isolated = !(kCheckZero && zeros > 0.f);
+                        isolated = !(kCheckZero && zeros > 0);
                     } else {
                         const float inv = 1.0f / sa;  // Weiszfeld quotient (lop.cpp:77)
                         nx = q.x + at.x.x * inv;
                         ny = q.y + at.y.x * inv;
                         nz = q.z + at.z.x * inv;
-                        n_attr = (unsigned long long)at.n;
+                        n_attr = (unsigned long long)at.hneg;
                         if (kRep != 0) {
-                            n_rep = (unsigned long long)rp.n;
+                            n_rep = (unsigned long long)rp.hneg;
                             if (rp.s.x > 0.f) {  // lop.cpp:95-96, x - x' = -(c - q)
                                 const float f = a.mu / rp.s.x;
                                 nx = fmaf(-f, rp.x.x, nx);
@@ -652,17 +685,15 @@ density_kernel(const DensityArgs a) {
                             eval_half<DL, K_DENSITY, false, true>(half, nrec, sub, q, ec, a.band,
                                                                  a.r2, A);
                         });
-            A.s.x = group_sum<DL>(A.s.x + A.s.y);
-            A.n = group_sum<DL>(A.n2.x + A.n2.y);
-            A.nr = group_sum<DL>(A.nr);
+            group_reduce<DL>(A, true);
             unsigned long long pairs = 0;
             if (member && sub == 0) {
                 // theta(0) = 1 for coincident duplicates; minus one for the point itself
-                const float dens = 1.0f + A.s.x * a.inv_scale + (A.nr - A.n - 1.0f);
+                const float dens = 1.0f + A.s.x * a.inv_scale + (float)(A.rneg - A.hneg - 1);
                 const float val = a.invert ? 1.0f / dens : dens;
                 if (a.out_sorted) a.out_sorted[qslot].w = val;
                 else a.out_internal[__ldg(&a.idx[qslot])].w = val;
-                pairs = (unsigned long long)A.n;
+                pairs = (unsigned long long)A.hneg;
             }
 #pragma unroll
             for (int o = 16; o; o >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, o);
