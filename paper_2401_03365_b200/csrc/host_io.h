@@ -1,0 +1,16 @@
+// host_io.h — staged host->device copies of caller buffers (host_io.cpp).
+#pragma once
+
+#include <cstddef>
+
+#include <cuda_runtime.h>
+
+namespace pcsb {
+
+// Copies `bytes` from pageable host memory to device memory on stream s; returns
+// when the host buffer may be reused (the copy itself is complete too).
+void h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t s);
+// Device -> pageable host after the work already queued on s; returns when dst is filled.
+void d2h_staged(void* dst, const void* src, size_t bytes, cudaStream_t s);
+
+}  // namespace pcsb

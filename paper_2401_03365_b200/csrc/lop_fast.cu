@@ -742,10 +742,14 @@ int fast_blocks_per_sm(int lanes_per_point, bool wlop, bool check_zero, int rep_
     (void)check_zero;
     (void)wlop;
     (void)rep_mode;
-    int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fast_kernel<4, false, false, 2>,
-                                                  FAST_THREADS, 0);
-    return b > 0 ? b : 1;
+    static int cached = 0;  // same for every variant (launch bounds + static smem)
+    if (!cached) {
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fast_kernel<4, false, false, 2>,
+                                                      FAST_THREADS, 0);
+        cached = b > 0 ? b : 1;
+    }
+    return cached;
 }
 
 void launch_density(const DensityArgs& a, int grid_blocks, cudaStream_t s) {

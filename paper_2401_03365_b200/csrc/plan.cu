@@ -8,8 +8,10 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <numeric>
 
+#include "host_io.h"
 #include "nccl_dl.h"
 
 namespace pcsb {
@@ -159,11 +161,14 @@ int select_device(int requested) {
     int dev = requested;
     if (dev < 0) PCSB_CUDA(cudaGetDevice(&dev));
     if (dev >= n) throw Failure(PCS_ERR_INVALID_PARAM, "device ordinal out of range");
-    cudaDeviceProp prop;
-    PCSB_CUDA(cudaGetDeviceProperties(&prop, dev));
-    if (prop.major != 10)
+    int major = 0;  // attribute query: cudaGetDeviceProperties costs milliseconds
+    PCSB_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    if (major != 10) {
+        cudaDeviceProp prop;
+        PCSB_CUDA(cudaGetDeviceProperties(&prop, dev));
         throw Failure(PCS_ERR_NO_DEVICE, std::string("device ") + prop.name +
                                              " is not sm_100 (B200); kernels are built for sm_100a only");
+    }
     PCSB_CUDA(cudaSetDevice(dev));
     return dev;
 }
@@ -204,15 +209,48 @@ Plan::~Plan() {
     if (stream_) cudaStreamDestroy(stream_);
 }
 
-void* Plan::dalloc(size_t bytes) {
+// Device memory comes from one stream-ordered pool per device that keeps what it
+// has reserved (release threshold = max): a plan's ~40 buffers and the upload
+// temporaries are then sub-allocations after the first run in a process, and
+// freeing them costs no device synchronisation.
+namespace {
+cudaMemPool_t device_pool(int dev) {
+    static std::mutex mu;
+    static std::vector<cudaMemPool_t> pools;
+    std::lock_guard<std::mutex> lock(mu);
+    if ((int)pools.size() <= dev) pools.resize(dev + 1, nullptr);
+    if (!pools[dev]) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        PCSB_CUDA(cudaMemPoolCreate(&pools[dev], &props));
+        uint64_t keep = ~0ull;
+        PCSB_CUDA(cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep));
+    }
+    return pools[dev];
+}
+}  // namespace
+
+void* Plan::talloc(size_t bytes) {
     void* p = nullptr;
-    PCSB_CUDA(cudaMalloc(&p, bytes ? bytes : 16));
+    PCSB_CUDA(cudaMallocFromPoolAsync(&p, bytes ? bytes : 16, device_pool(device_), stream_));
+    return p;
+}
+
+void Plan::tfree(void* p) {
+    if (p) PCSB_CUDA(cudaFreeAsync(p, stream_));
+}
+
+void* Plan::dalloc(size_t bytes) {
+    void* p = talloc(bytes);
     allocs_.push_back(p);
     return p;
 }
 
 void Plan::free_all() {
-    for (void* p : allocs_) cudaFree(p);
+    for (void* p : allocs_) cudaFreeAsync(p, stream_);
     allocs_.clear();
 }
 
@@ -257,12 +295,12 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     double *dP = nullptr, *dX0 = nullptr;
     V *Pv = nullptr, *X0v = nullptr;
     uint32_t *tk = nullptr, *tsk = nullptr;
-    PCSB_CUDA(cudaMalloc(&dP, n * 3 * sizeof(double)));
-    PCSB_CUDA(cudaMalloc(&dX0, (m ? m : 1) * 3 * sizeof(double)));
-    PCSB_CUDA(cudaMalloc(&Pv, n * sizeof(V)));
-    PCSB_CUDA(cudaMalloc(&X0v, (m ? m : 1) * sizeof(V)));
-    PCSB_CUDA(cudaMemcpyAsync(dP, P, n * 3 * sizeof(double), cudaMemcpyHostToDevice, stream_));
-    if (m) PCSB_CUDA(cudaMemcpyAsync(dX0, X0, m * 3 * sizeof(double), cudaMemcpyHostToDevice, stream_));
+    dP = (decltype(dP))talloc(n * 3 * sizeof(double));
+    dX0 = (decltype(dX0))talloc((m ? m : 1) * 3 * sizeof(double));
+    Pv = (decltype(Pv))talloc(n * sizeof(V));
+    X0v = (decltype(X0v))talloc((m ? m : 1) * sizeof(V));
+    h2d_staged(dP, P, n * 3 * sizeof(double), stream_);
+    if (m) h2d_staged(dX0, X0, m * 3 * sizeof(double), stream_);
     launch_convert_xyz<T>(dP, Pv, n, (T)1, stream_);
     launch_convert_xyz<T>(dX0, X0v, m, (T)0, stream_);
     launches_ += 2;
@@ -306,8 +344,8 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     st_ = (RunState*)dalloc(sizeof(RunState));
     PCSB_CUDA(cudaMemsetAsync(st_, 0, sizeof(RunState), stream_));
 
-    PCSB_CUDA(cudaMalloc(&tk, sort_cap * sizeof(uint32_t)));
-    PCSB_CUDA(cudaMalloc(&tsk, sort_cap * sizeof(uint32_t)));
+    tk = (decltype(tk))talloc(sort_cap * sizeof(uint32_t));
+    tsk = (decltype(tsk))talloc(sort_cap * sizeof(uint32_t));
     P_order_ = (uint32_t*)dalloc(nn * sizeof(uint32_t));
     P_sorted_ = dalloc((size_t)nn * sizeof(V));
     P_start_ = (uint32_t*)dalloc(((size_t)g_.ncells + 1) * sizeof(uint32_t));
@@ -332,9 +370,9 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
             PCSB_CUDA(cudaMemsetAsync(counter, 0, sizeof(uint32_t), stream_));
             DensityArgs da{};
             uint32_t *pf = nullptr, *pfs = nullptr, *pq = nullptr;
-            PCSB_CUDA(cudaMalloc(&pf, (size_t)nn * sizeof(uint32_t)));
-            PCSB_CUDA(cudaMalloc(&pfs, (size_t)nn * sizeof(uint32_t)));
-            PCSB_CUDA(cudaMalloc(&pq, (size_t)nn * sizeof(uint32_t)));
+            pf = (decltype(pf))talloc((size_t)nn * sizeof(uint32_t));
+            pfs = (decltype(pfs))talloc((size_t)nn * sizeof(uint32_t));
+            pq = (decltype(pq))talloc((size_t)nn * sizeof(uint32_t));
             int bsh = 0;
             launches_ += build_query_list(tsk, nn, g_, support_, nullptr, 0, 0, pf, pfs, pq, &bsh,
                                           rs_, nullptr, stream_);
@@ -364,9 +402,9 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
             launches_ += 1 + build_pairs((const float4*)P_sorted_, tsk, nn, g_, P_start_,
                                          P_start_pad_, P_pairs_, false, nullptr, stream_);
             PCSB_CUDA(cudaStreamSynchronize(stream_));
-            cudaFree(pf);
-            cudaFree(pfs);
-            cudaFree(pq);
+            tfree(pf);
+            tfree(pfs);
+            tfree(pq);
         } else {
             launch_exact_density<T>((const V*)P_sorted_, P_start_, nullptr, nn, g_, s_pad_, r2_,
                                     support_, d_.h, 0, (V*)P_sorted_, nullptr, nullptr, st_,
@@ -399,7 +437,7 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
         own_cnt_ = counts[rank_];
         orig_of_internal_ = (uint32_t*)dalloc((size_t)mpad_ * sizeof(uint32_t));
         uint32_t* iof = nullptr;
-        PCSB_CUDA(cudaMalloc(&iof, (m ? m : 1) * sizeof(uint32_t)));
+        iof = (decltype(iof))talloc((m ? m : 1) * sizeof(uint32_t));
         PCSB_CUDA(cudaMemcpyAsync(orig_of_internal_, ooi.data(), (size_t)mpad_ * sizeof(uint32_t),
                                   cudaMemcpyHostToDevice, stream_));
         if (m)
@@ -409,7 +447,7 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
         launch_scatter_init<T>(X0v, iof, (uint32_t)m, (V*)X_init_, stream_);
         launches_ += 2;
         PCSB_CUDA(cudaStreamSynchronize(stream_));
-        cudaFree(iof);
+        tfree(iof);
     } else {
         own_lo_ = 0;
         own_cnt_ = (uint32_t)m;
@@ -434,6 +472,8 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     q_list_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
     ever_iso_ = (uint8_t*)dalloc(mp);
     slots_ = (SweepSlot*)dalloc(kSlotCap * sizeof(SweepSlot));
+    out_xyz_ = (double*)dalloc((size_t)(m ? m : 1) * 3 * sizeof(double));
+    out_iso_ = (uint8_t*)dalloc(m ? m : 1);
     slot_cap_ = kSlotCap;
 
     PCSB_CUDA(cudaEventRecord(e1, stream_));
@@ -446,12 +486,12 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     RunState hs;
     PCSB_CUDA(cudaMemcpy(&hs, st_, sizeof(hs), cudaMemcpyDeviceToHost));
     setup_density_pairs_ = hs.density_pairs;
-    cudaFree(dP);
-    cudaFree(dX0);
-    cudaFree(Pv);
-    cudaFree(X0v);
-    cudaFree(tk);
-    cudaFree(tsk);
+    tfree(dP);
+    tfree(dX0);
+    tfree(Pv);
+    tfree(X0v);
+    tfree(tk);
+    tfree(tsk);
 }
 
 void Plan::reset() {
@@ -706,7 +746,7 @@ void Plan::download(double* X_out, pcs_lop_summary* s, uint32_t* iso, uint64_t c
     if (multi) {
         // per-rank counters -> job totals
         unsigned long long* tmp = nullptr;
-        PCSB_CUDA(cudaMalloc(&tmp, 7 * sizeof(unsigned long long)));
+        tmp = (decltype(tmp))talloc(7 * sizeof(unsigned long long));
         unsigned long long hv[7] = {hs.isolated_events, hs.coincident_pairs, hs.interactions_attr,
                                     hs.interactions_rep, hs.density_pairs, hs.careful_points,
                                     hs.lane_candidates};
@@ -715,7 +755,7 @@ void Plan::download(double* X_out, pcs_lop_summary* s, uint32_t* iso, uint64_t c
                    "ncclAllReduce");
         PCSB_CUDA(cudaMemcpyAsync(hv, tmp, sizeof(hv), cudaMemcpyDeviceToHost, stream_));
         PCSB_CUDA(cudaStreamSynchronize(stream_));
-        cudaFree(tmp);
+        tfree(tmp);
         hs.isolated_events = hv[0];
         hs.coincident_pairs = hv[1];
         hs.interactions_attr = hv[2];
@@ -728,10 +768,8 @@ void Plan::download(double* X_out, pcs_lop_summary* s, uint32_t* iso, uint64_t c
     }
     const int iters = hs.iterations_run;
     void* fin = X_[iters & 1];
-    double* dout = nullptr;
-    uint8_t* diso = nullptr;
-    PCSB_CUDA(cudaMalloc(&dout, (m_ ? m_ : 1) * 3 * sizeof(double)));
-    PCSB_CUDA(cudaMalloc(&diso, m_ ? m_ : 1));
+    double* dout = out_xyz_;
+    uint8_t* diso = out_iso_;
     PCSB_CUDA(cudaMemsetAsync(diso, 0, m_ ? m_ : 1, stream_));
     if (fp32_) launch_unpermute<float>((const float4*)fin, orig_of_internal_, mpad_, dout, stream_);
     else launch_unpermute<double>((const double4*)fin, orig_of_internal_, mpad_, dout, stream_);
@@ -741,12 +779,9 @@ void Plan::download(double* X_out, pcs_lop_summary* s, uint32_t* iso, uint64_t c
         nccl_check(nccl().AllReduce(diso, diso, m_, ncclUint8, ncclMax, (ncclComm_t)comm_, stream_),
                    "ncclAllReduce");
     std::vector<uint8_t> hiso(m_);
-    if (X_out && m_)
-        PCSB_CUDA(cudaMemcpyAsync(X_out, dout, m_ * 3 * sizeof(double), cudaMemcpyDeviceToHost, stream_));
     if (m_) PCSB_CUDA(cudaMemcpyAsync(hiso.data(), diso, m_, cudaMemcpyDeviceToHost, stream_));
+    if (X_out && m_) d2h_staged(X_out, dout, m_ * 3 * sizeof(double), stream_);
     PCSB_CUDA(cudaStreamSynchronize(stream_));
-    cudaFree(dout);
-    cudaFree(diso);
     uint64_t k = 0;
     for (uint64_t i = 0; i < m_; ++i)
         if (hiso[i]) {

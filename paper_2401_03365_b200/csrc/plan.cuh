@@ -59,6 +59,8 @@ private:
     void allgather_x(void* X, bool fp32);
     void free_all();
     void* dalloc(size_t bytes);
+    void* talloc(size_t bytes);  // stream-ordered, from the device pool
+    void tfree(void* p);
 
     pcs_lop_desc d_;
     bool fp32_;
@@ -91,6 +93,8 @@ private:
     uint32_t* X_skeys_ = nullptr;
     uint32_t* X_sidx_ = nullptr;
     uint32_t* X_start_ = nullptr;
+    double* out_xyz_ = nullptr;       // download staging (original order, fp64)
+    uint8_t* out_iso_ = nullptr;
     float4* X_pairs_ = nullptr;
     uint32_t* X_start_pad_ = nullptr;
     uint32_t* gap_list_ = nullptr;

@@ -13,4 +13,4 @@ done
 wait
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$d/libpcs_lop_b200.so" \
   "$d"/{grid_sort,lop_fast,lop_exact,plan,c_api}.o \
-  paper_2401_03365_b200/build/{nccl_dl,generators,pcs_api,shard}.o -ldl
+  paper_2401_03365_b200/build/{nccl_dl,generators,pcs_api,shard,host_io}.o -ldl -lgomp
