@@ -125,6 +125,16 @@ pcs_status pcs_lop_plan_upload(pcs_lop_plan* p, const double* P_xyz, uint64_t n,
 pcs_status pcs_nccl_unique_id(uint8_t id_out[128]);
 pcs_status pcs_lop_plan_set_comm(pcs_lop_plan* p, const uint8_t id[128], int32_t nranks,
                                  int32_t rank);
+/* Loopback groups: nranks (<= 8) plans of ONE process on one device, each driven
+ * by its own host thread, whose exchange step is a host rendezvous plus
+ * device-to-device copies instead of NCCL.  A validation facility for the
+ * sharded path on a single GPU (no kernel waits on another rank); not a
+ * performance mode.  set_loopback must precede upload; destroy the group after
+ * its plans. */
+typedef struct pcs_loopback_group pcs_loopback_group;
+pcs_status pcs_loopback_group_create(int32_t nranks, pcs_loopback_group** out);
+void pcs_loopback_group_destroy(pcs_loopback_group* g);
+pcs_status pcs_lop_plan_set_loopback(pcs_lop_plan* p, pcs_loopback_group* g, int32_t rank);
 /* Restores X to X0 and clears the summary (P, grid and v_j are kept). */
 pcs_status pcs_lop_plan_reset(pcs_lop_plan* p);
 /* Runs `sweeps` further Jacobi sweeps (<= 0: the descriptor's iteration count),

@@ -5,12 +5,14 @@ The operator runs as hand-written sm_100a CUDA kernels in
 """
 from .lop import (  # noqa: F401
     CONFIGS, EmptyCloud, Error, InvalidParam, KernelParams, LopParams, LopPlan, LopSummary,
+    LoopbackGroup,
     NumericalFailure, DeviceUnavailable, add_noise, config_params, config_sizes, density_weights, generate_config,
     generate_surface, grid_sort, lop_project, radius_query_all, shard_layout,
 )
 
 __all__ = [
     "CONFIGS", "EmptyCloud", "Error", "InvalidParam", "KernelParams", "LopParams", "LopPlan",
+    "LoopbackGroup",
     "LopSummary", "NumericalFailure", "DeviceUnavailable", "add_noise", "config_params",
     "config_sizes", "density_weights", "generate_config", "generate_surface", "grid_sort", "lop_project",
     "radius_query_all", "shard_layout",

@@ -35,6 +35,7 @@ EXPORTED = [
     "pcs_lop_plan_synchronize", "pcs_lop_plan_last_run_ms", "pcs_lop_plan_download",
     "pcs_lop_plan_launches", "pcs_radius_query_all", "pcs_density_weights", "pcs_grid_sort", "pcs_generate_surface",
     "pcs_add_noise", "pcs_config_sizes", "pcs_generate_config", "pcs_shard_layout",
+    "pcs_loopback_group_create", "pcs_loopback_group_destroy", "pcs_lop_plan_set_loopback",
 ]
 
 
@@ -109,6 +110,10 @@ def lib():
         L.pcs_lop_plan_upload.argtypes = [C.c_void_p, _dp, C.c_uint64, _dp, C.c_uint64]
         L.pcs_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8)]
         L.pcs_lop_plan_set_comm.argtypes = [C.c_void_p, C.POINTER(C.c_uint8), C.c_int32, C.c_int32]
+        L.pcs_loopback_group_create.argtypes = [C.c_int32, C.POINTER(C.c_void_p)]
+        L.pcs_loopback_group_destroy.argtypes = [C.c_void_p]
+        L.pcs_loopback_group_destroy.restype = None
+        L.pcs_lop_plan_set_loopback.argtypes = [C.c_void_p, C.c_void_p, C.c_int32]
         L.pcs_lop_plan_reset.argtypes = [C.c_void_p]
         L.pcs_lop_plan_run.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
         L.pcs_lop_plan_synchronize.argtypes = [C.c_void_p]

@@ -120,6 +120,24 @@ pcs_status pcs_lop_plan_set_comm(pcs_lop_plan* p, const uint8_t id[128], int32_t
     });
 }
 
+pcs_status pcs_loopback_group_create(int32_t nranks, pcs_loopback_group** out) {
+    return guarded([&] {
+        if (!out) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null output pointer");
+        *out = reinterpret_cast<pcs_loopback_group*>(new pcsb::LoopbackGroup(nranks));
+    });
+}
+
+void pcs_loopback_group_destroy(pcs_loopback_group* g) {
+    delete reinterpret_cast<pcsb::LoopbackGroup*>(g);
+}
+
+pcs_status pcs_lop_plan_set_loopback(pcs_lop_plan* p, pcs_loopback_group* g, int32_t rank) {
+    return guarded([&] {
+        PLAN(p);
+        plan.set_loopback(reinterpret_cast<pcsb::LoopbackGroup*>(g), rank);
+    });
+}
+
 pcs_status pcs_lop_plan_reset(pcs_lop_plan* p) {
     return guarded([&] {
         PLAN(p);

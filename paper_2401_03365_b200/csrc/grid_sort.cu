@@ -253,8 +253,8 @@ __device__ __forceinline__ uint32_t spread3(uint32_t v) {  // 10 bits -> 0,3,6,.
 
 __global__ void morton_keys_kernel(const uint32_t* __restrict__ skeys, uint32_t n, int sb, uint32_t gx,
                                    uint32_t gy, int shift, const uint32_t* __restrict__ sidx,
-                                   uint32_t lo, uint32_t hi, uint32_t* __restrict__ keys,
-                                   const uint32_t* done) {
+                                   uint32_t lo, uint32_t hi, uint32_t owner_bit,
+                                   uint32_t* __restrict__ keys, const uint32_t* done) {
     if (done && *done) return;
     const uint32_t smask = (1u << (3 * sb)) - 1u;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -268,7 +268,7 @@ __global__ void morton_keys_kernel(const uint32_t* __restrict__ skeys, uint32_t 
         uint32_t key = spread3(fx) | (spread3(fy) << 1) | (spread3(fz) << 2);
         if (sidx) {
             const uint32_t o = sidx[i];
-            if (o < lo || o >= hi) key |= 1u << 30;  // not owned: after the owned queries
+            if (o < lo || o >= hi) key |= owner_bit;  // not owned: after the owned queries
         }
         keys[i] = key;
     }
@@ -463,12 +463,14 @@ int build_query_list(const uint32_t* sorted_keys, uint32_t n, const GridGeom& g,
     k = std::max(0, std::min(k, 10));
     *block_shift = 3 * k;
     if (!n) return 0;
+    // the ownership flag sits right above the Morton code, inside the sorted bits
+    const int mbits = 3 * std::min(bits, 10);
     morton_keys_kernel<<<grid_for(n, 256), 256, 0, s>>>(sorted_keys, n, sb, (uint32_t)g.gx,
                                                         (uint32_t)g.gy, shift, sorted_idx, own_lo,
-                                                        own_hi, keys_tmp, done);
-    const int key_bits = 3 * std::min(bits, 10) + (sorted_idx ? 1 : 0);
-    return 1 + radix_sort(keys_tmp, nullptr, keys_sorted_tmp, qlist, n,
-                          key_bits > 30 ? (sorted_idx ? 31 : 30) : std::max(key_bits, 1), scr, done, s);
+                                                        own_hi, 1u << mbits, keys_tmp, done);
+    const int key_bits = mbits + (sorted_idx ? 1 : 0);
+    return 1 + radix_sort(keys_tmp, nullptr, keys_sorted_tmp, qlist, n, std::max(key_bits, 1), scr,
+                          done, s);
 }
 
 int build_cell_start(const uint32_t* sorted_keys, uint32_t n, int sub_shift, uint32_t ncells,

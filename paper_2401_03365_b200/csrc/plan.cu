@@ -12,24 +12,11 @@
 #include <numeric>
 
 #include "host_io.h"
-#include "nccl_dl.h"
 
 namespace pcsb {
 
 namespace {
 constexpr int kSlotCap = 4096;
-
-const NcclApi& nccl() {
-    std::string err;
-    const NcclApi* api = nccl_api(&err);
-    if (!api) throw Failure(PCS_ERR_NCCL, err);
-    return *api;
-}
-
-void nccl_check(ncclResult_t r, const char* what) {
-    if (r != ncclSuccess)
-        throw Failure(PCS_ERR_NCCL, std::string(what) + ": " + nccl().GetErrorString(r));
-}
 
 int bit_width_u64(uint64_t v) {
     int b = 0;
@@ -202,10 +189,7 @@ Plan::~Plan() {
         for (auto e : se.e) cudaEventDestroy(e);
     if (run_ev_[0]) cudaEventDestroy(run_ev_[0]);
     if (run_ev_[1]) cudaEventDestroy(run_ev_[1]);
-    if (comm_) {
-        std::string err;
-        if (const NcclApi* api = nccl_api(&err)) api->CommDestroy((ncclComm_t)comm_);
-    }
+    delete coll_;
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -261,12 +245,20 @@ void Plan::set_comm(const uint8_t id[128], int nranks, int rank) {
     nranks_ = nranks;
     rank_ = rank;
     if (nranks == 1) return;
-    ncclUniqueId uid;
-    static_assert(sizeof(uid) == 128, "ncclUniqueId is 128 bytes");
-    std::memcpy(&uid, id, 128);
-    ncclComm_t c;
-    nccl_check(nccl().CommInitRank(&c, nranks, uid, rank), "ncclCommInitRank");
-    comm_ = c;
+    delete coll_;
+    coll_ = nullptr;
+    coll_ = make_nccl_collectives(id, nranks, rank);
+}
+
+void Plan::set_loopback(LoopbackGroup* g, int rank) {
+    if (uploaded_) throw Failure(PCS_ERR_INVALID_PARAM, "set_loopback must precede upload");
+    if (!g || rank < 0 || rank >= g->nranks())
+        throw Failure(PCS_ERR_INVALID_PARAM, "invalid rank / loopback group");
+    nranks_ = g->nranks();
+    rank_ = rank;
+    delete coll_;
+    coll_ = nullptr;
+    if (nranks_ > 1) coll_ = make_loopback_collectives(g, rank);
 }
 
 void Plan::upload(const double* P, uint64_t n, const double* X0, uint64_t m) {
@@ -566,13 +558,7 @@ void Plan::grid_rebuild(const void* Xcur) {
 }
 
 void Plan::allgather_x(void* X, bool f32) {
-    const NcclApi& api = nccl();
-    const size_t elems = (size_t)chunk_ * 4;
-    char* base = (char*)X;
-    const size_t esz = f32 ? sizeof(float) : sizeof(double);
-    nccl_check(api.AllGather(base + (size_t)rank_ * elems * esz, base, elems,
-                             f32 ? ncclFloat : ncclDouble, (ncclComm_t)comm_, stream_),
-               "ncclAllGather");
+    coll_->allgather(X, (size_t)chunk_ * 4, f32 ? CDType::F32 : CDType::F64, stream_);
 }
 
 template <typename T>
@@ -723,13 +709,10 @@ void Plan::enqueue_sweep(int k) {
     }
     // (4) exchange + aggregation (lop.cpp:102-119)
     if (multi) {
-        const NcclApi& api = nccl();
-        nccl_check(api.GroupStart(), "ncclGroupStart");
+        coll_->group_start();
         allgather_x(nxt, fp32_);
-        nccl_check(api.AllReduce(&slot->max_disp_bits, &slot->max_disp_bits, 1, ncclUint64, ncclMax,
-                                 (ncclComm_t)comm_, stream_),
-                   "ncclAllReduce");
-        nccl_check(api.GroupEnd(), "ncclGroupEnd");
+        coll_->allreduce(&slot->max_disp_bits, 1, CDType::U64, COp::Max, stream_);
+        coll_->group_end();
     }
     launch_finalize_sweep(st_, slot, k, d_.convergence_tol, stream_);
     launches_ += 1;
@@ -751,8 +734,7 @@ void Plan::download(double* X_out, pcs_lop_summary* s, uint32_t* iso, uint64_t c
                                     hs.interactions_rep, hs.density_pairs, hs.careful_points,
                                     hs.lane_candidates};
         PCSB_CUDA(cudaMemcpy(tmp, hv, sizeof(hv), cudaMemcpyHostToDevice));
-        nccl_check(nccl().AllReduce(tmp, tmp, 7, ncclUint64, ncclSum, (ncclComm_t)comm_, stream_),
-                   "ncclAllReduce");
+        coll_->allreduce(tmp, 7, CDType::U64, COp::Sum, stream_);
         PCSB_CUDA(cudaMemcpyAsync(hv, tmp, sizeof(hv), cudaMemcpyDeviceToHost, stream_));
         PCSB_CUDA(cudaStreamSynchronize(stream_));
         tfree(tmp);
@@ -776,8 +758,7 @@ void Plan::download(double* X_out, pcs_lop_summary* s, uint32_t* iso, uint64_t c
     launch_iso_to_orig(ever_iso_, orig_of_internal_, mpad_, diso, stream_);
     launches_ += 2;
     if (multi && m_)
-        nccl_check(nccl().AllReduce(diso, diso, m_, ncclUint8, ncclMax, (ncclComm_t)comm_, stream_),
-                   "ncclAllReduce");
+        coll_->allreduce(diso, m_, CDType::U8, COp::Max, stream_);
     std::vector<uint8_t> hiso(m_);
     if (m_) PCSB_CUDA(cudaMemcpyAsync(hiso.data(), diso, m_, cudaMemcpyDeviceToHost, stream_));
     if (X_out && m_) d2h_staged(X_out, dout, m_ * 3 * sizeof(double), stream_);

@@ -16,6 +16,7 @@
 
 #include "../../include/pcs_lop.h"
 #include "common.cuh"
+#include "comm.h"
 #include "kernels.cuh"
 
 namespace pcsb {
@@ -43,6 +44,8 @@ public:
     Plan& operator=(const Plan&) = delete;
 
     void set_comm(const uint8_t id[128], int nranks, int rank);
+    // In-process rank of a loopback group (comm.h): validation of the sharded path.
+    void set_loopback(LoopbackGroup* g, int rank);
     void upload(const double* P, uint64_t n, const double* X0, uint64_t m);
     void reset();
     void run(int sweeps, bool sync);
@@ -67,7 +70,7 @@ private:
     int device_ = 0;
     cudaStream_t stream_ = nullptr;
     int nranks_ = 1, rank_ = 0;
-    void* comm_ = nullptr;  // ncclComm_t
+    Collectives* coll_ = nullptr;  // owned; NCCL or loopback (comm.h)
 
     uint64_t n_ = 0, m_ = 0;
     uint32_t mpad_ = 0, chunk_ = 0, own_lo_ = 0, own_cnt_ = 0;

@@ -208,6 +208,11 @@ class LopPlan:
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
         _check(L.lib().pcs_lop_plan_set_comm(self._h, buf, nranks, rank))
 
+    def set_loopback(self, group: "LoopbackGroup", rank: int) -> None:
+        """In-process rank of a loopback group (validation of the sharded path on one GPU)."""
+        _check(L.lib().pcs_lop_plan_set_loopback(self._h, group._h, rank))
+        self._group = group  # keep the group alive as long as the plan
+
     def upload(self, data, initial) -> None:
         P = _cloud(data)
         X0 = _cloud(initial)
@@ -238,6 +243,26 @@ class LopPlan:
         _check(L.lib().pcs_lop_plan_download(self._h, _ptr(out), C.byref(s), _ptr(iso, L._u32p),
                                              iso.size))
         return out, _summary(s, iso)
+
+
+class LoopbackGroup:
+    """R in-process ranks on one device (pcs_loopback_group_create).
+
+    Each rank's LopPlan must be driven by its own thread (the exchange step is a
+    host rendezvous).  A validation facility for the multi-GPU path, not a
+    performance mode.
+    """
+
+    def __init__(self, nranks: int):
+        h = C.c_void_p()
+        _check(L.lib().pcs_loopback_group_create(nranks, C.byref(h)))
+        self._h = h
+        self.nranks = nranks
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            L.lib().pcs_loopback_group_destroy(self._h)
+            self._h = None
 
 
 def radius_query_all(cloud, queries, r: float, precision: str = "fp64", device: int = -1):

@@ -129,3 +129,18 @@ def test_config_generators(pb):
     assert P5.shape == (100000, 3)
     # determinism
     assert np.array_equal(pb.generate_config(3, 0.001)[0], pb.generate_config(3, 0.001)[0])
+
+
+def test_loopback_group_host_object(pb):
+    """Loopback groups (in-process ranks) are host objects: creatable without a GPU,
+    1..8 ranks, and a plan on a CPU-only host still fails loudly before using one."""
+    from paper_2401_03365_b200 import _lib
+    lib = _lib.lib()
+    g = C.c_void_p()
+    assert lib.pcs_loopback_group_create(2, C.byref(g)) == 0 and g.value
+    lib.pcs_loopback_group_destroy(g)
+    for bad in (0, 9):
+        h = C.c_void_p()
+        assert lib.pcs_loopback_group_create(bad, C.byref(h)) != 0
+        assert b"1..8" in lib.pcs_last_error()
+    assert lib.pcs_lop_plan_set_loopback(None, None, 0) != 0
