@@ -244,9 +244,9 @@ void Plan::set_comm(const uint8_t id[128], int nranks, int rank) {
         throw Failure(PCS_ERR_INVALID_PARAM, "invalid rank / nranks");
     nranks_ = nranks;
     rank_ = rank;
-    if (nranks == 1) return;
     delete coll_;
     coll_ = nullptr;
+    // a 1-rank clique is legal: it runs the sharded path with real NCCL calls
     coll_ = make_nccl_collectives(id, nranks, rank);
 }
 
@@ -258,7 +258,7 @@ void Plan::set_loopback(LoopbackGroup* g, int rank) {
     rank_ = rank;
     delete coll_;
     coll_ = nullptr;
-    if (nranks_ > 1) coll_ = make_loopback_collectives(g, rank);
+    coll_ = make_loopback_collectives(g, rank);
 }
 
 void Plan::upload(const double* P, uint64_t n, const double* X0, uint64_t m) {
@@ -319,7 +319,7 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
 
     // ---- data grid (built once, lop.cpp:24) ----
     const uint32_t nn = (uint32_t)n;
-    if (nranks_ > 1) {
+    if (sharded()) {
         chunk_ = (uint32_t)((m + nranks_ - 1) / nranks_);
         mpad_ = chunk_ * nranks_;
     } else {
@@ -407,7 +407,7 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
 
     // ---- projected set layout ----
     X_init_ = dalloc((size_t)std::max<uint32_t>(mpad_, 1) * sizeof(V));
-    if (nranks_ > 1) {
+    if (sharded()) {
         // ownership: equal contiguous ranges of the initial cell-sorted order
         std::vector<uint32_t> sidx(m);
         if (m) {
@@ -564,7 +564,7 @@ void Plan::allgather_x(void* X, bool f32) {
 template <typename T>
 void Plan::density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur) {
     using V = typename Vec4<T>::type;
-    const bool multi = nranks_ > 1;
+    const bool multi = sharded();
     SweepSlot* slot = slots_ + (sweeps_issued_ - 1);
     if (fp32_) {
         DensityArgs da{};
@@ -616,7 +616,7 @@ void Plan::enqueue_sweep(int k) {
     void* cur = X_[(k - 1) & 1];
     void* nxt = X_[k & 1];
     const uint32_t* done = &st_->done;
-    const bool multi = nranks_ > 1;
+    const bool multi = sharded();
 
     SweepEvents se;
     if (!event_pool_.empty()) {
@@ -725,7 +725,7 @@ void Plan::download(double* X_out, pcs_lop_summary* s, uint32_t* iso, uint64_t c
     synchronize();
     RunState hs;
     PCSB_CUDA(cudaMemcpy(&hs, st_, sizeof(hs), cudaMemcpyDeviceToHost));
-    const bool multi = nranks_ > 1;
+    const bool multi = sharded();
     if (multi) {
         // per-rank counters -> job totals
         unsigned long long* tmp = nullptr;

@@ -71,6 +71,7 @@ private:
     cudaStream_t stream_ = nullptr;
     int nranks_ = 1, rank_ = 0;
     Collectives* coll_ = nullptr;  // owned; NCCL or loopback (comm.h)
+    bool sharded() const { return coll_ != nullptr; }
 
     uint64_t n_ = 0, m_ = 0;
     uint32_t mpad_ = 0, chunk_ = 0, own_lo_ = 0, own_cnt_ = 0;

@@ -110,3 +110,24 @@ def test_loopback_fp64_lop_config1():
         assert s.coincident_pairs == sref.coincident_pairs
         assert s.isolated_indices == sref.isolated_indices
         assert np.abs(X - ref).max() <= 1e-12 * float(np.linalg.norm(P.max(0) - P.min(0)))
+
+
+def test_nccl_single_rank_clique_matches_plain_run():
+    """A 1-rank NCCL clique runs the sharded plan path with real NCCL calls
+    (dlopen'ed libnccl, in-place all-gather, uint64 max/sum and uint8 max
+    all-reduces) on one GPU: results are bit-identical to the plain plan."""
+    P, X0 = pb.generate_config(4, 0.01)
+    prm, c = pb.config_params(4)
+    prm.iterations = 3
+    kw = dict(eta=c["eta"], density_weights=c["wlop"], precision="fp32")
+    ref, sref = _single(P, X0, prm, **kw)
+    plan = pb.LopPlan(prm, **kw)
+    plan.set_comm(pb.LopPlan.nccl_unique_id(), 1, 0)
+    plan.upload(P, X0)
+    plan.run(prm.iterations)
+    X, s = plan.download()
+    plan.close()
+    assert np.array_equal(X, ref)
+    assert s.interactions_attr == sref.interactions_attr
+    assert s.interactions_rep == sref.interactions_rep
+    assert s.density_pairs == sref.density_pairs
