@@ -164,15 +164,6 @@ rs_scan_rows_kernel(uint32_t* __restrict__ a, uint32_t nblocks, uint32_t* __rest
     if (threadIdx.x == 0) totals[blockIdx.x] = tot;
 }
 
-// Exclusive scan of the 256 digit totals -> digit bases (in place).
-__global__ void __launch_bounds__(256) rs_scan_totals_kernel(uint32_t* __restrict__ totals,
-                                                            const uint32_t* done) {
-    if (done && *done) return;
-    __shared__ uint32_t sh[33];
-    const uint32_t v = totals[threadIdx.x];
-    const uint32_t ex = block_exclusive_scan(v, sh, nullptr);
-    totals[threadIdx.x] = ex;
-}
 
 // Stable scatter: within a tile elements keep their order (round-major,
 // warp-major, lane-minor), ranks inside a warp come from __match_any_sync.
@@ -180,14 +171,17 @@ __global__ void __launch_bounds__(RS_THREADS)
 rs_scatter_kernel(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                   uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, uint32_t n, int shift,
                   uint32_t mask, const uint32_t* __restrict__ blockoff, uint32_t nblocks,
-                  const uint32_t* __restrict__ digit_base, const uint32_t* done) {
+                  const uint32_t* __restrict__ digit_totals, const uint32_t* done) {
     if (done && *done) return;
     __shared__ uint32_t run[256];
     __shared__ uint32_t wcnt[RS_WARPS][256];
     __shared__ uint32_t woff[RS_WARPS][256];
+    __shared__ uint32_t sh[33];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // digit bases: exclusive scan of the 256 digit totals (one digit per thread)
+    const uint32_t dbase = block_exclusive_scan(digit_totals[threadIdx.x], sh, nullptr);
     for (int d = threadIdx.x; d < 256; d += RS_THREADS) {
-        run[d] = digit_base[d] + blockoff[(size_t)d * nblocks + blockIdx.x];
+        run[d] = dbase + blockoff[(size_t)d * nblocks + blockIdx.x];
 #pragma unroll
         for (int w = 0; w < RS_WARPS; ++w) wcnt[w][d] = 0;
     }
@@ -233,39 +227,39 @@ __global__ void gather_kernel(const V* __restrict__ src, const uint32_t* __restr
 }
 
 // Query order of the fused kernels (kernels.cuh build_query_list): Morton
-// (Z-curve) code of the point's sub-cell, decoded from its grid key.
-__device__ __forceinline__ uint32_t compact3(uint32_t m) {  // bits 0,3,6,.. -> 0,1,2,..
-    m &= 0x09249249u;
-    m = (m ^ (m >> 2)) & 0x030C30C3u;
-    m = (m ^ (m >> 4)) & 0x0300F00Fu;
-    m = (m ^ (m >> 8)) & 0x030000FFu;
-    m = (m ^ (m >> 16)) & 0x000003FFu;
-    return m;
-}
-__device__ __forceinline__ uint32_t spread3(uint32_t v) {  // 10 bits -> 0,3,6,..
-    v &= 0x3FFu;
-    v = (v | (v << 16)) & 0x030000FFu;
-    v = (v | (v << 8)) & 0x0300F00Fu;
-    v = (v | (v << 4)) & 0x030C30C3u;
-    v = (v | (v << 2)) & 0x09249249u;
-    return v;
+// (Z-curve) code of the point's half-cell coordinates, with per-axis bit counts
+// (an axis with fewer cells drops out of the top levels), computed from the
+// sorted positions.
+struct MortonAxes {
+    int bits[3];  // code bits per axis (after coarsening by `shift`)
+    int shift;
+};
+
+__device__ __forceinline__ uint32_t half_cell(double x, double o, double inv2, int32_t g2) {
+    const double u = floor((x - o) * inv2);
+    if (!(u >= 0.0)) return 0u;
+    if (u >= (double)(g2 - 1)) return (uint32_t)(g2 - 1);
+    return (uint32_t)u;
 }
 
-__global__ void morton_keys_kernel(const uint32_t* __restrict__ skeys, uint32_t n, int sb, uint32_t gx,
-                                   uint32_t gy, int shift, const uint32_t* __restrict__ sidx,
-                                   uint32_t lo, uint32_t hi, uint32_t owner_bit,
-                                   uint32_t* __restrict__ keys, const uint32_t* done) {
+template <typename V>
+__global__ void morton_keys_kernel(const V* __restrict__ pts, uint32_t n, GridGeom g, MortonAxes ax,
+                                   const uint32_t* __restrict__ sidx, uint32_t lo, uint32_t hi,
+                                   uint32_t owner_bit, uint32_t* __restrict__ keys,
+                                   const uint32_t* done) {
     if (done && *done) return;
-    const uint32_t smask = (1u << (3 * sb)) - 1u;
+    const double inv2 = 2.0 * g.inv_cs;
+    const int top = max(ax.bits[0], max(ax.bits[1], ax.bits[2]));
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t k = skeys[i];
-        const uint32_t cell = k >> (3 * sb), sub = k & smask;
-        const uint32_t cx = cell % gx, r = cell / gx;
-        const uint32_t cy = r % gy, cz = r / gy;
-        const uint32_t fx = ((cx << sb) | compact3(sub)) >> shift;
-        const uint32_t fy = ((cy << sb) | compact3(sub >> 1)) >> shift;
-        const uint32_t fz = ((cz << sb) | compact3(sub >> 2)) >> shift;
-        uint32_t key = spread3(fx) | (spread3(fy) << 1) | (spread3(fz) << 2);
+        const V p = pts[i];
+        const uint32_t f[3] = {half_cell((double)p.x, g.ox, inv2, 2 * g.gx) >> ax.shift,
+                               half_cell((double)p.y, g.oy, inv2, 2 * g.gy) >> ax.shift,
+                               half_cell((double)p.z, g.oz, inv2, 2 * g.gz) >> ax.shift};
+        uint32_t key = 0;
+        for (int l = top - 1; l >= 0; --l)
+#pragma unroll
+            for (int a = 2; a >= 0; --a)
+                if (l < ax.bits[a]) key = (key << 1) | ((f[a] >> l) & 1u);
         if (sidx) {
             const uint32_t o = sidx[i];
             if (o < lo || o >= hi) key |= owner_bit;  // not owned: after the owned queries
@@ -274,38 +268,98 @@ __global__ void morton_keys_kernel(const uint32_t* __restrict__ skeys, uint32_t 
     }
 }
 
-constexpr uint32_t kShortGap = 64;
+// ---- cell table: start[c] = #points with cell < c = a prefix maximum of marks ----
+// mark: for every boundary between two consecutive sorted points (and after the
+// last), start[cell(k) + 1] = k + 1; all other entries 0; then an inclusive
+// prefix-max over [0, ncells] fills every empty cell with the next start.  Work
+// is O(points + cells) in coalesced passes (no per-gap loops).
+constexpr int CS_THREADS = 256;
+constexpr int CS_ITEMS = 16;
+constexpr int CS_TILE = CS_THREADS * CS_ITEMS;
 
-// Thread k (0..n) owns the cells in (cell[k-1], cell[k]]: their lower bound is k.
-__global__ void cell_start_kernel(const uint32_t* __restrict__ skeys, uint32_t n, int sub_shift,
-                                  uint32_t ncells, uint32_t* __restrict__ start,
-                                  uint32_t* __restrict__ gaps, uint32_t* gap_count,
-                                  const uint32_t* done) {
+__global__ void cell_mark_kernel(const uint32_t* __restrict__ skeys, uint32_t n, int sub_shift,
+                                 uint32_t* __restrict__ start, const uint32_t* done) {
     if (done && *done) return;
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k <= n; k += gridDim.x * blockDim.x) {
-        const int64_t cur = (k < n) ? (int64_t)(skeys[k] >> sub_shift) : (int64_t)ncells;
-        const int64_t prev = (k > 0) ? (int64_t)(skeys[k - 1] >> sub_shift) : -1;
-        const int64_t lo = prev + 1, hi = cur;
-        if (lo > hi) continue;
-        if (hi - lo < (int64_t)kShortGap) {
-            for (int64_t c = lo; c <= hi; ++c) start[c] = k;
-        } else {
-            const uint32_t g = atomicAdd(gap_count, 1u);
-            gaps[3 * g] = (uint32_t)lo;
-            gaps[3 * g + 1] = (uint32_t)hi;
-            gaps[3 * g + 2] = k;
-        }
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const uint32_t c = skeys[k] >> sub_shift;
+        if (k + 1 == n || (skeys[k + 1] >> sub_shift) != c) start[c + 1] = k + 1;
     }
 }
 
-__global__ void gap_fill_kernel(uint32_t* __restrict__ start, const uint32_t* __restrict__ gaps,
-                                const uint32_t* gap_count, const uint32_t* done) {
+__global__ void __launch_bounds__(CS_THREADS)
+cell_tile_max_kernel(const uint32_t* __restrict__ a, uint32_t count, uint32_t* __restrict__ tmax,
+                     const uint32_t* done) {
     if (done && *done) return;
-    const uint32_t ng = *gap_count;
-    for (uint32_t g = blockIdx.x; g < ng; g += gridDim.x) {
-        const uint32_t lo = gaps[3 * g], hi = gaps[3 * g + 1], v = gaps[3 * g + 2];
-        for (uint32_t c = lo + threadIdx.x; c <= hi; c += blockDim.x) start[c] = v;
+    __shared__ uint32_t sh[CS_THREADS / 32];
+    const size_t base = (size_t)blockIdx.x * CS_TILE;
+    uint32_t v = 0;
+#pragma unroll
+    for (int i = 0; i < CS_ITEMS; ++i) {
+        const size_t j = base + (size_t)i * CS_THREADS + threadIdx.x;
+        if (j < count) v = max(v, a[j]);
     }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t r = 0;
+        for (int w = 0; w < CS_THREADS / 32; ++w) r = max(r, sh[w]);
+        tmax[blockIdx.x] = r;
+    }
+}
+
+// exclusive prefix max of the tile maxima (one block)
+__global__ void __launch_bounds__(CS_THREADS)
+cell_tiles_scan_kernel(uint32_t* __restrict__ tmax, uint32_t ntiles, const uint32_t* done) {
+    if (done && *done) return;
+    __shared__ uint32_t sh[CS_THREADS];
+    const uint32_t per = (ntiles + CS_THREADS - 1) / CS_THREADS;
+    const uint32_t b = threadIdx.x * per, e = min(b + per, ntiles);
+    uint32_t m = 0;
+    for (uint32_t i = b; i < e; ++i) m = max(m, tmax[i]);
+    sh[threadIdx.x] = m;
+    __syncthreads();
+    uint32_t run = 0;  // exclusive over the preceding threads
+    for (int t = 0; t < (int)threadIdx.x; ++t) run = max(run, sh[t]);
+    for (uint32_t i = b; i < e; ++i) {
+        const uint32_t v = tmax[i];
+        tmax[i] = run;
+        run = max(run, v);
+    }
+}
+
+__global__ void __launch_bounds__(CS_THREADS)
+cell_apply_kernel(uint32_t* __restrict__ a, uint32_t count, const uint32_t* __restrict__ tprefix,
+                  const uint32_t* done) {
+    if (done && *done) return;
+    __shared__ uint32_t sh[CS_THREADS / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // thread t owns CS_ITEMS consecutive entries of the tile
+    const size_t base = (size_t)blockIdx.x * CS_TILE + (size_t)threadIdx.x * CS_ITEMS;
+    uint32_t v[CS_ITEMS];
+    uint32_t run = 0;
+#pragma unroll
+    for (int i = 0; i < CS_ITEMS; ++i) {
+        v[i] = (base + i < count) ? a[base + i] : 0u;
+        run = max(run, v[i]);
+        v[i] = run;
+    }
+    uint32_t incl = run;  // inclusive max over the warp's threads
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl = max(incl, t);
+    }
+    if (lane == 31) sh[warp] = incl;
+    const uint32_t left = __shfl_up_sync(0xffffffffu, incl, 1);
+    __syncthreads();
+    uint32_t pre = tprefix[blockIdx.x];
+    for (int w = 0; w < warp; ++w) pre = max(pre, sh[w]);
+    if (lane > 0) pre = max(pre, left);
+#pragma unroll
+    for (int i = 0; i < CS_ITEMS; ++i)
+        if (base + i < count) a[base + i] = max(pre, v[i]);
 }
 
 // ---- pair records (kernels.cuh) ----------------------------------------------
@@ -428,10 +482,9 @@ int radix_sort(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_
                                                       done);
         uint32_t* totals = scr.blockhist + 256 * (size_t)nblocks;
         rs_scan_rows_kernel<<<256, RS_ROW_THREADS, 0, s>>>(scr.blockhist, nblocks, totals, done);
-        rs_scan_totals_kernel<<<1, 256, 0, s>>>(totals, done);
         rs_scatter_kernel<<<nblocks, RS_THREADS, 0, s>>>(kin, vin, ko, vo, n, shift, mask,
                                                          scr.blockhist, nblocks, totals, done);
-        launches += 4;
+        launches += 3;
         kin = ko;
         vin = vo;
         (void)last;
@@ -446,41 +499,63 @@ void launch_gather(const typename Vec4<T>::type* src, const uint32_t* idx, uint3
     gather_kernel<typename Vec4<T>::type><<<grid_for(n, 256), 256, 0, s>>>(src, idx, n, dst, done);
 }
 
-int build_query_list(const uint32_t* sorted_keys, uint32_t n, const GridGeom& g, double support,
+template <typename V>
+int build_query_list(const V* sorted_pts, uint32_t n, const GridGeom& g, double support,
                      const uint32_t* sorted_idx, uint32_t own_lo, uint32_t own_hi, uint32_t* keys_tmp,
                      uint32_t* keys_sorted_tmp, uint32_t* qlist, int* block_shift,
                      RadixScratch& scr, const uint32_t* done, cudaStream_t s) {
-    const int sb = g.sub_bits;
-    uint32_t fmax = (uint32_t)std::max(g.gx, std::max(g.gy, g.gz)) << sb;
-    int bits = 0;
-    while (bits < 32 && (1ull << bits) < fmax) ++bits;
-    const int shift = bits > 10 ? bits - 10 : 0;
+    auto width = [](uint64_t v) {  // bits to represent 0..v-1
+        int b = 0;
+        while (b < 32 && (1ull << b) < v) ++b;
+        return b;
+    };
+    const int full[3] = {width(2ull * g.gx), width(2ull * g.gy), width(2ull * g.gz)};
+    MortonAxes ax;
+    ax.shift = std::max(0, std::max(full[0], std::max(full[1], full[2])) - 10);
+    int mbits = 0;
+    for (int a = 0; a < 3; ++a) {
+        ax.bits[a] = std::max(0, full[a] - ax.shift);
+        mbits += ax.bits[a];
+    }
     // Morton blocks of side ~2 support: 2^k code units per axis (measured best on
     // the height-field config: fuller groups outweigh their larger boxes)
-    const double unit = g.cs * std::ldexp(1.0, shift - sb);
+    const double unit = 0.5 * g.cs * std::ldexp(1.0, ax.shift);
     int k = (int)std::floor(std::log2(2.0 * support / unit) + 0.5);
     if (const char* e = std::getenv("PCSB_BLOCK_ADJ")) k += std::atoi(e);  // developer knob
     k = std::max(0, std::min(k, 10));
-    *block_shift = 3 * k;
+    *block_shift = 0;
+    for (int a = 0; a < 3; ++a) *block_shift += std::min(k, ax.bits[a]);
     if (!n) return 0;
     // the ownership flag sits right above the Morton code, inside the sorted bits
-    const int mbits = 3 * std::min(bits, 10);
-    morton_keys_kernel<<<grid_for(n, 256), 256, 0, s>>>(sorted_keys, n, sb, (uint32_t)g.gx,
-                                                        (uint32_t)g.gy, shift, sorted_idx, own_lo,
-                                                        own_hi, 1u << mbits, keys_tmp, done);
+    morton_keys_kernel<V><<<grid_for(n, 256), 256, 0, s>>>(sorted_pts, n, g, ax, sorted_idx, own_lo,
+                                                           own_hi, 1u << mbits, keys_tmp, done);
     const int key_bits = mbits + (sorted_idx ? 1 : 0);
     return 1 + radix_sort(keys_tmp, nullptr, keys_sorted_tmp, qlist, n, std::max(key_bits, 1), scr,
                           done, s);
 }
 
+template int build_query_list<float4>(const float4*, uint32_t, const GridGeom&, double,
+                                      const uint32_t*, uint32_t, uint32_t, uint32_t*, uint32_t*,
+                                      uint32_t*, int*, RadixScratch&, const uint32_t*, cudaStream_t);
+template int build_query_list<double4>(const double4*, uint32_t, const GridGeom&, double,
+                                       const uint32_t*, uint32_t, uint32_t, uint32_t*, uint32_t*,
+                                       uint32_t*, int*, RadixScratch&, const uint32_t*, cudaStream_t);
+
+size_t cell_scan_scratch_entries(uint32_t ncells) {
+    return ((size_t)ncells + 1 + CS_TILE - 1) / CS_TILE + 1;
+}
+
 int build_cell_start(const uint32_t* sorted_keys, uint32_t n, int sub_shift, uint32_t ncells,
-                     uint32_t* cell_start, uint32_t* gap_list, uint32_t* gap_count,
-                     const uint32_t* done, cudaStream_t s) {
-    cudaMemsetAsync(gap_count, 0, sizeof(uint32_t), s);
-    cell_start_kernel<<<grid_for((uint64_t)n + 1, 256), 256, 0, s>>>(
-        sorted_keys, n, sub_shift, ncells, cell_start, gap_list, gap_count, done);
-    gap_fill_kernel<<<148 * 2, 256, 0, s>>>(cell_start, gap_list, gap_count, done);
-    return 2;
+                     uint32_t* cell_start, uint32_t* scratch, const uint32_t* done,
+                     cudaStream_t s) {
+    const uint32_t count = ncells + 1;
+    const uint32_t ntiles = (count + CS_TILE - 1) / CS_TILE;
+    cudaMemsetAsync(cell_start, 0, (size_t)count * sizeof(uint32_t), s);
+    if (n) cell_mark_kernel<<<grid_for(n, 256), 256, 0, s>>>(sorted_keys, n, sub_shift, cell_start, done);
+    cell_tile_max_kernel<<<ntiles, CS_THREADS, 0, s>>>(cell_start, count, scratch, done);
+    cell_tiles_scan_kernel<<<1, CS_THREADS, 0, s>>>(scratch, ntiles, done);
+    cell_apply_kernel<<<ntiles, CS_THREADS, 0, s>>>(cell_start, count, scratch, done);
+    return 4;
 }
 
 size_t pairs_capacity(uint32_t n, const GridGeom& g) {

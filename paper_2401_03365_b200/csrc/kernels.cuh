@@ -41,12 +41,14 @@ void launch_gather(const typename Vec4<T>::type* src, const uint32_t* idx, uint3
                    typename Vec4<T>::type* dst, const uint32_t* done, cudaStream_t s);
 
 // Query list of the fused kernels: the sorted slots in Morton (Z-curve) order of
-// their sub-cells (<= 10 bits per axis; keys_sorted_tmp keeps the codes), so
-// that consecutive queries are spatially close; a query group never crosses a
-// Morton block of side ~2 support (code >> block_shift changes), which bounds its
-// box.  With sorted_idx, the queries whose internal index lies in [own_lo,
-// own_hi) come first (multi-GPU ownership).  Returns kernel count.
-int build_query_list(const uint32_t* sorted_keys, uint32_t n, const GridGeom& g, double support,
+// their half-cell coordinates (<= 10 bits per axis, per-axis bit counts;
+// keys_sorted_tmp keeps the codes), so that consecutive queries are spatially
+// close; a query group never crosses a Morton block of side ~2 support (code >>
+// block_shift changes), which bounds its box.  With sorted_idx, the queries
+// whose internal index lies in [own_lo, own_hi) come first (multi-GPU
+// ownership).  Returns kernel count.
+template <typename V>
+int build_query_list(const V* sorted_pts, uint32_t n, const GridGeom& g, double support,
                      const uint32_t* sorted_idx, uint32_t own_lo, uint32_t own_hi, uint32_t* keys_tmp,
                      uint32_t* keys_sorted_tmp, uint32_t* qlist, int* block_shift,
                      RadixScratch& scr, const uint32_t* done, cudaStream_t s);
@@ -54,9 +56,11 @@ int build_query_list(const uint32_t* sorted_keys, uint32_t n, const GridGeom& g,
 constexpr uint32_t kUnitQueries = 32;
 
 // cell_start[c] = first sorted position whose cell >= c, c in [0, ncells]
+// (marks + prefix max; scratch: cell_scan_scratch_entries(ncells) words).
+size_t cell_scan_scratch_entries(uint32_t ncells);
 int build_cell_start(const uint32_t* sorted_keys, uint32_t n, int sub_shift, uint32_t ncells,
-                     uint32_t* cell_start, uint32_t* gap_list, uint32_t* gap_count,
-                     const uint32_t* done, cudaStream_t s);
+                     uint32_t* cell_start, uint32_t* scratch, const uint32_t* done,
+                     cudaStream_t s);
 
 // Pair records: the fp32 candidate layout of the fused kernels.  A sorted cloud
 // is re-laid as records of two consecutive slots, record r = float4 pairs[2r] =

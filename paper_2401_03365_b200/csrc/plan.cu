@@ -73,26 +73,23 @@ GridGeom make_grid(const double lo_in[3], const double hi_in[3], double support)
         if (!(lo[a] <= hi[a])) lo[a] = hi[a] = 0.0;  // empty / non-finite
     }
     GridGeom g{};
+    // keys are plain linear cells (x fastest): the query order comes from a
+    // separate Morton sort of positions (build_query_list)
     double cs;
-    int sb;
     if (cells_for(lo, hi, support * 0.25) <= (double)(1u << 25)) {
         cs = support * 0.25;  // rows trimmed at s/4 granularity hug the ball-of-box
-        sb = 1;
     } else if (cells_for(lo, hi, support * 0.5) <= (double)(1u << 25)) {
         cs = support * 0.5;
-        sb = 1;
     } else {
         cs = support;
-        sb = cells_for(lo, hi, cs) <= (double)(1u << 25) ? 2 : 1;
         while (cells_for(lo, hi, cs) > (double)(1u << 27)) cs *= 1.25;
     }
-    // developer knobs (grid experiments): PCSB_CELL_FRAC = cell side / support,
-    // PCSB_SUB_BITS = morton bits per axis inside a cell
+    // developer knob (grid experiments): PCSB_CELL_FRAC = cell side / support
     if (const char* e = std::getenv("PCSB_CELL_FRAC")) {
         const double f = std::atof(e);
         if (f > 0.0 && cells_for(lo, hi, support * f) <= (double)(1u << 25)) cs = support * f;
     }
-    if (const char* e = std::getenv("PCSB_SUB_BITS")) sb = std::atoi(e);
+    const int sb = 0;
     g.cs = cs;
     g.inv_cs = 1.0 / cs;
     g.ox = lo[0] - cs;
@@ -331,8 +328,7 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     rs_.vals_alt = (uint32_t*)dalloc(sort_cap * sizeof(uint32_t));
     rs_.blockhist = (uint32_t*)dalloc(radix_blockhist_entries(sort_cap) * sizeof(uint32_t));
     rs_.capacity = sort_cap;
-    gap_list_ = (uint32_t*)dalloc(3 * ((size_t)sort_cap + 2) * sizeof(uint32_t));
-    gap_count_ = (uint32_t*)dalloc(sizeof(uint32_t));
+    cell_scratch_ = (uint32_t*)dalloc(cell_scan_scratch_entries(g_.ncells) * sizeof(uint32_t));
     st_ = (RunState*)dalloc(sizeof(RunState));
     PCSB_CUDA(cudaMemsetAsync(st_, 0, sizeof(RunState), stream_));
 
@@ -346,8 +342,8 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     launches_ += radix_sort(tk, nullptr, tsk, P_order_, nn, g_.key_bits, rs_, nullptr, stream_);
     launch_gather<T>(Pv, P_order_, nn, (V*)P_sorted_, nullptr, stream_);
     launches_ += 1;
-    launches_ += build_cell_start(tsk, nn, 3 * g_.sub_bits, g_.ncells, P_start_, gap_list_,
-                                  gap_count_, nullptr, stream_);
+    launches_ += build_cell_start(tsk, nn, 3 * g_.sub_bits, g_.ncells, P_start_, cell_scratch_,
+                                  nullptr, stream_);
     if (fp32_) {
         P_pairs_ = (float4*)dalloc(pairs_capacity(nn, g_) * sizeof(float4));
         P_start_pad_ = (uint32_t*)dalloc(((size_t)g_.ncells + 1) * sizeof(uint32_t));
@@ -366,8 +362,8 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
             pfs = (decltype(pfs))talloc((size_t)nn * sizeof(uint32_t));
             pq = (decltype(pq))talloc((size_t)nn * sizeof(uint32_t));
             int bsh = 0;
-            launches_ += build_query_list(tsk, nn, g_, support_, nullptr, 0, 0, pf, pfs, pq, &bsh,
-                                          rs_, nullptr, stream_);
+            launches_ += build_query_list((const float4*)P_sorted_, nn, g_, support_, nullptr, 0, 0,
+                                          pf, pfs, pq, &bsh, rs_, nullptr, stream_);
             da.C = (const float4*)P_sorted_;
             da.Cpairs = P_pairs_;
             da.Cstart = P_start_pad_;
@@ -551,7 +547,7 @@ void Plan::grid_rebuild(const void* Xcur) {
     launch_gather<T>((const V*)Xcur, X_sidx_, (uint32_t)m_, (V*)X_sorted_, done, stream_);
     launches_ += 1;
     launches_ += build_cell_start(X_skeys_, (uint32_t)m_, 3 * g_.sub_bits, g_.ncells, X_start_,
-                                  gap_list_, gap_count_, done, stream_);
+                                  cell_scratch_, done, stream_);
     if (fp32_)
         launches_ += build_pairs((const float4*)X_sorted_, X_skeys_, (uint32_t)m_, g_, X_start_,
                                  X_start_pad_, X_pairs_, true, done, stream_);
@@ -630,9 +626,9 @@ void Plan::enqueue_sweep(int k) {
     // (1) index over the moving set (lop.cpp:39)
     grid_rebuild<T>(cur);
     // query order (Morton; owned queries first when sharded)
-    launches_ += build_query_list(X_skeys_, (uint32_t)m_, g_, support_, multi ? X_sidx_ : nullptr,
-                                  own_lo_, own_lo_ + own_cnt_, q_keys_, q_skeys_, q_list_,
-                                  &block_shift_, rs_, done, stream_);
+    launches_ += build_query_list((const V*)X_sorted_, (uint32_t)m_, g_, support_,
+                                  multi ? X_sidx_ : nullptr, own_lo_, own_lo_ + own_cnt_, q_keys_,
+                                  q_skeys_, q_list_, &block_shift_, rs_, done, stream_);
     const uint32_t* qlist = q_list_;
     const uint32_t nq = multi ? own_cnt_ : (uint32_t)m_;
     // (2) WLOP density of the projected set on X^k
@@ -858,12 +854,11 @@ struct TmpGrid {
         rs.vals_alt = (uint32_t*)alloc(nn * sizeof(uint32_t));
         rs.blockhist = (uint32_t*)alloc(radix_blockhist_entries(nn) * sizeof(uint32_t));
         rs.capacity = nn;
-        uint32_t* gaps = (uint32_t*)alloc(3 * ((size_t)nn + 2) * sizeof(uint32_t));
-        uint32_t* gc = (uint32_t*)alloc(sizeof(uint32_t));
+        uint32_t* cscr = (uint32_t*)alloc(cell_scan_scratch_entries(g.ncells) * sizeof(uint32_t));
         launch_keys<T>(g, Cv, nn, keys, nullptr, s);
         radix_sort(keys, nullptr, skeys, order, nn, g.key_bits, rs, nullptr, s);
         launch_gather<T>(Cv, order, nn, sorted, nullptr, s);
-        build_cell_start(skeys, nn, 3 * g.sub_bits, g.ncells, start, gaps, gc, nullptr, s);
+        build_cell_start(skeys, nn, 3 * g.sub_bits, g.ncells, start, cscr, nullptr, s);
     }
 };
 
@@ -958,8 +953,8 @@ void density_weights_t(const pcs_lop_desc& d, const double* C, uint64_t n, doubl
         rs.blockhist = (uint32_t*)tg.alloc(radix_blockhist_entries((uint32_t)n) * sizeof(uint32_t));
         rs.capacity = (uint32_t)n;
         int bsh = 0;
-        build_query_list(tg.skeys, (uint32_t)n, tg.g, support, nullptr, 0, 0, pf, pfs, pq, &bsh, rs,
-                         nullptr, s);
+        build_query_list((const float4*)tg.sorted, (uint32_t)n, tg.g, support, nullptr, 0, 0, pf, pfs,
+                         pq, &bsh, rs, nullptr, s);
         float4* cp = (float4*)tg.alloc(pairs_capacity((uint32_t)n, tg.g) * sizeof(float4));
         uint32_t* cps = (uint32_t*)tg.alloc(((size_t)tg.g.ncells + 1) * sizeof(uint32_t));
         build_pairs((const float4*)tg.sorted, tg.skeys, (uint32_t)n, tg.g, tg.start, cps, cp, true,

@@ -101,8 +101,7 @@ private:
     uint8_t* out_iso_ = nullptr;
     float4* X_pairs_ = nullptr;
     uint32_t* X_start_pad_ = nullptr;
-    uint32_t* gap_list_ = nullptr;
-    uint32_t* gap_count_ = nullptr;
+    uint32_t* cell_scratch_ = nullptr;  // cell-table scan (build_cell_start)
     uint32_t* q_keys_ = nullptr;      // Morton codes of the query order (build_query_list)
     int block_shift_ = 0;
     uint32_t* q_skeys_ = nullptr;

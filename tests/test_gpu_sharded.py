@@ -115,7 +115,8 @@ def test_loopback_fp64_lop_config1():
 def test_nccl_single_rank_clique_matches_plain_run():
     """A 1-rank NCCL clique runs the sharded plan path with real NCCL calls
     (dlopen'ed libnccl, in-place all-gather, uint64 max/sum and uint8 max
-    all-reduces) on one GPU: results are bit-identical to the plain plan."""
+    all-reduces) on one GPU.  The sharded layout renumbers points (ties inside a
+    grid cell sort by that number), so only the fp32 summation order differs."""
     P, X0 = pb.generate_config(4, 0.01)
     prm, c = pb.config_params(4)
     prm.iterations = 3
@@ -127,7 +128,7 @@ def test_nccl_single_rank_clique_matches_plain_run():
     plan.run(prm.iterations)
     X, s = plan.download()
     plan.close()
-    assert np.array_equal(X, ref)
+    assert np.abs(X - ref).max() <= 1e-6 * float(np.linalg.norm(P.max(0) - P.min(0)))
     assert s.interactions_attr == sref.interactions_attr
     assert s.interactions_rep == sref.interactions_rep
     assert s.density_pairs == sref.density_pairs
