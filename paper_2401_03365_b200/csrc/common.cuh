@@ -90,6 +90,15 @@ __device__ __forceinline__ uint32_t point_key(const GridGeom& g, double x, doubl
     return (cell << (3 * g.sub_bits)) | m;
 }
 
+// Pair-record layout (kernels.cuh): the first point of grid row `row` sits at
+// record slot start[row*gx] + pair_row_delta(row) — even, and rows never
+// overlap (the delta grows by 0..2 per row).  start = the sorted cloud's cell table.
+__device__ __forceinline__ uint32_t pair_row_delta(const uint32_t* __restrict__ start, uint32_t row,
+                                                   uint32_t gx) {
+    const uint32_t rs = __ldg(&start[(size_t)row * gx]);
+    return row + ((rs + row) & 1u);
+}
+
 // MUFU.EX2 / MUFU.RSQ, flush-to-zero forms (one SFU op each, no range fix-up).
 // Hits have arg >= -band (ex2 >= ~1) and d2 >= FLT_MIN unless the pair is
 // (nearly) coincident, which surfaces as a non-finite sum and is deferred to

@@ -363,16 +363,8 @@ cell_apply_kernel(uint32_t* __restrict__ a, uint32_t count, const uint32_t* __re
 }
 
 // ---- pair records (kernels.cuh) ----------------------------------------------
-// Slot of the first point of grid row `row` is start[row*gx] + row_delta(row):
-// even, and rows never overlap (delta grows by at most 2 per row).
-__device__ __forceinline__ uint32_t row_delta(const uint32_t* __restrict__ start, uint32_t row,
-                                              uint32_t gx) {
-    const uint32_t rs = start[(size_t)row * gx];
-    return row + ((rs + row) & 1u);
-}
-
 __device__ __forceinline__ void write_slot(float* __restrict__ pairs, uint32_t p, float x, float y,
-                                           float z, float w) {
+                                          float z, float w) {
     float* r = pairs + 8 * (size_t)(p >> 1) + (p & 1u);
     r[0] = x;
     r[2] = y;
@@ -382,34 +374,29 @@ __device__ __forceinline__ void write_slot(float* __restrict__ pairs, uint32_t p
 
 constexpr float kPadFar = 1.0e18f;  // padding slot: far from everything, weight 0
 
-// start_pad[c] = start[c] + row_delta(row of c); the slots between two rows
-// (and after the last) become far padding points.
-__global__ void pad_table_kernel(const uint32_t* __restrict__ start, uint32_t ncells, uint32_t gx,
-                                 uint32_t* __restrict__ start_pad, float* __restrict__ pairs,
-                                 const uint32_t* done) {
-    if (done && *done) return;
-    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c <= ncells;
-         c += gridDim.x * blockDim.x) {
-        const uint32_t row = c / gx;
-        const uint32_t d = row_delta(start, row, gx);
-        const uint32_t v = start[c];
-        start_pad[c] = v + d;
-        if (c == row * gx && row > 0) {
-            const uint32_t dp = row_delta(start, row - 1, gx);
-            for (uint32_t p = v + dp; p < v + d; ++p) write_slot(pairs, p, kPadFar, kPadFar, kPadFar, 0.f);
-        }
-    }
-}
-
-__global__ void pack_pairs_kernel(const float4* __restrict__ sorted, const uint32_t* __restrict__ skeys,
-                                  uint32_t n, int sub_shift, uint32_t gx,
-                                  const uint32_t* __restrict__ start, float* __restrict__ pairs,
-                                  const uint32_t* done) {
+// Point i (sorted order) -> its record slot; the last point of a row also
+// writes the padding slots up to the next point's slot (or the even end).
+// With idx, the point is gathered from src[idx[i]] and also stored to sorted_out[i].
+__global__ void pack_pairs_kernel(const float4* __restrict__ src, const uint32_t* __restrict__ idx,
+                                  float4* __restrict__ sorted_out,
+                                  const uint32_t* __restrict__ skeys, uint32_t n, int sub_shift,
+                                  uint32_t gx, const uint32_t* __restrict__ start,
+                                  float* __restrict__ pairs, const uint32_t* done) {
     if (done && *done) return;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const float4 c = sorted[i];
+        const float4 c = src[idx ? idx[i] : i];
+        if (sorted_out) sorted_out[i] = c;
         const uint32_t row = (skeys[i] >> sub_shift) / gx;
-        write_slot(pairs, i + row_delta(start, row, gx), c.x, c.y, c.z, c.w);
+        const uint32_t p = i + pair_row_delta(start, row, gx);
+        write_slot(pairs, p, c.x, c.y, c.z, c.w);
+        uint32_t next;
+        if (i + 1 < n) {
+            const uint32_t nrow = (skeys[i + 1] >> sub_shift) / gx;
+            next = nrow == row ? p + 1 : (i + 1) + pair_row_delta(start, nrow, gx);
+        } else {
+            next = (p + 2) & ~1u;
+        }
+        for (uint32_t q = p + 1; q < next; ++q) write_slot(pairs, q, kPadFar, kPadFar, kPadFar, 0.f);
     }
 }
 
@@ -563,22 +550,14 @@ size_t pairs_capacity(uint32_t n, const GridGeom& g) {
     return (size_t)n + 2 * rows + 4;
 }
 
-int build_pairs(const float4* sorted, const uint32_t* sorted_keys, uint32_t n, const GridGeom& g,
-                const uint32_t* cell_start, uint32_t* start_pad, float4* pairs, bool table,
-                const uint32_t* done, cudaStream_t s) {
-    int k = 0;
-    if (table) {
-        pad_table_kernel<<<grid_for((uint64_t)g.ncells + 1, 256), 256, 0, s>>>(
-            cell_start, g.ncells, (uint32_t)g.gx, start_pad, (float*)pairs, done);
-        ++k;
-    }
-    if (n) {
-        pack_pairs_kernel<<<grid_for(n, 256), 256, 0, s>>>(sorted, sorted_keys, n, 3 * g.sub_bits,
-                                                          (uint32_t)g.gx, cell_start,
-                                                          (float*)pairs, done);
-        ++k;
-    }
-    return k;
+int build_pairs(const float4* src, const uint32_t* idx, float4* sorted_out,
+                const uint32_t* sorted_keys, uint32_t n, const GridGeom& g,
+                const uint32_t* cell_start, float4* pairs, const uint32_t* done, cudaStream_t s) {
+    if (!n) return 0;
+    pack_pairs_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, idx, sorted_out, sorted_keys, n,
+                                                      3 * g.sub_bits, (uint32_t)g.gx, cell_start,
+                                                      (float*)pairs, done);
+    return 1;
 }
 
 template void launch_convert_xyz<float>(const double*, float4*, uint64_t, float, cudaStream_t);

@@ -65,22 +65,23 @@ int build_cell_start(const uint32_t* sorted_keys, uint32_t n, int sub_shift, uin
 // Pair records: the fp32 candidate layout of the fused kernels.  A sorted cloud
 // is re-laid as records of two consecutive slots, record r = float4 pairs[2r] =
 // (x0 x1 y0 y1) and pairs[2r+1] = (z0 z1 w0 w1), with every grid row (fixed
-// y, z) starting at an even slot, so any x-range of a row is a contiguous,
-// 32-byte aligned byte range (one bulk copy).  The slots that pad the rows hold
-// far points of weight 0.  start_pad is the cell table in slot units.
+// y, z) starting at an even slot (slot = sorted position + pair_row_delta(row),
+// common.cuh), so any x-range of a row is a contiguous, 32-byte aligned byte
+// range (one bulk copy).  The slots between rows hold far points of weight 0.
 size_t pairs_capacity(uint32_t n, const GridGeom& g);  // float4 elements
-// table: also (re)build start_pad and the padding (positions changed)
-int build_pairs(const float4* sorted, const uint32_t* sorted_keys, uint32_t n, const GridGeom& g,
-                const uint32_t* cell_start, uint32_t* start_pad, float4* pairs, bool table,
-                const uint32_t* done, cudaStream_t s);
+// Packs the sorted cloud src[0..n) — or, with idx, gathers src[idx[i]] and also
+// writes sorted_out[i] — into records; cell_start = the sorted cloud's cell table.
+int build_pairs(const float4* src, const uint32_t* idx, float4* sorted_out,
+                const uint32_t* sorted_keys, uint32_t n, const GridGeom& g,
+                const uint32_t* cell_start, float4* pairs, const uint32_t* done, cudaStream_t s);
 
 // ---- fused fp32 kernels (lop_fast.cu) ---------------------------------------
 struct FastArgs {
     const float4* Ppairs;     // data, pair records; w = 1/v_j (WLOP) or 1
-    const uint32_t* Pstart;   // slot table of Ppairs
+    const uint32_t* Pstart;   // cell table of the sorted data (+ row delta = record slot)
     const float4* Xs;         // projected set, sorted (queries)
     const float4* Xpairs;     // projected set, pair records; w = w_i (WLOP)
-    const uint32_t* Xstart;   // slot table of Xpairs
+    const uint32_t* Xstart;   // cell table of the sorted projected set
     const uint32_t* Xs_idx;   // sorted slot -> internal index
     const uint32_t* qlist;    // queries (sorted slots, build_query_list order)
     const uint32_t* qcodes;   // their Morton codes
@@ -111,7 +112,7 @@ int fast_blocks_per_sm(int lanes_per_point, bool wlop, bool check_zero, int rep_
 struct DensityArgs {
     const float4* C;          // cloud, sorted (queries)
     const float4* Cpairs;     // cloud, pair records (candidates)
-    const uint32_t* Cstart;   // slot table of Cpairs
+    const uint32_t* Cstart;   // cell table of the sorted cloud
     const uint32_t* qlist;    // queries (sorted slots, build_query_list order)
     const uint32_t* qcodes;
     int block_shift;

@@ -189,7 +189,7 @@ struct GroupQ {
     float cull2;
 };
 
-// (begin, end) of row r of the span, in slot units; begin == end if the row is
+// (begin, end) of row r of the span, in record-slot units; begin == end if the row is
 // empty.  The row's x range is the union over the group's queries of the chord
 // of each query's ball through the row (gaps to the row's y/z cell intervals;
 // boundary cells, which also hold clamped outside points, are unbounded).
@@ -219,9 +219,11 @@ __device__ __forceinline__ void row_range(const uint32_t* __restrict__ start, co
     if (!(lo <= hi)) return;
     const int lox = cell_coord((double)lo, g.ox, g.inv_cs, g.gx);
     const int hix = cell_coord((double)hi, g.ox, g.inv_cs, g.gx);
-    const uint32_t base = ((uint32_t)zz * (uint32_t)g.gy + (uint32_t)yy) * (uint32_t)g.gx;
-    rb = __ldg(&start[base + lox]);
-    re = __ldg(&start[base + hix + 1]);
+    const uint32_t row = (uint32_t)zz * (uint32_t)g.gy + (uint32_t)yy;
+    const uint32_t base = row * (uint32_t)g.gx;
+    const uint32_t delta = pair_row_delta(start, row, (uint32_t)g.gx);  // record-slot shift
+    rb = __ldg(&start[base + lox]) + delta;
+    re = __ldg(&start[base + hix + 1]) + delta;
 }
 
 // Streams every record of the trimmed rows through the double buffer and calls

@@ -346,9 +346,8 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
                                   nullptr, stream_);
     if (fp32_) {
         P_pairs_ = (float4*)dalloc(pairs_capacity(nn, g_) * sizeof(float4));
-        P_start_pad_ = (uint32_t*)dalloc(((size_t)g_.ncells + 1) * sizeof(uint32_t));
-        launches_ += build_pairs((const float4*)P_sorted_, tsk, nn, g_, P_start_, P_start_pad_,
-                                 P_pairs_, true, nullptr, stream_);
+        launches_ += build_pairs((const float4*)P_sorted_, nullptr, nullptr, tsk, nn, g_, P_start_,
+                                 P_pairs_, nullptr, stream_);
     }
 
     // ---- WLOP data density v_j (once) ----
@@ -366,7 +365,7 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
                                           pf, pfs, pq, &bsh, rs_, nullptr, stream_);
             da.C = (const float4*)P_sorted_;
             da.Cpairs = P_pairs_;
-            da.Cstart = P_start_pad_;
+            da.Cstart = P_start_;
             da.qlist = pq;
             da.qcodes = pfs;
             da.block_shift = bsh;
@@ -387,8 +386,8 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
             da.done = nullptr;
             launch_density(da, density_grid_, stream_);
             // the records carry 1/v_j too
-            launches_ += 1 + build_pairs((const float4*)P_sorted_, tsk, nn, g_, P_start_,
-                                         P_start_pad_, P_pairs_, false, nullptr, stream_);
+            launches_ += 1 + build_pairs((const float4*)P_sorted_, nullptr, nullptr, tsk, nn, g_,
+                                         P_start_, P_pairs_, nullptr, stream_);
             PCSB_CUDA(cudaStreamSynchronize(stream_));
             tfree(pf);
             tfree(pfs);
@@ -452,7 +451,6 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     X_start_ = (uint32_t*)dalloc(((size_t)g_.ncells + 1) * sizeof(uint32_t));
     if (fp32_) {
         X_pairs_ = (float4*)dalloc(pairs_capacity((uint32_t)mp, g_) * sizeof(float4));
-        X_start_pad_ = (uint32_t*)dalloc(((size_t)g_.ncells + 1) * sizeof(uint32_t));
     }
     careful_list_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
     q_keys_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
@@ -544,13 +542,15 @@ void Plan::grid_rebuild(const void* Xcur) {
     launches_ += 1;
     launches_ += radix_sort(X_keys_, nullptr, X_skeys_, X_sidx_, mpad_, g_.key_bits, rs_, done,
                             stream_);
-    launch_gather<T>((const V*)Xcur, X_sidx_, (uint32_t)m_, (V*)X_sorted_, done, stream_);
-    launches_ += 1;
     launches_ += build_cell_start(X_skeys_, (uint32_t)m_, 3 * g_.sub_bits, g_.ncells, X_start_,
                                   cell_scratch_, done, stream_);
-    if (fp32_)
-        launches_ += build_pairs((const float4*)X_sorted_, X_skeys_, (uint32_t)m_, g_, X_start_,
-                                 X_start_pad_, X_pairs_, true, done, stream_);
+    if (fp32_) {  // gather + pack in one pass
+        launches_ += build_pairs((const float4*)Xcur, X_sidx_, (float4*)X_sorted_, X_skeys_,
+                                 (uint32_t)m_, g_, X_start_, X_pairs_, done, stream_);
+    } else {
+        launch_gather<T>((const V*)Xcur, X_sidx_, (uint32_t)m_, (V*)X_sorted_, done, stream_);
+        launches_ += 1;
+    }
 }
 
 void Plan::allgather_x(void* X, bool f32) {
@@ -566,7 +566,7 @@ void Plan::density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur) {
         DensityArgs da{};
         da.C = (const float4*)X_sorted_;
         da.Cpairs = X_pairs_;
-        da.Cstart = X_start_pad_;
+        da.Cstart = X_start_;
         da.qlist = qlist;
         da.qcodes = q_skeys_;
         da.block_shift = block_shift_;
@@ -601,8 +601,8 @@ void Plan::density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur) {
     }
     // the records carry w_i too
     if (fp32_)
-        launches_ += build_pairs((const float4*)X_sorted_, X_skeys_, (uint32_t)m_, g_, X_start_,
-                                 X_start_pad_, X_pairs_, false, &st_->done, stream_);
+        launches_ += build_pairs((const float4*)X_sorted_, nullptr, nullptr, X_skeys_, (uint32_t)m_,
+                                 g_, X_start_, X_pairs_, &st_->done, stream_);
 }
 
 template <typename T>
@@ -639,10 +639,10 @@ void Plan::enqueue_sweep(int k) {
     if (fp32_) {
         FastArgs a{};
         a.Ppairs = P_pairs_;
-        a.Pstart = P_start_pad_;
+        a.Pstart = P_start_;
         a.Xs = (const float4*)X_sorted_;
         a.Xpairs = X_pairs_;
-        a.Xstart = X_start_pad_;
+        a.Xstart = X_start_;
         a.Xs_idx = X_sidx_;
         a.qlist = qlist;
         a.qcodes = q_skeys_;
@@ -956,12 +956,11 @@ void density_weights_t(const pcs_lop_desc& d, const double* C, uint64_t n, doubl
         build_query_list((const float4*)tg.sorted, (uint32_t)n, tg.g, support, nullptr, 0, 0, pf, pfs,
                          pq, &bsh, rs, nullptr, s);
         float4* cp = (float4*)tg.alloc(pairs_capacity((uint32_t)n, tg.g) * sizeof(float4));
-        uint32_t* cps = (uint32_t*)tg.alloc(((size_t)tg.g.ncells + 1) * sizeof(uint32_t));
-        build_pairs((const float4*)tg.sorted, tg.skeys, (uint32_t)n, tg.g, tg.start, cps, cp, true,
+        build_pairs((const float4*)tg.sorted, nullptr, nullptr, tg.skeys, (uint32_t)n, tg.g, tg.start, cp,
                     nullptr, s);
         da.C = (const float4*)tg.sorted;
         da.Cpairs = cp;
-        da.Cstart = cps;
+        da.Cstart = tg.start;
         da.qlist = pq;
         da.qcodes = pfs;
         da.block_shift = bsh;

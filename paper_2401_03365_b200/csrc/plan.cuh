@@ -88,7 +88,6 @@ private:
     uint32_t* P_order_ = nullptr;
     uint32_t* P_start_ = nullptr;
     float4* P_pairs_ = nullptr;      // fp32 candidate records (kernels.cuh)
-    uint32_t* P_start_pad_ = nullptr;
     // projected set
     void* X_[2] = {nullptr, nullptr};
     void* X_init_ = nullptr;
@@ -100,7 +99,6 @@ private:
     double* out_xyz_ = nullptr;       // download staging (original order, fp64)
     uint8_t* out_iso_ = nullptr;
     float4* X_pairs_ = nullptr;
-    uint32_t* X_start_pad_ = nullptr;
     uint32_t* cell_scratch_ = nullptr;  // cell-table scan (build_cell_start)
     uint32_t* q_keys_ = nullptr;      // Morton codes of the query order (build_query_list)
     int block_shift_ = 0;
