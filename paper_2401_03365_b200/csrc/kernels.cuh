@@ -87,7 +87,7 @@ struct FastArgs {
     const uint32_t* qcodes;   // their Morton codes
     int block_shift;          // groups stay inside one (code >> block_shift) block
     uint32_t nq;
-    GridGeom g;
+    GridGeom gP, gX;          // grids of the data and of the projected set
     double s_pad;             // support with margin (cell ranges)
     double r2;                // support^2 in fp64: exact re-decision of borderline pairs
     float scull2;             // row trimming radius^2 (s_pad + fp32 slack)
@@ -144,7 +144,7 @@ struct ExactArgs {
     const uint32_t* qlist;    // queries (sorted slots); nullptr = 0..nq-1
     const uint32_t* nq_dev;   // if non-null, the query count lives on the device
     uint32_t nq;
-    GridGeom g;
+    GridGeom g, gX;           // grids of the data and of the projected set
     double s_pad, r2, support, h, mu;
     int eta_kind;             // 0 inv-cube, 1 neg-linear
     int wlop;

@@ -163,7 +163,8 @@ __global__ void __launch_bounds__(EX_THREADS) exact_kernel(const ExactArgs<T> a)
             // ---- repulsion over the projected set (lop.cpp:79-97) ----
             if (a.mu > 0.0) {
                 double rs = 0.0, rx = 0.0, ry = 0.0, rz = 0.0;
-                for_each_candidate(a.Xstart, a.g, rw, lane, [&](uint32_t k) {
+                const Rows rx_ = rows_around(a.gX, x, y, z, a.s_pad);
+                for_each_candidate(a.Xstart, a.gX, rx_, lane, [&](uint32_t k) {
                     if (a.Xs_idx[k] == q_int) return;
                     const V c = a.Xs[k];
                     const double cx = (double)c.x, cy = (double)c.y, cz = (double)c.z;

@@ -548,7 +548,7 @@ fast_kernel(const FastArgs a) {
             // ---------------- attraction: data candidates (lop.cpp:49-65) ----------------
             Acc at = acc_zero();
             uint32_t evals = 0;  // staged candidates evaluated (x Q queries)
-            gather_eval(a.Ppairs, a.Pstart, a.g, box, a.s_pad, G, S, lane,
+            gather_eval(a.Ppairs, a.Pstart, a.gP, box, a.s_pad, G, S, lane,
                         [&](const float4* half, int nrec) {
                             eval_half<L, K_ATTR, kWlop, kCheckZero>(half, nrec, sub, q, ec, a.band,
                                                                   a.r2, at);
@@ -558,7 +558,7 @@ fast_kernel(const FastArgs a) {
             // ---------------- repulsion: projected-set candidates (lop.cpp:79-97) ----------------
             Acc rp = acc_zero();
             if (kRep != 0) {
-                gather_eval(a.Xpairs, a.Xstart, a.g, box, a.s_pad, G, S, lane,
+                gather_eval(a.Xpairs, a.Xstart, a.gX, box, a.s_pad, G, S, lane,
                             [&](const float4* half, int nrec) {
                                 eval_half<L, KREP, kWlop, true>(half, nrec, sub, q, ec, a.band,
                                                                 a.r2, rp);

@@ -104,6 +104,44 @@ GridGeom make_grid(const double lo_in[3], const double hi_in[3], double support)
     return g;
 }
 
+// Grid of the projected set: the data grid's cell side times `scale` (>= 1),
+// over the same box; the projected set is usually much sparser than the data,
+// so coarser rows carry enough candidates to amortise their per-row cost.
+GridGeom make_grid_scaled(const double lo_in[3], const double hi_in[3], double support, double scale,
+                          const GridGeom& base) {
+    if (!(scale > 1.0)) return base;
+    double lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = lo_in[a];
+        hi[a] = hi_in[a];
+        if (!(lo[a] <= hi[a])) lo[a] = hi[a] = 0.0;
+    }
+    (void)support;
+    GridGeom g = base;
+    g.cs = base.cs * scale;
+    g.inv_cs = 1.0 / g.cs;
+    g.ox = lo[0] - g.cs;
+    g.oy = lo[1] - g.cs;
+    g.oz = lo[2] - g.cs;
+    g.gx = (int32_t)std::floor((hi[0] - g.ox) * g.inv_cs) + 2;
+    g.gy = (int32_t)std::floor((hi[1] - g.oy) * g.inv_cs) + 2;
+    g.gz = (int32_t)std::floor((hi[2] - g.oz) * g.inv_cs) + 2;
+    g.sub_bits = 0;
+    g.ncells = (uint32_t)g.gx * (uint32_t)g.gy * (uint32_t)g.gz;
+    g.key_bits = bit_width_u64((uint64_t)g.ncells);
+    return g;
+}
+
+// x-grid scale (developer knob PCSB_XCELL, default 1 = the data grid).  Measured
+// with 2x: config 3 -2.4% sweep time, config 2 -6%, but config 5 +5% and the
+// WLOP config 4 +9% (its density pass over X loses more to coarse rows).
+double x_cell_scale(uint64_t n, uint64_t m) {
+    (void)n;
+    (void)m;
+    if (const char* e = std::getenv("PCSB_XCELL")) return std::atof(e);
+    return 1.0;
+}
+
 void validate_desc(const pcs_lop_desc& d) {
     // LopParams::validate + KernelParams::validate (proj/include/pcs/lop.hpp:18-26,
     // proj/include/pcs/kernels.hpp:18-23), same messages.
@@ -311,6 +349,7 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
         maxabs = std::max(maxabs, std::max(std::fabs(lo[a]), std::fabs(hi[a])));
     }
     g_ = make_grid(lo, hi, support_);
+    gX_ = make_grid_scaled(lo, hi, support_, x_cell_scale(n, m), g_);
     s_pad_ = support_ * (1.0 + std::ldexp(1.0, -10)) + 1e-12 * maxabs;
     maxabs_ = maxabs;
 
@@ -328,7 +367,8 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     rs_.vals_alt = (uint32_t*)dalloc(sort_cap * sizeof(uint32_t));
     rs_.blockhist = (uint32_t*)dalloc(radix_blockhist_entries(sort_cap) * sizeof(uint32_t));
     rs_.capacity = sort_cap;
-    cell_scratch_ = (uint32_t*)dalloc(cell_scan_scratch_entries(g_.ncells) * sizeof(uint32_t));
+    cell_scratch_ = (uint32_t*)dalloc(
+        cell_scan_scratch_entries(std::max(g_.ncells, gX_.ncells)) * sizeof(uint32_t));
     st_ = (RunState*)dalloc(sizeof(RunState));
     PCSB_CUDA(cudaMemsetAsync(st_, 0, sizeof(RunState), stream_));
 
@@ -448,9 +488,9 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     X_keys_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
     X_skeys_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
     X_sidx_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
-    X_start_ = (uint32_t*)dalloc(((size_t)g_.ncells + 1) * sizeof(uint32_t));
+    X_start_ = (uint32_t*)dalloc(((size_t)gX_.ncells + 1) * sizeof(uint32_t));
     if (fp32_) {
-        X_pairs_ = (float4*)dalloc(pairs_capacity((uint32_t)mp, g_) * sizeof(float4));
+        X_pairs_ = (float4*)dalloc(pairs_capacity((uint32_t)mp, gX_) * sizeof(float4));
     }
     careful_list_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
     q_keys_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
@@ -538,15 +578,15 @@ template <typename T>
 void Plan::grid_rebuild(const void* Xcur) {
     using V = typename Vec4<T>::type;
     const uint32_t* done = &st_->done;
-    launch_keys<T>(g_, (const V*)Xcur, mpad_, X_keys_, done, stream_);
+    launch_keys<T>(gX_, (const V*)Xcur, mpad_, X_keys_, done, stream_);
     launches_ += 1;
-    launches_ += radix_sort(X_keys_, nullptr, X_skeys_, X_sidx_, mpad_, g_.key_bits, rs_, done,
+    launches_ += radix_sort(X_keys_, nullptr, X_skeys_, X_sidx_, mpad_, gX_.key_bits, rs_, done,
                             stream_);
-    launches_ += build_cell_start(X_skeys_, (uint32_t)m_, 3 * g_.sub_bits, g_.ncells, X_start_,
+    launches_ += build_cell_start(X_skeys_, (uint32_t)m_, 3 * gX_.sub_bits, gX_.ncells, X_start_,
                                   cell_scratch_, done, stream_);
     if (fp32_) {  // gather + pack in one pass
         launches_ += build_pairs((const float4*)Xcur, X_sidx_, (float4*)X_sorted_, X_skeys_,
-                                 (uint32_t)m_, g_, X_start_, X_pairs_, done, stream_);
+                                 (uint32_t)m_, gX_, X_start_, X_pairs_, done, stream_);
     } else {
         launch_gather<T>((const V*)Xcur, X_sidx_, (uint32_t)m_, (V*)X_sorted_, done, stream_);
         launches_ += 1;
@@ -571,7 +611,7 @@ void Plan::density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur) {
         da.qcodes = q_skeys_;
         da.block_shift = block_shift_;
         da.nq = nq;
-        da.g = g_;
+        da.g = gX_;
         da.s_pad = s_pad_;
         da.r2 = r2_;
         const F32Consts fc = fp32_consts(d_.h, r2_, s_pad_, maxabs_);
@@ -589,7 +629,7 @@ void Plan::density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur) {
         da.done = &st_->done;
         launch_density(da, density_grid_, stream_);
     } else {
-        launch_exact_density<T>((const V*)X_sorted_, X_start_, qlist, nq, g_, s_pad_, r2_, support_,
+        launch_exact_density<T>((const V*)X_sorted_, X_start_, qlist, nq, gX_, s_pad_, r2_, support_,
                                 d_.h, 0, multi ? nullptr : (V*)X_sorted_, multi ? (V*)Xcur : nullptr,
                                 X_sidx_, st_, &st_->done, stream_);
     }
@@ -602,7 +642,7 @@ void Plan::density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur) {
     // the records carry w_i too
     if (fp32_)
         launches_ += build_pairs((const float4*)X_sorted_, nullptr, nullptr, X_skeys_, (uint32_t)m_,
-                                 g_, X_start_, X_pairs_, &st_->done, stream_);
+                                 gX_, X_start_, X_pairs_, &st_->done, stream_);
 }
 
 template <typename T>
@@ -648,7 +688,8 @@ void Plan::enqueue_sweep(int k) {
         a.qcodes = q_skeys_;
         a.block_shift = block_shift_;
         a.nq = nq;
-        a.g = g_;
+        a.gP = g_;
+        a.gX = gX_;
         a.s_pad = s_pad_;
         a.r2 = r2_;
         const F32Consts fc = fp32_consts(d_.h, r2_, s_pad_, maxabs_);
@@ -678,6 +719,7 @@ void Plan::enqueue_sweep(int k) {
         e.Xstart = X_start_;
         e.Xs_idx = X_sidx_;
         e.g = g_;
+        e.gX = gX_;
         e.s_pad = s_pad_;
         e.r2 = r2_;
         e.support = support_;

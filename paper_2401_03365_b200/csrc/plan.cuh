@@ -32,6 +32,9 @@ void cuda_check(cudaError_t e, const char* what);
 
 // Derives the shared grid for a bounding box and a support radius.
 GridGeom make_grid(const double lo[3], const double hi[3], double support);
+GridGeom make_grid_scaled(const double lo[3], const double hi[3], double support, double scale,
+                          const GridGeom& base);
+double x_cell_scale(uint64_t n, uint64_t m);
 
 void validate_desc(const pcs_lop_desc& d);  // throws Failure(INVALID_PARAM)
 int select_device(int requested);           // throws Failure(NO_DEVICE)
@@ -76,6 +79,7 @@ private:
     uint64_t n_ = 0, m_ = 0;
     uint32_t mpad_ = 0, chunk_ = 0, own_lo_ = 0, own_cnt_ = 0;
     GridGeom g_{};
+    GridGeom gX_{};                 // grid of the projected set (make_grid_scaled)
     double support_ = 0, r2_ = 0, s_pad_ = 0;
     double maxabs_ = 0;               // largest |coordinate| at upload (fp32 rounding scale)
     int lanes_ = 4;
