@@ -51,6 +51,8 @@ struct SweepSlot {
     uint32_t careful_count;            // queries deferred to the exact path
     uint32_t density_counter;          // dynamic group fetch of the w_i pass
     uint32_t exact_counter;            // dynamic fetch of the exact kernel
+    uint32_t group_counter2;           // dynamic group fetch of the repulsion pass
+    uint32_t pad_;
 };
 
 template <typename T> struct Vec4;

@@ -171,7 +171,8 @@ __global__ void __launch_bounds__(RS_THREADS)
 rs_scatter_kernel(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                   uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, uint32_t n, int shift,
                   uint32_t mask, const uint32_t* __restrict__ blockoff, uint32_t nblocks,
-                  const uint32_t* __restrict__ digit_totals, const uint32_t* done) {
+                  const uint32_t* __restrict__ digit_totals, uint32_t val_base,
+                  const uint32_t* done) {
     if (done && *done) return;
     __shared__ uint32_t run[256];
     __shared__ uint32_t wcnt[RS_WARPS][256];
@@ -192,7 +193,7 @@ rs_scatter_kernel(const uint32_t* __restrict__ kin, const uint32_t* __restrict__
         const uint32_t i = base + r * RS_THREADS + threadIdx.x;
         const bool valid = i < n;
         const uint32_t key = valid ? kin[i] : 0u;
-        const uint32_t val = valid ? (vin ? vin[i] : i) : 0u;
+        const uint32_t val = valid ? (vin ? vin[i] : val_base + i) : 0u;
         const uint32_t d = valid ? ((key >> shift) & mask) : 256u;
         const unsigned peers = __match_any_sync(0xffffffffu, d);
         const uint32_t rank = __popc(peers & lt);
@@ -448,7 +449,7 @@ size_t radix_blockhist_entries(uint32_t n) {
 
 int radix_sort(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
                uint32_t* vals_out, uint32_t n, int key_bits, RadixScratch& scr,
-               const uint32_t* done, cudaStream_t s) {
+               const uint32_t* done, cudaStream_t s, uint32_t val_base) {
     if (n == 0) return 0;
     const uint32_t nblocks = (n + RS_TILE - 1) / RS_TILE;
     const int passes = key_bits <= 0 ? 1 : (key_bits + 7) / 8;
@@ -470,7 +471,8 @@ int radix_sort(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_
         uint32_t* totals = scr.blockhist + 256 * (size_t)nblocks;
         rs_scan_rows_kernel<<<256, RS_ROW_THREADS, 0, s>>>(scr.blockhist, nblocks, totals, done);
         rs_scatter_kernel<<<nblocks, RS_THREADS, 0, s>>>(kin, vin, ko, vo, n, shift, mask,
-                                                         scr.blockhist, nblocks, totals, done);
+                                                         scr.blockhist, nblocks, totals, val_base,
+                                                         done);
         launches += 3;
         kin = ko;
         vin = vo;
@@ -490,7 +492,7 @@ template <typename V>
 int build_query_list(const V* sorted_pts, uint32_t n, const GridGeom& g, double support,
                      const uint32_t* sorted_idx, uint32_t own_lo, uint32_t own_hi, uint32_t* keys_tmp,
                      uint32_t* keys_sorted_tmp, uint32_t* qlist, int* block_shift,
-                     RadixScratch& scr, const uint32_t* done, cudaStream_t s) {
+                     RadixScratch& scr, const uint32_t* done, cudaStream_t s, uint32_t val_base) {
     auto width = [](uint64_t v) {  // bits to represent 0..v-1
         int b = 0;
         while (b < 32 && (1ull << b) < v) ++b;
@@ -518,15 +520,17 @@ int build_query_list(const V* sorted_pts, uint32_t n, const GridGeom& g, double 
                                                            own_hi, 1u << mbits, keys_tmp, done);
     const int key_bits = mbits + (sorted_idx ? 1 : 0);
     return 1 + radix_sort(keys_tmp, nullptr, keys_sorted_tmp, qlist, n, std::max(key_bits, 1), scr,
-                          done, s);
+                          done, s, val_base);
 }
 
 template int build_query_list<float4>(const float4*, uint32_t, const GridGeom&, double,
                                       const uint32_t*, uint32_t, uint32_t, uint32_t*, uint32_t*,
-                                      uint32_t*, int*, RadixScratch&, const uint32_t*, cudaStream_t);
+                                      uint32_t*, int*, RadixScratch&, const uint32_t*, cudaStream_t,
+                                      uint32_t);
 template int build_query_list<double4>(const double4*, uint32_t, const GridGeom&, double,
                                        const uint32_t*, uint32_t, uint32_t, uint32_t*, uint32_t*,
-                                       uint32_t*, int*, RadixScratch&, const uint32_t*, cudaStream_t);
+                                       uint32_t*, int*, RadixScratch&, const uint32_t*, cudaStream_t,
+                                       uint32_t);
 
 size_t cell_scan_scratch_entries(uint32_t ncells) {
     return ((size_t)ncells + 1 + CS_TILE - 1) / CS_TILE + 1;

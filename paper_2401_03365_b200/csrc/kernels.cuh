@@ -32,9 +32,10 @@ struct RadixScratch {
 size_t radix_blockhist_entries(uint32_t n);
 // Stable LSD sort of (keys, values = 0..n-1 when vals_in == nullptr) on the low
 // key_bits bits.  Results land in keys_out / vals_out.  Returns kernel count.
+// (values = val_base + i when vals_in == nullptr)
 int radix_sort(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
                uint32_t* vals_out, uint32_t n, int key_bits, RadixScratch& scr,
-               const uint32_t* done, cudaStream_t s);
+               const uint32_t* done, cudaStream_t s, uint32_t val_base = 0);
 
 template <typename T>
 void launch_gather(const typename Vec4<T>::type* src, const uint32_t* idx, uint32_t n,
@@ -47,11 +48,13 @@ void launch_gather(const typename Vec4<T>::type* src, const uint32_t* idx, uint3
 // block_shift changes), which bounds its box.  With sorted_idx, the queries
 // whose internal index lies in [own_lo, own_hi) come first (multi-GPU
 // ownership).  Returns kernel count.
+// pts[0..n) are the queries; qlist receives val_base + their positions.
 template <typename V>
 int build_query_list(const V* sorted_pts, uint32_t n, const GridGeom& g, double support,
                      const uint32_t* sorted_idx, uint32_t own_lo, uint32_t own_hi, uint32_t* keys_tmp,
                      uint32_t* keys_sorted_tmp, uint32_t* qlist, int* block_shift,
-                     RadixScratch& scr, const uint32_t* done, cudaStream_t s);
+                     RadixScratch& scr, const uint32_t* done, cudaStream_t s,
+                     uint32_t val_base = 0);
 // Work unit of the fused kernels: kUnitQueries consecutive entries of the query list.
 constexpr uint32_t kUnitQueries = 32;
 
@@ -79,11 +82,10 @@ int build_pairs(const float4* src, const uint32_t* idx, float4* sorted_out,
 struct FastArgs {
     const float4* Ppairs;     // data, pair records; w = 1/v_j (WLOP) or 1
     const uint32_t* Pstart;   // cell table of the sorted data (+ row delta = record slot)
-    const float4* Xs;         // projected set, sorted (queries)
+    const float4* Xq;         // projected set X^k, internal index order (queries)
     const float4* Xpairs;     // projected set, pair records; w = w_i (WLOP)
     const uint32_t* Xstart;   // cell table of the sorted projected set
-    const uint32_t* Xs_idx;   // sorted slot -> internal index
-    const uint32_t* qlist;    // queries (sorted slots, build_query_list order)
+    const uint32_t* qlist;    // queries (internal indices, build_query_list order)
     const uint32_t* qcodes;   // their Morton codes
     int block_shift;          // groups stay inside one (code >> block_shift) block
     uint32_t nq;
@@ -97,16 +99,19 @@ struct FastArgs {
     float support;            // s (fp32), repulsion scale
     float mu;
     float4* Xnext;            // internal index order
-    uint32_t* careful_list;   // deferred queries (sorted slots)
+    uint32_t* careful_list;   // deferred queries (internal indices)
+    float4* attr;             // PH_ATTR -> PH_REP: per list position (sum w, sum w d)
+    int2* attr_n;             //   (hits, zero-distance candidates)
     uint8_t* ever_isolated;   // internal index
     RunState* st;
     SweepSlot* slot;
     const uint32_t* done;
 };
 
-// mode: 0 = attraction only (mu == 0), 1 = inv-cube repulsion, 2 = neg-linear
+// rep_mode: 0 = attraction only (mu == 0), 1 = inv-cube repulsion, 2 = neg-linear.
+// phase: 0 = fused, 1 = attraction pass (writes attr), 2 = repulsion + update.
 void launch_fast(const FastArgs& a, int lanes_per_point, bool wlop, bool check_zero,
-                 int rep_mode, int grid_blocks, cudaStream_t s);
+                 int rep_mode, int phase, int grid_blocks, cudaStream_t s);
 int fast_blocks_per_sm(int lanes_per_point, bool wlop, bool check_zero, int rep_mode);
 
 struct DensityArgs {
@@ -140,8 +145,9 @@ struct ExactArgs {
     const uint32_t* Pstart;
     const V* Xs;              // sorted projected set; .w = w_i (WLOP)
     const uint32_t* Xstart;
-    const uint32_t* Xs_idx;   // sorted slot -> internal index
-    const uint32_t* qlist;    // queries (sorted slots); nullptr = 0..nq-1
+    const uint32_t* Xs_idx;   // sorted slot -> internal index (self exclusion)
+    const V* Xq;              // X^k, internal order (query positions)
+    const uint32_t* qlist;    // queries (internal indices); nullptr = 0..nq-1
     const uint32_t* nq_dev;   // if non-null, the query count lives on the device
     uint32_t nq;
     GridGeom g, gX;           // grids of the data and of the projected set
@@ -158,13 +164,16 @@ struct ExactArgs {
 template <typename T>
 void launch_exact(const ExactArgs<T>& a, int grid_blocks, cudaStream_t s);
 
-// Exact (fp64) density weights over a sorted cloud: v = 1 + sum theta (j' != j).
+// Exact (fp64) density weights: for query q = qlist[i] (or i) at Cq[q],
+// v = 1 + sum theta over the sorted cloud C (cell table Cstart) minus the query
+// itself (candidate k is the query when (qself ? qself[k] : k) == q); written to
+// out[out_idx ? out_idx[q] : q].w (inverted if invert).
 template <typename T>
 void launch_exact_density(const typename Vec4<T>::type* C, const uint32_t* Cstart,
-                          const uint32_t* qlist, uint32_t nq, const GridGeom& g, double s_pad,
-                          double r2, double support, double h, int invert,
-                          typename Vec4<T>::type* out_sorted, typename Vec4<T>::type* out_internal,
-                          const uint32_t* idx, RunState* st, const uint32_t* done,
+                          const typename Vec4<T>::type* Cq, const uint32_t* qlist, uint32_t nq,
+                          const uint32_t* qself, const GridGeom& g, double s_pad, double r2,
+                          double support, double h, int invert, typename Vec4<T>::type* out,
+                          const uint32_t* out_idx, RunState* st, const uint32_t* done,
                           cudaStream_t s);
 
 // Radius queries (parity facility): count (idx == nullptr) or fill CSR (unsorted).

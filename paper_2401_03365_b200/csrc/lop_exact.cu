@@ -104,9 +104,8 @@ __global__ void __launch_bounds__(EX_THREADS) exact_kernel(const ExactArgs<T> a)
         if (lane == 0) qn = atomicAdd(counter, 1u);
         qn = __shfl_sync(0xffffffffu, qn, 0);
         if (qn >= nq) break;
-        const uint32_t qslot = a.qlist ? a.qlist[qn] : qn;
-        const V qv = a.Xs[qslot];
-        const uint32_t q_int = a.Xs_idx[qslot];
+        const uint32_t q_int = a.qlist ? a.qlist[qn] : qn;  // internal index
+        const V qv = a.Xq[q_int];
         const double x = (double)qv.x, y = (double)qv.y, z = (double)qv.z;
         const Rows rw = rows_around(a.g, x, y, z, a.s_pad);
 
@@ -223,24 +222,25 @@ __global__ void __launch_bounds__(EX_THREADS) exact_kernel(const ExactArgs<T> a)
 template <typename T>
 __global__ void __launch_bounds__(EX_THREADS)
 exact_density_kernel(const typename Vec4<T>::type* __restrict__ C, const uint32_t* __restrict__ Cstart,
-                     const uint32_t* __restrict__ qlist, uint32_t nq, GridGeom g, double s_pad,
-                     double r2, double support, double h, int invert,
-                     typename Vec4<T>::type* out_sorted, typename Vec4<T>::type* out_internal,
-                     const uint32_t* __restrict__ idx, RunState* st, const uint32_t* done) {
+                     const typename Vec4<T>::type* __restrict__ Cq,
+                     const uint32_t* __restrict__ qlist, uint32_t nq,
+                     const uint32_t* __restrict__ qself, GridGeom g, double s_pad, double r2,
+                     double support, double h, int invert, typename Vec4<T>::type* out,
+                     const uint32_t* __restrict__ out_idx, RunState* st, const uint32_t* done) {
     using V = typename Vec4<T>::type;
     if (done && *done) return;
     const int lane = threadIdx.x & 31;
     const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t qn = wid; qn < nq; qn += nw) {
-        const uint32_t qslot = qlist ? qlist[qn] : qn;
-        const V qv = C[qslot];
+        const uint32_t qid = qlist ? qlist[qn] : qn;
+        const V qv = Cq[qid];
         const double x = (double)qv.x, y = (double)qv.y, z = (double)qv.z;
         const Rows rw = rows_around(g, x, y, z, s_pad);
         double acc = 0.0;
         unsigned long long pairs = 0;
         for_each_candidate(Cstart, g, rw, lane, [&](uint32_t k) {
-            if (k == qslot) return;
+            if ((qself ? qself[k] : k) == qid) return;
             const V c = C[k];
             const double d2 = exact_d2((double)c.x, (double)c.y, (double)c.z, x, y, z);
             if (!(d2 <= r2)) return;
@@ -253,8 +253,7 @@ exact_density_kernel(const typename Vec4<T>::type* __restrict__ C, const uint32_
         if (lane == 0) {
             const double dens = 1.0 + acc;
             const T val = invert ? (T)(1.0 / dens) : (T)dens;
-            if (out_sorted) out_sorted[qslot].w = val;
-            else out_internal[idx[qslot]].w = val;
+            out[out_idx ? out_idx[qid] : qid].w = val;
             if (pairs) atomicAdd(&st->density_pairs, pairs);
         }
     }
@@ -372,15 +371,14 @@ void launch_exact(const ExactArgs<T>& a, int grid_blocks, cudaStream_t s) {
 
 template <typename T>
 void launch_exact_density(const typename Vec4<T>::type* C, const uint32_t* Cstart,
-                          const uint32_t* qlist, uint32_t nq, const GridGeom& g, double s_pad,
-                          double r2, double support, double h, int invert,
-                          typename Vec4<T>::type* out_sorted, typename Vec4<T>::type* out_internal,
-                          const uint32_t* idx, RunState* st, const uint32_t* done,
+                          const typename Vec4<T>::type* Cq, const uint32_t* qlist, uint32_t nq,
+                          const uint32_t* qself, const GridGeom& g, double s_pad, double r2,
+                          double support, double h, int invert, typename Vec4<T>::type* out,
+                          const uint32_t* out_idx, RunState* st, const uint32_t* done,
                           cudaStream_t s) {
     if (!nq) return;
     exact_density_kernel<T><<<blocks_for((uint64_t)nq * 32, EX_THREADS), EX_THREADS, 0, s>>>(
-        C, Cstart, qlist, nq, g, s_pad, r2, support, h, invert, out_sorted, out_internal, idx, st,
-        done);
+        C, Cstart, Cq, qlist, nq, qself, g, s_pad, r2, support, h, invert, out, out_idx, st, done);
 }
 
 template <typename T>
@@ -428,11 +426,11 @@ void launch_fill_invalid(typename Vec4<T>::type* X, uint32_t mpad, const uint32_
 
 #define PCSB_INST(T)                                                                              \
     template void launch_exact<T>(const ExactArgs<T>&, int, cudaStream_t);                       \
-    template void launch_exact_density<T>(const Vec4<T>::type*, const uint32_t*, const uint32_t*, \
-                                          uint32_t, const GridGeom&, double, double, double,      \
-                                          double, int, Vec4<T>::type*, Vec4<T>::type*,            \
-                                          const uint32_t*, RunState*, const uint32_t*,            \
-                                          cudaStream_t);                                          \
+    template void launch_exact_density<T>(const Vec4<T>::type*, const uint32_t*,                 \
+                                          const Vec4<T>::type*, const uint32_t*, uint32_t,        \
+                                          const uint32_t*, const GridGeom&, double, double,       \
+                                          double, double, int, Vec4<T>::type*, const uint32_t*,   \
+                                          RunState*, const uint32_t*, cudaStream_t);              \
     template void launch_radius_dump<T>(const Vec4<T>::type*, const uint32_t*, const uint32_t*,   \
                                         const GridGeom&, const double*, uint32_t, double, double, \
                                         uint64_t*, uint32_t*, cudaStream_t);                      \

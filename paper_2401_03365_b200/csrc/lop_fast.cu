@@ -516,11 +516,20 @@ __device__ __forceinline__ uint32_t group_end(unsigned brk, uint32_t r0, uint32_
     return min(e, min(g0 + Q, r1));
 }
 
-template <int L, bool kWlop, bool kCheckZero, int kRep>
+// Phases of the per-point update.  PH_ALL: attraction, repulsion and the update
+// in one pass.  PH_ATTR: attraction only; the per-query sums go to a.attr (the
+// projected set's grid is rebuilt meanwhile on another stream).  PH_REP:
+// repulsion, then the update from a.attr.  PH_ATTR and PH_REP form the same
+// groups (same list, same cuts), so a.attr is indexed by list position.
+enum : int { PH_ALL = 0, PH_ATTR = 1, PH_REP = 2 };
+
+template <int L, bool kWlop, bool kCheckZero, int kRep, int PH>
 __global__ void __launch_bounds__(FAST_THREADS, PCSB_FAST_MINB)
 fast_kernel(const FastArgs a) {
     constexpr int Q = 32 / L;
     constexpr int KREP = kRep == 1 ? K_REP_INVCUBE : K_REP_NEGLIN;
+    constexpr bool kAttr = PH != PH_REP;
+    constexpr bool kRepul = kRep != 0 && PH != PH_ATTR;
     __shared__ __align__(128) float4 smem[FAST_WARPS * 4 * HR];
     __shared__ __align__(8) uint64_t bars[FAST_WARPS * 2];
     __shared__ float4 qsh[FAST_WARPS][Q];
@@ -528,53 +537,71 @@ fast_kernel(const FastArgs a) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     Stage S = make_stage(smem + warp * 4 * HR, bars + 2 * warp, lane);
     const int qi = lane / L, sub = lane % L;
+    uint32_t* counter = PH == PH_REP ? &a.slot->group_counter2 : &a.slot->group_counter;
 
     uint32_t r0, r1;
-    while (next_unit(&a.slot->group_counter, a.nq, lane, r0, r1)) {
+    while (next_unit(counter, a.nq, lane, r0, r1)) {
         const unsigned brk = group_breaks(a.qcodes, a.block_shift, r0, r1, lane);
         for (uint32_t g0 = r0, g1; g0 < r1; g0 = g1) {
             g1 = group_end(brk, r0, r1, g0, Q);
             const uint32_t qpos = g0 + qi;
             const bool member = qpos < g1;
             const uint32_t qp = member ? qpos : g0;  // padding lanes duplicate the first query
-            const uint32_t qslot = __ldg(&a.qlist[qp]);
-            const float4 q = __ldg(&a.Xs[qslot]);
+            const uint32_t qint = __ldg(&a.qlist[qp]);  // internal index
+            const float4 q = __ldg(&a.Xq[qint]);
             const EvalConsts ec = make_consts(q, a.kneg, a.K0, a.support);
             const Box box = member_box(q, member);
             if (member && sub == 0) qsh[warp][qi] = q;
             __syncwarp();
             const GroupQ G{qsh[warp], (int)(g1 - g0), a.scull2};
+            uint32_t evals = 0;  // staged candidates evaluated (x Q queries)
 
             // ---------------- attraction: data candidates (lop.cpp:49-65) ----------------
             Acc at = acc_zero();
-            uint32_t evals = 0;  // staged candidates evaluated (x Q queries)
-            gather_eval(a.Ppairs, a.Pstart, a.gP, box, a.s_pad, G, S, lane,
-                        [&](const float4* half, int nrec) {
-                            eval_half<L, K_ATTR, kWlop, kCheckZero>(half, nrec, sub, q, ec, a.band,
-                                                                  a.r2, at);
-                            evals += 2 * nrec;
-                        });
+            if (kAttr) {
+                gather_eval(a.Ppairs, a.Pstart, a.gP, box, a.s_pad, G, S, lane,
+                            [&](const float4* half, int nrec) {
+                                eval_half<L, K_ATTR, kWlop, kCheckZero>(half, nrec, sub, q, ec,
+                                                                      a.band, a.r2, at);
+                                evals += 2 * nrec;
+                            });
+                group_reduce<L>(at, kCheckZero);
+            }
+            if (PH == PH_ATTR) {
+                if (member && sub == 0) {
+                    a.attr[qpos] = make_float4(at.s.x, at.x.x, at.y.x, at.z.x);
+                    a.attr_n[qpos] = make_int2(at.hneg, kCheckZero ? at.rneg - at.hneg : 0);
+                }
+                if (lane == 0) atomicAdd(&a.st->lane_candidates, (unsigned long long)evals * Q);
+                continue;
+            }
+            if (PH == PH_REP && member && sub == 0) {
+                const float4 v = a.attr[qpos];
+                const int2 c = a.attr_n[qpos];
+                at.s.x = v.x;
+                at.x.x = v.y;
+                at.y.x = v.z;
+                at.z.x = v.w;
+                at.hneg = c.x;
+                at.rneg = c.x + c.y;
+            }
 
             // ---------------- repulsion: projected-set candidates (lop.cpp:79-97) ----------------
             Acc rp = acc_zero();
-            if (kRep != 0) {
+            if (kRepul) {
                 gather_eval(a.Xpairs, a.Xstart, a.gX, box, a.s_pad, G, S, lane,
                             [&](const float4* half, int nrec) {
                                 eval_half<L, KREP, kWlop, true>(half, nrec, sub, q, ec, a.band,
                                                                 a.r2, rp);
                                 evals += 2 * nrec;
                             });
+                group_reduce<L>(rp, true);
             }
 
-            // ---------------- per-query reduction over its L lanes ----------------
-            group_reduce<L>(at, kCheckZero);
-            if (kRep != 0) group_reduce<L>(rp, true);
-
-            // ---------------- finalize (lane sub == 0 of each member query) ----------------
+            // ---------------- update (lane sub == 0 of each member query) ----------------
             float disp = 0.f;
             unsigned long long n_attr = 0, n_rep = 0;
             if (member && sub == 0) {
-                const uint32_t qi_int = __ldg(&a.Xs_idx[qslot]);
                 const float sa = at.s.x;
                 bool bad = !isfinite(sa) || !isfinite(at.x.x) || !isfinite(at.y.x) ||
                            !isfinite(at.z.x);
@@ -594,7 +621,7 @@ fast_kernel(const FastArgs a) {
                 }
                 if (bad) {
                     const uint32_t pos = atomicAdd(&a.slot->careful_count, 1u);
-                    a.careful_list[pos] = qslot;
+                    a.careful_list[pos] = qint;
                 } else {
                     float nx = q.x, ny = q.y, nz = q.z;
                     bool isolated = false;
@@ -618,11 +645,11 @@ fast_kernel(const FastArgs a) {
                             }
                         }
                     }
-                    a.Xnext[qi_int] = make_float4(nx, ny, nz, 0.f);
+                    a.Xnext[qint] = make_float4(nx, ny, nz, 0.f);
                     const float ddx = nx - q.x, ddy = ny - q.y, ddz = nz - q.z;
                     disp = sqrtf(fmaf(ddz, ddz, fmaf(ddy, ddy, ddx * ddx)));
                     if (isolated) {
-                        a.ever_isolated[qi_int] = 1;
+                        a.ever_isolated[qint] = 1;
                         atomicAdd(&a.st->isolated_events, 1ull);
                     }
                 }
@@ -705,14 +732,16 @@ density_kernel(const DensityArgs a) {
 }
 
 template <int L, bool W, bool Z, int R>
-void launch_one(const FastArgs& a, int grid, cudaStream_t s) {
-    fast_kernel<L, W, Z, R><<<grid, FAST_THREADS, 0, s>>>(a);
+void launch_one(const FastArgs& a, int phase, int grid, cudaStream_t s) {
+    if (phase == PH_ATTR) fast_kernel<L, W, Z, R, PH_ATTR><<<grid, FAST_THREADS, 0, s>>>(a);
+    else if (phase == PH_REP) fast_kernel<L, W, Z, R, PH_REP><<<grid, FAST_THREADS, 0, s>>>(a);
+    else fast_kernel<L, W, Z, R, PH_ALL><<<grid, FAST_THREADS, 0, s>>>(a);
 }
 
 template <int L>
-void launch_l(const FastArgs& a, bool wlop, bool cz, int rep, int grid, cudaStream_t s) {
+void launch_l(const FastArgs& a, bool wlop, bool cz, int rep, int phase, int grid, cudaStream_t s) {
 #define PCSB_DISPATCH(W, Z, R) \
-    if (wlop == W && cz == Z && rep == R) return launch_one<L, W, Z, R>(a, grid, s);
+    if (wlop == W && cz == Z && rep == R) return launch_one<L, W, Z, R>(a, phase, grid, s);
     PCSB_DISPATCH(false, false, 0)
     PCSB_DISPATCH(false, false, 1)
     PCSB_DISPATCH(false, false, 2)
@@ -731,11 +760,11 @@ void launch_l(const FastArgs& a, bool wlop, bool cz, int rep, int grid, cudaStre
 }  // namespace
 
 void launch_fast(const FastArgs& a, int lanes_per_point, bool wlop, bool check_zero, int rep_mode,
-                 int grid_blocks, cudaStream_t s) {
+                 int phase, int grid_blocks, cudaStream_t s) {
     switch (lanes_per_point) {
-        case 2: return launch_l<2>(a, wlop, check_zero, rep_mode, grid_blocks, s);
-        case 8: return launch_l<8>(a, wlop, check_zero, rep_mode, grid_blocks, s);
-        default: return launch_l<4>(a, wlop, check_zero, rep_mode, grid_blocks, s);
+        case 2: return launch_l<2>(a, wlop, check_zero, rep_mode, phase, grid_blocks, s);
+        case 8: return launch_l<8>(a, wlop, check_zero, rep_mode, phase, grid_blocks, s);
+        default: return launch_l<4>(a, wlop, check_zero, rep_mode, phase, grid_blocks, s);
     }
 }
 
@@ -747,7 +776,7 @@ int fast_blocks_per_sm(int lanes_per_point, bool wlop, bool check_zero, int rep_
     static int cached = 0;  // same for every variant (launch bounds + static smem)
     if (!cached) {
         int b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fast_kernel<4, false, false, 2>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fast_kernel<4, false, false, 2, PH_ALL>,
                                                       FAST_THREADS, 0);
         cached = b > 0 ? b : 1;
     }

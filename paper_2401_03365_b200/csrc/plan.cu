@@ -204,18 +204,34 @@ Plan::Plan(const pcs_lop_desc& d) : d_(d) {
     lanes_ = d_.lanes_per_point ? d_.lanes_per_point : 4;
     device_ = select_device(d_.device);
     PCSB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    {
+        // the side stream (projected-set grid) gets the higher priority so its
+        // small kernels take free block slots as soon as they appear
+        int lo = 0, hi = 0;
+        PCSB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        PCSB_CUDA(cudaStreamCreateWithPriority(&stream2_, cudaStreamNonBlocking, hi));
+    }
+    PCSB_CUDA(cudaEventCreateWithFlags(&ev_xready_, cudaEventDisableTiming));
     PCSB_CUDA(cudaEventCreate(&run_ev_[0]));
     PCSB_CUDA(cudaEventCreate(&run_ev_[1]));
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_);
     fast_grid_ = sms * fast_blocks_per_sm(lanes_, d_.density_weights != 0, false, 2);
     density_grid_ = fast_grid_;
+    {
+        // all block slots: fewer warps slow the pass more (+13% at 5 of 6 slots)
+        // than the side stream's overlap gains; its kernels fill the pass's tail
+        int per_sm = fast_grid_ / sms;
+        if (const char* e = std::getenv("PCSB_ATTR_BLOCKS")) per_sm = std::atoi(e);  // developer knob
+        attr_grid_ = sms * std::max(1, per_sm);
+    }
     exact_grid_ = sms * 8;
     support_ = d_.h * d_.cutoff_multiple;
     r2_ = support_ * support_;
 }
 
 Plan::~Plan() {
+    if (stream2_) cudaStreamSynchronize(stream2_);
     if (stream_) cudaStreamSynchronize(stream_);
     free_all();
     for (auto& se : event_pool_)
@@ -225,6 +241,8 @@ Plan::~Plan() {
     if (run_ev_[0]) cudaEventDestroy(run_ev_[0]);
     if (run_ev_[1]) cudaEventDestroy(run_ev_[1]);
     delete coll_;
+    if (ev_xready_) cudaEventDestroy(ev_xready_);
+    if (stream2_) cudaStreamDestroy(stream2_);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -367,6 +385,10 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     rs_.vals_alt = (uint32_t*)dalloc(sort_cap * sizeof(uint32_t));
     rs_.blockhist = (uint32_t*)dalloc(radix_blockhist_entries(sort_cap) * sizeof(uint32_t));
     rs_.capacity = sort_cap;
+    rs2_.keys_alt = (uint32_t*)dalloc(sort_cap * sizeof(uint32_t));
+    rs2_.vals_alt = (uint32_t*)dalloc(sort_cap * sizeof(uint32_t));
+    rs2_.blockhist = (uint32_t*)dalloc(radix_blockhist_entries(sort_cap) * sizeof(uint32_t));
+    rs2_.capacity = sort_cap;
     cell_scratch_ = (uint32_t*)dalloc(
         cell_scan_scratch_entries(std::max(g_.ncells, gX_.ncells)) * sizeof(uint32_t));
     st_ = (RunState*)dalloc(sizeof(RunState));
@@ -433,9 +455,9 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
             tfree(pfs);
             tfree(pq);
         } else {
-            launch_exact_density<T>((const V*)P_sorted_, P_start_, nullptr, nn, g_, s_pad_, r2_,
-                                    support_, d_.h, 0, (V*)P_sorted_, nullptr, nullptr, st_,
-                                    nullptr, stream_);
+            launch_exact_density<T>((const V*)P_sorted_, P_start_, (const V*)P_sorted_, nullptr, nn,
+                                    nullptr, g_, s_pad_, r2_, support_, d_.h, 0, (V*)P_sorted_,
+                                    nullptr, st_, nullptr, stream_);
         }
         launches_ += 1;
     }
@@ -493,6 +515,8 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
         X_pairs_ = (float4*)dalloc(pairs_capacity((uint32_t)mp, gX_) * sizeof(float4));
     }
     careful_list_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
+    attr_ = (float4*)dalloc(mp * sizeof(float4));
+    attr_n_ = (int2*)dalloc(mp * sizeof(int2));
     q_keys_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
     q_skeys_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
     q_list_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
@@ -564,31 +588,37 @@ void Plan::synchronize() {
         run_pending_ = false;
     }
     for (auto& se : pending_) {
-        float a = 0.f, b = 0.f;
-        PCSB_CUDA(cudaEventElapsedTime(&a, se.e[0], se.e[1]));
-        PCSB_CUDA(cudaEventElapsedTime(&b, se.e[1], se.e[2]));
-        sort_ms_ += a;
-        kernel_ms_ += b;
+        // grid work = the query order + the part of the projected-set grid
+        // (side stream) not hidden behind the attraction pass; kernels = the
+        // attraction, repulsion and update passes
+        float q = 0.f, ta = 0.f, tg = 0.f, tk = 0.f;
+        PCSB_CUDA(cudaEventElapsedTime(&q, se.e[0], se.e[3]));
+        PCSB_CUDA(cudaEventElapsedTime(&ta, se.e[0], se.e[6]));
+        PCSB_CUDA(cudaEventElapsedTime(&tg, se.e[0], se.e[2]));
+        PCSB_CUDA(cudaEventElapsedTime(&tk, se.e[0], se.e[4]));
+        const float exposed = tg > ta ? tg - ta : 0.f;
+        sort_ms_ += q + exposed;
+        kernel_ms_ += tk - q - exposed;
         event_pool_.push_back(se);
     }
     pending_.clear();
 }
 
 template <typename T>
-void Plan::grid_rebuild(const void* Xcur) {
+void Plan::grid_rebuild(const void* Xcur, cudaStream_t st) {
     using V = typename Vec4<T>::type;
     const uint32_t* done = &st_->done;
-    launch_keys<T>(gX_, (const V*)Xcur, mpad_, X_keys_, done, stream_);
+    RadixScratch& scr = st == stream2_ ? rs2_ : rs_;
+    launch_keys<T>(gX_, (const V*)Xcur, mpad_, X_keys_, done, st);
     launches_ += 1;
-    launches_ += radix_sort(X_keys_, nullptr, X_skeys_, X_sidx_, mpad_, gX_.key_bits, rs_, done,
-                            stream_);
+    launches_ += radix_sort(X_keys_, nullptr, X_skeys_, X_sidx_, mpad_, gX_.key_bits, scr, done, st);
     launches_ += build_cell_start(X_skeys_, (uint32_t)m_, 3 * gX_.sub_bits, gX_.ncells, X_start_,
-                                  cell_scratch_, done, stream_);
+                                  cell_scratch_, done, st);
     if (fp32_) {  // gather + pack in one pass
         launches_ += build_pairs((const float4*)Xcur, X_sidx_, (float4*)X_sorted_, X_skeys_,
-                                 (uint32_t)m_, gX_, X_start_, X_pairs_, done, stream_);
+                                 (uint32_t)m_, gX_, X_start_, X_pairs_, done, st);
     } else {
-        launch_gather<T>((const V*)Xcur, X_sidx_, (uint32_t)m_, (V*)X_sorted_, done, stream_);
+        launch_gather<T>((const V*)Xcur, X_sidx_, (uint32_t)m_, (V*)X_sorted_, done, st);
         launches_ += 1;
     }
 }
@@ -597,6 +627,9 @@ void Plan::allgather_x(void* X, bool f32) {
     coll_->allgather(X, (size_t)chunk_ * 4, f32 ? CDType::F32 : CDType::F64, stream_);
 }
 
+// WLOP w_i of the owned queries on X^k (internal indices in qlist), written to
+// Xcur.w; after the exchange (sharded) the sorted copy and the records are
+// refreshed from Xcur so that the repulsion pass sees every w_i'.
 template <typename T>
 void Plan::density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur) {
     using V = typename Vec4<T>::type;
@@ -604,7 +637,7 @@ void Plan::density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur) {
     SweepSlot* slot = slots_ + (sweeps_issued_ - 1);
     if (fp32_) {
         DensityArgs da{};
-        da.C = (const float4*)X_sorted_;
+        da.C = (const float4*)Xcur;
         da.Cpairs = X_pairs_;
         da.Cstart = X_start_;
         da.qlist = qlist;
@@ -621,28 +654,25 @@ void Plan::density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur) {
         da.band = fc.band;
         da.inv_scale = fc.inv_scale;
         da.invert = 0;
-        da.out_sorted = multi ? nullptr : (float4*)X_sorted_;
-        da.out_internal = multi ? (float4*)Xcur : nullptr;
-        da.idx = X_sidx_;
+        da.out_sorted = (float4*)Xcur;
         da.st = st_;
         da.counter = &slot->density_counter;
         da.done = &st_->done;
         launch_density(da, density_grid_, stream_);
     } else {
-        launch_exact_density<T>((const V*)X_sorted_, X_start_, qlist, nq, gX_, s_pad_, r2_, support_,
-                                d_.h, 0, multi ? nullptr : (V*)X_sorted_, multi ? (V*)Xcur : nullptr,
-                                X_sidx_, st_, &st_->done, stream_);
+        launch_exact_density<T>((const V*)X_sorted_, X_start_, (const V*)Xcur, qlist, nq, X_sidx_,
+                                gX_, s_pad_, r2_, support_, d_.h, 0, (V*)Xcur, nullptr, st_,
+                                &st_->done, stream_);
     }
     launches_ += 1;
-    if (multi) {
-        allgather_x(Xcur, fp32_);
+    if (multi) allgather_x(Xcur, fp32_);
+    if (fp32_) {
+        launches_ += build_pairs((const float4*)Xcur, X_sidx_, (float4*)X_sorted_, X_skeys_,
+                                 (uint32_t)m_, gX_, X_start_, X_pairs_, &st_->done, stream_);
+    } else {
         launch_gather<T>((const V*)Xcur, X_sidx_, (uint32_t)m_, (V*)X_sorted_, &st_->done, stream_);
         launches_ += 1;
     }
-    // the records carry w_i too
-    if (fp32_)
-        launches_ += build_pairs((const float4*)X_sorted_, nullptr, nullptr, X_skeys_, (uint32_t)m_,
-                                 gX_, X_start_, X_pairs_, &st_->done, stream_);
 }
 
 template <typename T>
@@ -662,28 +692,38 @@ void Plan::enqueue_sweep(int k) {
         for (auto& e : se.e) PCSB_CUDA(cudaEventCreate(&e));
     }
     PCSB_CUDA(cudaEventRecord(se.e[0], stream_));
+    const int rep = d_.mu > 0.0 ? (d_.eta_kind == PCS_ETA_INV_CUBE ? 1 : 2) : 0;
+    // the projected set's grid is needed by the repulsion (and WLOP w_i) only
+    const bool xgrid = rep != 0;
 
-    // (1) index over the moving set (lop.cpp:39)
-    grid_rebuild<T>(cur);
-    // query order (Morton; owned queries first when sharded)
-    launches_ += build_query_list((const V*)X_sorted_, (uint32_t)m_, g_, support_,
-                                  multi ? X_sidx_ : nullptr, own_lo_, own_lo_ + own_cnt_, q_keys_,
-                                  q_skeys_, q_list_, &block_shift_, rs_, done, stream_);
+    // (1) index over the moving set (lop.cpp:39), on the side stream: it overlaps
+    //     the query ordering and the attraction pass, which need only P's grid
+    if (xgrid) {
+        PCSB_CUDA(cudaEventRecord(ev_xready_, stream_));
+        PCSB_CUDA(cudaStreamWaitEvent(stream2_, ev_xready_, 0));
+        PCSB_CUDA(cudaEventRecord(se.e[1], stream2_));
+        grid_rebuild<T>(cur, stream2_);
+        PCSB_CUDA(cudaEventRecord(se.e[2], stream2_));
+    } else {
+        PCSB_CUDA(cudaEventRecord(se.e[1], stream_));
+        PCSB_CUDA(cudaEventRecord(se.e[2], stream_));
+    }
+    // query order: the owned range of X^k in Morton order (internal indices)
+    launches_ += build_query_list((const V*)cur + own_lo_, own_cnt_, g_, support_, nullptr, 0, 0,
+                                  q_keys_, q_skeys_, q_list_, &block_shift_, rs_, done, stream_,
+                                  own_lo_);
     const uint32_t* qlist = q_list_;
-    const uint32_t nq = multi ? own_cnt_ : (uint32_t)m_;
-    // (2) WLOP density of the projected set on X^k
-    if (d_.density_weights) density_pass_x<T>(qlist, nq, cur);
-    PCSB_CUDA(cudaEventRecord(se.e[1], stream_));
+    const uint32_t nq = own_cnt_;
+    PCSB_CUDA(cudaEventRecord(se.e[3], stream_));
 
-    // (3) per-point update (lop.cpp:41-100)
+    // (2) per-point update (lop.cpp:41-100)
     if (fp32_) {
         FastArgs a{};
         a.Ppairs = P_pairs_;
         a.Pstart = P_start_;
-        a.Xs = (const float4*)X_sorted_;
+        a.Xq = (const float4*)cur;
         a.Xpairs = X_pairs_;
         a.Xstart = X_start_;
-        a.Xs_idx = X_sidx_;
         a.qlist = qlist;
         a.qcodes = q_skeys_;
         a.block_shift = block_shift_;
@@ -701,15 +741,33 @@ void Plan::enqueue_sweep(int k) {
         a.mu = (float)d_.mu;
         a.Xnext = (float4*)nxt;
         a.careful_list = careful_list_;
+        a.attr = attr_;
+        a.attr_n = attr_n_;
         a.ever_isolated = ever_iso_;
         a.st = st_;
         a.slot = slot;
         a.done = done;
-        const int rep = d_.mu > 0.0 ? (d_.eta_kind == PCS_ETA_INV_CUBE ? 1 : 2) : 0;
-        launch_fast(a, lanes_, d_.density_weights != 0, k == 1, rep, fast_grid_, stream_);
-        launches_ += 1;
+        const bool wl = d_.density_weights != 0;
+        if (xgrid) {
+            launch_fast(a, lanes_, wl, k == 1, rep, 1, attr_grid_, stream_);  // attraction
+            PCSB_CUDA(cudaEventRecord(se.e[6], stream_));
+            PCSB_CUDA(cudaStreamWaitEvent(stream_, se.e[2], 0));
+            if (d_.density_weights) density_pass_x<T>(qlist, nq, cur);  // (WLOP) w_i on X^k
+            launch_fast(a, lanes_, wl, k == 1, rep, 2, fast_grid_, stream_);  // repulsion + update
+            launches_ += 2;
+        } else {
+            launch_fast(a, lanes_, wl, k == 1, rep, 0, fast_grid_, stream_);
+            launches_ += 1;
+            PCSB_CUDA(cudaEventRecord(se.e[6], stream_));
+        }
+    } else {
+        PCSB_CUDA(cudaEventRecord(se.e[6], stream_));
+        if (xgrid) {
+            PCSB_CUDA(cudaStreamWaitEvent(stream_, se.e[2], 0));
+            if (d_.density_weights) density_pass_x<T>(qlist, nq, cur);
+        }
     }
-    PCSB_CUDA(cudaEventRecord(se.e[2], stream_));
+    PCSB_CUDA(cudaEventRecord(se.e[4], stream_));
     {
         ExactArgs<T> e{};
         e.P = (const V*)P_sorted_;
@@ -718,6 +776,7 @@ void Plan::enqueue_sweep(int k) {
         e.Xs = (const V*)X_sorted_;
         e.Xstart = X_start_;
         e.Xs_idx = X_sidx_;
+        e.Xq = (const V*)cur;
         e.g = g_;
         e.gX = gX_;
         e.s_pad = s_pad_;
@@ -754,7 +813,7 @@ void Plan::enqueue_sweep(int k) {
     }
     launch_finalize_sweep(st_, slot, k, d_.convergence_tol, stream_);
     launches_ += 1;
-    PCSB_CUDA(cudaEventRecord(se.e[3], stream_));
+    PCSB_CUDA(cudaEventRecord(se.e[5], stream_));
     pending_.push_back(se);
 }
 
@@ -1026,8 +1085,8 @@ void density_weights_t(const pcs_lop_desc& d, const double* C, uint64_t n, doubl
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         launch_density(da, sms * fast_blocks_per_sm(4, true, false, 0), s);
     } else {
-        launch_exact_density<T>(tg.sorted, tg.start, nullptr, (uint32_t)n, tg.g, tg.s_pad, r2,
-                                support, d.h, 0, nullptr, tg.unsorted, tg.order, st, nullptr, s);
+        launch_exact_density<T>(tg.sorted, tg.start, tg.sorted, nullptr, (uint32_t)n, nullptr, tg.g,
+                                tg.s_pad, r2, support, d.h, 0, tg.unsorted, tg.order, st, nullptr, s);
     }
     std::vector<V> h(n);
     PCSB_CUDA(cudaMemcpyAsync(h.data(), tg.unsorted, n * sizeof(V), cudaMemcpyDeviceToHost, s));

@@ -61,7 +61,7 @@ private:
     template <typename T> void upload_t(const double* P, uint64_t n, const double* X0, uint64_t m);
     template <typename T> void enqueue_sweep(int k);
     template <typename T> void density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur);
-    template <typename T> void grid_rebuild(const void* Xcur);
+    template <typename T> void grid_rebuild(const void* Xcur, cudaStream_t st);
     void allgather_x(void* X, bool fp32);
     void free_all();
     void* dalloc(size_t bytes);
@@ -72,6 +72,8 @@ private:
     bool fp32_;
     int device_ = 0;
     cudaStream_t stream_ = nullptr;
+    cudaStream_t stream2_ = nullptr;  // projected-set grid, overlapped with the attraction pass
+    cudaEvent_t ev_xready_ = nullptr;  // X^k final on stream_
     int nranks_ = 1, rank_ = 0;
     Collectives* coll_ = nullptr;  // owned; NCCL or loopback (comm.h)
     bool sharded() const { return coll_ != nullptr; }
@@ -84,6 +86,7 @@ private:
     double maxabs_ = 0;               // largest |coordinate| at upload (fp32 rounding scale)
     int lanes_ = 4;
     int fast_grid_ = 0, exact_grid_ = 0, density_grid_ = 0;
+    int attr_grid_ = 0;  // attraction pass blocks
 
     std::vector<void*> allocs_;
     size_t vec_bytes_ = 16;
@@ -112,6 +115,9 @@ private:
     uint8_t* ever_iso_ = nullptr;
     uint32_t* orig_of_internal_ = nullptr;  // multi-GPU only
     RadixScratch rs_{};
+    RadixScratch rs2_{};              // stream2_'s sorts
+    float4* attr_ = nullptr;          // attraction sums per query-list position (PH_ATTR -> PH_REP)
+    int2* attr_n_ = nullptr;
     RunState* st_ = nullptr;
     SweepSlot* slots_ = nullptr;
     int slot_cap_ = 0;
@@ -125,7 +131,8 @@ private:
     double setup_ms_ = 0, last_run_ms_ = 0, sweeps_ms_ = 0, kernel_ms_ = 0, sort_ms_ = 0;
     cudaEvent_t run_ev_[2] = {nullptr, nullptr};
     struct SweepEvents {
-        cudaEvent_t e[4];
+        // start | X grid begin, end (side stream) | queries | kernels | end | attraction end
+        cudaEvent_t e[7];
     };
     std::vector<SweepEvents> pending_;  // per issued sweep in the current run
     std::vector<SweepEvents> event_pool_;
