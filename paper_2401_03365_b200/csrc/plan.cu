@@ -202,6 +202,8 @@ Plan::Plan(const pcs_lop_desc& d) : d_(d) {
     fp32_ = d_.precision == PCS_PREC_FP32;
     vec_bytes_ = fp32_ ? sizeof(float4) : sizeof(double4);
     lanes_ = d_.lanes_per_point ? d_.lanes_per_point : 4;
+    rep_lanes_ = lanes_;
+    if (const char* e = std::getenv("PCSB_REP_LANES")) rep_lanes_ = std::atoi(e);  // developer knob
     device_ = select_device(d_.device);
     PCSB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     {
@@ -753,7 +755,7 @@ void Plan::enqueue_sweep(int k) {
             PCSB_CUDA(cudaEventRecord(se.e[6], stream_));
             PCSB_CUDA(cudaStreamWaitEvent(stream_, se.e[2], 0));
             if (d_.density_weights) density_pass_x<T>(qlist, nq, cur);  // (WLOP) w_i on X^k
-            launch_fast(a, lanes_, wl, k == 1, rep, 2, fast_grid_, stream_);  // repulsion + update
+            launch_fast(a, rep_lanes_, wl, k == 1, rep, 2, fast_grid_, stream_);  // repulsion + update
             launches_ += 2;
         } else {
             launch_fast(a, lanes_, wl, k == 1, rep, 0, fast_grid_, stream_);

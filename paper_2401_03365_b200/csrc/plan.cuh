@@ -85,6 +85,7 @@ private:
     double support_ = 0, r2_ = 0, s_pad_ = 0;
     double maxabs_ = 0;               // largest |coordinate| at upload (fp32 rounding scale)
     int lanes_ = 4;
+    int rep_lanes_ = 4;  // lanes per query of the repulsion pass
     int fast_grid_ = 0, exact_grid_ = 0, density_grid_ = 0;
     int attr_grid_ = 0;  // attraction pass blocks
 
