@@ -322,19 +322,28 @@ def main():
     # ---------------- e2e through the public API ----------------
     e2e = None
     if not args.no_e2e:
-        barrier()
-        t = time.perf_counter()
-        if world == 1:
-            prm2 = pb.LopParams(kernel=params.kernel, mu=params.mu, iterations=args.steps,
-                                convergence_tol=params.convergence_tol)
-            out, se = pb.lop_project(P, X0, prm2, eta=c["eta"], density_weights=c["wlop"],
-                                     precision=precision, device=dev, lanes_per_point=args.lanes)
-        else:
+        # steady state of a process that calls the API repeatedly: the device-side
+        # plan of the timed region is released first (its memory returns to the
+        # library's pool) and one untimed call warms the pinned staging buffers
+        plan.close()
+        prm2 = pb.LopParams(kernel=params.kernel, mu=params.mu, iterations=args.steps,
+                            convergence_tol=params.convergence_tol)
+
+        def e2e_call():
+            if world == 1:
+                return pb.lop_project(P, X0, prm2, eta=c["eta"], density_weights=c["wlop"],
+                                      precision=precision, device=dev, lanes_per_point=args.lanes)
             p2 = make_plan()
             p2.upload(P, X0)
             p2.run(args.steps)
-            out, se = p2.download()
+            res = p2.download()
             p2.close()
+            return res
+
+        e2e_call()
+        barrier()
+        t = time.perf_counter()
+        out, se = e2e_call()
         wall = time.perf_counter() - t
         wall = max_over_ranks(wall)
         inter_e = se.interactions_attr + se.interactions_rep
@@ -343,7 +352,9 @@ def main():
                "d2h_bytes_per_step": int(out.nbytes / max(1, args.steps)),
                "h2d_bytes_total": int(P.nbytes + X0.nbytes), "d2h_bytes_total": int(out.nbytes),
                "wall_s": wall, "api": "pcs_lop_run (C ABI) with host buffers" if world == 1
-               else "pcs_lop_plan_{create,set_comm,upload,run,download} with host buffers"}
+               else "pcs_lop_plan_{create,set_comm,upload,run,download} with host buffers",
+               "state": "warm process (second call; the library's device pool and pinned "
+                        "staging buffers are reused, CUDA context already up)"}
 
     # ---------------- CPU baseline (rank 0, N = 1 only) ----------------
     cb = None
