@@ -306,7 +306,7 @@ def main():
         "achieved": kernel_rate,
         "peak": pk["peak"],
         "frac": kernel_rate / pk["peak"],
-        "kernel": "fast_kernel (fused attraction+repulsion, lop_fast.cu)",
+        "kernel": "fast_kernel attraction + repulsion passes (lop_fast.cu), per sweep",
         "kernel_share_of_step": kernel_ms / ms if ms > 0 else None,
         "peak_source": pk["source"] + " at sm_max 1965 MHz",
         "frac_at_measured_clock": kernel_rate / (pk["per_sm_clk"] * 148 * sm_mhz * 1e6),
@@ -315,6 +315,7 @@ def main():
     prof = os.path.join(HERE, "profiles", "fast_kernel_ncu.json")
     if os.path.exists(prof):
         try:
+            # DRAM bytes of one sweep's attraction + repulsion launches (ncu --set full)
             roofline["traffic"] = json.load(open(prof)).get("dram_bytes_per_launch")
         except Exception:
             pass

@@ -37,12 +37,8 @@ def to_bytes(v, unit):
     return v * scale if scale else None
 
 
-def full(rep, out):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
-    r = list(csv.reader(io.StringIO(raw)))
-    h, u, v = r[0], r[1], r[2]
-    res = {"report": rep.split("/")[-1], "kernel": v[h.index("Kernel Name")][:120]}
+def _one(h, u, v):
+    res = {"kernel": v[h.index("Kernel Name")][:120]}
     for k in FULL_KEYS:
         if k in h:
             i = h.index(k)
@@ -64,7 +60,21 @@ def full(rep, out):
     rd = res.get("dram__bytes_read.sum")
     wr = res.get("dram__bytes_write.sum")
     if rd and wr:
-        res["dram_bytes_per_launch"] = to_bytes(rd["value"], rd["unit"]) + to_bytes(wr["value"], wr["unit"])
+        res["dram_bytes"] = to_bytes(rd["value"], rd["unit"]) + to_bytes(wr["value"], wr["unit"])
+    return res
+
+
+def full(rep, out):
+    """Every kernel launch of the capture; dram_bytes_per_launch sums them (one sweep's
+    attraction + repulsion passes when the capture holds that pair)."""
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    r = list(csv.reader(io.StringIO(raw)))
+    h, u = r[0], r[1]
+    kernels = [_one(h, u, v) for v in r[2:]]
+    res = {"report": rep.split("/")[-1], "kernels": kernels}
+    if all("dram_bytes" in k for k in kernels):
+        res["dram_bytes_per_launch"] = sum(k["dram_bytes"] for k in kernels)
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps(res, indent=1))
 
