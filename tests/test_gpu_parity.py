@@ -290,3 +290,57 @@ def test_determinism_and_plan_reset(pb):
     c2, _ = plan.download()
     assert np.array_equal(a, c2)
     plan.close()
+
+
+# ----------------------------------------------------------------------------
+# layout / trimming edge cases of the fp32 kernels
+# ----------------------------------------------------------------------------
+@pytest.mark.parametrize("offset", [(0.0, 0.0, 0.0), (512.0, -300.0, 800.0), (-4096.0, 17.0, 0.5)])
+def test_fp32_neighbours_exact_far_from_origin(pb, orc, offset):
+    """Row trimming runs in fp32 with a slack of 32 ulps of the coordinate scale;
+    far from the origin fp32 rounding is large relative to the support, and the
+    neighbour sets must still be the reference's (identical counts)."""
+    P, X0 = pb.generate_config(3, 0.004)
+    off = np.array(offset)
+    P, X0 = r32(P + off), r32(X0 + off)
+    prm, c = pb.config_params(3, h=0.2)
+    prm.iterations = 1
+    out, s = pb.lop_project(P, X0, prm, eta=c["eta"], precision="fp32")
+    r = orc.lop_project(P, X0, prm.kernel.h, prm.kernel.cutoff_multiple, prm.mu, 1,
+                        eta=orc.ETA_NEG_LINEAR, store_f32=True)
+    assert (s.interactions_attr, s.interactions_rep) == (r.interactions_attr, r.interactions_rep)
+    assert np.abs(out - r.points).max() <= 8 * np.finfo(F32).eps * np.abs(P).max()
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_plan_with_tiny_projected_sets(pb, orc, prec):
+    """m = 0, 1, 2 through the plan API (empty work lists, one-point groups)."""
+    P, _ = pb.generate_config(3, 0.002)
+    prm, c = pb.config_params(3, h=0.2)
+    prm.iterations = 3
+    for m in (0, 1, 2):
+        X0 = P[:m] + 1e-3
+        plan = pb.LopPlan(prm, eta=c["eta"], precision=prec)
+        plan.upload(P, X0)
+        plan.run(3)
+        out, s = plan.download()
+        plan.close()
+        assert out.shape == (m, 3)
+        if m:
+            r = orc.lop_project(r32(P) if prec == "fp32" else P, r32(X0) if prec == "fp32" else X0,
+                                prm.kernel.h, prm.kernel.cutoff_multiple, prm.mu, 3,
+                                eta=orc.ETA_NEG_LINEAR, store_f32=(prec == "fp32"))
+            assert s.interactions_attr == r.interactions_attr
+            assert np.abs(out - r.points).max() <= 1e-5 * bbox_diag(P)
+
+
+def test_mu0_skips_projected_grid_but_matches(pb, orc):
+    """mu = 0: one fused pass, no projected-set grid; same result as the oracle."""
+    P, X0, prm, c = scaled_case(pb, 5, 0.001, 0.3)
+    prm.mu = 0.0
+    prm.iterations = 2
+    out, s = pb.lop_project(P, X0, prm, eta=c["eta"], precision="fp32")
+    r = orc.lop_project(P, X0, prm.kernel.h, prm.kernel.cutoff_multiple, 0.0, 2,
+                        eta=orc.ETA_INV_CUBE, store_f32=True)
+    assert s.interactions_attr == r.interactions_attr and s.interactions_rep == 0
+    assert np.abs(out - r.points).max() <= 1e-5 * bbox_diag(P)
