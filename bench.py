@@ -57,7 +57,7 @@ class ClockSampler:
         0x100: "display_clock_setting",
     }
 
-    def __init__(self, device_index: int, period_s: float = 0.005):
+    def __init__(self, device_index: int, period_s: float = 0.0005):
         self.samples = []
         self.reasons = 0
         self.max_mhz = None
@@ -88,6 +88,11 @@ class ClockSampler:
         if self.nv:
             self._thr = threading.Thread(target=self._run, daemon=True)
             self._thr.start()
+            # the timed region is short (~70 ms on the default config): make sure the
+            # sampler is running before it starts
+            t0 = time.time()
+            while not self.samples and time.time() - t0 < 1.0:
+                time.sleep(0.0005)
 
     def stop(self) -> dict:
         if not self._thr:
