@@ -174,6 +174,13 @@ pcs_status pcs_grid_sort(const pcs_lop_desc* d, const double* C_xyz, uint64_t n,
 pcs_status pcs_shard_layout(const uint32_t* sorted_order, uint64_t m, int32_t nranks,
                             uint32_t* orig_of_internal, uint32_t* internal_of_orig,
                             uint32_t* chunk, uint32_t* counts);
+/* Same, with the cuts at equal cumulative work: weights[o] = estimated work of
+ * original point o (NULL = 1 each); chunk = the largest shard (the others are
+ * padded).  Used by sharded plans with the data density around each X0 point. */
+pcs_status pcs_shard_layout_weighted(const uint32_t* sorted_order, const float* weights,
+                                     uint64_t m, int32_t nranks, uint32_t* orig_of_internal,
+                                     uint32_t* internal_of_orig, uint32_t* chunk,
+                                     uint32_t* counts);
 
 /* ---- host generators (proj/include/pcs/rng.hpp, proj/src/bench.cpp:40-87) -- */
 /* kind: 0 plane, 1 sphere, 2 torus(R=1,r=0.35), 3 gaussian bump */

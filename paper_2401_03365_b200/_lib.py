@@ -36,6 +36,7 @@ EXPORTED = [
     "pcs_lop_plan_launches", "pcs_radius_query_all", "pcs_density_weights", "pcs_grid_sort", "pcs_generate_surface",
     "pcs_add_noise", "pcs_config_sizes", "pcs_generate_config", "pcs_shard_layout",
     "pcs_loopback_group_create", "pcs_loopback_group_destroy", "pcs_lop_plan_set_loopback",
+    "pcs_shard_layout_weighted",
 ]
 
 
@@ -131,6 +132,8 @@ def lib():
         L.pcs_config_sizes.argtypes = [C.c_int32, C.c_double, _u64p, _u64p]
         L.pcs_generate_config.argtypes = [C.c_int32, C.c_double, _dp, _dp]
         L.pcs_shard_layout.argtypes = [_u32p, C.c_uint64, C.c_int32, _u32p, _u32p, _u32p, _u32p]
+        L.pcs_shard_layout_weighted.argtypes = [_u32p, C.POINTER(C.c_float), C.c_uint64, C.c_int32,
+                                                _u32p, _u32p, _u32p, _u32p]
         for name in EXPORTED:
             fn = getattr(L, name)
             if fn.restype is C.c_int:  # default restype -> pcs_status

@@ -424,8 +424,39 @@ void launch_fill_invalid(typename Vec4<T>::type* X, uint32_t mpad, const uint32_
     fill_invalid_kernel<typename Vec4<T>::type, T><<<blocks_for(mpad, 256), 256, 0, s>>>(X, mpad, orig);
 }
 
+// Work estimate of an X0 point for the sharded layout: the data points in the
+// 3x3x3 cells around it (cell side s/4 or s/2: a local density proxy; the
+// sweep's work per point is proportional to it).
+template <typename V>
+__global__ void shard_work_kernel(const V* __restrict__ X0, uint32_t m, GridGeom g,
+                                  const uint32_t* __restrict__ Pstart, float* __restrict__ w) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+        const V p = X0[i];
+        const int cx = cell_coord((double)p.x, g.ox, g.inv_cs, g.gx);
+        const int cy = cell_coord((double)p.y, g.oy, g.inv_cs, g.gy);
+        const int cz = cell_coord((double)p.z, g.oz, g.inv_cs, g.gz);
+        const int lx = max(cx - 1, 0), hx = min(cx + 1, g.gx - 1);
+        uint32_t cnt = 0;
+        for (int z = max(cz - 1, 0); z <= min(cz + 1, g.gz - 1); ++z)
+            for (int y = max(cy - 1, 0); y <= min(cy + 1, g.gy - 1); ++y) {
+                const uint32_t base = ((uint32_t)z * (uint32_t)g.gy + (uint32_t)y) * (uint32_t)g.gx;
+                cnt += Pstart[base + hx + 1] - Pstart[base + lx];
+            }
+        w[i] = 1.0f + (float)cnt;
+    }
+}
+
+template <typename T>
+void launch_shard_work(const typename Vec4<T>::type* X0, uint32_t m, const GridGeom& g,
+                       const uint32_t* Pstart, float* w, cudaStream_t s) {
+    if (!m) return;
+    shard_work_kernel<typename Vec4<T>::type><<<blocks_for(m, 256), 256, 0, s>>>(X0, m, g, Pstart, w);
+}
+
 #define PCSB_INST(T)                                                                              \
     template void launch_exact<T>(const ExactArgs<T>&, int, cudaStream_t);                       \
+    template void launch_shard_work<T>(const Vec4<T>::type*, uint32_t, const GridGeom&,           \
+                                       const uint32_t*, float*, cudaStream_t);                    \
     template void launch_exact_density<T>(const Vec4<T>::type*, const uint32_t*,                 \
                                           const Vec4<T>::type*, const uint32_t*, uint32_t,        \
                                           const uint32_t*, const GridGeom&, double, double,       \

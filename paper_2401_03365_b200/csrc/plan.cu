@@ -467,25 +467,47 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     }
 
     // ---- projected set layout ----
-    X_init_ = dalloc((size_t)std::max<uint32_t>(mpad_, 1) * sizeof(V));
     if (sharded()) {
-        // ownership: equal contiguous ranges of the initial cell-sorted order
+        // ownership: contiguous ranges of the initial cell-sorted order, cut at
+        // equal estimated work (data density around each point)
         std::vector<uint32_t> sidx(m);
+        std::vector<float> work(m);
         if (m) {
             launch_keys<T>(g_, X0v, (uint32_t)m, tk, nullptr, stream_);
             launches_ += 1;
             uint32_t* order = (uint32_t*)dalloc(m * sizeof(uint32_t));
             launches_ += radix_sort(tk, nullptr, tsk, order, (uint32_t)m, g_.key_bits, rs_, nullptr,
                                     stream_);
+            float* wd = (float*)talloc(m * sizeof(float));
+            launch_shard_work<T>(X0v, (uint32_t)m, g_, P_start_, wd, stream_);
+            launches_ += 1;
             PCSB_CUDA(cudaMemcpyAsync(sidx.data(), order, m * sizeof(uint32_t),
                                       cudaMemcpyDeviceToHost, stream_));
+            PCSB_CUDA(cudaMemcpyAsync(work.data(), wd, m * sizeof(float), cudaMemcpyDeviceToHost,
+                                      stream_));
             PCSB_CUDA(cudaStreamSynchronize(stream_));
+            tfree(wd);
         }
-        std::vector<uint32_t> ooi(mpad_), ioo(m ? m : 1), counts(nranks_);
+        std::vector<uint32_t> counts(nranks_);
         uint32_t chunk = 0;
-        if (pcs_shard_layout(sidx.data(), m, nranks_, ooi.data(), ioo.data(), &chunk,
-                             counts.data()) != PCS_OK || chunk != chunk_)
+        if (pcs_shard_layout_weighted(sidx.data(), work.data(), m, nranks_, nullptr, nullptr, &chunk,
+                                      counts.data()) != PCS_OK)
             throw Failure(PCS_ERR_NUMERICAL, "shard layout failed");
+        chunk_ = std::max<uint32_t>(chunk, 1);
+        mpad_ = chunk_ * (uint32_t)nranks_;
+        std::vector<uint32_t> ooi(mpad_), ioo(m ? m : 1);
+        if (pcs_shard_layout_weighted(sidx.data(), work.data(), m, nranks_, ooi.data(), ioo.data(),
+                                      &chunk, counts.data()) != PCS_OK)
+            throw Failure(PCS_ERR_NUMERICAL, "shard layout failed");
+        if (mpad_ > rs_.capacity) {  // the projected set's sorts run over mpad_ slots
+            for (RadixScratch* r : {&rs_, &rs2_}) {
+                r->keys_alt = (uint32_t*)dalloc((size_t)mpad_ * sizeof(uint32_t));
+                r->vals_alt = (uint32_t*)dalloc((size_t)mpad_ * sizeof(uint32_t));
+                r->blockhist = (uint32_t*)dalloc(radix_blockhist_entries(mpad_) * sizeof(uint32_t));
+                r->capacity = mpad_;
+            }
+        }
+        X_init_ = dalloc((size_t)std::max<uint32_t>(mpad_, 1) * sizeof(V));
         own_lo_ = (uint32_t)rank_ * chunk_;
         own_cnt_ = counts[rank_];
         orig_of_internal_ = (uint32_t*)dalloc((size_t)mpad_ * sizeof(uint32_t));
@@ -502,6 +524,7 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
         PCSB_CUDA(cudaStreamSynchronize(stream_));
         tfree(iof);
     } else {
+        X_init_ = dalloc((size_t)std::max<uint32_t>(mpad_, 1) * sizeof(V));
         own_lo_ = 0;
         own_cnt_ = (uint32_t)m;
         if (m)

@@ -305,19 +305,32 @@ def grid_sort(cloud, support: float, precision: str = "fp64", device: int = -1):
     return keys[:n], order[:n]
 
 
-def shard_layout(sorted_order, nranks: int):
-    """Multi-GPU ownership layout (pcs_shard_layout): returns (chunk, counts,
-    orig_of_internal[nranks*chunk], internal_of_orig[m])."""
+def shard_layout(sorted_order, nranks: int, weights=None):
+    """Multi-GPU ownership layout: returns (chunk, counts, orig_of_internal[nranks*chunk],
+    internal_of_orig[m]).  Without weights: equal counts (pcs_shard_layout); with
+    weights[o] = estimated work of original point o: cuts at equal cumulative
+    work (pcs_shard_layout_weighted, what sharded plans use)."""
     so = np.ascontiguousarray(np.asarray(sorted_order, dtype=np.uint32))
     m = so.size
     chunk = C.c_uint32()
     counts = np.zeros(nranks, dtype=np.uint32)
-    cap = max(1, (m + nranks - 1) // nranks * nranks)
-    ooi = np.zeros(cap, dtype=np.uint32)
     ioo = np.zeros(max(m, 1), dtype=np.uint32)
-    _check(L.lib().pcs_shard_layout(_ptr(so, L._u32p), m, nranks, ooi.ctypes.data_as(L._u32p),
-                                    ioo.ctypes.data_as(L._u32p), C.byref(chunk),
-                                    counts.ctypes.data_as(L._u32p)))
+    if weights is None:
+        cap = max(1, (m + nranks - 1) // nranks * nranks)
+        ooi = np.zeros(cap, dtype=np.uint32)
+        _check(L.lib().pcs_shard_layout(_ptr(so, L._u32p), m, nranks, ooi.ctypes.data_as(L._u32p),
+                                        ioo.ctypes.data_as(L._u32p), C.byref(chunk),
+                                        counts.ctypes.data_as(L._u32p)))
+    else:
+        w = np.ascontiguousarray(np.asarray(weights, dtype=np.float32))
+        wp = w.ctypes.data_as(C.POINTER(C.c_float))
+        _check(L.lib().pcs_shard_layout_weighted(_ptr(so, L._u32p), wp, m, nranks, None, None,
+                                                 C.byref(chunk), counts.ctypes.data_as(L._u32p)))
+        ooi = np.zeros(max(1, chunk.value * nranks), dtype=np.uint32)
+        _check(L.lib().pcs_shard_layout_weighted(_ptr(so, L._u32p), wp, m, nranks,
+                                                 ooi.ctypes.data_as(L._u32p),
+                                                 ioo.ctypes.data_as(L._u32p), C.byref(chunk),
+                                                 counts.ctypes.data_as(L._u32p)))
     return chunk.value, counts, ooi[: chunk.value * nranks], ioo[:m]
 
 

@@ -123,3 +123,61 @@ def test_shard_layout_properties(pb):
             assert np.all(np.diff(r.astype(np.int64)) >= 0)
     with pytest.raises(pb.InvalidParam):
         pb.shard_layout(np.array([5, 1], dtype=np.uint32), 2)   # not a permutation of 0..m-1
+
+
+def test_weighted_shard_layout_balances_work(pb):
+    """Cuts at equal cumulative work: contiguous ranges of the sorted
+    order, every rank's work within one point's weight of the ideal share."""
+    rng = np.random.default_rng(9)
+    for m, world in [(1, 4), (10, 3), (5000, 8), (4001, 7)]:
+        order = rng.permutation(m).astype(np.uint32)
+        # density rising 50x along the sorted order, like config 4's pole
+        w = np.exp(3.9 * np.linspace(-1, 1, m)).astype(np.float32)[np.argsort(order)]
+        chunk, counts, ooi, ioo = pb.shard_layout(order, world, weights=w)
+        assert counts.sum() == m and counts.max() == chunk
+        valid = ooi != 0xFFFFFFFF
+        assert np.array_equal(np.sort(ooi[valid]), np.arange(m))
+        assert np.array_equal(ooi[ioo], np.arange(m))
+        r = ioo[order] // chunk
+        assert np.all(np.diff(r.astype(np.int64)) >= 0)
+        if m >= world:
+            share = np.array([w[ooi[k * chunk:k * chunk + counts[k]]].sum() for k in range(world)])
+            assert np.abs(share - w.sum() / world).max() <= w.max() + 1e-3 * w.sum()
+        if m > 100:  # unequal counts: the dense end gets fewer points per rank
+            assert counts[0] > counts[-1]
+    # unit weights = near-equal counts
+    order = rng.permutation(1000).astype(np.uint32)
+    _, counts, _, _ = pb.shard_layout(order, 8, weights=np.ones(1000, np.float32))
+    assert counts.max() - counts.min() <= 1
+
+
+def test_weighted_layout_evens_config4_work(pb):
+    """Config 4 (density ~ e^{3.9z}): with equal-count shards the rank holding the
+    dense pole does several times the mean work; cutting at the density proxy the
+    plans use (data points in the 3x3x3 cells of side s/4 around each point)
+    brings the max/mean work ratio near 1.  Work = true neighbour counts."""
+    from scipy.spatial import cKDTree
+    P, X0 = pb.generate_config(4, 0.01)
+    s = 0.03
+    work = np.array([len(l) for l in cKDTree(P).query_ball_point(X0, s)], dtype=np.float64)
+    cs = s / 4
+    lo = np.minimum(P.min(0), X0.min(0)) - cs
+    cP = np.floor((P - lo) / cs).astype(np.int64)
+    cX = np.floor((X0 - lo) / cs).astype(np.int64)
+    from collections import Counter
+    cnt = Counter(map(tuple, cP))
+    proxy = np.array([1 + sum(cnt.get((x + a, y + b, z + c), 0) for a in (-1, 0, 1)
+                              for b in (-1, 0, 1) for c in (-1, 0, 1)) for x, y, z in cX],
+                     dtype=np.float32)
+    g = (cX[:, 2] * 10000 + cX[:, 1]) * 10000 + cX[:, 0]   # cell order (x fastest)
+    order = np.argsort(g, kind="stable").astype(np.uint32)
+    world = 8
+
+    def imbalance(weights):
+        chunk, counts, ooi, _ = pb.shard_layout(order, world, weights=weights)
+        per = [work[ooi[k * chunk:k * chunk + counts[k]]].sum() for k in range(world)]
+        return max(per) / (sum(per) / world)
+
+    equal, weighted = imbalance(None), imbalance(proxy)
+    assert equal > 1.5
+    assert weighted < 1.25 and weighted < equal
