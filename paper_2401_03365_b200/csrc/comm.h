@@ -65,4 +65,9 @@ private:
 
 Collectives* make_loopback_collectives(LoopbackGroup* g, int rank);
 
+// No-op collectives: one rank of an N-rank layout computing alone (developer
+// knob PCSB_EMULATE_RANK="N:r" — the per-rank compute of an N-GPU run without
+// its exchange; the other ranks' points simply stay where they are).
+Collectives* make_null_collectives();
+
 }  // namespace pcsb

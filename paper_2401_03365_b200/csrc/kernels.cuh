@@ -55,8 +55,9 @@ int build_query_list(const V* sorted_pts, uint32_t n, const GridGeom& g, double 
                      uint32_t* keys_sorted_tmp, uint32_t* qlist, int* block_shift,
                      RadixScratch& scr, const uint32_t* done, cudaStream_t s,
                      uint32_t val_base = 0);
-// Work unit of the fused kernels: kUnitQueries consecutive entries of the query list.
-constexpr uint32_t kUnitQueries = 32;
+// Work unit of the fused kernels: `unit` (<= 32) consecutive entries of the query
+// list, fetched with one atomic.
+uint32_t work_unit_queries(uint32_t nq, int total_warps);
 
 // cell_start[c] = first sorted position whose cell >= c, c in [0, ncells]
 // (marks + prefix max; scratch: cell_scan_scratch_entries(ncells) words).
@@ -89,6 +90,7 @@ struct FastArgs {
     const uint32_t* qcodes;   // their Morton codes
     int block_shift;          // groups stay inside one (code >> block_shift) block
     uint32_t nq;
+    uint32_t unit;            // queries per work unit (work_unit_queries)
     GridGeom gP, gX;          // grids of the data and of the projected set
     double s_pad;             // support with margin (cell ranges)
     double r2;                // support^2 in fp64: exact re-decision of borderline pairs
@@ -122,6 +124,7 @@ struct DensityArgs {
     const uint32_t* qcodes;
     int block_shift;
     uint32_t nq;
+    uint32_t unit;
     GridGeom g;
     double s_pad, r2;
     float scull2, kneg, K0, band;

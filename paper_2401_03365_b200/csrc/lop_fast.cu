@@ -27,6 +27,7 @@
 //    projected pair or a non-finite sum are deferred to the exact fp64 kernel
 //    (lop_exact.cu).  The neighbour SET is always the reference's.
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -486,14 +487,14 @@ __device__ __forceinline__ EvalConsts make_consts(const float4& q, float kneg, f
 }
 
 // The next work unit for this warp: [r0, r1) positions in the query list.
-__device__ __forceinline__ bool next_unit(uint32_t* counter, uint32_t nq, int lane, uint32_t& r0,
-                                          uint32_t& r1) {
+__device__ __forceinline__ bool next_unit(uint32_t* counter, uint32_t nq, uint32_t unit, int lane,
+                                          uint32_t& r0, uint32_t& r1) {
     uint32_t u = 0;
     if (lane == 0) u = atomicAdd(counter, 1u);
     u = __shfl_sync(0xffffffffu, u, 0);
-    r0 = u * kUnitQueries;
+    r0 = u * unit;
     if (r0 >= nq) return false;
-    r1 = min(r0 + kUnitQueries, nq);
+    r1 = min(r0 + unit, nq);
     return true;
 }
 
@@ -540,7 +541,7 @@ fast_kernel(const FastArgs a) {
     uint32_t* counter = PH == PH_REP ? &a.slot->group_counter2 : &a.slot->group_counter;
 
     uint32_t r0, r1;
-    while (next_unit(counter, a.nq, lane, r0, r1)) {
+    while (next_unit(counter, a.nq, a.unit, lane, r0, r1)) {
         const unsigned brk = group_breaks(a.qcodes, a.block_shift, r0, r1, lane);
         for (uint32_t g0 = r0, g1; g0 < r1; g0 = g1) {
             g1 = group_end(brk, r0, r1, g0, Q);
@@ -694,7 +695,7 @@ density_kernel(const DensityArgs a) {
     Stage S = make_stage(smem + warp * 4 * HR, bars + 2 * warp, lane);
     const int qi = lane / DL, sub = lane % DL;
     uint32_t r0, r1;
-    while (next_unit(a.counter, a.nq, lane, r0, r1)) {
+    while (next_unit(a.counter, a.nq, a.unit, lane, r0, r1)) {
         const unsigned brk = group_breaks(a.qcodes, a.block_shift, r0, r1, lane);
         for (uint32_t g0 = r0, g1; g0 < r1; g0 = g1) {
             g1 = group_end(brk, r0, r1, g0, Q);
@@ -781,6 +782,19 @@ int fast_blocks_per_sm(int lanes_per_point, bool wlop, bool check_zero, int rep_
         cached = b > 0 ? b : 1;
     }
     return cached;
+}
+
+uint32_t work_unit_queries(uint32_t nq, int total_warps) {
+    // measured (config 3, tools/unit_probe.py, tools/scaling_probe.py): 16 beats 32
+    // (shorter tail) and 8 (more fetches and partial groups), at 1/1, 1/4 and 1/8 of X
+    (void)nq;
+    (void)total_warps;
+    static const uint32_t u = [] {
+        const char* e = std::getenv("PCSB_UNIT");  // developer knob (1..32)
+        const int v = e ? std::atoi(e) : 16;
+        return (uint32_t)(v >= 1 && v <= 32 ? v : 16);
+    }();
+    return u;
 }
 
 void launch_density(const DensityArgs& a, int grid_blocks, cudaStream_t s) {

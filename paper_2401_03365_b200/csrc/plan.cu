@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -232,6 +233,14 @@ Plan::Plan(const pcs_lop_desc& d) : d_(d) {
     exact_grid_ = sms * 8;
     support_ = d_.h * d_.cutoff_multiple;
     r2_ = support_ * support_;
+    if (const char* e = std::getenv("PCSB_EMULATE_RANK")) {  // developer knob "N:r"
+        int n = 0, r = 0;
+        if (std::sscanf(e, "%d:%d", &n, &r) == 2 && n >= 1 && r >= 0 && r < n) {
+            nranks_ = n;
+            rank_ = r;
+            coll_ = make_null_collectives();
+        }
+    }
 }
 
 Plan::~Plan() {
@@ -436,6 +445,7 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
             da.qcodes = pfs;
             da.block_shift = bsh;
             da.nq = nn;
+            da.unit = work_unit_queries(nn, density_grid_ * 4);
             da.g = g_;
             da.s_pad = s_pad_;
             da.r2 = r2_;
@@ -671,6 +681,7 @@ void Plan::density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur) {
         da.qcodes = q_skeys_;
         da.block_shift = block_shift_;
         da.nq = nq;
+        da.unit = work_unit_queries(nq, density_grid_ * 4);
         da.g = gX_;
         da.s_pad = s_pad_;
         da.r2 = r2_;
@@ -755,6 +766,7 @@ void Plan::enqueue_sweep(int k) {
         a.qcodes = q_skeys_;
         a.block_shift = block_shift_;
         a.nq = nq;
+        a.unit = work_unit_queries(nq, fast_grid_ * 4);
         a.gP = g_;
         a.gX = gX_;
         a.s_pad = s_pad_;
@@ -1110,7 +1122,9 @@ void density_weights_t(const pcs_lop_desc& d, const double* C, uint64_t n, doubl
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        launch_density(da, sms * fast_blocks_per_sm(4, true, false, 0), s);
+        const int blocks = sms * fast_blocks_per_sm(4, true, false, 0);
+        da.unit = work_unit_queries((uint32_t)n, blocks * 4);
+        launch_density(da, blocks, s);
     } else {
         launch_exact_density<T>(tg.sorted, tg.start, tg.sorted, nullptr, (uint32_t)n, nullptr, tg.g,
                                 tg.s_pad, r2, support, d.h, 0, tg.unsorted, tg.order, st, nullptr, s);
