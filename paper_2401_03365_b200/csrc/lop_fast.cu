@@ -311,14 +311,16 @@ enum : int { K_ATTR = 0, K_REP_INVCUBE = 1, K_REP_NEGLIN = 2, K_DENSITY = 3 };
 
 struct Acc {
     float2 s, x, y, z;  // sum w, sum w*(c - q), per candidate parity
-    int hneg;           // -(hits)
-    int rneg;           // -(candidates in range, incl. zero distance) (kZero)
+    int miss;           // -(fp32 decisions "out of range", re-decided in the band)
+    int zero;           // -(zero-distance candidates) (kZero)
+    int evald;          // candidates evaluated by this lane
+    int hneg, rneg;     // after group_reduce: hits (d > 0), in range (incl. d == 0)
 };
 
 __device__ __forceinline__ Acc acc_zero() {
     Acc A;
     A.s = A.x = A.y = A.z = make_float2(0.f, 0.f);
-    A.hneg = A.rneg = 0;
+    A.miss = A.zero = A.evald = A.hneg = A.rneg = 0;
     return A;
 }
 
@@ -361,17 +363,24 @@ __device__ __forceinline__ float2 pair_weight(const float2& d2, const float2& ar
     return w;
 }
 
-// all-ones if v >= 0 (FSET: an integer mask, kept off the predicate/select path)
-__device__ __forceinline__ uint32_t ge0_mask(float v) {
+// All-ones iff v < 0: the sign bit spread by one arithmetic shift (inline PTX so
+// that it is not turned back into compare + select).  For arg = fma(d2, kneg,
+// K0), K0 > 0, this is exactly "arg < 0": arg is never -0 (an exactly
+// cancelling fma rounds to +0) and never NaN (candidates and padding are finite).
+__device__ __forceinline__ uint32_t sign_mask(float v) {
     uint32_t m;
-    asm("set.ge.u32.f32 %0, %1, 0f00000000;" : "=r"(m) : "f"(v));
+    asm("shr.s32 %0, %1, 31;" : "=r"(m) : "r"(__float_as_uint(v)));
     return m;
 }
-__device__ __forceinline__ uint32_t gt0_mask(float v) {
+// All-ones iff d2 == +0 (d2 >= 0 is a sum of squares).
+__device__ __forceinline__ uint32_t zero_mask(float d2) {
     uint32_t m;
-    asm("set.gt.u32.f32 %0, %1, 0f00000000;" : "=r"(m) : "f"(v));
+    asm("{\n\t.reg .u32 t;\n\tadd.u32 t, %1, 0xffffffff;\n\tshr.s32 %0, t, 31;\n\t}"
+        : "=r"(m)
+        : "r"(__float_as_uint(d2)));
     return m;
 }
+
 
 // kZero: exclude d2 == 0 from the hits (and count in-range candidates in rneg).
 template <int L, int KIND, bool kWlop, bool kZero>
@@ -392,14 +401,16 @@ __device__ __forceinline__ void eval_pairs(const float4* __restrict__ pb, int nr
             d2 = __ffma2_rn(dz, dz, d2);
             const float2 arg = __ffma2_rn(d2, ec.kneg, ec.K0);  // >= 0 <=> d2 <= r2 (fp32)
             bmin = fminf(bmin, fminf(fabsf(arg.x), fabsf(arg.y)));
-            uint2 m = make_uint2(ge0_mask(arg.x), ge0_mask(arg.y));
+            const uint2 sg = make_uint2(sign_mask(arg.x), sign_mask(arg.y));  // -1: out
+            uint2 m = make_uint2(~sg.x, ~sg.y);  // weight mask (folds into LOP3)
+            A.miss += (int)sg.x + (int)sg.y;
             if (kZero) {
-                A.rneg += (int)m.x + (int)m.y;
-                m.x &= gt0_mask(d2.x);
-                m.y &= gt0_mask(d2.y);
+                const uint2 z = make_uint2(zero_mask(d2.x), zero_mask(d2.y));
+                A.zero += (int)z.x + (int)z.y;
+                m.x &= ~z.x;
+                m.y &= ~z.y;
             }
             const float2 w = pair_weight<KIND, kWlop, kZero>(d2, arg, m, B, ec);
-            A.hneg += (int)m.x + (int)m.y;
             A.s = __fadd2_rn(A.s, w);
             if (KIND != K_DENSITY) {
                 A.x = __ffma2_rn(w, dx, A.x);
@@ -431,10 +442,9 @@ __device__ __forceinline__ void fix_band(const float4* buf, int nrec, int sub, c
             const float4 B = make_float4(cc.z, cc.z, cc.w, cc.w);
             const float2 w2 = pair_weight<KIND, kWlop, kZero>(f2(d2, d2), f2(arg, arg),
                                                               make_uint2(~0u, ~0u), B, ec);
-            if (kZero) A.rneg -= sgn;
+            A.miss += sgn;  // the fast path counted the fp32 decision
             if (!kZero || d2 > 0.f) {
                 const float w = w2.x * (float)sgn;
-                A.hneg -= sgn;
                 A.s.x += w;
                 if (KIND != K_DENSITY) {
                     A.x.x = fmaf(w, dx, A.x.x);
@@ -452,6 +462,7 @@ __device__ __forceinline__ void eval_half(const float4* half, int nrec, int sub,
                                           const EvalConsts& ec, float band, double r2, Acc& A) {
     float bmin = INFINITY;
     eval_pairs<L, KIND, kWlop, kZero>(half, nrec, sub, ec, A, bmin);
+    A.evald += 2 * nrec / L;  // nrec is a multiple of STEP = L * U: every lane the same
     if (__any_sync(0xffffffffu, bmin <= band))
         fix_band<L, KIND, kWlop, kZero>(half, nrec, sub, q, ec, band, r2, A);
 }
@@ -463,15 +474,17 @@ __device__ __forceinline__ int group_isum(int v) {
     return v;
 }
 
-// Per-query totals over its L lanes; afterwards hneg/rneg hold the positive counts.
+// Per-query totals over its L lanes; afterwards hneg = hits, rneg = in range.
 template <int L>
 __device__ __forceinline__ void group_reduce(Acc& A, bool with_nr) {
     A.s.x = group_sum<L>(A.s.x + A.s.y);
     A.x.x = group_sum<L>(A.x.x + A.x.y);
     A.y.x = group_sum<L>(A.y.x + A.y.y);
     A.z.x = group_sum<L>(A.z.x + A.z.y);
-    A.hneg = -group_isum<L>(A.hneg);
-    if (with_nr) A.rneg = -group_isum<L>(A.rneg);
+    (void)with_nr;
+    const int ev = group_isum<L>(A.evald), miss = group_isum<L>(A.miss);
+    A.rneg = ev + miss;                          // in range (d2 <= r2)
+    A.hneg = A.rneg + group_isum<L>(A.zero);     // hits (and d > 0 when kZero)
 }
 
 __device__ __forceinline__ EvalConsts make_consts(const float4& q, float kneg, float K0,
