@@ -166,7 +166,10 @@ rs_scan_rows_kernel(uint32_t* __restrict__ a, uint32_t nblocks, uint32_t* __rest
 
 
 // Stable scatter: within a tile elements keep their order (round-major,
-// warp-major, lane-minor), ranks inside a warp come from __match_any_sync.
+// warp-major, lane-minor), ranks inside a warp come from __match_any_sync.  The
+// tile is first reordered by digit in shared memory, then written out as
+// contiguous digit runs (~8 keys = one 32-byte sector per run for 8-bit digits
+// and 2048-key tiles), instead of 4-byte writes scattered over 256 buckets.
 __global__ void __launch_bounds__(RS_THREADS)
 rs_scatter_kernel(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                   uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, uint32_t n, int shift,
@@ -174,18 +177,26 @@ rs_scatter_kernel(const uint32_t* __restrict__ kin, const uint32_t* __restrict__
                   const uint32_t* __restrict__ digit_totals, uint32_t val_base,
                   const uint32_t* done) {
     if (done && *done) return;
-    __shared__ uint32_t run[256];
+    __shared__ uint32_t run[256];    // tile-local running offset per digit
+    __shared__ uint32_t gbase[256];  // global position = gbase[d] + tile-local position
     __shared__ uint32_t wcnt[RS_WARPS][256];
     __shared__ uint32_t woff[RS_WARPS][256];
+    __shared__ uint32_t skey[RS_TILE];
+    __shared__ uint32_t sval[RS_TILE];
     __shared__ uint32_t sh[33];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // digit bases: exclusive scan of the 256 digit totals (one digit per thread)
-    const uint32_t dbase = block_exclusive_scan(digit_totals[threadIdx.x], sh, nullptr);
-    for (int d = threadIdx.x; d < 256; d += RS_THREADS) {
-        run[d] = dbase + blockoff[(size_t)d * nblocks + blockIdx.x];
+    const int d0 = threadIdx.x;  // RS_THREADS == 256: one digit per thread
+    // digit bases (exclusive scan of the digit totals) and this tile's digit counts
+    const uint32_t tot = digit_totals[d0];
+    const uint32_t dbase = block_exclusive_scan(tot, sh, nullptr);
+    const uint32_t boff = blockoff[(size_t)d0 * nblocks + blockIdx.x];
+    const uint32_t bnext =
+        blockIdx.x + 1 < nblocks ? blockoff[(size_t)d0 * nblocks + blockIdx.x + 1] : tot;
+    const uint32_t tstart = block_exclusive_scan(bnext - boff, sh, nullptr);
+    run[d0] = tstart;
+    gbase[d0] = dbase + boff - tstart;
 #pragma unroll
-        for (int w = 0; w < RS_WARPS; ++w) wcnt[w][d] = 0;
-    }
+    for (int w = 0; w < RS_WARPS; ++w) wcnt[w][d0] = 0;
     __syncthreads();
     const uint32_t base = blockIdx.x * RS_TILE;
     const unsigned lt = (1u << lane) - 1u;
@@ -199,23 +210,31 @@ rs_scatter_kernel(const uint32_t* __restrict__ kin, const uint32_t* __restrict__
         const uint32_t rank = __popc(peers & lt);
         if (valid && (__ffs(peers) - 1) == lane) wcnt[warp][d] = __popc(peers);
         __syncthreads();
-        for (int dd = threadIdx.x; dd < 256; dd += RS_THREADS) {
-            uint32_t acc = run[dd];
+        {
+            uint32_t acc = run[d0];
 #pragma unroll
             for (int w = 0; w < RS_WARPS; ++w) {
-                const uint32_t c = wcnt[w][dd];
-                woff[w][dd] = acc;
+                const uint32_t c = wcnt[w][d0];
+                woff[w][d0] = acc;
                 acc += c;
-                wcnt[w][dd] = 0;
+                wcnt[w][d0] = 0;
             }
-            run[dd] = acc;
+            run[d0] = acc;
         }
         __syncthreads();
         if (valid) {
-            const uint32_t pos = woff[warp][d] + rank;
-            kout[pos] = key;
-            vout[pos] = val;
+            const uint32_t pos = woff[warp][d] + rank;  // tile-local
+            skey[pos] = key;
+            sval[pos] = val;
         }
+    }
+    __syncthreads();
+    const uint32_t cnt = min((uint32_t)RS_TILE, n - base);
+    for (uint32_t p = threadIdx.x; p < cnt; p += RS_THREADS) {
+        const uint32_t key = skey[p];
+        const uint32_t g = gbase[(key >> shift) & mask] + p;
+        kout[g] = key;
+        vout[g] = sval[p];
     }
 }
 
