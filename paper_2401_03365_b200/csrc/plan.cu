@@ -79,7 +79,9 @@ GridGeom make_grid(const double lo_in[3], const double hi_in[3], double support)
     double cs;
     if (cells_for(lo, hi, support * 0.25) <= (double)(1u << 25)) {
         cs = support * 0.25;  // rows trimmed at s/4 granularity hug the ball-of-box
-    } else if (cells_for(lo, hi, support * 0.5) <= (double)(1u << 25)) {
+    } else if (cells_for(lo, hi, support * 0.5) <= (double)(1u << 28)) {
+        // up to 2^28 cells (a 1 GB table): config 5 at h = 0.01 (8 ellipsoids in a
+        // 3.2^3 box) needs 2.6e8; cell side = s would cost ~2x the candidates
         cs = support * 0.5;
     } else {
         cs = support;
@@ -133,14 +135,16 @@ GridGeom make_grid_scaled(const double lo_in[3], const double hi_in[3], double s
     return g;
 }
 
-// x-grid scale (developer knob PCSB_XCELL, default 1 = the data grid).  Measured
+// x-grid scale (developer knob PCSB_XCELL; default 1 = the data grid).  Measured
 // with 2x: config 3 -2.4% sweep time, config 2 -6%, but config 5 +5% and the
 // WLOP config 4 +9% (its density pass over X loses more to coarse rows).
-double x_cell_scale(uint64_t n, uint64_t m) {
+double x_cell_scale(uint64_t n, uint64_t m, const GridGeom& g) {
     (void)n;
     (void)m;
     if (const char* e = std::getenv("PCSB_XCELL")) return std::atof(e);
-    return 1.0;
+    // a data grid past 2^25 cells: the projected set's table (rebuilt every
+    // sweep) is kept 8x smaller
+    return g.ncells > (1u << 25) ? 2.0 : 1.0;
 }
 
 void validate_desc(const pcs_lop_desc& d) {
@@ -380,7 +384,7 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
         maxabs = std::max(maxabs, std::max(std::fabs(lo[a]), std::fabs(hi[a])));
     }
     g_ = make_grid(lo, hi, support_);
-    gX_ = make_grid_scaled(lo, hi, support_, x_cell_scale(n, m), g_);
+    gX_ = make_grid_scaled(lo, hi, support_, x_cell_scale(n, m, g_), g_);
     s_pad_ = support_ * (1.0 + std::ldexp(1.0, -10)) + 1e-12 * maxabs;
     maxabs_ = maxabs;
 

@@ -34,7 +34,7 @@ void cuda_check(cudaError_t e, const char* what);
 GridGeom make_grid(const double lo[3], const double hi[3], double support);
 GridGeom make_grid_scaled(const double lo[3], const double hi[3], double support, double scale,
                           const GridGeom& base);
-double x_cell_scale(uint64_t n, uint64_t m);
+double x_cell_scale(uint64_t n, uint64_t m, const GridGeom& g);
 
 void validate_desc(const pcs_lop_desc& d);  // throws Failure(INVALID_PARAM)
 int select_device(int requested);           // throws Failure(NO_DEVICE)
