@@ -19,9 +19,12 @@ namespace pcsb {
 // key is  linear_cell << (3*sub_bits) | morton(sub-cell)  so that every row of
 // cells (fixed y,z, a run of x) is one contiguous range of the sorted array and
 // points inside a cell are ordered along a Z-curve (compact query groups).
+// Cells may be finer along x (the row direction): csx = cs / xsub.
 struct GridGeom {
     double ox, oy, oz;   // origin
-    double cs, inv_cs;   // cell side and its inverse
+    double cs, inv_cs;   // y/z cell side and its inverse
+    double csx, inv_csx; // x cell side (cs / xsub) and its inverse
+    int32_t xsub;        // x cells per y/z cell side
     int32_t gx, gy, gz;  // cells per axis
     int32_t sub_bits;    // morton bits per axis inside a cell
     uint32_t ncells;     // gx*gy*gz
@@ -74,7 +77,7 @@ __device__ __forceinline__ int32_t cell_coord(double x, double o, double inv, in
 }
 
 __device__ __forceinline__ uint32_t point_key(const GridGeom& g, double x, double y, double z) {
-    const double ux = (x - g.ox) * g.inv_cs, uy = (y - g.oy) * g.inv_cs, uz = (z - g.oz) * g.inv_cs;
+    const double ux = (x - g.ox) * g.inv_csx, uy = (y - g.oy) * g.inv_cs, uz = (z - g.oz) * g.inv_cs;
     const double fx = floor(ux), fy = floor(uy), fz = floor(uz);
     int32_t cx = (fx >= 0.0) ? (fx >= (double)(g.gx - 1) ? g.gx - 1 : (int32_t)fx) : 0;
     int32_t cy = (fy >= 0.0) ? (fy >= (double)(g.gy - 1) ? g.gy - 1 : (int32_t)fy) : 0;

@@ -250,6 +250,9 @@ __global__ void gather_kernel(const V* __restrict__ src, const uint32_t* __restr
 // (Z-curve) code of the point's half-cell coordinates, with per-axis bit counts
 // (an axis with fewer cells drops out of the top levels), computed from the
 // sorted positions.
+// x extent in y/z-sized cells (the Morton code is isotropic)
+__host__ __device__ inline int32_t gx_iso(const GridGeom& g) { return (g.gx + g.xsub - 1) / g.xsub; }
+
 struct MortonAxes {
     int bits[3];  // code bits per axis (after coarsening by `shift`)
     int shift;
@@ -272,7 +275,7 @@ __global__ void morton_keys_kernel(const V* __restrict__ pts, uint32_t n, GridGe
     const int top = max(ax.bits[0], max(ax.bits[1], ax.bits[2]));
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const V p = pts[i];
-        const uint32_t f[3] = {half_cell((double)p.x, g.ox, inv2, 2 * g.gx) >> ax.shift,
+        const uint32_t f[3] = {half_cell((double)p.x, g.ox, inv2, 2 * gx_iso(g)) >> ax.shift,
                                half_cell((double)p.y, g.oy, inv2, 2 * g.gy) >> ax.shift,
                                half_cell((double)p.z, g.oz, inv2, 2 * g.gz) >> ax.shift};
         uint32_t key = 0;
@@ -517,7 +520,7 @@ int build_query_list(const V* sorted_pts, uint32_t n, const GridGeom& g, double 
         while (b < 32 && (1ull << b) < v) ++b;
         return b;
     };
-    const int full[3] = {width(2ull * g.gx), width(2ull * g.gy), width(2ull * g.gz)};
+    const int full[3] = {width(2ull * gx_iso(g)), width(2ull * g.gy), width(2ull * g.gz)};
     MortonAxes ax;
     ax.shift = std::max(0, std::max(full[0], std::max(full[1], full[2])) - 10);
     int mbits = 0;

@@ -66,8 +66,8 @@ struct Rows {
 __device__ __forceinline__ Rows rows_around(const GridGeom& g, double x, double y, double z,
                                             double s_pad) {
     Rows r;
-    r.lox = cell_coord(x - s_pad, g.ox, g.inv_cs, g.gx);
-    r.hix = cell_coord(x + s_pad, g.ox, g.inv_cs, g.gx);
+    r.lox = cell_coord(x - s_pad, g.ox, g.inv_csx, g.gx);
+    r.hix = cell_coord(x + s_pad, g.ox, g.inv_csx, g.gx);
     r.loy = cell_coord(y - s_pad, g.oy, g.inv_cs, g.gy);
     const int hiy = cell_coord(y + s_pad, g.oy, g.inv_cs, g.gy);
     r.loz = cell_coord(z - s_pad, g.oz, g.inv_cs, g.gz);
@@ -432,10 +432,10 @@ __global__ void shard_work_kernel(const V* __restrict__ X0, uint32_t m, GridGeom
                                   const uint32_t* __restrict__ Pstart, float* __restrict__ w) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
         const V p = X0[i];
-        const int cx = cell_coord((double)p.x, g.ox, g.inv_cs, g.gx);
+        const int cx = cell_coord((double)p.x, g.ox, g.inv_csx, g.gx);
         const int cy = cell_coord((double)p.y, g.oy, g.inv_cs, g.gy);
         const int cz = cell_coord((double)p.z, g.oz, g.inv_cs, g.gz);
-        const int lx = max(cx - 1, 0), hx = min(cx + 1, g.gx - 1);
+        const int lx = max(cx - g.xsub, 0), hx = min(cx + g.xsub, g.gx - 1);
         uint32_t cnt = 0;
         for (int z = max(cz - 1, 0); z <= min(cz + 1, g.gz - 1); ++z)
             for (int y = max(cy - 1, 0); y <= min(cy + 1, g.gy - 1); ++y) {

@@ -218,8 +218,8 @@ __device__ __forceinline__ void row_range(const uint32_t* __restrict__ start, co
         }
     }
     if (!(lo <= hi)) return;
-    const int lox = cell_coord((double)lo, g.ox, g.inv_cs, g.gx);
-    const int hix = cell_coord((double)hi, g.ox, g.inv_cs, g.gx);
+    const int lox = cell_coord((double)lo, g.ox, g.inv_csx, g.gx);
+    const int hix = cell_coord((double)hi, g.ox, g.inv_csx, g.gx);
     const uint32_t row = (uint32_t)zz * (uint32_t)g.gy + (uint32_t)yy;
     const uint32_t base = row * (uint32_t)g.gx;
     const uint32_t delta = pair_row_delta(start, row, (uint32_t)g.gx);  // record-slot shift

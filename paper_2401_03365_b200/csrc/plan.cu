@@ -93,12 +93,25 @@ GridGeom make_grid(const double lo_in[3], const double hi_in[3], double support)
         if (f > 0.0 && cells_for(lo, hi, support * f) <= (double)(1u << 25)) cs = support * f;
     }
     const int sb = 0;
+    // finer cells along x (rows are unchanged; x-trimming gets tighter) while the
+    // table stays within 2^27 cells.  Measured sweep time, xsub 1 -> 2 -> 4:
+    // config 3 -2.6%, config 4 -11% / -19%, config 5 -5% / -3%.
+    int xsub = 1;
+    for (int t : {4, 2})
+        if (cells_for(lo, hi, cs) * t <= (double)(1u << 27)) {
+            xsub = t;
+            break;
+        }
+    if (const char* e = std::getenv("PCSB_XSUB")) xsub = std::max(1, std::atoi(e));  // developer knob
     g.cs = cs;
     g.inv_cs = 1.0 / cs;
+    g.xsub = xsub;
+    g.csx = cs / xsub;
+    g.inv_csx = 1.0 / g.csx;
     g.ox = lo[0] - cs;
     g.oy = lo[1] - cs;
     g.oz = lo[2] - cs;
-    g.gx = (int32_t)std::floor((hi[0] - g.ox) * g.inv_cs) + 2;
+    g.gx = (int32_t)std::floor((hi[0] - g.ox) * g.inv_csx) + 2;
     g.gy = (int32_t)std::floor((hi[1] - g.oy) * g.inv_cs) + 2;
     g.gz = (int32_t)std::floor((hi[2] - g.oz) * g.inv_cs) + 2;
     g.sub_bits = sb;
@@ -123,10 +136,13 @@ GridGeom make_grid_scaled(const double lo_in[3], const double hi_in[3], double s
     GridGeom g = base;
     g.cs = base.cs * scale;
     g.inv_cs = 1.0 / g.cs;
+    g.xsub = 1;
+    g.csx = g.cs;
+    g.inv_csx = g.inv_cs;
     g.ox = lo[0] - g.cs;
     g.oy = lo[1] - g.cs;
     g.oz = lo[2] - g.cs;
-    g.gx = (int32_t)std::floor((hi[0] - g.ox) * g.inv_cs) + 2;
+    g.gx = (int32_t)std::floor((hi[0] - g.ox) * g.inv_csx) + 2;
     g.gy = (int32_t)std::floor((hi[1] - g.oy) * g.inv_cs) + 2;
     g.gz = (int32_t)std::floor((hi[2] - g.oz) * g.inv_cs) + 2;
     g.sub_bits = 0;
