@@ -658,6 +658,14 @@ void Plan::synchronize() {
         const float exposed = tg > ta ? tg - ta : 0.f;
         sort_ms_ += q + exposed;
         kernel_ms_ += tk - q - exposed;
+        static const bool dbg = std::getenv("PCSB_DEBUG_TIMES") != nullptr;  // developer knob
+        if (dbg) {
+            float te = 0.f;
+            PCSB_CUDA(cudaEventElapsedTime(&te, se.e[0], se.e[5]));
+            std::fprintf(stderr, "[pcsb] sweep: queries %.3f attraction %.3f grid-exposed %.3f "
+                         "repulsion+update %.3f tail %.3f total %.3f ms\n", q, ta - q, exposed,
+                         tk - std::max(ta, tg), te - tk, te);
+        }
         event_pool_.push_back(se);
     }
     pending_.clear();
