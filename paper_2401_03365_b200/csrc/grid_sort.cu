@@ -7,10 +7,14 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace pcsb {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -87,15 +91,14 @@ __global__ void keys_kernel(GridGeom g, const V* __restrict__ pts, uint32_t n,
 
 // ---- radix sort -------------------------------------------------------------
 
-__global__ void __launch_bounds__(RS_THREADS)
-rs_hist_kernel(const uint32_t* __restrict__ keys, uint32_t n, int shift, uint32_t mask,
-               uint32_t* __restrict__ blockhist, uint32_t nblocks, const uint32_t* done) {
-    if (done && *done) return;
-    __shared__ uint32_t h[RS_WARPS][256];
+// Histogram of tile `tile` (digit-major layout: blockhist[d * ntiles + tile]).
+__device__ __forceinline__ void hist_tile(const uint32_t* __restrict__ keys, uint32_t n, int shift,
+                                          uint32_t mask, uint32_t* __restrict__ blockhist,
+                                          uint32_t ntiles, uint32_t tile, uint32_t (*h)[256]) {
     for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_THREADS) (&h[0][0])[i] = 0;
     __syncthreads();
     const int warp = threadIdx.x >> 5;
-    const uint32_t base = blockIdx.x * RS_TILE;
+    const uint32_t base = tile * RS_TILE;
 #pragma unroll
     for (int r = 0; r < RS_ITEMS; ++r) {
         const uint32_t i = base + r * RS_THREADS + threadIdx.x;
@@ -106,8 +109,17 @@ rs_hist_kernel(const uint32_t* __restrict__ keys, uint32_t n, int shift, uint32_
         uint32_t s = 0;
 #pragma unroll
         for (int w = 0; w < RS_WARPS; ++w) s += h[w][d];
-        blockhist[(size_t)d * nblocks + blockIdx.x] = s;
+        blockhist[(size_t)d * ntiles + tile] = s;
     }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(RS_THREADS)
+rs_hist_kernel(const uint32_t* __restrict__ keys, uint32_t n, int shift, uint32_t mask,
+               uint32_t* __restrict__ blockhist, uint32_t nblocks, const uint32_t* done) {
+    if (done && *done) return;
+    __shared__ uint32_t h[RS_WARPS][256];
+    hist_tile(keys, n, shift, mask, blockhist, nblocks, blockIdx.x, h);
 }
 
 // Exclusive scan of the digit-major block histograms, one block per digit row
@@ -143,15 +155,13 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
     return r;
 }
 
-__global__ void __launch_bounds__(RS_ROW_THREADS)
-rs_scan_rows_kernel(uint32_t* __restrict__ a, uint32_t nblocks, uint32_t* __restrict__ totals,
-                    const uint32_t* done) {
-    if (done && *done) return;
-    __shared__ uint32_t sh[33];
-    uint32_t* row = a + (size_t)blockIdx.x * nblocks;
-    const uint32_t chunk = (nblocks + RS_ROW_THREADS - 1) / RS_ROW_THREADS;
+// Exclusive scan of digit row d across the tiles; the row total goes to totals[d].
+__device__ __forceinline__ void scan_row(uint32_t* __restrict__ a, uint32_t ntiles,
+                                         uint32_t* __restrict__ totals, uint32_t d, uint32_t* sh) {
+    uint32_t* row = a + (size_t)d * ntiles;
+    const uint32_t chunk = (ntiles + RS_ROW_THREADS - 1) / RS_ROW_THREADS;
     const uint32_t b = threadIdx.x * chunk;
-    const uint32_t e = min(b + chunk, nblocks);
+    const uint32_t e = min(b + chunk, ntiles);
     uint32_t s = 0;
     for (uint32_t i = b; i < e; ++i) s += row[i];
     uint32_t tot = 0;
@@ -161,9 +171,93 @@ rs_scan_rows_kernel(uint32_t* __restrict__ a, uint32_t nblocks, uint32_t* __rest
         row[i] = run;
         run += v;
     }
-    if (threadIdx.x == 0) totals[blockIdx.x] = tot;
+    if (threadIdx.x == 0) totals[d] = tot;
+    __syncthreads();
 }
 
+__global__ void __launch_bounds__(RS_ROW_THREADS)
+rs_scan_rows_kernel(uint32_t* __restrict__ a, uint32_t nblocks, uint32_t* __restrict__ totals,
+                    const uint32_t* done) {
+    if (done && *done) return;
+    __shared__ uint32_t sh[33];
+    scan_row(a, nblocks, totals, blockIdx.x, sh);
+}
+
+// Stable scatter: within a tile elements keep their order (round-major,
+// warp-major, lane-minor), ranks inside a warp come from __match_any_sync.  The
+// tile is first reordered by digit in shared memory, then written out as
+// contiguous digit runs (~8 keys = one 32-byte sector per run for 8-bit digits
+// and 2048-key tiles), instead of 4-byte writes scattered over 256 buckets.
+struct ScatterSmem {
+    uint32_t run[256];    // tile-local running offset per digit
+    uint32_t gbase[256];  // global position = gbase[d] + tile-local position
+    uint32_t wcnt[RS_WARPS][256];
+    uint32_t woff[RS_WARPS][256];
+    uint32_t skey[RS_TILE];
+    uint32_t sval[RS_TILE];
+    uint32_t sh[33];
+};
+
+__device__ __forceinline__ void scatter_tile(const uint32_t* __restrict__ kin,
+                                             const uint32_t* __restrict__ vin,
+                                             uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                                             uint32_t n, int shift, uint32_t mask,
+                                             const uint32_t* __restrict__ blockoff, uint32_t ntiles,
+                                             const uint32_t* __restrict__ digit_totals,
+                                             uint32_t val_base, uint32_t tile, ScatterSmem& S) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int d0 = threadIdx.x;  // RS_THREADS == 256: one digit per thread
+    // digit bases (exclusive scan of the digit totals) and this tile's digit counts
+    const uint32_t tot = digit_totals[d0];
+    const uint32_t dbase = block_exclusive_scan(tot, S.sh, nullptr);
+    const uint32_t boff = blockoff[(size_t)d0 * ntiles + tile];
+    const uint32_t bnext = tile + 1 < ntiles ? blockoff[(size_t)d0 * ntiles + tile + 1] : tot;
+    const uint32_t tstart = block_exclusive_scan(bnext - boff, S.sh, nullptr);
+    S.run[d0] = tstart;
+    S.gbase[d0] = dbase + boff - tstart;
+#pragma unroll
+    for (int w = 0; w < RS_WARPS; ++w) S.wcnt[w][d0] = 0;
+    __syncthreads();
+    const uint32_t base = tile * RS_TILE;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int r = 0; r < RS_ITEMS; ++r) {
+        const uint32_t i = base + r * RS_THREADS + threadIdx.x;
+        const bool valid = i < n;
+        const uint32_t key = valid ? kin[i] : 0u;
+        const uint32_t val = valid ? (vin ? vin[i] : val_base + i) : 0u;
+        const uint32_t d = valid ? ((key >> shift) & mask) : 256u;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t rank = __popc(peers & lt);
+        if (valid && (__ffs(peers) - 1) == lane) S.wcnt[warp][d] = __popc(peers);
+        __syncthreads();
+        {
+            uint32_t acc = S.run[d0];
+#pragma unroll
+            for (int w = 0; w < RS_WARPS; ++w) {
+                const uint32_t c = S.wcnt[w][d0];
+                S.woff[w][d0] = acc;
+                acc += c;
+                S.wcnt[w][d0] = 0;
+            }
+            S.run[d0] = acc;
+        }
+        __syncthreads();
+        if (valid) {
+            const uint32_t pos = S.woff[warp][d] + rank;  // tile-local
+            S.skey[pos] = key;
+            S.sval[pos] = val;
+        }
+    }
+    __syncthreads();
+    const uint32_t cnt = min((uint32_t)RS_TILE, n - base);
+    for (uint32_t p = threadIdx.x; p < cnt; p += RS_THREADS) {
+        const uint32_t key = S.skey[p];
+        const uint32_t g = S.gbase[(key >> shift) & mask] + p;
+        kout[g] = key;
+        vout[g] = S.sval[p];
+    }
+    __syncthreads();
+}
 
 // Stable scatter: within a tile elements keep their order (round-major,
 // warp-major, lane-minor), ranks inside a warp come from __match_any_sync.  The
@@ -177,64 +271,45 @@ rs_scatter_kernel(const uint32_t* __restrict__ kin, const uint32_t* __restrict__
                   const uint32_t* __restrict__ digit_totals, uint32_t val_base,
                   const uint32_t* done) {
     if (done && *done) return;
-    __shared__ uint32_t run[256];    // tile-local running offset per digit
-    __shared__ uint32_t gbase[256];  // global position = gbase[d] + tile-local position
-    __shared__ uint32_t wcnt[RS_WARPS][256];
-    __shared__ uint32_t woff[RS_WARPS][256];
-    __shared__ uint32_t skey[RS_TILE];
-    __shared__ uint32_t sval[RS_TILE];
-    __shared__ uint32_t sh[33];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int d0 = threadIdx.x;  // RS_THREADS == 256: one digit per thread
-    // digit bases (exclusive scan of the digit totals) and this tile's digit counts
-    const uint32_t tot = digit_totals[d0];
-    const uint32_t dbase = block_exclusive_scan(tot, sh, nullptr);
-    const uint32_t boff = blockoff[(size_t)d0 * nblocks + blockIdx.x];
-    const uint32_t bnext =
-        blockIdx.x + 1 < nblocks ? blockoff[(size_t)d0 * nblocks + blockIdx.x + 1] : tot;
-    const uint32_t tstart = block_exclusive_scan(bnext - boff, sh, nullptr);
-    run[d0] = tstart;
-    gbase[d0] = dbase + boff - tstart;
-#pragma unroll
-    for (int w = 0; w < RS_WARPS; ++w) wcnt[w][d0] = 0;
-    __syncthreads();
-    const uint32_t base = blockIdx.x * RS_TILE;
-    const unsigned lt = (1u << lane) - 1u;
-    for (int r = 0; r < RS_ITEMS; ++r) {
-        const uint32_t i = base + r * RS_THREADS + threadIdx.x;
-        const bool valid = i < n;
-        const uint32_t key = valid ? kin[i] : 0u;
-        const uint32_t val = valid ? (vin ? vin[i] : val_base + i) : 0u;
-        const uint32_t d = valid ? ((key >> shift) & mask) : 256u;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
-        const uint32_t rank = __popc(peers & lt);
-        if (valid && (__ffs(peers) - 1) == lane) wcnt[warp][d] = __popc(peers);
-        __syncthreads();
-        {
-            uint32_t acc = run[d0];
-#pragma unroll
-            for (int w = 0; w < RS_WARPS; ++w) {
-                const uint32_t c = wcnt[w][d0];
-                woff[w][d0] = acc;
-                acc += c;
-                wcnt[w][d0] = 0;
-            }
-            run[d0] = acc;
-        }
-        __syncthreads();
-        if (valid) {
-            const uint32_t pos = woff[warp][d] + rank;  // tile-local
-            skey[pos] = key;
-            sval[pos] = val;
-        }
-    }
-    __syncthreads();
-    const uint32_t cnt = min((uint32_t)RS_TILE, n - base);
-    for (uint32_t p = threadIdx.x; p < cnt; p += RS_THREADS) {
-        const uint32_t key = skey[p];
-        const uint32_t g = gbase[(key >> shift) & mask] + p;
-        kout[g] = key;
-        vout[g] = sval[p];
+    __shared__ ScatterSmem S;
+    scatter_tile(kin, vin, kout, vout, n, shift, mask, blockoff, nblocks, digit_totals, val_base,
+                 blockIdx.x, S);
+}
+
+// The whole LSD sort in ONE cooperative launch (per pass: histograms, row
+// scans, scatters, separated by grid-wide barriers; tiles and digit rows are
+// looped over the co-resident grid).  For the per-sweep sorts (<= a few M
+// keys) the multi-kernel version is launch/latency-bound.
+__global__ void __launch_bounds__(RS_THREADS)
+rs_coop_kernel(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
+               uint32_t* vals_out, uint32_t* keys_alt, uint32_t* vals_alt, uint32_t n, int key_bits,
+               uint32_t* blockhist, uint32_t ntiles, uint32_t val_base, const uint32_t* done) {
+    if (done && *done) return;  // the flag is constant during the launch: uniform exit
+    cg::grid_group grid = cg::this_grid();
+    __shared__ ScatterSmem S;
+    __shared__ uint32_t h[RS_WARPS][256];
+    const int passes = key_bits <= 0 ? 1 : (key_bits + 7) / 8;
+    const uint32_t* kin = keys_in;
+    const uint32_t* vin = vals_in;
+    uint32_t* totals = blockhist + 256 * (size_t)ntiles;
+    for (int p = 0; p < passes; ++p) {
+        const int shift = 8 * p;
+        const int bits = (key_bits - shift) < 8 ? (key_bits - shift) : 8;
+        const uint32_t mask = bits <= 0 ? 0u : ((1u << bits) - 1u);
+        const bool to_out = ((passes - 1 - p) % 2) == 0;
+        uint32_t* ko = to_out ? keys_out : keys_alt;
+        uint32_t* vo = to_out ? vals_out : vals_alt;
+        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+            hist_tile(kin, n, shift, mask, blockhist, ntiles, t, h);
+        grid.sync();
+        for (uint32_t d = blockIdx.x; d < 256; d += gridDim.x) scan_row(blockhist, ntiles, totals, d, S.sh);
+        grid.sync();
+        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+            scatter_tile(kin, vin, ko, vo, n, shift, mask, blockhist, ntiles, totals,
+                         p == 0 ? val_base : 0u, t, S);
+        grid.sync();
+        kin = ko;
+        vin = vo;
     }
 }
 
@@ -473,6 +548,38 @@ int radix_sort(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_
                uint32_t* vals_out, uint32_t n, int key_bits, RadixScratch& scr,
                const uint32_t* done, cudaStream_t s, uint32_t val_base) {
     if (n == 0) return 0;
+    static const int coop_blocks = [] {
+        int dev = 0, sms = 0, per = 0, ok = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&ok, cudaDevAttrCooperativeLaunch, dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rs_coop_kernel, RS_THREADS, 0);
+        if (const char* e = std::getenv("PCSB_COOP_SORT"))  // developer knob: 0 disables
+            if (std::atoi(e) == 0) ok = 0;
+        return ok ? sms * per : 0;
+    }();
+    const uint32_t ntiles = (n + RS_TILE - 1) / RS_TILE;
+    // measured: one cooperative launch wins for small sorts (config 2's 100K keys:
+    // 0.14 -> 0.10 ms per query order) and loses from ~1M keys on
+    if (coop_blocks > 0 && n <= (256u << 10)) {
+        // half the co-resident capacity: the two per-sweep sorts (query order on
+        // the main stream, projected-set grid on the side stream) can co-run
+        const int grid = (int)std::min<uint32_t>(ntiles, (uint32_t)std::max(1, coop_blocks / 2));
+        const uint32_t* ki = keys_in;
+        const uint32_t* vi = vals_in;
+        uint32_t* ka = scr.keys_alt;
+        uint32_t* va = scr.vals_alt;
+        uint32_t* bh = scr.blockhist;
+        uint32_t nn = n, nt = ntiles, vb = val_base;
+        int kb = key_bits;
+        void* args[] = {(void*)&ki, (void*)&vi, (void*)&keys_out, (void*)&vals_out, (void*)&ka,
+                        (void*)&va, (void*)&nn, (void*)&kb, (void*)&bh, (void*)&nt, (void*)&vb,
+                        (void*)&done};
+        if (cudaLaunchCooperativeKernel((const void*)rs_coop_kernel, grid, RS_THREADS, args, 0, s) ==
+            cudaSuccess)
+            return 1;
+        cudaGetLastError();  // fall through to the multi-kernel sort
+    }
     const uint32_t nblocks = (n + RS_TILE - 1) / RS_TILE;
     const int passes = key_bits <= 0 ? 1 : (key_bits + 7) / 8;
     // ping-pong so that the last pass writes keys_out/vals_out
