@@ -228,6 +228,7 @@ Plan::Plan(const pcs_lop_desc& d) : d_(d) {
     // repulsion over the sparser projected set: 16-query groups amortise the
     // per-row cost better (measured -1..2% sweep time on configs 3 and 4)
     rep_lanes_ = d_.lanes_per_point ? lanes_ : 2;
+    if (const char* e = std::getenv("PCSB_REORDER_EVERY")) reorder_every_ = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("PCSB_REP_LANES")) rep_lanes_ = std::atoi(e);  // developer knob
     device_ = select_device(d_.device);
     PCSB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
@@ -615,6 +616,7 @@ void Plan::reset() {
     PCSB_CUDA(cudaMemsetAsync(ever_iso_, 0, std::max<uint32_t>(mpad_, 1), stream_));
     PCSB_CUDA(cudaStreamSynchronize(stream_));
     sweeps_issued_ = 0;
+    q_stale_ = true;
     sweeps_ms_ = kernel_ms_ = sort_ms_ = 0.0;
 }
 
@@ -776,10 +778,18 @@ void Plan::enqueue_sweep(int k) {
         PCSB_CUDA(cudaEventRecord(se.e[1], stream_));
         PCSB_CUDA(cudaEventRecord(se.e[2], stream_));
     }
-    // query order: the owned range of X^k in Morton order (internal indices)
-    launches_ += build_query_list((const V*)cur + own_lo_, own_cnt_, g_, support_, nullptr, 0, 0,
-                                  q_keys_, q_skeys_, q_list_, &block_shift_, rs_, done, stream_,
-                                  own_lo_);
+    // query order: the owned range in Morton order (internal indices), rebuilt
+    // from X^k every `reorder_every_` sweeps; in between the order is reused (the
+    // grouping only decides which queries share staged candidates; group boxes
+    // and neighbour sets always come from the current positions)
+    if (k == 1 || sweeps_since_order_ >= reorder_every_ || q_stale_) {
+        launches_ += build_query_list((const V*)cur + own_lo_, own_cnt_, g_, support_, nullptr, 0, 0,
+                                      q_keys_, q_skeys_, q_list_, &block_shift_, rs_, done, stream_,
+                                      own_lo_);
+        sweeps_since_order_ = 0;
+        q_stale_ = false;
+    }
+    ++sweeps_since_order_;
     const uint32_t* qlist = q_list_;
     const uint32_t nq = own_cnt_;
     PCSB_CUDA(cudaEventRecord(se.e[3], stream_));

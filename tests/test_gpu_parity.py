@@ -155,7 +155,8 @@ def test_fp32_full_trajectory(pb, orc, cfg, scale, h, its):
     iterate to fp32 each sweep moves 1.5-1.7% of those points by up to 2e-2
     (configs 3 and 5: nothing).  Configs 3 and 5 must meet the bar on every
     point; for 2 and 4 the share of points beyond it is bounded by the oracle's
-    own sensitivity and the projected sets must agree statistically."""
+    own sensitivity and the projected sets must agree statistically (within the
+    oracle's own spread under 1-ulp input jitter)."""
     P, X0, prm, c = scaled_case(pb, cfg, scale, h)
     prm.iterations = its
     eta = orc.ETA_NEG_LINEAR if c["eta"] == "neg_linear" else orc.ETA_INV_CUBE
@@ -173,14 +174,29 @@ def test_fp32_full_trajectory(pb, orc, cfg, scale, h, its):
     assert (err > tol).mean() <= max(0.005, 2.0 * own.mean())
     if cfg in (3, 5):
         assert err.max() <= tol
-    # and the projected sets are statistically the same surface sample
+    # and the projected sets are statistically the same surface sample: mean fit
+    # distance and mean spacing within 1%, or within 1.5x the oracle's own spread
+    # when its input is jittered by one fp32 ulp (chaotic configs 2 and 4: a
+    # 1-ulp jitter of X0 moves config 2's 30-sweep mean fit by up to ~4.5%)
     from scipy.spatial import cKDTree
     tP = cKDTree(P)
-    fit_gpu, fit_orc = tP.query(out)[0].mean(), tP.query(r.points)[0].mean()
-    assert abs(fit_gpu - fit_orc) <= 0.01 * fit_orc
-    sp_gpu = cKDTree(out).query(out, k=2)[0][:, 1].mean()
-    sp_orc = cKDTree(r.points).query(r.points, k=2)[0][:, 1].mean()
-    assert abs(sp_gpu - sp_orc) <= 0.01 * sp_orc
+    fit = lambda X: tP.query(X)[0].mean()  # noqa: E731
+    spacing = lambda X: cKDTree(X).query(X, k=2)[0][:, 1].mean()  # noqa: E731
+    fit_gpu, fit_orc = fit(out), fit(r.points)
+    sp_gpu, sp_orc = spacing(out), spacing(r.points)
+    fit_spread, sp_spread = 0.01 * fit_orc, 0.01 * sp_orc
+    if cfg in (2, 4):
+        rng = np.random.default_rng(7)
+        for _ in range(2):
+            away = np.where(rng.random(X0.shape) < 0.5, -np.inf, np.inf).astype(F32)
+            Xj = np.nextafter(X0.astype(F32), away).astype(np.float64)
+            rj = orc.lop_project(P, Xj, prm.kernel.h, 4.0, prm.mu, its, store_f32=True, **kw)
+            fit_spread = max(fit_spread, 1.5 * abs(fit(rj.points) - fit_orc))
+            sp_spread = max(sp_spread, 1.5 * abs(spacing(rj.points) - sp_orc))
+    print(f"fit {fit_gpu:.5e} vs {fit_orc:.5e} (bound {fit_spread:.2e}); "
+          f"spacing {sp_gpu:.5e} vs {sp_orc:.5e} (bound {sp_spread:.2e})")
+    assert abs(fit_gpu - fit_orc) <= fit_spread
+    assert abs(sp_gpu - sp_orc) <= sp_spread
 
 
 # ----------------------------------------------------------------------------
