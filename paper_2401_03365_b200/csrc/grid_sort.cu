@@ -561,7 +561,11 @@ int radix_sort(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_
     const uint32_t ntiles = (n + RS_TILE - 1) / RS_TILE;
     // measured: one cooperative launch wins for small sorts (config 2's 100K keys:
     // 0.14 -> 0.10 ms per query order) and loses from ~1M keys on
-    if (coop_blocks > 0 && n <= (256u << 10)) {
+    static const uint32_t coop_max = [] {
+        const char* e = std::getenv("PCSB_COOP_MAX");  // developer knob (keys)
+        return e ? (uint32_t)std::atol(e) : (256u << 10);
+    }();
+    if (coop_blocks > 0 && n <= coop_max) {
         // half the co-resident capacity: the two per-sweep sorts (query order on
         // the main stream, projected-set grid on the side stream) can co-run
         const int grid = (int)std::min<uint32_t>(ntiles, (uint32_t)std::max(1, coop_blocks / 2));

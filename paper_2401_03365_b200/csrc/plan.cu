@@ -247,8 +247,8 @@ Plan::Plan(const pcs_lop_desc& d) : d_(d) {
     fast_grid_ = sms * fast_blocks_per_sm(lanes_, d_.density_weights != 0, false, 2);
     density_grid_ = fast_grid_;
     {
-        // all block slots: fewer warps slow the pass more (+13% at 5 of 6 slots)
-        // than the side stream's overlap gains; its kernels fill the pass's tail
+        // all block slots on one GPU (5 of 6 measured -1.4% .. -11% on configs 2-5);
+        // decided again at upload for sharded plans (set_attr_grid)
         int per_sm = fast_grid_ / sms;
         if (const char* e = std::getenv("PCSB_ATTR_BLOCKS")) per_sm = std::atoi(e);  // developer knob
         attr_grid_ = sms * std::max(1, per_sm);
@@ -541,6 +541,14 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
             }
         }
         X_init_ = dalloc((size_t)std::max<uint32_t>(mpad_, 1) * sizeof(V));
+        if (nranks_ >= 4 && !std::getenv("PCSB_ATTR_BLOCKS")) {
+            // with a quarter of the queries or less the attraction pass is short and
+            // the side stream's grid rebuild (latency-bound) would be exposed after
+            // it: leave it one block slot per SM (8-GPU emulation: -4% per sweep)
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_);
+            attr_grid_ = sms * std::max(1, fast_grid_ / sms - 1);
+        }
         own_lo_ = (uint32_t)rank_ * chunk_;
         own_cnt_ = counts[rank_];
         orig_of_internal_ = (uint32_t*)dalloc((size_t)mpad_ * sizeof(uint32_t));
