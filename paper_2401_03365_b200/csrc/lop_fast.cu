@@ -505,13 +505,6 @@ __device__ __forceinline__ bool next_unit(uint32_t* counter, uint32_t nq, uint32
     uint32_t u = 0;
     if (lane == 0) u = atomicAdd(counter, 1u);
     u = __shfl_sync(0xffffffffu, u, 0);
-#ifdef PCSB_REVERSE_UNITS
-    {
-        const uint32_t nu = (nq + unit - 1) / unit;
-        if (u >= nu) return false;
-        u = nu - 1 - u;
-    }
-#endif
     r0 = u * unit;
     if (r0 >= nq) return false;
     r1 = min(r0 + unit, nq);
