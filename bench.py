@@ -131,50 +131,63 @@ def sfu_peak(sm_mhz: float, sms: int = 148) -> dict:
 # ------------------------------------------------------------------------------
 # CPU baseline: the reference's own lop_project on the host cores
 # ------------------------------------------------------------------------------
-def cpu_baseline(cfg: int, P: np.ndarray, X0: np.ndarray, params, c: dict, budget_s: float = 20.0,
-                 steps: int = 1) -> dict:
+def cpu_baseline(cfg: int, P: np.ndarray, X0: np.ndarray, params, c: dict, repeats: int = 1,
+                 sweeps: int = 6) -> dict:
+    """The reference's own CPU path (oracle/_ref = the unmodified reference
+    compiled from /root/reference) on a bounded, seeded sample of the workload.
+
+    pcs::lop_project builds the kd-tree of the FULL data cloud inside the call
+    (lop.cpp:24), which alone takes seconds at 10M points.  The sweep rate is
+    therefore measured by differencing two calls on the same sample: one sweep
+    and `sweeps` sweeps (the index build cancels); the interactions of sweeps
+    2..K are counted by the oracle port on the same sample (counting is not
+    timed).  Medians over `repeats`."""
     from oracle import oracle as O
 
     nthreads = os.cpu_count() or 1
     os.environ.setdefault("OMP_NUM_THREADS", str(nthreads))
     rng = np.random.default_rng(12345)
-    frac = 0.01 if X0.shape[0] >= 100000 else 1.0
+    frac = 0.02 if X0.shape[0] >= 100000 else 1.0
     nsub = max(1, int(X0.shape[0] * frac))
     sub = np.sort(rng.choice(X0.shape[0], nsub, replace=False))
     Xs = X0[sub]
     h, cut, mu = params.kernel.h, params.kernel.cutoff_multiple, params.mu
-    # exact interaction count of one sweep of this sample (the port counts; counting is not timed)
     eta_kind = O.ETA_NEG_LINEAR if c["eta"] == "neg_linear" else O.ETA_INV_CUBE
-    cnt = O.lop_project(P, Xs, h, cut, mu, 1, eta=eta_kind, wlop=c["wlop"])
-    inter = cnt.interactions_attr + cnt.interactions_rep
     use_ref = O.ref_available() and not c["wlop"]
-    times = []
-    build_ms = 0.0
     if use_ref:
-        build_ms = O.ref_index_build_ms(P)
-        for _ in range(steps):
-            t = time.perf_counter()
-            O.ref_lop_project(P, Xs, h, cut, mu, 1)
-            times.append(time.perf_counter() - t)
+        # the reference implements only eta = 1/(3r^3): count with that eta
+        eta_kind = O.ETA_INV_CUBE
+    c1 = O.lop_project(P, Xs, h, cut, mu, 1, eta=eta_kind, wlop=c["wlop"])
+    cK = O.lop_project(P, Xs, h, cut, mu, sweeps, eta=eta_kind, wlop=c["wlop"])
+    inter = (cK.interactions_attr + cK.interactions_rep) - (c1.interactions_attr + c1.interactions_rep)
+
+    def call(k):
+        t = time.perf_counter()
+        if use_ref:
+            O.ref_lop_project(P, Xs, h, cut, mu, k)
+        else:
+            O.lop_project(P, Xs, h, cut, mu, k, eta=eta_kind, wlop=c["wlop"])
+        return time.perf_counter() - t
+
+    t1 = statistics.median(call(1) for _ in range(repeats))
+    tK = statistics.median(call(sweeps) for _ in range(repeats))
+    t_sweeps = max(1e-9, tK - t1)
+    if use_ref:
         kind = "reference"
-        what = (f"reference pcs::lop_project (oracle/_ref, built from /root/reference), 1 sweep of a "
-                f"seeded {nsub}-point subset of X0 against the full P ({P.shape[0]} pts); the "
-                f"data kd-tree build ({build_ms/1e3:.2f} s, timed separately) is subtracted")
+        what = (f"reference pcs::lop_project (oracle/_ref, built from /root/reference) on a seeded "
+                f"{nsub}-point subset of X0 against the full P ({P.shape[0]} pts): time of a "
+                f"{sweeps}-sweep call minus a 1-sweep call (the in-call kd-tree build of P cancels), "
+                f"median of {repeats}; interactions of sweeps 2..{sweeps} counted by the oracle")
         if c["eta"] != "inv_cube":
             what += "; eta=1/(3r^3) (the only eta the reference implements; same neighbour work)"
     else:
-        for _ in range(steps):
-            t = time.perf_counter()
-            O.lop_project(P, Xs, h, cut, mu, 1, eta=eta_kind, wlop=c["wlop"])
-            times.append(time.perf_counter() - t)
         kind = "port"
-        what = (f"oracle port (oracle/lop_oracle.c, OpenMP), 1 sweep of a seeded {nsub}-point "
-                f"subset of X0 against the full P ({P.shape[0]} pts)")
-    t_sweep = max(1e-9, statistics.median(times) - build_ms / 1e3)
-    return {"value": inter / t_sweep, "unit": "interactions/s", "cores": int(os.environ.get(
+        what = (f"oracle port (oracle/lop_oracle.c, OpenMP) on a seeded {nsub}-point subset of X0 "
+                f"against the full P ({P.shape[0]} pts): {sweeps}-sweep call minus 1-sweep call")
+    return {"value": inter / t_sweeps, "unit": "interactions/s", "cores": int(os.environ.get(
         "OMP_NUM_THREADS", nthreads)), "kind": kind, "sample": what,
-        "sample_interactions": int(inter), "sample_seconds": t_sweep,
-        "raw_call_seconds": statistics.median(times), "index_build_seconds": build_ms / 1e3}
+        "sample_interactions": int(inter), "sample_seconds": t_sweeps,
+        "seconds_per_sweep": t_sweeps / (sweeps - 1), "call_seconds": [t1, tK]}
 
 
 # ------------------------------------------------------------------------------
@@ -211,11 +224,11 @@ def main():
         if precision == "fp32":
             P = P.astype(np.float32).astype(np.float64)
             X0 = X0.astype(np.float32).astype(np.float64)
-        cb = cpu_baseline(cfg, P, X0, params, c, steps=max(1, args.steps))
+        cb = cpu_baseline(cfg, P, X0, params, c, repeats=2)
         line = {
             "impl": "reference", "metric": "neighbour interactions/sec (LOP sweep)",
             "value": cb["value"], "unit": "interactions/s", "n_gpus": ngpu, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": cb["sample_seconds"] * 1e3,
+            "warmup": args.warmup, "ms_per_step": cb["seconds_per_sweep"] * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded host generator, BASELINE.md §4)",
             "config": {"workload": WORKLOADS[cfg], "sample": cb["sample"]},
