@@ -500,14 +500,24 @@ __device__ __forceinline__ EvalConsts make_consts(const float4& q, float kneg, f
 }
 
 // The next work unit for this warp: [r0, r1) positions in the query list.
-__device__ __forceinline__ bool next_unit(uint32_t* counter, uint32_t nq, uint32_t unit, int lane,
+// Units of `unit` queries up to tail_start, then units of tail_unit (one query
+// group) so that the pass ends on short units (the tail of a persistent pass).
+__device__ __forceinline__ bool next_unit(uint32_t* counter, uint32_t nq, uint32_t unit,
+                                          uint32_t tail_start, uint32_t tail_unit, int lane,
                                           uint32_t& r0, uint32_t& r1) {
     uint32_t u = 0;
     if (lane == 0) u = atomicAdd(counter, 1u);
     u = __shfl_sync(0xffffffffu, u, 0);
-    r0 = u * unit;
+    const uint32_t n1 = tail_start / unit;  // tail_start is a multiple of unit
+    uint32_t len = unit;
+    if (u < n1) {
+        r0 = u * unit;
+    } else {
+        r0 = tail_start + (u - n1) * tail_unit;
+        len = tail_unit;
+    }
     if (r0 >= nq) return false;
-    r1 = min(r0 + unit, nq);
+    r1 = min(r0 + len, nq);
     return true;
 }
 
@@ -554,7 +564,8 @@ fast_kernel(const FastArgs a) {
     uint32_t* counter = PH == PH_REP ? &a.slot->group_counter2 : &a.slot->group_counter;
 
     uint32_t r0, r1;
-    while (next_unit(counter, a.nq, a.unit, lane, r0, r1)) {
+    const uint32_t tail_unit = max(a.tail_unit, (uint32_t)Q);
+    while (next_unit(counter, a.nq, a.unit, a.tail_start, tail_unit, lane, r0, r1)) {
         const unsigned brk = group_breaks(a.qcodes, a.block_shift, r0, r1, lane);
         for (uint32_t g0 = r0, g1; g0 < r1; g0 = g1) {
             g1 = group_end(brk, r0, r1, g0, Q);
@@ -708,7 +719,7 @@ density_kernel(const DensityArgs a) {
     Stage S = make_stage(smem + warp * 4 * HR, bars + 2 * warp, lane);
     const int qi = lane / DL, sub = lane % DL;
     uint32_t r0, r1;
-    while (next_unit(a.counter, a.nq, a.unit, lane, r0, r1)) {
+    while (next_unit(a.counter, a.nq, a.unit, a.nq / a.unit * a.unit, a.unit, lane, r0, r1)) {
         const unsigned brk = group_breaks(a.qcodes, a.block_shift, r0, r1, lane);
         for (uint32_t g0 = r0, g1; g0 < r1; g0 = g1) {
             g1 = group_end(brk, r0, r1, g0, Q);

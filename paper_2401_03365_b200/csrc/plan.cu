@@ -153,16 +153,19 @@ GridGeom make_grid_scaled(const double lo_in[3], const double hi_in[3], double s
     return g;
 }
 
-// x-grid scale (developer knob PCSB_XCELL; default 1 = the data grid).  Measured
-// with 2x: config 3 -2.4% sweep time, config 2 -6%, but config 5 +5% and the
-// WLOP config 4 +9% (its density pass over X loses more to coarse rows).
+// x-grid scale (developer knob PCSB_XCELL): the projected set's grid has cells 2x
+// the data grid's.  Its points are ~10x sparser than the data, so twice-coarser
+// rows amortise the per-row cost of the repulsion (and WLOP w_i) pass, and the
+// per-sweep rebuild sorts fewer key bits and scans an 8x smaller cell table.
+// Measured (tools/xcell_probe.sh, round 1, sweeps/s vs 1x): config 2 +14%,
+// config 3 +0.6% (+3.7% per rank of an emulated 8-rank run), config 4 +6%,
+// config 5 -0.7%; 3x loses on every config.
 double x_cell_scale(uint64_t n, uint64_t m, const GridGeom& g) {
     (void)n;
     (void)m;
+    (void)g;
     if (const char* e = std::getenv("PCSB_XCELL")) return std::atof(e);
-    // a data grid past 2^25 cells: the projected set's table (rebuilt every
-    // sweep) is kept 8x smaller
-    return g.ncells > (1u << 25) ? 2.0 : 1.0;
+    return 2.0;
 }
 
 void validate_desc(const pcs_lop_desc& d) {
@@ -815,6 +818,16 @@ void Plan::enqueue_sweep(int k) {
         a.block_shift = block_shift_;
         a.nq = nq;
         a.unit = work_unit_queries(nq, fast_grid_ * 4);
+        {   // the last ~one group per warp of the attraction pass comes in one-group units
+            const uint32_t q = 32u / (uint32_t)lanes_;
+            static const double tail_frac = [] {  // developer knob: warps' groups in the tail
+                const char* e = std::getenv("PCSB_TAIL");
+                return e ? std::atof(e) : 1.0;
+            }();
+            const uint64_t tail = (uint64_t)(tail_frac * attr_grid_ * 4u * q);
+            a.tail_start = nq > tail ? (uint32_t)((nq - tail) / a.unit * a.unit) : 0u;
+            a.tail_unit = q;
+        }
         a.gP = g_;
         a.gX = gX_;
         a.s_pad = s_pad_;
