@@ -232,6 +232,7 @@ Plan::Plan(const pcs_lop_desc& d) : d_(d) {
     // per-row cost better (measured -1..2% sweep time on configs 3 and 4)
     rep_lanes_ = d_.lanes_per_point ? lanes_ : 2;
     if (const char* e = std::getenv("PCSB_REORDER_EVERY")) reorder_every_ = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("PCSB_ASYNC_ORDER")) async_order_ = std::atoi(e) != 0;  // developer knob
     if (const char* e = std::getenv("PCSB_REP_LANES")) rep_lanes_ = std::atoi(e);  // developer knob
     device_ = select_device(d_.device);
     PCSB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
@@ -243,6 +244,7 @@ Plan::Plan(const pcs_lop_desc& d) : d_(d) {
         PCSB_CUDA(cudaStreamCreateWithPriority(&stream2_, cudaStreamNonBlocking, hi));
     }
     PCSB_CUDA(cudaEventCreateWithFlags(&ev_xready_, cudaEventDisableTiming));
+    PCSB_CUDA(cudaEventCreateWithFlags(&ev_qready_, cudaEventDisableTiming));
     PCSB_CUDA(cudaEventCreate(&run_ev_[0]));
     PCSB_CUDA(cudaEventCreate(&run_ev_[1]));
     int sms = 148;
@@ -281,6 +283,7 @@ Plan::~Plan() {
     if (run_ev_[1]) cudaEventDestroy(run_ev_[1]);
     delete coll_;
     if (ev_xready_) cudaEventDestroy(ev_xready_);
+    if (ev_qready_) cudaEventDestroy(ev_qready_);
     if (stream2_) cudaStreamDestroy(stream2_);
     if (stream_) cudaStreamDestroy(stream_);
 }
@@ -591,6 +594,10 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     q_keys_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
     q_skeys_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
     q_list_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
+    q_keys_alt_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
+    q_skeys_alt_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
+    q_list_alt_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
+    q_next_ready_ = false;
     ever_iso_ = (uint8_t*)dalloc(mp);
     slots_ = (SweepSlot*)dalloc(kSlotCap * sizeof(SweepSlot));
     out_xyz_ = (double*)dalloc((size_t)(m ? m : 1) * 3 * sizeof(double));
@@ -639,6 +646,7 @@ void Plan::run(int sweeps, bool sync) {
     PCSB_CUDA(cudaSetDevice(device_));
     synchronize();
     PCSB_CUDA(cudaEventRecord(run_ev_[0], stream_));
+    last_sweep_ = sweeps_issued_ + sweeps;
     for (int i = 0; i < sweeps; ++i) {
         const int k = ++sweeps_issued_;
         if (fp32_) enqueue_sweep<float>(k);
@@ -794,13 +802,33 @@ void Plan::enqueue_sweep(int k) {
     // grouping only decides which queries share staged candidates; group boxes
     // and neighbour sets always come from the current positions)
     if (k == 1 || sweeps_since_order_ >= reorder_every_ || q_stale_) {
-        launches_ += build_query_list((const V*)cur + own_lo_, own_cnt_, g_, support_, nullptr, 0, 0,
-                                      q_keys_, q_skeys_, q_list_, &block_shift_, rs_, done, stream_,
-                                      own_lo_);
+        if (q_next_ready_ && k != 1 && !q_stale_) {
+            // built on stream2_ during the previous sweep (from X^{k-1})
+            PCSB_CUDA(cudaStreamWaitEvent(stream_, ev_qready_, 0));
+            std::swap(q_skeys_, q_skeys_alt_);
+            std::swap(q_list_, q_list_alt_);
+            std::swap(block_shift_, block_shift_alt_);
+        } else {
+            launches_ += build_query_list((const V*)cur + own_lo_, own_cnt_, g_, support_, nullptr, 0,
+                                          0, q_keys_, q_skeys_, q_list_, &block_shift_, rs_, done,
+                                          stream_, own_lo_);
+        }
         sweeps_since_order_ = 0;
         q_stale_ = false;
     }
+    q_next_ready_ = false;
     ++sweeps_since_order_;
+    // the next re-ordering's list, off the critical path: on stream2_ behind the
+    // grid rebuild (its kernels fill the SM slots the passes leave free); the
+    // previous sweep's readers of the alternate buffers completed before X^k was
+    // ready, which stream2_ waited for
+    if (xgrid && async_order_ && sweeps_since_order_ >= reorder_every_ && k < last_sweep_) {
+        launches_ += build_query_list((const V*)cur + own_lo_, own_cnt_, g_, support_, nullptr, 0, 0,
+                                      q_keys_alt_, q_skeys_alt_, q_list_alt_, &block_shift_alt_, rs2_,
+                                      done, stream2_, own_lo_);
+        PCSB_CUDA(cudaEventRecord(ev_qready_, stream2_));
+        q_next_ready_ = true;
+    }
     const uint32_t* qlist = q_list_;
     const uint32_t nq = own_cnt_;
     PCSB_CUDA(cudaEventRecord(se.e[3], stream_));

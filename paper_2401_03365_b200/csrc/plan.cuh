@@ -117,6 +117,16 @@ private:
     bool q_stale_ = true;             // no order for the current X yet (upload / reset)
     uint32_t* q_skeys_ = nullptr;
     uint32_t* q_list_ = nullptr;
+    // the next query order, built on stream2_ from X^k during sweep k (after the
+    // projected-set grid) for the re-ordering sweep k+1, which swaps it in
+    uint32_t* q_keys_alt_ = nullptr;
+    uint32_t* q_skeys_alt_ = nullptr;
+    uint32_t* q_list_alt_ = nullptr;
+    int block_shift_alt_ = 0;
+    bool q_next_ready_ = false;
+    bool async_order_ = true;         // developer knob PCSB_ASYNC_ORDER=0: build in line
+    int last_sweep_ = 0;              // last sweep index of the current run()
+    cudaEvent_t ev_qready_ = nullptr;
     uint32_t* careful_list_ = nullptr;
     uint8_t* ever_iso_ = nullptr;
     uint32_t* orig_of_internal_ = nullptr;  // multi-GPU only
