@@ -42,7 +42,8 @@ typedef enum pcs_status {
     PCS_ERR_CUDA = 4,           /* device / driver failure (reported as NumericalFailure in C++) */
     PCS_ERR_NCCL = 5,           /* collective failure */
     PCS_ERR_NO_DEVICE = 6,      /* no usable sm_100 device: there is no CPU fallback */
-    PCS_ERR_CAPACITY = 7        /* caller buffer too small; required size reported */
+    PCS_ERR_CAPACITY = 7,       /* caller buffer too small; required size reported */
+    PCS_ERR_EMPTY_MESH = 8      /* pcs::EmptyMesh     (errors.hpp:20-23) */
 } pcs_status;
 
 /* Repulsion penalty eta.  The reference hard-codes eta = 1/(3 r^3),
@@ -166,6 +167,38 @@ pcs_status pcs_density_weights(const pcs_lop_desc* d, const double* C_xyz, uint6
  * and the 32-bit cell keys, for a cloud (parity: stable sort by key). */
 pcs_status pcs_grid_sort(const pcs_lop_desc* d, const double* C_xyz, uint64_t n, double support,
                          uint32_t* keys_out, uint32_t* order_out);
+
+/* ---- deviation metrics (the next caller beside LOP) ---------
+ * DeviationReport (proj/include/pcs/metrics.hpp:11-17): n, mean distance, RMS
+ * ("std_deviation") and max distance of a cloud to a reference. */
+typedef struct pcs_deviation_report {
+    uint64_t n;
+    double mean_distance;
+    double std_deviation;
+    double max_distance;
+} pcs_deviation_report;
+
+/* SpatialIndex::nearest (proj/src/spatial.cpp:119-158) for every query, on the
+ * device: index of the nearest point of C (smallest index among equal squared
+ * distances) and its distance sqrt(norm2(c - q)), bit-identical to the
+ * reference.  n == 0 -> PCS_ERR_EMPTY_CLOUD. */
+pcs_status pcs_nearest_all(const pcs_lop_desc* d, const double* C_xyz, uint64_t n,
+                           const double* Q_xyz, uint64_t m, uint32_t* idx_out, double* dist_out);
+/* pcs::deviation (proj/src/metrics.cpp:39-53): nearest-reference distance of
+ * every cloud point (device), aggregated in index order as the reference does
+ * (:11-37).  distances_out (m values) may be NULL.  Empty cloud, then empty
+ * reference -> PCS_ERR_EMPTY_CLOUD. */
+pcs_status pcs_deviation(const pcs_lop_desc* d, const double* cloud_xyz, uint64_t m,
+                         const double* ref_xyz, uint64_t n, pcs_deviation_report* report,
+                         double* distances_out);
+/* pcs::deviation_to_mesh (proj/src/metrics.cpp:115-133): distance of every cloud
+ * point to the nearest triangle of a triangle soup (9 doubles per triangle:
+ * a, b, c), point_triangle_distance evaluated on the device with the
+ * reference's operation order; aggregated like pcs_deviation.  Empty cloud ->
+ * PCS_ERR_EMPTY_CLOUD, no triangles -> PCS_ERR_EMPTY_MESH. */
+pcs_status pcs_deviation_to_mesh(const pcs_lop_desc* d, const double* cloud_xyz, uint64_t m,
+                                 const double* tri_xyz, uint64_t ntri,
+                                 pcs_deviation_report* report, double* distances_out);
 
 /* Multi-GPU ownership layout (host only, no device needed): shard r owns the
  * r-th contiguous range of `sorted_order` (the initial grid order of X0) and

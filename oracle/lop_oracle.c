@@ -655,3 +655,145 @@ int orc_lop_project(const double* P, size_t n, const double* X0, size_t m,
     grid_free(&pg);
     return rc;
 }
+
+
+/* ======================================================================== *
+ * Deviation metrics.
+ *   nearest            proj/src/spatial.cpp:119-158  (min norm2(c - q), smallest
+ *                      index on equal d2; distance = sqrt(d2))
+ *   deviation          proj/src/metrics.cpp:39-53 + aggregate :11-37
+ *   point-triangle     proj/src/metrics.cpp:55-113 (Ericson's Voronoi walk)
+ *   deviation_to_mesh  proj/src/metrics.cpp:115-133
+ * Brute force over the reference points / triangles (the kd-tree only prunes;
+ * the minimum and its tie-break are the same).
+ * ======================================================================== */
+static double o_norm2(double x, double y, double z) { return x * x + y * y + z * z; }
+
+int orc_nearest_all(const double* C, size_t n, const double* Q, size_t m, uint32_t* idx_out,
+                    double* dist_out, int threads) {
+    if (n == 0) return ORC_EMPTY_CLOUD;
+    set_threads(threads);
+#pragma omp parallel for schedule(dynamic, 64)
+    for (size_t i = 0; i < m; ++i) {
+        const double qx = Q[3 * i], qy = Q[3 * i + 1], qz = Q[3 * i + 2];
+        double best = 0.0;
+        size_t bi = 0;
+        for (size_t k = 0; k < n; ++k) {
+            const double d2 = o_norm2(C[3 * k] - qx, C[3 * k + 1] - qy, C[3 * k + 2] - qz);
+            if (k == 0 || d2 < best) { /* ascending k: equal d2 keeps the smaller index */
+                best = d2;
+                bi = k;
+            }
+        }
+        idx_out[i] = (uint32_t)bi;
+        dist_out[i] = sqrt(best);
+    }
+    return ORC_OK;
+}
+
+/* metrics.cpp:11-37: index-order sums; returns 0 or ORC_INVALID_PARAM when the
+ * power-mean check fails (the reference throws pcs::Error). */
+static int o_aggregate(const double* d, size_t m, double out[4]) {
+    double sum = 0.0, sum_sq = 0.0, max_d = 0.0;
+    for (size_t i = 0; i < m; ++i) {
+        sum += d[i];
+        sum_sq += d[i] * d[i];
+        max_d = d[i] > max_d ? d[i] : max_d; /* std::max(max_d, d) */
+    }
+    const double nd = (double)m;
+    out[0] = nd;
+    out[1] = sum / nd;
+    out[2] = sqrt(sum_sq / nd);
+    out[3] = max_d;
+    return out[2] < out[1] * (1.0 - 1e-12) ? ORC_INVALID_PARAM : ORC_OK;
+}
+
+/* out = {n, mean, rms, max}; dist_out (m values) may be NULL */
+int orc_deviation(const double* cloud, size_t m, const double* ref, size_t n, double out[4],
+                  double* dist_out, int threads) {
+    if (m == 0 || n == 0) return ORC_EMPTY_CLOUD;
+    double* d = dist_out ? dist_out : (double*)malloc(m * sizeof(double));
+    uint32_t* ix = (uint32_t*)malloc(m * sizeof(uint32_t));
+    if (!d || !ix) return ORC_NO_MEMORY;
+    orc_nearest_all(ref, n, cloud, m, ix, d, threads);
+    const int st = o_aggregate(d, m, out);
+    free(ix);
+    if (!dist_out) free(d);
+    return st;
+}
+
+typedef struct { double x, y, z; } o3;
+static o3 o_sub(o3 a, o3 b) { o3 r = {a.x - b.x, a.y - b.y, a.z - b.z}; return r; }
+static o3 o_add(o3 a, o3 b) { o3 r = {a.x + b.x, a.y + b.y, a.z + b.z}; return r; }
+static o3 o_scale(double s, o3 a) { o3 r = {s * a.x, s * a.y, s * a.z}; return r; }
+static double o_dot(o3 a, o3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+static double o_len(o3 a) { return sqrt(o_dot(a, a)); }
+
+static double o_segment(o3 p, o3 s0, o3 s1) {
+    const o3 d = o_sub(s1, s0);
+    const double len2 = o_dot(d, d);
+    if (len2 == 0.0) return o_len(o_sub(p, s0));
+    double t = o_dot(o_sub(p, s0), d) / len2;
+    t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t); /* std::clamp(t, 0, 1) */
+    return o_len(o_sub(p, o_add(s0, o_scale(t, d))));
+}
+
+double orc_point_triangle_distance(const double p_[3], const double t[9]) {
+    const o3 p = {p_[0], p_[1], p_[2]};
+    const o3 a = {t[0], t[1], t[2]}, b = {t[3], t[4], t[5]}, c = {t[6], t[7], t[8]};
+    const o3 ab = o_sub(b, a), ac = o_sub(c, a), ap = o_sub(p, a);
+    const double d1 = o_dot(ab, ap), d2 = o_dot(ac, ap);
+    if (d1 <= 0.0 && d2 <= 0.0) return o_len(o_sub(p, a));
+    const o3 bp = o_sub(p, b);
+    const double d3 = o_dot(ab, bp), d4 = o_dot(ac, bp);
+    if (d3 >= 0.0 && d4 <= d3) return o_len(o_sub(p, b));
+    const double vc = d1 * d4 - d3 * d2;
+    if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) {
+        const double v = d1 / (d1 - d3);
+        return o_len(o_sub(p, o_add(a, o_scale(v, ab))));
+    }
+    const o3 cp = o_sub(p, c);
+    const double d5 = o_dot(ab, cp), d6 = o_dot(ac, cp);
+    if (d6 >= 0.0 && d5 <= d6) return o_len(o_sub(p, c));
+    const double vb = d5 * d2 - d1 * d6;
+    if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) {
+        const double w = d2 / (d2 - d6);
+        return o_len(o_sub(p, o_add(a, o_scale(w, ac))));
+    }
+    const double va = d3 * d6 - d5 * d4;
+    if (va <= 0.0 && (d4 - d3) >= 0.0 && (d5 - d6) >= 0.0) {
+        const double w = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+        return o_len(o_sub(p, o_add(b, o_scale(w, o_sub(c, b)))));
+    }
+    if (!(va + vb + vc > 0.0)) {
+        const double s1 = o_segment(p, a, b), s2 = o_segment(p, b, c), s3 = o_segment(p, a, c);
+        double best = s1;
+        if (s2 < best) best = s2;
+        if (s3 < best) best = s3;
+        return best;
+    }
+    const double denom = 1.0 / (va + vb + vc);
+    const double v = vb * denom, w = vc * denom;
+    return o_len(o_sub(p, o_add(o_add(a, o_scale(v, ab)), o_scale(w, ac))));
+}
+
+int orc_deviation_to_mesh(const double* cloud, size_t m, const double* tri, size_t ntri,
+                          double out[4], double* dist_out, int threads) {
+    if (m == 0) return ORC_EMPTY_CLOUD;
+    if (ntri == 0) return ORC_EMPTY_MESH;
+    double* d = dist_out ? dist_out : (double*)malloc(m * sizeof(double));
+    if (!d) return ORC_NO_MEMORY;
+    set_threads(threads);
+#pragma omp parallel for schedule(static)
+    for (size_t i = 0; i < m; ++i) {
+        double best = orc_point_triangle_distance(cloud + 3 * i, tri);
+        for (size_t t = 1; t < ntri; ++t) {
+            const double v = orc_point_triangle_distance(cloud + 3 * i, tri + 9 * t);
+            best = v < best ? v : best; /* std::min(best, v) */
+        }
+        d[i] = best;
+    }
+    const int st = o_aggregate(d, m, out);
+    if (!dist_out) free(d);
+    return st;
+}

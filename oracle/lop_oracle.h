@@ -35,7 +35,8 @@ enum {
     ORC_OK = 0,
     ORC_INVALID_PARAM = 1,
     ORC_EMPTY_CLOUD = 2,
-    ORC_NO_MEMORY = 3
+    ORC_NO_MEMORY = 3,
+    ORC_EMPTY_MESH = 4
 };
 
 typedef struct orc_params {
@@ -94,6 +95,17 @@ void orc_add_noise(double* xyz, size_t n, double sigma, uint64_t seed);
 void orc_plane(double* xyz, size_t n, uint64_t seed);
 void orc_sphere(double* xyz, size_t n, uint64_t seed);
 double orc_theta(double d, double h, double cutoff);
+
+/* Deviation metrics: proj/src/spatial.cpp:119-158 (nearest),
+ * proj/src/metrics.cpp:11-133 (aggregate, deviation, point_triangle_distance,
+ * deviation_to_mesh).  out = {n, mean, rms, max}. */
+int orc_nearest_all(const double* C, size_t n, const double* Q, size_t m, uint32_t* idx_out,
+                    double* dist_out, int threads);
+int orc_deviation(const double* cloud, size_t m, const double* ref, size_t n, double out[4],
+                  double* dist_out, int threads);
+double orc_point_triangle_distance(const double p[3], const double tri[9]);
+int orc_deviation_to_mesh(const double* cloud, size_t m, const double* tri, size_t ntri,
+                          double out[4], double* dist_out, int threads);
 
 #ifdef __cplusplus
 }

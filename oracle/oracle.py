@@ -115,6 +115,14 @@ def orc():
         lib.orc_sphere.argtypes = [_c_dbl_p, C.c_size_t, C.c_uint64]
         lib.orc_theta.argtypes = [C.c_double, C.c_double, C.c_double]
         lib.orc_theta.restype = C.c_double
+        lib.orc_nearest_all.argtypes = [_c_dbl_p, C.c_size_t, _c_dbl_p, C.c_size_t, _c_u32_p,
+                                        _c_dbl_p, C.c_int]
+        lib.orc_deviation.argtypes = [_c_dbl_p, C.c_size_t, _c_dbl_p, C.c_size_t, _c_dbl_p,
+                                      _c_dbl_p, C.c_int]
+        lib.orc_point_triangle_distance.argtypes = [_c_dbl_p, _c_dbl_p]
+        lib.orc_point_triangle_distance.restype = C.c_double
+        lib.orc_deviation_to_mesh.argtypes = [_c_dbl_p, C.c_size_t, _c_dbl_p, C.c_size_t,
+                                              _c_dbl_p, _c_dbl_p, C.c_int]
         _orc = lib
     return _orc
 
@@ -141,6 +149,14 @@ def ref():
         lib.ref_index_build_ms.argtypes = [_c_dbl_p, C.c_uint64]
         lib.ref_index_build_ms.restype = C.c_double
         lib.ref_last_error.restype = C.c_char_p
+        lib.ref_nearest_all.argtypes = [_c_dbl_p, C.c_uint64, _c_dbl_p, C.c_uint64, _c_u32_p,
+                                        _c_dbl_p, C.c_int]
+        lib.ref_deviation.argtypes = [_c_dbl_p, C.c_uint64, _c_dbl_p, C.c_uint64, _c_dbl_p,
+                                      _c_dbl_p]
+        lib.ref_deviation_to_mesh.argtypes = [_c_dbl_p, C.c_uint64, _c_dbl_p, C.c_uint64,
+                                              _c_dbl_p, _c_dbl_p]
+        lib.ref_point_triangle_distance.argtypes = [_c_dbl_p, _c_dbl_p]
+        lib.ref_point_triangle_distance.restype = C.c_double
         _ref = lib
     return _ref
 
@@ -311,3 +327,92 @@ def ref_add_noise(xyz, sigma, seed):
 def ref_index_build_ms(P) -> float:
     P = _xyz(P)
     return float(ref().ref_index_build_ms(_ptr(P, _c_dbl_p), P.shape[0]))
+
+
+# --- deviation metrics (proj/src/spatial.cpp:119-158, proj/src/metrics.cpp) -------
+def _dptr(a):
+    return a.ctypes.data_as(_c_dbl_p) if a.size else None
+
+
+def nearest_all(C_pts, Q, threads=0):
+    """Restated SpatialIndex::nearest for every query: (idx uint32, dist)."""
+    Cc, Qq = _xyz(C_pts), _xyz(Q)
+    m = Qq.shape[0]
+    idx = np.zeros(max(m, 1), np.uint32)
+    dist = np.zeros(max(m, 1), np.float64)
+    st = orc().orc_nearest_all(_dptr(Cc), Cc.shape[0], _dptr(Qq), m, _ptr(idx, _c_u32_p),
+                               _ptr(dist, _c_dbl_p), threads)
+    if st:
+        raise OracleError(st, "nearest")
+    return idx[:m], dist[:m]
+
+
+def deviation(cloud, reference, threads=0):
+    """Restated pcs::deviation: ({n, mean, rms, max} array, distances)."""
+    Cc, Rr = _xyz(cloud), _xyz(reference)
+    out = np.zeros(4, np.float64)
+    dist = np.zeros(max(Cc.shape[0], 1), np.float64)
+    st = orc().orc_deviation(_dptr(Cc), Cc.shape[0], _dptr(Rr), Rr.shape[0], _ptr(out, _c_dbl_p),
+                             _ptr(dist, _c_dbl_p), threads)
+    if st:
+        raise OracleError(st, "deviation")
+    return out, dist[: Cc.shape[0]]
+
+
+def point_triangle_distance(p, tri) -> float:
+    pp = np.ascontiguousarray(np.asarray(p, np.float64).reshape(3))
+    tt = np.ascontiguousarray(np.asarray(tri, np.float64).reshape(9))
+    return orc().orc_point_triangle_distance(_ptr(pp, _c_dbl_p), _ptr(tt, _c_dbl_p))
+
+
+def deviation_to_mesh(cloud, triangles, threads=0):
+    Cc = _xyz(cloud)
+    T = np.ascontiguousarray(np.asarray(triangles, np.float64).reshape(-1, 9))
+    out = np.zeros(4, np.float64)
+    dist = np.zeros(max(Cc.shape[0], 1), np.float64)
+    st = orc().orc_deviation_to_mesh(_dptr(Cc), Cc.shape[0], _dptr(T), T.shape[0],
+                                     _ptr(out, _c_dbl_p), _ptr(dist, _c_dbl_p), threads)
+    if st:
+        raise OracleError(st, "deviation_to_mesh")
+    return out, dist[: Cc.shape[0]]
+
+
+def ref_nearest_all(C_pts, Q, threads=0):
+    Cc, Qq = _xyz(C_pts), _xyz(Q)
+    m = Qq.shape[0]
+    idx = np.zeros(max(m, 1), np.uint32)
+    dist = np.zeros(max(m, 1), np.float64)
+    st = ref().ref_nearest_all(_dptr(Cc), Cc.shape[0], _dptr(Qq), m, _ptr(idx, _c_u32_p),
+                               _ptr(dist, _c_dbl_p), threads)
+    if st:
+        raise OracleError(st, ref().ref_last_error().decode())
+    return idx[:m], dist[:m]
+
+
+def ref_deviation(cloud, reference):
+    Cc, Rr = _xyz(cloud), _xyz(reference)
+    out = np.zeros(4, np.float64)
+    dist = np.zeros(max(Cc.shape[0], 1), np.float64)
+    st = ref().ref_deviation(_dptr(Cc), Cc.shape[0], _dptr(Rr), Rr.shape[0], _ptr(out, _c_dbl_p),
+                             _ptr(dist, _c_dbl_p))
+    if st:
+        raise OracleError(st, ref().ref_last_error().decode())
+    return out, dist[: Cc.shape[0]]
+
+
+def ref_deviation_to_mesh(cloud, triangles):
+    Cc = _xyz(cloud)
+    T = np.ascontiguousarray(np.asarray(triangles, np.float64).reshape(-1, 9))
+    out = np.zeros(4, np.float64)
+    dist = np.zeros(max(Cc.shape[0], 1), np.float64)
+    st = ref().ref_deviation_to_mesh(_dptr(Cc), Cc.shape[0], _dptr(T), T.shape[0],
+                                     _ptr(out, _c_dbl_p), _ptr(dist, _c_dbl_p))
+    if st:
+        raise OracleError(st, ref().ref_last_error().decode())
+    return out, dist[: Cc.shape[0]]
+
+
+def ref_point_triangle_distance(p, tri) -> float:
+    pp = np.ascontiguousarray(np.asarray(p, np.float64).reshape(3))
+    tt = np.ascontiguousarray(np.asarray(tri, np.float64).reshape(9))
+    return ref().ref_point_triangle_distance(_ptr(pp, _c_dbl_p), _ptr(tt, _c_dbl_p))

@@ -11,7 +11,10 @@
 //   pcs::SpatialIndex           proj/include/pcs/spatial.hpp:19-56
 //   pcs::add_noise              proj/include/pcs/noise.hpp
 //   pcs::generate_surface       proj/include/pcs/bench.hpp
+//   pcs::deviation, deviation_to_mesh, point_triangle_distance
+//                               proj/include/pcs/metrics.hpp
 #include <chrono>
+#include <omp.h>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -21,6 +24,7 @@
 #include "pcs/bench.hpp"
 #include "pcs/errors.hpp"
 #include "pcs/lop.hpp"
+#include "pcs/metrics.hpp"
 #include "pcs/mls.hpp"
 #include "pcs/noise.hpp"
 #include "pcs/parallel.hpp"
@@ -60,6 +64,7 @@ int code_of(const std::exception& e) {
     g_err = e.what();
     if (dynamic_cast<const pcs::InvalidParam*>(&e)) return 1;
     if (dynamic_cast<const pcs::EmptyCloud*>(&e)) return 2;
+    if (dynamic_cast<const pcs::EmptyMesh*>(&e)) return 8;
     return 9;
 }
 }  // namespace
@@ -164,6 +169,72 @@ double ref_index_build_ms(const double* P, std::uint64_t n) {
     const pcs::SpatialIndex index(cloud);
     const auto t1 = std::chrono::steady_clock::now();
     return std::chrono::duration<double, std::milli>(t1 - t0).count() + 0.0 * index.size();
+}
+
+// SpatialIndex::nearest for every query (reference kd-tree).
+int ref_nearest_all(const double* C, std::uint64_t n, const double* Q, std::uint64_t m,
+                    std::uint32_t* idx, double* dist, int threads) {
+    try {
+        const auto cloud = to_cloud(C, n);
+        const pcs::SpatialIndex index(cloud);
+        int err = 0;
+#pragma omp parallel for schedule(dynamic, 256) num_threads(threads > 0 ? threads : omp_get_max_threads())
+        for (std::int64_t i = 0; i < (std::int64_t)m; ++i) {
+            try {
+                const auto h = index.nearest({Q[3 * i], Q[3 * i + 1], Q[3 * i + 2]});
+                idx[i] = static_cast<std::uint32_t>(h.index);
+                dist[i] = h.distance;
+            } catch (...) {
+#pragma omp atomic write
+                err = 1;
+            }
+        }
+        if (err) throw pcs::EmptyCloud("nearest: index built over an empty cloud");
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+// pcs::deviation; out = {n, mean, std (RMS), max}; dist may be null.
+int ref_deviation(const double* cloud, std::uint64_t m, const double* ref, std::uint64_t n,
+                  double* out, double* dist) {
+    try {
+        const auto r = pcs::deviation(to_cloud(cloud, m), to_cloud(ref, n), dist != nullptr);
+        out[0] = (double)r.n;
+        out[1] = r.mean_distance;
+        out[2] = r.std_deviation;
+        out[3] = r.max_distance;
+        if (dist) std::memcpy(dist, r.distances.data(), m * sizeof(double));
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+int ref_deviation_to_mesh(const double* cloud, std::uint64_t m, const double* tri,
+                          std::uint64_t ntri, double* out, double* dist) {
+    try {
+        pcs::TriangleMesh mesh;
+        for (std::uint64_t t = 0; t < ntri; ++t) {
+            const double* v = tri + 9 * t;
+            mesh.triangles.push_back({{v[0], v[1], v[2]}, {v[3], v[4], v[5]}, {v[6], v[7], v[8]}});
+        }
+        const auto r = pcs::deviation_to_mesh(to_cloud(cloud, m), mesh, dist != nullptr);
+        out[0] = (double)r.n;
+        out[1] = r.mean_distance;
+        out[2] = r.std_deviation;
+        out[3] = r.max_distance;
+        if (dist) std::memcpy(dist, r.distances.data(), m * sizeof(double));
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+double ref_point_triangle_distance(const double* p, const double* t) {
+    return pcs::point_triangle_distance({p[0], p[1], p[2]},
+                                        {{t[0], t[1], t[2]}, {t[3], t[4], t[5]}, {t[6], t[7], t[8]}});
 }
 
 double ref_theta(double d, double h, double cutoff) {

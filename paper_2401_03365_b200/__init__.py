@@ -4,10 +4,11 @@ The operator runs as hand-written sm_100a CUDA kernels in
 ``lib/libpcs_lop_b200.so`` behind the C ABI of ``include/pcs_lop.h``.
 """
 from .lop import (  # noqa: F401
-    CONFIGS, EmptyCloud, Error, InvalidParam, KernelParams, LopParams, LopPlan, LopSummary,
+    CONFIGS, DeviationReport, EmptyCloud, EmptyMesh, Error, InvalidParam, KernelParams, LopParams, LopPlan, LopSummary,
     LoopbackGroup,
     NumericalFailure, DeviceUnavailable, add_noise, config_params, config_sizes, density_weights, generate_config,
     generate_surface, grid_sort, lop_project, radius_query_all, shard_layout,
+    nearest_all, deviation, deviation_to_mesh,
 )
 
 __all__ = [
@@ -15,5 +16,6 @@ __all__ = [
     "LoopbackGroup",
     "LopSummary", "NumericalFailure", "DeviceUnavailable", "add_noise", "config_params",
     "config_sizes", "density_weights", "generate_config", "generate_surface", "grid_sort", "lop_project",
-    "radius_query_all", "shard_layout",
+    "radius_query_all", "shard_layout", "DeviationReport", "EmptyMesh", "nearest_all",
+    "deviation", "deviation_to_mesh",
 ]

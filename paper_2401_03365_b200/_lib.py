@@ -21,6 +21,7 @@ PCS_ERR_CUDA = 4
 PCS_ERR_NCCL = 5
 PCS_ERR_NO_DEVICE = 6
 PCS_ERR_CAPACITY = 7
+PCS_ERR_EMPTY_MESH = 8
 
 PCS_ETA_INV_CUBE = 0
 PCS_ETA_NEG_LINEAR = 1
@@ -36,7 +37,7 @@ EXPORTED = [
     "pcs_lop_plan_launches", "pcs_radius_query_all", "pcs_density_weights", "pcs_grid_sort", "pcs_generate_surface",
     "pcs_add_noise", "pcs_config_sizes", "pcs_generate_config", "pcs_shard_layout",
     "pcs_loopback_group_create", "pcs_loopback_group_destroy", "pcs_lop_plan_set_loopback",
-    "pcs_shard_layout_weighted",
+    "pcs_shard_layout_weighted", "pcs_nearest_all", "pcs_deviation", "pcs_deviation_to_mesh",
 ]
 
 
@@ -55,6 +56,12 @@ class LopDesc(C.Structure):
         ("lanes_per_point", C.c_int32),
         ("reserved", C.c_int32 * 7),
     ]
+
+
+class DeviationReportC(C.Structure):
+    """pcs_deviation_report (DeviationReport, proj/include/pcs/metrics.hpp)."""
+    _fields_ = [("n", C.c_uint64), ("mean_distance", C.c_double),
+                ("std_deviation", C.c_double), ("max_distance", C.c_double)]
 
 
 class LopSummaryC(C.Structure):
@@ -134,6 +141,12 @@ def lib():
         L.pcs_shard_layout.argtypes = [_u32p, C.c_uint64, C.c_int32, _u32p, _u32p, _u32p, _u32p]
         L.pcs_shard_layout_weighted.argtypes = [_u32p, C.POINTER(C.c_float), C.c_uint64, C.c_int32,
                                                 _u32p, _u32p, _u32p, _u32p]
+        L.pcs_nearest_all.argtypes = [C.POINTER(LopDesc), _dp, C.c_uint64, _dp, C.c_uint64, _u32p,
+                                      _dp]
+        L.pcs_deviation.argtypes = [C.POINTER(LopDesc), _dp, C.c_uint64, _dp, C.c_uint64,
+                                    C.POINTER(DeviationReportC), _dp]
+        L.pcs_deviation_to_mesh.argtypes = [C.POINTER(LopDesc), _dp, C.c_uint64, _dp, C.c_uint64,
+                                            C.POINTER(DeviationReportC), _dp]
         for name in EXPORTED:
             fn = getattr(L, name)
             if fn.restype is C.c_int:  # default restype -> pcs_status

@@ -200,6 +200,27 @@ pcs_status pcs_grid_sort(const pcs_lop_desc* d, const double* C_xyz, uint64_t n,
     });
 }
 
+pcs_status pcs_nearest_all(const pcs_lop_desc* d, const double* C_xyz, uint64_t n,
+                           const double* Q_xyz, uint64_t m, uint32_t* idx_out, double* dist_out) {
+    return guarded([&] { pcsb::nearest_all(checked(d), C_xyz, n, Q_xyz, m, idx_out, dist_out); });
+}
+
+pcs_status pcs_deviation(const pcs_lop_desc* d, const double* cloud_xyz, uint64_t m,
+                         const double* ref_xyz, uint64_t n, pcs_deviation_report* report,
+                         double* distances_out) {
+    return guarded([&] {
+        pcsb::deviation(checked(d), cloud_xyz, m, ref_xyz, n, report, distances_out);
+    });
+}
+
+pcs_status pcs_deviation_to_mesh(const pcs_lop_desc* d, const double* cloud_xyz, uint64_t m,
+                                 const double* tri_xyz, uint64_t ntri,
+                                 pcs_deviation_report* report, double* distances_out) {
+    return guarded([&] {
+        pcsb::deviation_to_mesh(checked(d), cloud_xyz, m, tri_xyz, ntri, report, distances_out);
+    });
+}
+
 }  // extern "C"
 
 #include "nccl_dl.h"

@@ -12,8 +12,10 @@
 #include "../../include/pcs/kernels.hpp"
 #include "../../include/pcs/lop.hpp"
 #include "../../include/pcs/lop_ex.hpp"
+#include "../../include/pcs/metrics.hpp"
 #include "../../include/pcs/noise.hpp"
 #include "../../include/pcs_lop.h"
+#include "ptri.h"
 
 namespace pcs {
 
@@ -24,6 +26,7 @@ namespace {
     switch (st) {
         case PCS_ERR_INVALID_PARAM: throw InvalidParam(msg);
         case PCS_ERR_EMPTY_CLOUD: throw EmptyCloud(msg);
+        case PCS_ERR_EMPTY_MESH: throw EmptyMesh(msg);
         default: throw NumericalFailure(msg);
     }
 }
@@ -140,6 +143,57 @@ PointCloud generate_surface(const SyntheticSurface& surface) {
         pcs_generate_surface(static_cast<int32_t>(surface.kind), surface.n, surface.seed, &c.points[0].x);
     if (st != PCS_OK) throw InvalidParam("generate_surface: invalid surface kind");
     return c;
+}
+
+// ---- deviation metrics (proj/include/pcs/metrics.hpp, proj/src/metrics.cpp) ----
+
+namespace {
+
+DeviationReport to_report(const pcs_deviation_report& r, std::vector<double>&& d, bool keep) {
+    DeviationReport out;
+    out.n = (std::size_t)r.n;
+    out.mean_distance = r.mean_distance;
+    out.std_deviation = r.std_deviation;
+    out.max_distance = r.max_distance;
+    if (keep) out.distances = std::move(d);
+    return out;
+}
+
+pcs_lop_desc metrics_desc() {
+    pcs_lop_desc d;
+    pcs_lop_desc_default(&d);
+    return d;
+}
+
+}  // namespace
+
+DeviationReport deviation(const PointCloud& cloud, const PointCloud& reference,
+                          bool keep_distances) {
+    const pcs_lop_desc d = metrics_desc();
+    pcs_deviation_report r{};
+    std::vector<double> dist(keep_distances ? cloud.size() : 0);
+    const pcs_status st = pcs_deviation(&d, xyz(cloud), cloud.size(), xyz(reference),
+                                        reference.size(), &r, keep_distances ? dist.data() : nullptr);
+    if (st != PCS_OK) raise(st);
+    return to_report(r, std::move(dist), keep_distances);
+}
+
+double point_triangle_distance(Point3 p, const Triangle& tri) {
+    using pcsb::ptri::V3;
+    return pcsb::ptri::distance(V3{p.x, p.y, p.z}, V3{tri.a.x, tri.a.y, tri.a.z},
+                                V3{tri.b.x, tri.b.y, tri.b.z}, V3{tri.c.x, tri.c.y, tri.c.z});
+}
+
+DeviationReport deviation_to_mesh(const PointCloud& cloud, const TriangleMesh& mesh,
+                                  bool keep_distances) {
+    const pcs_lop_desc d = metrics_desc();
+    pcs_deviation_report r{};
+    std::vector<double> dist(keep_distances ? cloud.size() : 0);
+    const double* tri = mesh.empty() ? nullptr : &mesh.triangles[0].a.x;
+    const pcs_status st = pcs_deviation_to_mesh(&d, xyz(cloud), cloud.size(), tri, mesh.size(), &r,
+                                                keep_distances ? dist.data() : nullptr);
+    if (st != PCS_OK) raise(st);
+    return to_report(r, std::move(dist), keep_distances);
 }
 
 }  // namespace pcs

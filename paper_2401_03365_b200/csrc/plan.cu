@@ -233,6 +233,7 @@ Plan::Plan(const pcs_lop_desc& d) : d_(d) {
     rep_lanes_ = d_.lanes_per_point ? lanes_ : 2;
     if (const char* e = std::getenv("PCSB_REORDER_EVERY")) reorder_every_ = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("PCSB_ASYNC_ORDER")) async_order_ = std::atoi(e) != 0;  // developer knob
+    if (const char* e = std::getenv("PCSB_FUSED")) fused_ = std::atoi(e) != 0;  // developer knob
     if (const char* e = std::getenv("PCSB_REP_LANES")) rep_lanes_ = std::atoi(e);  // developer knob
     device_ = select_device(d_.device);
     PCSB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
@@ -876,7 +877,7 @@ void Plan::enqueue_sweep(int k) {
         a.slot = slot;
         a.done = done;
         const bool wl = d_.density_weights != 0;
-        if (xgrid) {
+        if (xgrid && !fused_) {
             launch_fast(a, lanes_, wl, k == 1, rep, 1, attr_grid_, stream_);  // attraction
             PCSB_CUDA(cudaEventRecord(se.e[6], stream_));
             PCSB_CUDA(cudaStreamWaitEvent(stream_, se.e[2], 0));
@@ -884,6 +885,10 @@ void Plan::enqueue_sweep(int k) {
             launch_fast(a, rep_lanes_, wl, k == 1, rep, 2, fast_grid_, stream_);  // repulsion + update
             launches_ += 2;
         } else {
+            if (xgrid) {  // fused: attraction and repulsion per query group in one pass
+                PCSB_CUDA(cudaStreamWaitEvent(stream_, se.e[2], 0));
+                if (d_.density_weights) density_pass_x<T>(qlist, nq, cur);
+            }
             launch_fast(a, lanes_, wl, k == 1, rep, 0, fast_grid_, stream_);
             launches_ += 1;
             PCSB_CUDA(cudaEventRecord(se.e[6], stream_));

@@ -124,6 +124,7 @@ private:
     uint32_t* q_list_alt_ = nullptr;
     int block_shift_alt_ = 0;
     bool q_next_ready_ = false;
+    bool fused_ = false;              // one pass (attraction + repulsion) after the X grid
     bool async_order_ = true;         // developer knob PCSB_ASYNC_ORDER=0: build in line
     int last_sweep_ = 0;              // last sweep index of the current run()
     cudaEvent_t ev_qready_ = nullptr;
@@ -160,5 +161,13 @@ void radius_query_all(const pcs_lop_desc& d, const double* C, uint64_t n, const 
 void density_weights(const pcs_lop_desc& d, const double* C, uint64_t n, double* v_out);
 void grid_sort(const pcs_lop_desc& d, const double* C, uint64_t n, double support,
                uint32_t* keys_out, uint32_t* order_out);
+
+// Deviation metrics (nn.cu; proj/src/metrics.cpp, proj/src/spatial.cpp:119-158).
+void nearest_all(const pcs_lop_desc& d, const double* C, uint64_t n, const double* Q, uint64_t m,
+                 uint32_t* idx_out, double* dist_out);
+void deviation(const pcs_lop_desc& d, const double* cloud, uint64_t m, const double* ref,
+               uint64_t n, pcs_deviation_report* rep, double* distances_out);
+void deviation_to_mesh(const pcs_lop_desc& d, const double* cloud, uint64_t m, const double* tri,
+                       uint64_t ntri, pcs_deviation_report* rep, double* distances_out);
 
 }  // namespace pcsb

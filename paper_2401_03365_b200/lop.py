@@ -29,6 +29,10 @@ class InvalidParam(Error):
     pass
 
 
+class EmptyMesh(Error):
+    pass
+
+
 class NumericalFailure(Error):
     """Numerical or device failure (CUDA / NCCL error, no sm_100 device)."""
 
@@ -43,6 +47,8 @@ def _raise(status: int) -> None:
         raise InvalidParam(msg)
     if status == L.PCS_ERR_EMPTY_CLOUD:
         raise EmptyCloud(msg)
+    if status == L.PCS_ERR_EMPTY_MESH:
+        raise EmptyMesh(msg)
     if status == L.PCS_ERR_NO_DEVICE:
         raise DeviceUnavailable(msg)
     raise NumericalFailure(f"[status {status}] {msg}")
@@ -280,6 +286,68 @@ def radius_query_all(cloud, queries, r: float, precision: str = "fp64", device: 
     _check(L.lib().pcs_radius_query_all(C.byref(d), _ptr(Cc), Cc.shape[0], _ptr(Q), m, float(r),
                                         off.ctypes.data_as(L._u64p), _ptr(idx, L._u32p), tot))
     return off, idx[:tot]
+
+
+# ---- deviation metrics (proj/include/pcs/metrics.hpp, proj/src/metrics.cpp) ----
+@dataclass
+class DeviationReport:
+    """n, mean distance, RMS distance (``std_deviation``) and max distance;
+    ``distances`` (per cloud point) when requested."""
+    n: int = 0
+    mean_distance: float = 0.0
+    std_deviation: float = 0.0
+    max_distance: float = 0.0
+    distances: Optional[np.ndarray] = None
+
+
+def nearest_all(cloud, queries, device: int = -1) -> Tuple[np.ndarray, np.ndarray]:
+    """SpatialIndex::nearest (proj/src/spatial.cpp:119-158) for every query, on the
+    device: ``(index, distance)`` of the nearest cloud point, smallest index on
+    equal distance, distances bit-identical to the reference."""
+    Cc = _cloud(cloud)
+    Q = _cloud(queries)
+    m = Q.shape[0]
+    idx = np.zeros(max(m, 1), dtype=np.uint32)
+    dist = np.zeros(max(m, 1), dtype=np.float64)
+    d = make_desc(LopParams(), device=device)
+    _check(L.lib().pcs_nearest_all(C.byref(d), _ptr(Cc), Cc.shape[0], _ptr(Q), m,
+                                   _ptr(idx, L._u32p), _ptr(dist)))
+    return idx[:m], dist[:m]
+
+
+def _report(r, dist, keep):
+    return DeviationReport(int(r.n), r.mean_distance, r.std_deviation, r.max_distance,
+                           dist if keep else None)
+
+
+def deviation(cloud, reference, keep_distances: bool = False, device: int = -1) -> DeviationReport:
+    """pcs::deviation (proj/src/metrics.cpp:39-53): nearest-reference distance of
+    every cloud point (device), aggregated in index order like the reference."""
+    Cc = _cloud(cloud)
+    R = _cloud(reference)
+    m = Cc.shape[0]
+    dist = np.zeros(max(m, 1), dtype=np.float64)
+    r = L.DeviationReportC()
+    d = make_desc(LopParams(), device=device)
+    _check(L.lib().pcs_deviation(C.byref(d), _ptr(Cc), m, _ptr(R), R.shape[0], C.byref(r),
+                                 _ptr(dist)))
+    return _report(r, dist[:m], keep_distances)
+
+
+def deviation_to_mesh(cloud, triangles, keep_distances: bool = False,
+                      device: int = -1) -> DeviationReport:
+    """pcs::deviation_to_mesh (proj/src/metrics.cpp:115-133); ``triangles`` is a
+    ``(T, 3, 3)`` array of vertices a, b, c."""
+    Cc = _cloud(cloud)
+    T = np.ascontiguousarray(np.asarray(triangles, dtype=np.float64).reshape(-1, 9))
+    m = Cc.shape[0]
+    dist = np.zeros(max(m, 1), dtype=np.float64)
+    r = L.DeviationReportC()
+    d = make_desc(LopParams(), device=device)
+    tp = _ptr(T) if T.shape[0] else None
+    _check(L.lib().pcs_deviation_to_mesh(C.byref(d), _ptr(Cc), m, tp, T.shape[0], C.byref(r),
+                                         _ptr(dist)))
+    return _report(r, dist[:m], keep_distances)
 
 
 def density_weights(cloud, h: float, cutoff_multiple: float = 3.0, precision: str = "fp64",

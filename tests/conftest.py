@@ -37,3 +37,11 @@ def pb():
 def bbox_diag(P) -> float:
     P = np.asarray(P).reshape(-1, 3)
     return float(np.linalg.norm(P.max(0) - P.min(0)))
+
+
+GOLDEN_METRICS = os.path.join(ROOT, "tests", "golden", "reference_metrics.npz")
+
+
+@pytest.fixture(scope="session")
+def golden_metrics():
+    return np.load(GOLDEN_METRICS)

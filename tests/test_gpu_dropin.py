@@ -1,8 +1,8 @@
-"""Drop-in proof: the reference's own, unmodified proj/tests/test_lop.cpp runs
-against this library (GPU).
+"""Drop-in proof: the reference's own, unmodified proj/tests/test_lop.cpp and
+proj/tests/test_metrics.cpp run against this library (GPU).
 
-tests/dropin/Makefile compiles /root/reference/proj/tests/test_lop.cpp with this
-repo's include/pcs headers first on the include path and links
+tests/dropin/Makefile compiles /root/reference/proj/tests/test_{lop,metrics}.cpp
+with this repo's include/pcs headers first on the include path and links
 lib/libpcs_lop_b200.so.  The binary is built by __graft_entry__.build() where
 the reference exists and travels with the repo snapshot to the GPU box.
 """
@@ -15,17 +15,27 @@ from conftest import ROOT
 
 pytestmark = pytest.mark.gpu
 
-BIN = os.path.join(ROOT, "tests", "dropin", "bin", "test_lop")
 
-
-def test_reference_test_lop_passes_unmodified():
+def _run(name: str, expect: str):
+    BIN = os.path.join(ROOT, "tests", "dropin", "bin", name)
     if not os.path.exists(BIN):
         if os.path.isdir("/root/reference/proj/tests"):
             subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "dropin")], check=True)
         else:
-            pytest.fail("tests/dropin/bin/test_lop was not built (run __graft_entry__.build() "
+            pytest.fail(f"tests/dropin/bin/{name} was not built (run __graft_entry__.build() "
                         "where /root/reference exists)")
     r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert "10 passed | 0 failed" in r.stdout
+    assert expect in r.stdout
+
+
+def test_reference_test_lop_passes_unmodified():
+    _run("test_lop", "10 passed | 0 failed")
+
+
+def test_reference_test_metrics_passes_unmodified():
+    """proj/tests/test_metrics.cpp: deviation (device nearest-neighbour grid) and
+    deviation_to_mesh (device point-triangle kernel) against the reference's own
+    exhaustive oracles, fixed cases and error contracts."""
+    _run("test_metrics", "11 passed | 0 failed")

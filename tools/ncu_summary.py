@@ -26,6 +26,9 @@ FULL_KEYS = [
     "dram__bytes_write.sum",
     "lts__t_sector_hit_rate.pct",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "l1tex__t_sector_hit_rate.pct",
+    "smsp__warps_active.avg.per_cycle_active",
     "launch__registers_per_thread",
     "launch__occupancy_limit_registers",
     "launch__occupancy_limit_shared_mem",
