@@ -198,10 +198,10 @@ void launch_iso_to_orig(const uint8_t* ever_iso, const uint32_t* orig_of_interna
 template <typename T>
 void launch_scatter_init(const typename Vec4<T>::type* X0, const uint32_t* internal_of_orig,
                          uint32_t m, typename Vec4<T>::type* X, cudaStream_t s);
-// work estimate per X0 point (data points in its 3x3x3 cells + 1), sharded layout
+// work estimate per X0 point (data points its own row-trimmed ball stages + 64), sharded layout
 template <typename T>
 void launch_shard_work(const typename Vec4<T>::type* X0, uint32_t m, const GridGeom& g,
-                       const uint32_t* Pstart, float* w, cudaStream_t s);
+                       double s_pad, const uint32_t* Pstart, float* w, cudaStream_t s);
 template <typename T>
 void launch_fill_invalid(typename Vec4<T>::type* X, uint32_t mpad, const uint32_t* orig_of_internal,
                          cudaStream_t s);

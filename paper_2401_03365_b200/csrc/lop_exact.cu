@@ -1,3 +1,4 @@
+#include <cstdlib>
 // lop_exact.cu — the exact-arithmetic path (fp64 math, reference predicate).
 //
 // One warp per query; lanes stride over the candidates of the cell rows that
@@ -424,38 +425,59 @@ void launch_fill_invalid(typename Vec4<T>::type* X, uint32_t mpad, const uint32_
     fill_invalid_kernel<typename Vec4<T>::type, T><<<blocks_for(mpad, 256), 256, 0, s>>>(X, mpad, orig);
 }
 
-// Work estimate of an X0 point for the sharded layout: the data points in the
-// 3x3x3 cells around it (cell side s/4 or s/2: a local density proxy; the
-// sweep's work per point is proportional to it).
+// Work estimate of an X0 point for the sharded layout: the data points the
+// fused kernel would stage for this point alone — every grid row (y, z) within
+// the support, trimmed in x to the point's ball chord through the row (the
+// kernel's per-row trimming, lop_fast.cu row_range, for a group of one) — plus
+// a per-query constant for the group setup.  Unlike a plain density count it
+// sees the surface's slope against the rows (measured: config 3's middle
+// z-slab costs ~6% more per interaction than the others).
 template <typename V>
-__global__ void shard_work_kernel(const V* __restrict__ X0, uint32_t m, GridGeom g,
-                                  const uint32_t* __restrict__ Pstart, float* __restrict__ w) {
+__global__ void shard_work_kernel(const V* __restrict__ X0, uint32_t m, GridGeom g, double s_pad,
+                                  float per_query, const uint32_t* __restrict__ Pstart,
+                                  float* __restrict__ w) {
+    const int R = (int)ceil(s_pad * g.inv_cs);
+    const double r2 = s_pad * s_pad;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
         const V p = X0[i];
-        const int cx = cell_coord((double)p.x, g.ox, g.inv_csx, g.gx);
-        const int cy = cell_coord((double)p.y, g.oy, g.inv_cs, g.gy);
-        const int cz = cell_coord((double)p.z, g.oz, g.inv_cs, g.gz);
-        const int lx = max(cx - g.xsub, 0), hx = min(cx + g.xsub, g.gx - 1);
+        const double px = (double)p.x, py = (double)p.y, pz = (double)p.z;
+        const int cy = cell_coord(py, g.oy, g.inv_cs, g.gy);
+        const int cz = cell_coord(pz, g.oz, g.inv_cs, g.gz);
         uint32_t cnt = 0;
-        for (int z = max(cz - 1, 0); z <= min(cz + 1, g.gz - 1); ++z)
-            for (int y = max(cy - 1, 0); y <= min(cy + 1, g.gy - 1); ++y) {
+        for (int z = max(cz - R, 0); z <= min(cz + R, g.gz - 1); ++z) {
+            const double z0 = g.oz + g.cs * (double)z, z1 = z0 + g.cs;
+            const double gz = fmax(0.0, fmax(z0 - pz, pz - z1));
+            for (int y = max(cy - R, 0); y <= min(cy + R, g.gy - 1); ++y) {
+                const double y0 = g.oy + g.cs * (double)y, y1 = y0 + g.cs;
+                const double gy = fmax(0.0, fmax(y0 - py, py - y1));
+                const double rem = r2 - gy * gy - gz * gz;
+                if (rem < 0.0) continue;
+                const double hx = sqrt(rem);
+                const int lx = cell_coord(px - hx, g.ox, g.inv_csx, g.gx);
+                const int hxc = cell_coord(px + hx, g.ox, g.inv_csx, g.gx);
                 const uint32_t base = ((uint32_t)z * (uint32_t)g.gy + (uint32_t)y) * (uint32_t)g.gx;
-                cnt += Pstart[base + hx + 1] - Pstart[base + lx];
+                cnt += Pstart[base + hxc + 1] - Pstart[base + lx];
             }
-        w[i] = 1.0f + (float)cnt;
+        }
+        w[i] = per_query + (float)cnt;
     }
 }
 
 template <typename T>
 void launch_shard_work(const typename Vec4<T>::type* X0, uint32_t m, const GridGeom& g,
-                       const uint32_t* Pstart, float* w, cudaStream_t s) {
+                       double s_pad, const uint32_t* Pstart, float* w, cudaStream_t s) {
     if (!m) return;
-    shard_work_kernel<typename Vec4<T>::type><<<blocks_for(m, 256), 256, 0, s>>>(X0, m, g, Pstart, w);
+    static const float per_query = [] {  // developer knob: per-query constant of the estimate
+        const char* e = std::getenv("PCSB_SHARD_C");
+        return e ? (float)std::atof(e) : 64.0f;
+    }();
+    shard_work_kernel<typename Vec4<T>::type><<<blocks_for(m, 256), 256, 0, s>>>(
+        X0, m, g, s_pad, per_query, Pstart, w);
 }
 
 #define PCSB_INST(T)                                                                              \
     template void launch_exact<T>(const ExactArgs<T>&, int, cudaStream_t);                       \
-    template void launch_shard_work<T>(const Vec4<T>::type*, uint32_t, const GridGeom&,           \
+    template void launch_shard_work<T>(const Vec4<T>::type*, uint32_t, const GridGeom&, double,   \
                                        const uint32_t*, float*, cudaStream_t);                    \
     template void launch_exact_density<T>(const Vec4<T>::type*, const uint32_t*,                 \
                                           const Vec4<T>::type*, const uint32_t*, uint32_t,        \

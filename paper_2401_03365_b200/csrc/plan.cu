@@ -519,7 +519,7 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
             launches_ += radix_sort(tk, nullptr, tsk, order, (uint32_t)m, g_.key_bits, rs_, nullptr,
                                     stream_);
             float* wd = (float*)talloc(m * sizeof(float));
-            launch_shard_work<T>(X0v, (uint32_t)m, g_, P_start_, wd, stream_);
+            launch_shard_work<T>(X0v, (uint32_t)m, g_, s_pad_, P_start_, wd, stream_);
             launches_ += 1;
             PCSB_CUDA(cudaMemcpyAsync(sidx.data(), order, m * sizeof(uint32_t),
                                       cudaMemcpyDeviceToHost, stream_));
