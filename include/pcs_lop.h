@@ -43,7 +43,8 @@ typedef enum pcs_status {
     PCS_ERR_NCCL = 5,           /* collective failure */
     PCS_ERR_NO_DEVICE = 6,      /* no usable sm_100 device: there is no CPU fallback */
     PCS_ERR_CAPACITY = 7,       /* caller buffer too small; required size reported */
-    PCS_ERR_EMPTY_MESH = 8      /* pcs::EmptyMesh     (errors.hpp:20-23) */
+    PCS_ERR_EMPTY_MESH = 8,     /* pcs::EmptyMesh     (errors.hpp:20-23) */
+    PCS_ERR_PARSE = 9           /* pcs::ParseError    (errors.hpp): see pcs_parse_error */
 } pcs_status;
 
 /* Repulsion penalty eta.  The reference hard-codes eta = 1/(3 r^3),
@@ -199,6 +200,42 @@ pcs_status pcs_deviation(const pcs_lop_desc* d, const double* cloud_xyz, uint64_
 pcs_status pcs_deviation_to_mesh(const pcs_lop_desc* d, const double* cloud_xyz, uint64_t m,
                                  const double* tri_xyz, uint64_t ntri,
                                  pcs_deviation_report* report, double* distances_out);
+
+/* ---- cloud IO (the data format either side of the path) -----
+ * CloudFormat (proj/include/pcs/io.hpp): XYZ, or ASCII PLY. */
+typedef enum pcs_cloud_format { PCS_FMT_XYZ = 0, PCS_FMT_PLY_ASCII = 1 } pcs_cloud_format;
+
+/* Location and reason of a ParseError (the reference's "name:line: reason"). */
+typedef struct pcs_parse_error {
+    int64_t line;
+    char reason[256];
+} pcs_parse_error;
+
+/* write_cloud_stream (proj/src/io.cpp:277-290): the file text of n points
+ * (3 doubles each), coordinates in std::to_chars shortest round-trip form,
+ * formatted on the device.  *len = bytes; out (cap bytes) may be NULL to size
+ * the text first (PCS_ERR_CAPACITY when cap < *len). */
+pcs_status pcs_format_cloud(const pcs_lop_desc* d, const double* xyz, uint64_t n, int32_t format,
+                            char* out, uint64_t cap, uint64_t* len);
+/* Same text in one pass, in a buffer the library allocates (release it with
+ * pcs_free_buffer). */
+pcs_status pcs_format_cloud_alloc(const pcs_lop_desc* d, const double* xyz, uint64_t n,
+                                  int32_t format, char** out, uint64_t* len);
+void pcs_free_buffer(void* p);
+/* read_cloud_stream (proj/src/io.cpp:143-236, 260-264): parse a cloud file's text
+ * on the device (lines the device cannot settle are re-read on the host with the
+ * reference's rules).  *n_out = points; xyz_out receives 3*n doubles when
+ * cap >= n (else PCS_ERR_CAPACITY, nothing written).  PCS_ERR_PARSE fills err
+ * (may be NULL). */
+pcs_status pcs_parse_cloud(const pcs_lop_desc* d, const char* text, uint64_t len, int32_t format,
+                           double* xyz_out, uint64_t cap, uint64_t* n_out, pcs_parse_error* err);
+/* read_mesh_stream (proj/src/io.cpp:306-325): triangles (9 doubles each) of an
+ * ASCII PLY with a face element, fan-triangulated; host parser. */
+pcs_status pcs_parse_mesh(const char* text, uint64_t len, double* tri_out, uint64_t cap,
+                          uint64_t* ntri_out, pcs_parse_error* err);
+/* format_double (proj/src/io.cpp:240-245): shortest round-trip text of v
+ * (<= 32 bytes, not NUL-terminated); returns the length. */
+int32_t pcs_format_double(double v, char* out32);
 
 /* Multi-GPU ownership layout (host only, no device needed): shard r owns the
  * r-th contiguous range of `sorted_order` (the initial grid order of X0) and

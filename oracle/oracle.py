@@ -155,6 +155,10 @@ def ref():
                                       _c_dbl_p]
         lib.ref_deviation_to_mesh.argtypes = [_c_dbl_p, C.c_uint64, _c_dbl_p, C.c_uint64,
                                               _c_dbl_p, _c_dbl_p]
+        lib.ref_format_cloud.argtypes = [_c_dbl_p, C.c_uint64, C.c_int, C.c_char_p, C.c_uint64,
+                                         _c_u64_p]
+        lib.ref_parse_cloud.argtypes = [C.c_char_p, C.c_uint64, C.c_int, _c_dbl_p, C.c_uint64,
+                                        _c_u64_p, C.POINTER(C.c_int64)]
         lib.ref_point_triangle_distance.argtypes = [_c_dbl_p, _c_dbl_p]
         lib.ref_point_triangle_distance.restype = C.c_double
         _ref = lib
@@ -416,3 +420,30 @@ def ref_point_triangle_distance(p, tri) -> float:
     pp = np.ascontiguousarray(np.asarray(p, np.float64).reshape(3))
     tt = np.ascontiguousarray(np.asarray(tri, np.float64).reshape(9))
     return ref().ref_point_triangle_distance(_ptr(pp, _c_dbl_p), _ptr(tt, _c_dbl_p))
+
+
+# --- cloud IO through the reference (proj/src/io.cpp) ------------------------------
+def ref_format_cloud(xyz, fmt=0) -> bytes:
+    X = _xyz(xyz)
+    n = C.c_uint64(0)
+    ref().ref_format_cloud(_dptr(X), X.shape[0], fmt, None, 0, C.byref(n))
+    buf = C.create_string_buffer(max(n.value, 1))
+    st = ref().ref_format_cloud(_dptr(X), X.shape[0], fmt, buf, n.value, C.byref(n))
+    if st:
+        raise OracleError(st, ref().ref_last_error().decode())
+    return buf.raw[: n.value]
+
+
+def ref_parse_cloud(text: bytes, fmt=0):
+    """(points, None) or (None, (line, message)) for a ParseError."""
+    cap = len(text) // 6 + 1
+    out = np.zeros((cap, 3), np.float64)
+    n = C.c_uint64(0)
+    line = C.c_int64(0)
+    st = ref().ref_parse_cloud(text, len(text), fmt, _ptr(out, _c_dbl_p), cap, C.byref(n),
+                               C.byref(line))
+    if st == 10:
+        return None, (line.value, ref().ref_last_error().decode())
+    if st:
+        raise OracleError(st, ref().ref_last_error().decode())
+    return out[: n.value], None

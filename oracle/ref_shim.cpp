@@ -11,9 +11,11 @@
 //   pcs::SpatialIndex           proj/include/pcs/spatial.hpp:19-56
 //   pcs::add_noise              proj/include/pcs/noise.hpp
 //   pcs::generate_surface       proj/include/pcs/bench.hpp
+//   pcs::write_cloud_stream, read_cloud_stream  proj/include/pcs/io.hpp
 //   pcs::deviation, deviation_to_mesh, point_triangle_distance
 //                               proj/include/pcs/metrics.hpp
 #include <chrono>
+#include <sstream>
 #include <omp.h>
 #include <cstdint>
 #include <cstring>
@@ -23,6 +25,7 @@
 
 #include "pcs/bench.hpp"
 #include "pcs/errors.hpp"
+#include "pcs/io.hpp"
 #include "pcs/lop.hpp"
 #include "pcs/metrics.hpp"
 #include "pcs/mls.hpp"
@@ -235,6 +238,44 @@ int ref_deviation_to_mesh(const double* cloud, std::uint64_t m, const double* tr
 double ref_point_triangle_distance(const double* p, const double* t) {
     return pcs::point_triangle_distance({p[0], p[1], p[2]},
                                         {{t[0], t[1], t[2]}, {t[3], t[4], t[5]}, {t[6], t[7], t[8]}});
+}
+
+// write_cloud_stream into out (cap bytes); *len = bytes (returns 7 when cap is short)
+int ref_format_cloud(const double* xyz, std::uint64_t n, int fmt, char* out, std::uint64_t cap,
+                     std::uint64_t* len) {
+    try {
+        std::ostringstream os;
+        pcs::write_cloud_stream(to_cloud(xyz, n), os,
+                                fmt == 0 ? pcs::CloudFormat::Xyz : pcs::CloudFormat::PlyAscii);
+        const std::string t = os.str();
+        *len = t.size();
+        if (!out || cap < t.size()) return 7;
+        std::memcpy(out, t.data(), t.size());
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+// read_cloud_stream; *n = points (returns 7 when cap is short); a ParseError
+// returns 10 with its line number and message
+int ref_parse_cloud(const char* text, std::uint64_t len, int fmt, double* out, std::uint64_t cap,
+                    std::uint64_t* n, std::int64_t* line) {
+    try {
+        std::istringstream is(std::string(text, len));
+        const auto c = pcs::read_cloud_stream(
+            is, fmt == 0 ? pcs::CloudFormat::Xyz : pcs::CloudFormat::PlyAscii, "<memory>");
+        *n = c.size();
+        if (cap < c.size()) return 7;
+        from_cloud(c, out);
+        return 0;
+    } catch (const pcs::ParseError& e) {
+        g_err = e.what();
+        *line = e.line_number;
+        return 10;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
 }
 
 double ref_theta(double d, double h, double cutoff) {

@@ -8,7 +8,8 @@ from .lop import (  # noqa: F401
     LoopbackGroup,
     NumericalFailure, DeviceUnavailable, add_noise, config_params, config_sizes, density_weights, generate_config,
     generate_surface, grid_sort, lop_project, radius_query_all, shard_layout,
-    nearest_all, deviation, deviation_to_mesh,
+    nearest_all, deviation, deviation_to_mesh, ParseError, format_from_path, format_cloud,
+    parse_cloud, read_cloud, write_cloud, parse_mesh, format_double,
 )
 
 __all__ = [
@@ -17,5 +18,6 @@ __all__ = [
     "LopSummary", "NumericalFailure", "DeviceUnavailable", "add_noise", "config_params",
     "config_sizes", "density_weights", "generate_config", "generate_surface", "grid_sort", "lop_project",
     "radius_query_all", "shard_layout", "DeviationReport", "EmptyMesh", "nearest_all",
-    "deviation", "deviation_to_mesh",
+    "deviation", "deviation_to_mesh", "ParseError", "format_from_path", "format_cloud",
+    "parse_cloud", "read_cloud", "write_cloud", "parse_mesh", "format_double",
 ]

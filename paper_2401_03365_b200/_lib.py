@@ -22,6 +22,9 @@ PCS_ERR_NCCL = 5
 PCS_ERR_NO_DEVICE = 6
 PCS_ERR_CAPACITY = 7
 PCS_ERR_EMPTY_MESH = 8
+PCS_ERR_PARSE = 9
+PCS_FMT_XYZ = 0
+PCS_FMT_PLY_ASCII = 1
 
 PCS_ETA_INV_CUBE = 0
 PCS_ETA_NEG_LINEAR = 1
@@ -38,6 +41,8 @@ EXPORTED = [
     "pcs_add_noise", "pcs_config_sizes", "pcs_generate_config", "pcs_shard_layout",
     "pcs_loopback_group_create", "pcs_loopback_group_destroy", "pcs_lop_plan_set_loopback",
     "pcs_shard_layout_weighted", "pcs_nearest_all", "pcs_deviation", "pcs_deviation_to_mesh",
+    "pcs_format_cloud", "pcs_parse_cloud", "pcs_parse_mesh", "pcs_format_double",
+    "pcs_format_cloud_alloc", "pcs_free_buffer",
 ]
 
 
@@ -62,6 +67,11 @@ class DeviationReportC(C.Structure):
     """pcs_deviation_report (DeviationReport, proj/include/pcs/metrics.hpp)."""
     _fields_ = [("n", C.c_uint64), ("mean_distance", C.c_double),
                 ("std_deviation", C.c_double), ("max_distance", C.c_double)]
+
+
+class ParseErrorC(C.Structure):
+    """pcs_parse_error: line number and reason of a ParseError."""
+    _fields_ = [("line", C.c_int64), ("reason", C.c_char * 256)]
 
 
 class LopSummaryC(C.Structure):
@@ -147,8 +157,22 @@ def lib():
                                     C.POINTER(DeviationReportC), _dp]
         L.pcs_deviation_to_mesh.argtypes = [C.POINTER(LopDesc), _dp, C.c_uint64, _dp, C.c_uint64,
                                             C.POINTER(DeviationReportC), _dp]
+        L.pcs_format_cloud.argtypes = [C.POINTER(LopDesc), _dp, C.c_uint64, C.c_int32, C.c_char_p,
+                                       C.c_uint64, _u64p]
+        L.pcs_parse_cloud.argtypes = [C.POINTER(LopDesc), C.c_char_p, C.c_uint64, C.c_int32, _dp,
+                                      C.c_uint64, _u64p, C.POINTER(ParseErrorC)]
+        L.pcs_parse_mesh.argtypes = [C.c_char_p, C.c_uint64, _dp, C.c_uint64, _u64p,
+                                     C.POINTER(ParseErrorC)]
+        L.pcs_format_cloud_alloc.argtypes = [C.POINTER(LopDesc), _dp, C.c_uint64, C.c_int32,
+                                             C.POINTER(C.c_void_p), _u64p]
+        L.pcs_free_buffer.argtypes = [C.c_void_p]
+        L.pcs_free_buffer.restype = None
+        L.pcs_format_double.argtypes = [C.c_double, C.c_char_p]
+        L.pcs_format_double.restype = C.c_int32
         for name in EXPORTED:
             fn = getattr(L, name)
+            if name in ("pcs_format_double", "pcs_free_buffer"):
+                continue
             if fn.restype is C.c_int:  # default restype -> pcs_status
                 fn.restype = C.c_int
         _lib = L

@@ -3,6 +3,7 @@
 // Every entry point converts pcsb::Failure / std::exception into a pcs_status
 // and a thread-local message (pcs_last_error), the C rendering of the
 // reference's exception hierarchy (proj/include/pcs/errors.hpp:9-53).
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <new>
@@ -10,6 +11,10 @@
 
 #include "../../include/pcs_lop.h"
 #include "plan.cuh"
+#include "io.h"
+#include "dconv.h"
+#include <functional>
+#include <cstdio>
 
 namespace {
 thread_local std::string g_last_error;
@@ -38,6 +43,23 @@ const pcs_lop_desc& checked(const pcs_lop_desc* d) {
         throw pcsb::Failure(PCS_ERR_INVALID_PARAM,
                             "pcs_lop_desc.struct_size mismatch (initialise with pcs_lop_desc_default)");
     return *d;
+}
+}  // namespace
+
+namespace {
+pcs_status parse_guarded(pcs_parse_error* err, const std::function<void()>& f) {
+    try {
+        f();
+        return PCS_OK;
+    } catch (const pcsb::ParseFailure& e) {
+        if (err) {
+            err->line = e.line;
+            std::snprintf(err->reason, sizeof(err->reason), "%s", e.reason.c_str());
+        }
+        return guarded([&] { throw pcsb::Failure(PCS_ERR_PARSE, e.reason); });
+    } catch (...) {
+        return guarded([&] { throw; });
+    }
 }
 }  // namespace
 
@@ -219,6 +241,71 @@ pcs_status pcs_deviation_to_mesh(const pcs_lop_desc* d, const double* cloud_xyz,
     return guarded([&] {
         pcsb::deviation_to_mesh(checked(d), cloud_xyz, m, tri_xyz, ntri, report, distances_out);
     });
+}
+
+pcs_status pcs_format_cloud(const pcs_lop_desc* d, const double* xyz, uint64_t n, int32_t format,
+                            char* out, uint64_t cap, uint64_t* len) {
+    return guarded([&] {
+        const pcs_lop_desc& desc = checked(d);
+        if (format != PCS_FMT_XYZ && format != PCS_FMT_PLY_ASCII)
+            throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "unknown cloud format");
+        if (n && !xyz) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null points");
+        if (!len) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null length");
+        if (n) pcsb::select_device(desc.device);
+        *len = pcsb::format_cloud(xyz, n, format, out, cap);
+        if (!out || cap < *len) throw pcsb::Failure(PCS_ERR_CAPACITY, "output buffer too small");
+    });
+}
+
+
+pcs_status pcs_parse_cloud(const pcs_lop_desc* d, const char* text, uint64_t len, int32_t format,
+                           double* xyz_out, uint64_t cap, uint64_t* n_out, pcs_parse_error* err) {
+    return parse_guarded(err, [&] {
+        const pcs_lop_desc& desc = checked(d);
+        if (format != PCS_FMT_XYZ && format != PCS_FMT_PLY_ASCII)
+            throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "unknown cloud format");
+        if (len && !text) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null text");
+        if (!n_out) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null count");
+        if (len) pcsb::select_device(desc.device);
+        const std::vector<double> xyz = pcsb::parse_cloud(text, len, format);
+        *n_out = xyz.size() / 3;
+        if (!xyz_out || cap < *n_out) throw pcsb::Failure(PCS_ERR_CAPACITY, "output buffer too small");
+        if (!xyz.empty()) std::memcpy(xyz_out, xyz.data(), xyz.size() * sizeof(double));
+    });
+}
+
+pcs_status pcs_parse_mesh(const char* text, uint64_t len, double* tri_out, uint64_t cap,
+                          uint64_t* ntri_out, pcs_parse_error* err) {
+    return parse_guarded(err, [&] {
+        if (len && !text) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null text");
+        if (!ntri_out) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null count");
+        const std::vector<double> tri = pcsb::parse_mesh(text, len);
+        *ntri_out = tri.size() / 9;
+        if (!tri_out || cap < *ntri_out) throw pcsb::Failure(PCS_ERR_CAPACITY, "output buffer too small");
+        std::memcpy(tri_out, tri.data(), tri.size() * sizeof(double));
+    });
+}
+
+pcs_status pcs_format_cloud_alloc(const pcs_lop_desc* d, const double* xyz, uint64_t n,
+                                  int32_t format, char** out, uint64_t* len) {
+    return guarded([&] {
+        const pcs_lop_desc& desc = checked(d);
+        if (format != PCS_FMT_XYZ && format != PCS_FMT_PLY_ASCII)
+            throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "unknown cloud format");
+        if (n && !xyz) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null points");
+        if (!out || !len) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null output");
+        if (n) pcsb::select_device(desc.device);
+        *len = pcsb::format_cloud_alloc(xyz, n, format, out);
+    });
+}
+
+void pcs_free_buffer(void* p) { std::free(p); }
+
+int32_t pcs_format_double(double v, char* out32) {
+    char buf[40];
+    const int n = pcsb::dconv::format(v, buf);
+    if (out32) std::memcpy(out32, buf, (size_t)n);
+    return n;
 }
 
 }  // extern "C"

@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "host_io.h"
 #include "plan.cuh"
 #include "ptri.h"
 
@@ -184,8 +185,8 @@ void nearest_device(const double* C, uint64_t n, const double* Qh, uint64_t m, u
     const uint32_t nn = (uint32_t)n, mm = (uint32_t)m;
     double* dC = mem.get<double>(n * 3);
     double* dQ = mem.get<double>(m * 3);
-    PCSB_CUDA(cudaMemcpyAsync(dC, C, n * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
-    PCSB_CUDA(cudaMemcpyAsync(dQ, Qh, m * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+    h2d_staged(dC, C, n * 3 * sizeof(double), s);
+    h2d_staged(dQ, Qh, m * 3 * sizeof(double), s);
     double4* Cv = mem.get<double4>(n);
     double4* Qv = mem.get<double4>(m);
     launch_convert_xyz<double>(dC, Cv, n, 1.0, s);

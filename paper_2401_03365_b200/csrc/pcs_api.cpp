@@ -4,14 +4,21 @@
 // exception types of proj/include/pcs/lop.hpp:51-53 / proj/src/lop.cpp:13-20,
 // so the reference's own proj/tests/test_lop.cpp compiles and runs against
 // this library unchanged (tests/test_dropin.py).
+#include <algorithm>
+#include <cctype>
 #include <cmath>
 #include <cstring>
+#include <fstream>
+#include <iterator>
+#include <sstream>
 #include <string>
+#include <vector>
 
 #include "../../include/pcs/bench.hpp"
 #include "../../include/pcs/kernels.hpp"
 #include "../../include/pcs/lop.hpp"
 #include "../../include/pcs/lop_ex.hpp"
+#include "../../include/pcs/io.hpp"
 #include "../../include/pcs/metrics.hpp"
 #include "../../include/pcs/noise.hpp"
 #include "../../include/pcs_lop.h"
@@ -194,6 +201,110 @@ DeviationReport deviation_to_mesh(const PointCloud& cloud, const TriangleMesh& m
                                                 keep_distances ? dist.data() : nullptr);
     if (st != PCS_OK) raise(st);
     return to_report(r, std::move(dist), keep_distances);
+}
+
+// ---- cloud files (proj/include/pcs/io.hpp, proj/src/io.cpp) ----------------------
+
+namespace {
+
+int32_t fmt_code(CloudFormat f) { return f == CloudFormat::Xyz ? PCS_FMT_XYZ : PCS_FMT_PLY_ASCII; }
+
+std::string slurp(std::istream& in) {
+    return std::string(std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>());
+}
+
+[[noreturn]] void raise_parse(pcs_status st, const pcs_parse_error& e, const std::string& name) {
+    if (st == PCS_ERR_PARSE) throw ParseError(name, (long)e.line, e.reason);
+    raise(st);
+}
+
+}  // namespace
+
+std::string format_double(double value) {
+    char buf[40];
+    const int32_t n = pcs_format_double(value, buf);
+    return std::string(buf, (size_t)n);
+}
+
+CloudFormat format_from_path(const std::string& path) {
+    const auto dot = path.find_last_of('.');
+    std::string ext = dot == std::string::npos ? std::string() : path.substr(dot);
+    for (char& c : ext) c = (char)std::tolower((unsigned char)c);
+    if (ext == ".xyz") return CloudFormat::Xyz;
+    if (ext == ".ply") return CloudFormat::PlyAscii;
+    throw InvalidParam("cannot infer cloud format from '" + path +
+                       "' (expected .xyz or .ply); pass the format explicitly");
+}
+
+PointCloud read_cloud_stream(std::istream& in, CloudFormat format, const std::string& name) {
+    const std::string text = slurp(in);
+    pcs_lop_desc d;
+    pcs_lop_desc_default(&d);
+    // every point needs at least 6 bytes ("0 0 0\n"): an upper bound, no second pass
+    std::vector<double> xyz(3 * (text.size() / 6 + 1));
+    uint64_t n = 0;
+    pcs_parse_error err{};
+    const pcs_status st = pcs_parse_cloud(&d, text.data(), text.size(), fmt_code(format), xyz.data(),
+                                          xyz.size() / 3, &n, &err);
+    if (st != PCS_OK) raise_parse(st, err, name);
+    PointCloud cloud;
+    cloud.points.resize((size_t)n);
+    if (n) std::memcpy(&cloud.points[0].x, xyz.data(), (size_t)n * 3 * sizeof(double));
+    return cloud;
+}
+
+PointCloud read_cloud(const std::string& path, CloudFormat format) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw IoError("cannot open '" + path + "' for reading");
+    return read_cloud_stream(in, format, path);
+}
+
+PointCloud read_cloud(const std::string& path) { return read_cloud(path, format_from_path(path)); }
+
+void write_cloud_stream(const PointCloud& cloud, std::ostream& out, CloudFormat format) {
+    pcs_lop_desc d;
+    pcs_lop_desc_default(&d);
+    char* text = nullptr;
+    uint64_t len = 0;
+    const pcs_status st = pcs_format_cloud_alloc(&d, xyz(cloud), cloud.size(), fmt_code(format), &text, &len);
+    if (st != PCS_OK) raise(st);
+    out.write(text, (std::streamsize)len);
+    pcs_free_buffer(text);
+}
+
+void write_cloud(const PointCloud& cloud, const std::string& path, CloudFormat format) {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw IoError("cannot open '" + path + "' for writing");
+    write_cloud_stream(cloud, out, format);
+    out.flush();
+    if (!out) throw IoError("write to '" + path + "' failed");
+}
+
+void write_cloud(const PointCloud& cloud, const std::string& path) {
+    write_cloud(cloud, path, format_from_path(path));
+}
+
+TriangleMesh read_mesh_stream(std::istream& in, const std::string& name) {
+    const std::string text = slurp(in);
+    uint64_t nt = 0;
+    pcs_parse_error err{};
+    pcs_status st = pcs_parse_mesh(text.data(), text.size(), nullptr, 0, &nt, &err);
+    std::vector<double> tri;
+    if (st == PCS_ERR_CAPACITY) {
+        tri.resize((size_t)nt * 9);
+        st = pcs_parse_mesh(text.data(), text.size(), tri.data(), nt, &nt, &err);
+    }
+    if (st != PCS_OK) raise_parse(st, err, name);
+    TriangleMesh mesh;
+    mesh.triangles.resize((size_t)nt);
+    if (nt) std::memcpy(&mesh.triangles[0].a.x, tri.data(), tri.size() * sizeof(double));
+    return mesh;
+}
+
+TriangleMesh read_mesh(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw IoError("cannot open '" + path + "' for reading");
+    return read_mesh_stream(in, path);
 }
 
 }  // namespace pcs

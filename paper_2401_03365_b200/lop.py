@@ -8,6 +8,7 @@ errors.hpp:9-53); the work is done by the sm_100a library through the C ABI
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import List, Optional, Tuple
 
@@ -31,6 +32,16 @@ class InvalidParam(Error):
 
 class EmptyMesh(Error):
     pass
+
+
+class ParseError(Error):
+    """Malformed cloud / mesh text; ``line`` is the 1-based line number (0 when
+    the error concerns the whole file), message "name:line: reason"."""
+
+    def __init__(self, name: str, line: int, reason: str):
+        super().__init__(f"{name}:{line}: {reason}")
+        self.line = line
+        self.reason = reason
 
 
 class NumericalFailure(Error):
@@ -286,6 +297,83 @@ def radius_query_all(cloud, queries, r: float, precision: str = "fp64", device: 
     _check(L.lib().pcs_radius_query_all(C.byref(d), _ptr(Cc), Cc.shape[0], _ptr(Q), m, float(r),
                                         off.ctypes.data_as(L._u64p), _ptr(idx, L._u32p), tot))
     return off, idx[:tot]
+
+
+# ---- cloud files (proj/include/pcs/io.hpp, proj/src/io.cpp) -------------------------
+_FORMATS = {"xyz": L.PCS_FMT_XYZ, "ply": L.PCS_FMT_PLY_ASCII}
+
+
+def format_from_path(path: str) -> str:
+    """'xyz' or 'ply' from the extension (case-insensitive), else InvalidParam."""
+    ext = os.path.splitext(path)[1].lower()
+    if ext in (".xyz", ".ply"):
+        return ext[1:]
+    raise InvalidParam(f"cannot infer cloud format from '{path}' (expected .xyz or .ply); "
+                       "pass the format explicitly")
+
+
+def format_cloud(cloud, fmt: str = "xyz", device: int = -1) -> bytes:
+    """write_cloud_stream (proj/src/io.cpp:277-290): the file bytes, coordinates
+    as shortest round-trip decimals, formatted on the device (one pass)."""
+    Cc = _cloud(cloud)
+    d = make_desc(LopParams(), device=device)
+    p = C.c_void_p()
+    n = C.c_uint64(0)
+    _check(L.lib().pcs_format_cloud_alloc(C.byref(d), _ptr(Cc), Cc.shape[0], _FORMATS[fmt],
+                                          C.byref(p), C.byref(n)))
+    try:
+        return C.string_at(p, n.value)
+    finally:
+        L.lib().pcs_free_buffer(p)
+
+
+def parse_cloud(text: bytes, fmt: str = "xyz", name: str = "<memory>", device: int = -1) -> np.ndarray:
+    """read_cloud_stream (proj/src/io.cpp:143-236): ``(n, 3)`` float64 points,
+    parsed on the device; ParseError(name, line, reason) like the reference."""
+    d = make_desc(LopParams(), device=device)
+    cap = len(text) // 6 + 1
+    out = np.zeros((cap, 3), dtype=np.float64)
+    n = C.c_uint64(0)
+    err = L.ParseErrorC()
+    st = L.lib().pcs_parse_cloud(C.byref(d), text, len(text), _FORMATS[fmt], _ptr(out), cap,
+                                 C.byref(n), C.byref(err))
+    if st == L.PCS_ERR_PARSE:
+        raise ParseError(name, int(err.line), err.reason.decode())
+    _check(st)
+    return out[: n.value]
+
+
+def read_cloud(path: str, fmt: Optional[str] = None, device: int = -1) -> np.ndarray:
+    fmt = fmt or format_from_path(path)
+    with open(path, "rb") as f:
+        return parse_cloud(f.read(), fmt, name=path, device=device)
+
+
+def write_cloud(cloud, path: str, fmt: Optional[str] = None, device: int = -1) -> None:
+    fmt = fmt or format_from_path(path)
+    data = format_cloud(cloud, fmt, device=device)
+    with open(path, "wb") as f:
+        f.write(data)
+
+
+def parse_mesh(text: bytes, name: str = "<memory>") -> np.ndarray:
+    """read_mesh_stream: ``(T, 3, 3)`` triangles of an ASCII PLY face element."""
+    n = C.c_uint64(0)
+    err = L.ParseErrorC()
+    st = L.lib().pcs_parse_mesh(text, len(text), None, 0, C.byref(n), C.byref(err))
+    if st == L.PCS_ERR_PARSE:
+        raise ParseError(name, int(err.line), err.reason.decode())
+    if st != L.PCS_ERR_CAPACITY:
+        _check(st)
+    out = np.zeros((max(n.value, 1), 9), dtype=np.float64)
+    _check(L.lib().pcs_parse_mesh(text, len(text), _ptr(out), n.value, C.byref(n), C.byref(err)))
+    return out[: n.value].reshape(-1, 3, 3)
+
+
+def format_double(v: float) -> str:
+    buf = C.create_string_buffer(40)
+    n = L.lib().pcs_format_double(float(v), buf)
+    return buf.raw[:n].decode()
 
 
 # ---- deviation metrics (proj/include/pcs/metrics.hpp, proj/src/metrics.cpp) ----

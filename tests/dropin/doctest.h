@@ -1,7 +1,7 @@
 // Minimal doctest-compatible test shim (our own code; the reference's vendored
 // doctest is not shipped, proj/.gitignore:2).  Supports exactly what the
-// reference's LOP tests use: TEST_CASE, CHECK, CHECK_FALSE, REQUIRE,
-// CHECK_THROWS_AS, doctest::Approx(..).epsilon(..), and
+// reference's LOP / metrics / IO tests use: TEST_CASE, CHECK, CHECK_FALSE,
+// REQUIRE, FAIL, CHECK_THROWS_AS, doctest::Approx(..).epsilon(..), and
 // DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN.  Prints one line per failed check and a
 // summary; exit status = number of failed test cases (capped at 255).
 #pragma once
@@ -52,6 +52,13 @@ inline void report(bool ok, const char* expr, const char* file, int line, bool r
     std::printf("%s:%d: FAILED %s( %s )\n", file, line, require ? "REQUIRE" : "CHECK", expr);
     if (require) throw RequireFailure{};
 }
+[[noreturn]] inline void fail_now(const char* msg, const char* file, int line) {
+    auto& r = Registry::get();
+    ++r.failed_checks;
+    r.current_failed = true;
+    std::printf("%s:%d: FAIL( %s )\n", file, line, msg);
+    throw RequireFailure{};
+}
 }  // namespace detail
 }  // namespace doctest
 
@@ -65,6 +72,7 @@ inline void report(bool ok, const char* expr, const char* file, int line, bool r
 #define CHECK(...) ::doctest::detail::report(static_cast<bool>(__VA_ARGS__), #__VA_ARGS__, __FILE__, __LINE__, false)
 #define CHECK_FALSE(...) ::doctest::detail::report(!static_cast<bool>(__VA_ARGS__), "!(" #__VA_ARGS__ ")", __FILE__, __LINE__, false)
 #define REQUIRE(...) ::doctest::detail::report(static_cast<bool>(__VA_ARGS__), #__VA_ARGS__, __FILE__, __LINE__, true)
+#define FAIL(msg) ::doctest::detail::fail_now(msg, __FILE__, __LINE__)
 #define CHECK_THROWS_AS(expr, type)                                                 \
     do {                                                                            \
         bool doctest_ok_ = false;                                                   \

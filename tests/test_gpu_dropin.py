@@ -1,5 +1,6 @@
-"""Drop-in proof: the reference's own, unmodified proj/tests/test_lop.cpp and
-proj/tests/test_metrics.cpp run against this library (GPU).
+"""Drop-in proof: the reference's own, unmodified proj/tests/test_lop.cpp,
+proj/tests/test_metrics.cpp and proj/tests/test_io.cpp run against this
+library (GPU).
 
 tests/dropin/Makefile compiles /root/reference/proj/tests/test_{lop,metrics}.cpp
 with this repo's include/pcs headers first on the include path and links
@@ -39,3 +40,10 @@ def test_reference_test_metrics_passes_unmodified():
     deviation_to_mesh (device point-triangle kernel) against the reference's own
     exhaustive oracles, fixed cases and error contracts."""
     _run("test_metrics", "11 passed | 0 failed")
+
+
+def test_reference_test_io_passes_unmodified():
+    """proj/tests/test_io.cpp: XYZ / PLY reading (device parser, host re-read of
+    bad lines), byte-stable writing (device shortest round-trip formatter),
+    meshes, format inference and file-level errors."""
+    _run("test_io", "13 passed | 0 failed")
