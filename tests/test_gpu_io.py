@@ -128,3 +128,28 @@ def test_mesh_and_format_double(pb, ref):
         pb.parse_mesh(quad.replace(b"4 0 1 2 3", b"4 0 1 2 9"))
     for v in (0.1, 1e22, 5e-324, -0.0, 123456789012345678.0):
         assert pb.format_double(v) == ref.ref_format_cloud(np.array([[v, 0, 0]]), 0).split(b" ")[0].decode()
+
+
+def test_against_reference_fixture(pb):
+    """The same checks against tests/golden/reference_io.npz (made by the
+    reference, tests/golden/make_golden_io.py) — no reference build needed."""
+    import os
+    from conftest import ROOT
+    g = np.load(os.path.join(ROOT, "tests", "golden", "reference_io.npz"))
+    X = g["cloud"]
+    assert pb.format_cloud(X, "xyz", device=0) == g["cloud_xyz"].tobytes()
+    assert pb.format_cloud(X, "ply", device=0) == g["cloud_ply"].tobytes()
+    for key in g.files:
+        if not key.endswith("_text"):
+            continue
+        base = key[: -len("_text")]
+        fmt = "xyz" if base.startswith("case_0_") else "ply"
+        text = g[key].tobytes()
+        if base + "_points" in g.files:
+            got = pb.parse_cloud(text, fmt, device=0)
+            assert np.array_equal(got.view(np.uint64), g[base + "_points"].view(np.uint64)), base
+        else:
+            with pytest.raises(pb.ParseError) as e:
+                pb.parse_cloud(text, fmt, device=0)
+            assert e.value.line == int(g[base + "_line"]), base
+            assert str(e.value) == g[base + "_msg"].tobytes().decode(), base
