@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include <cooperative_groups.h>
 
@@ -331,7 +332,44 @@ __host__ __device__ inline int32_t gx_iso(const GridGeom& g) { return (g.gx + g.
 struct MortonAxes {
     int bits[3];  // code bits per axis (after coarsening by `shift`)
     int shift;
+    int hilbert;  // 1: Hilbert index over max(bits) bits per axis, 0: Morton interleave
 };
+
+// 3-D Hilbert index of (x, y, z), B bits each (Skilling's transpose algorithm,
+// "Programming the Hilbert curve", AIP Conf. Proc. 707, 2004): undo the excess
+// rotations level by level, Gray-encode, interleave.  Consecutive indices are
+// face-adjacent cells, so runs of the order stay more compact than Z-curve runs
+// (which jump across blocks); the top 3k bits still name aligned blocks of 2^k
+// cells.
+__device__ __forceinline__ uint32_t hilbert3(uint32_t x, uint32_t y, uint32_t z, int B) {
+    uint32_t X[3] = {x, y, z};
+    const uint32_t M = 1u << (B - 1);
+    for (uint32_t Q = M; Q > 1; Q >>= 1) {
+        const uint32_t P = Q - 1;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            if (X[i] & Q) {
+                X[0] ^= P;
+            } else {
+                const uint32_t t = (X[0] ^ X[i]) & P;
+                X[0] ^= t;
+                X[i] ^= t;
+            }
+        }
+    }
+    X[1] ^= X[0];
+    X[2] ^= X[1];
+    uint32_t t = 0;
+    for (uint32_t Q = M; Q > 1; Q >>= 1)
+        if (X[2] & Q) t ^= Q - 1;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) X[i] ^= t;
+    uint32_t key = 0;
+    for (int b = B - 1; b >= 0; --b)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) key = (key << 1) | ((X[i] >> b) & 1u);
+    return key;
+}
 
 __device__ __forceinline__ uint32_t half_cell(double x, double o, double inv2, int32_t g2) {
     const double u = floor((x - o) * inv2);
@@ -354,10 +392,14 @@ __global__ void morton_keys_kernel(const V* __restrict__ pts, uint32_t n, GridGe
                                half_cell((double)p.y, g.oy, inv2, 2 * g.gy) >> ax.shift,
                                half_cell((double)p.z, g.oz, inv2, 2 * g.gz) >> ax.shift};
         uint32_t key = 0;
-        for (int l = top - 1; l >= 0; --l)
+        if (ax.hilbert) {
+            key = top > 0 ? hilbert3(f[0], f[1], f[2], top) : 0u;
+        } else {
+            for (int l = top - 1; l >= 0; --l)
 #pragma unroll
-            for (int a = 2; a >= 0; --a)
-                if (l < ax.bits[a]) key = (key << 1) | ((f[a] >> l) & 1u);
+                for (int a = 2; a >= 0; --a)
+                    if (l < ax.bits[a]) key = (key << 1) | ((f[a] >> l) & 1u);
+        }
         if (sidx) {
             const uint32_t o = sidx[i];
             if (o < lo || o >= hi) key |= owner_bit;  // not owned: after the owned queries
@@ -639,6 +681,15 @@ int build_query_list(const V* sorted_pts, uint32_t n, const GridGeom& g, double 
         ax.bits[a] = std::max(0, full[a] - ax.shift);
         mbits += ax.bits[a];
     }
+    // query curve: Hilbert (measured tighter groups than the Z-curve) unless the
+    // developer knob PCSB_CURVE=morton
+    static const int hilbert = [] {
+        const char* e = std::getenv("PCSB_CURVE");
+        return (e && std::string(e) == "morton") ? 0 : 1;
+    }();
+    ax.hilbert = hilbert;
+    const int hb = std::max(ax.bits[0], std::max(ax.bits[1], ax.bits[2]));
+    if (ax.hilbert) mbits = 3 * hb;
     // Morton blocks of side ~2 support: 2^k code units per axis (measured best on
     // the height-field config: fuller groups outweigh their larger boxes)
     const double unit = 0.5 * g.cs * std::ldexp(1.0, ax.shift);
@@ -646,7 +697,9 @@ int build_query_list(const V* sorted_pts, uint32_t n, const GridGeom& g, double 
     if (const char* e = std::getenv("PCSB_BLOCK_ADJ")) k += std::atoi(e);  // developer knob
     k = std::max(0, std::min(k, 10));
     *block_shift = 0;
-    for (int a = 0; a < 3; ++a) *block_shift += std::min(k, ax.bits[a]);
+    if (ax.hilbert) *block_shift = 3 * std::min(k, hb);
+    else
+        for (int a = 0; a < 3; ++a) *block_shift += std::min(k, ax.bits[a]);
     if (!n) return 0;
     // the ownership flag sits right above the Morton code, inside the sorted bits
     morton_keys_kernel<V><<<grid_for(n, 256), 256, 0, s>>>(sorted_pts, n, g, ax, sorted_idx, own_lo,
