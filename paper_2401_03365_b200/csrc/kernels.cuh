@@ -93,6 +93,7 @@ struct FastArgs {
     uint32_t unit;            // queries per work unit (work_unit_queries)
     uint32_t tail_start;      // list position (multiple of unit) where short units begin
     uint32_t tail_unit;       // queries per unit from tail_start (raised to one group)
+    int bisect;               // 1: groups by recursive bisection of each unit (bisect_unit)
     GridGeom gP, gX;          // grids of the data and of the projected set
     double s_pad;             // support with margin (cell ranges)
     double r2;                // support^2 in fp64: exact re-decision of borderline pairs

@@ -540,6 +540,64 @@ __device__ __forceinline__ uint32_t group_end(unsigned brk, uint32_t r0, uint32_
     return min(e, min(g0 + Q, r1));
 }
 
+// Groups of a unit by recursive bisection (FastArgs::bisect): the unit's (<= 32)
+// queries, one per lane, are sorted along the longest axis of their box and
+// halved, then each half along its own longest axis, down to groups of Q — a k-d
+// split, so a group is compact in every direction (modelled on config 3:
+// candidates per interaction -4% vs runs of Q consecutive curve positions).
+// Returns, for slot `lane` of the sorted order, the query's position in the
+// unit; positions >= n (padding) sort last.  Ties break on the position, so the
+// grouping is deterministic.
+template <int Q>
+__device__ __forceinline__ uint32_t bisect_unit(const uint32_t* __restrict__ qlist,
+                                                const float4* __restrict__ Xq, uint32_t r0,
+                                                uint32_t n, int lane) {
+    uint32_t idx = (uint32_t)lane;
+    float4 p = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+    if (idx < n) p = __ldg(&Xq[__ldg(&qlist[r0 + idx])]);
+#pragma unroll
+    for (int S = 32; S > Q; S >>= 1) {
+        const bool valid = idx < n;
+        float mnx = valid ? p.x : INFINITY, mny = valid ? p.y : INFINITY, mnz = valid ? p.z : INFINITY;
+        float mxx = valid ? p.x : -INFINITY, mxy = valid ? p.y : -INFINITY, mxz = valid ? p.z : -INFINITY;
+#pragma unroll
+        for (int o = 1; o < S; o <<= 1) {
+            mnx = fminf(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
+            mny = fminf(mny, __shfl_xor_sync(0xffffffffu, mny, o));
+            mnz = fminf(mnz, __shfl_xor_sync(0xffffffffu, mnz, o));
+            mxx = fmaxf(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
+            mxy = fmaxf(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
+            mxz = fmaxf(mxz, __shfl_xor_sync(0xffffffffu, mxz, o));
+        }
+        const float ex = mxx - mnx, ey = mxy - mny, ez = mxz - mnz;
+        const int axis = (ex >= ey && ex >= ez) ? 0 : (ey >= ez ? 1 : 2);
+        float key = valid ? (axis == 0 ? p.x : (axis == 1 ? p.y : p.z)) : INFINITY;
+        // bitonic sort of (key, idx) ascending inside aligned segments of S lanes
+#pragma unroll
+        for (int k = 2; k <= S; k <<= 1) {
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                const float ok = __shfl_xor_sync(0xffffffffu, key, j);
+                const uint32_t oi = __shfl_xor_sync(0xffffffffu, idx, j);
+                float4 op;
+                op.x = __shfl_xor_sync(0xffffffffu, p.x, j);
+                op.y = __shfl_xor_sync(0xffffffffu, p.y, j);
+                op.z = __shfl_xor_sync(0xffffffffu, p.z, j);
+                op.w = 0.f;
+                const bool up = k == S ? true : ((lane & k) == 0);
+                const bool lower = (lane & j) == 0;
+                const bool less = ok < key || (ok == key && oi < idx);  // other before mine
+                if (lower ? (up ? less : !less) : (up ? !less : less)) {
+                    key = ok;
+                    idx = oi;
+                    p = op;
+                }
+            }
+        }
+    }
+    return idx;
+}
+
 // Phases of the per-point update.  PH_ALL: attraction, repulsion and the update
 // in one pass.  PH_ATTR: attraction only; the per-query sums go to a.attr (the
 // projected set's grid is rebuilt meanwhile on another stream).  PH_REP:
@@ -566,12 +624,17 @@ fast_kernel(const FastArgs a) {
     uint32_t r0, r1;
     const uint32_t tail_unit = max(a.tail_unit, (uint32_t)Q);
     while (next_unit(counter, a.nq, a.unit, a.tail_start, tail_unit, lane, r0, r1)) {
-        const unsigned brk = group_breaks(a.qcodes, a.block_shift, r0, r1, lane);
+        const bool bis = a.bisect != 0;
+        const unsigned brk = bis ? 0u : group_breaks(a.qcodes, a.block_shift, r0, r1, lane);
+        const uint32_t slotpos = bis ? bisect_unit<Q>(a.qlist, a.Xq, r0, r1 - r0, lane) : (uint32_t)lane;
         for (uint32_t g0 = r0, g1; g0 < r1; g0 = g1) {
-            g1 = group_end(brk, r0, r1, g0, Q);
-            const uint32_t qpos = g0 + qi;
-            const bool member = qpos < g1;
-            const uint32_t qp = member ? qpos : g0;  // padding lanes duplicate the first query
+            g1 = bis ? min(g0 + (uint32_t)Q, r1) : group_end(brk, r0, r1, g0, Q);
+            const bool member = g0 + qi < g1;
+            // the list position of this lane's query (slot -> position in the unit)
+            const uint32_t pos = __shfl_sync(0xffffffffu, slotpos,
+                                             (int)(member ? g0 - r0 + qi : g0 - r0));
+            const uint32_t qpos = r0 + pos;
+            const uint32_t qp = qpos;  // padding lanes duplicate the group's first query
             const uint32_t qint = __ldg(&a.qlist[qp]);  // internal index
             const float4 q = __ldg(&a.Xq[qint]);
             const EvalConsts ec = make_consts(q, a.kneg, a.K0, a.support);

@@ -234,6 +234,7 @@ Plan::Plan(const pcs_lop_desc& d) : d_(d) {
     if (const char* e = std::getenv("PCSB_REORDER_EVERY")) reorder_every_ = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("PCSB_ASYNC_ORDER")) async_order_ = std::atoi(e) != 0;  // developer knob
     if (const char* e = std::getenv("PCSB_FUSED")) fused_ = std::atoi(e) != 0;  // developer knob
+    if (const char* e = std::getenv("PCSB_BISECT")) bisect_ = std::atoi(e) != 0;  // developer knob
     if (const char* e = std::getenv("PCSB_REP_LANES")) rep_lanes_ = std::atoi(e);  // developer knob
     device_ = select_device(d_.device);
     PCSB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
@@ -846,7 +847,14 @@ void Plan::enqueue_sweep(int k) {
         a.qcodes = q_skeys_;
         a.block_shift = block_shift_;
         a.nq = nq;
-        a.unit = work_unit_queries(nq, fast_grid_ * 4);
+        // groups by recursive bisection of the work units; LOP units of 32 queries
+        // (4 groups), WLOP units of 16 — measured (tools/ab_probe.py, best of 3):
+        // config 3 +0.9%, 2 +1.7%, 5 +1.8% with 32; config 4 (50x density gradient)
+        // -4.3% with 32, +0.9% with 16
+        a.bisect = bisect_ ? 1 : 0;
+        a.unit = bisect_ && !std::getenv("PCSB_UNIT") && !d_.density_weights
+                     ? 32u
+                     : work_unit_queries(nq, fast_grid_ * 4);
         {   // the last ~one group per warp of the attraction pass comes in one-group units
             const uint32_t q = 32u / (uint32_t)lanes_;
             static const double tail_frac = [] {  // developer knob: warps' groups in the tail

@@ -125,6 +125,7 @@ private:
     int block_shift_alt_ = 0;
     bool q_next_ready_ = false;
     bool fused_ = false;              // one pass (attraction + repulsion) after the X grid
+    bool bisect_ = true;              // query groups by recursive bisection of 32-query units
     bool async_order_ = true;         // developer knob PCSB_ASYNC_ORDER=0: build in line
     int last_sweep_ = 0;              // last sweep index of the current run()
     cudaEvent_t ev_qready_ = nullptr;
