@@ -851,8 +851,14 @@ void Plan::enqueue_sweep(int k) {
         // (4 groups), WLOP units of 16 — measured (tools/ab_probe.py, best of 3):
         // config 3 +0.9%, 2 +1.7%, 5 +1.8% with 32; config 4 (50x density gradient)
         // -4.3% with 32, +0.9% with 16
-        a.bisect = bisect_ ? 1 : 0;
-        a.unit = bisect_ && !std::getenv("PCSB_UNIT") && !d_.density_weights
+        // Sharded plans keep runs of consecutive curve positions cut at curve
+        // blocks: a rank's queries are a slab of the projected set, where
+        // consecutive positions of the whole domain's curve can lie far apart, and
+        // a 32-query unit spanning two such pieces bisects into straddling groups
+        // (emulated 8-rank sweep: slowest rank 1.03 ms bisected vs 0.72 ms cut).
+        const bool bis = bisect_ && !multi;
+        a.bisect = bis ? 1 : 0;
+        a.unit = bis && !std::getenv("PCSB_UNIT") && !d_.density_weights
                      ? 32u
                      : work_unit_queries(nq, fast_grid_ * 4);
         {   // the last ~one group per warp of the attraction pass comes in one-group units
