@@ -21,6 +21,8 @@
 // and reason.  PLY headers, meshes and every PLY anomaly (short files, header
 // errors) take the host path, which implements the complete format.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include <algorithm>
 #include <cctype>
@@ -482,7 +484,7 @@ DevParse device_parse(const char* t, uint64_t len, bool ply, int ntok, int ix, i
     uint64_t* starts = mem.get<uint64_t>(len);
     uint64_t* nsel = mem.get<uint64_t>(2);
     auto select = [&](const uint8_t* f, uint64_t n, uint64_t* outsel, uint64_t* count) {
-        cub::CountingInputIterator<uint64_t> it(0);
+        thrust::counting_iterator<uint64_t> it(0);
         size_t bytes = 0;
         PCSB_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, f, outsel, count, (int64_t)n, st.s));
         void* tmp = mem.get<uint8_t>(bytes);
@@ -512,9 +514,9 @@ DevParse device_parse(const char* t, uint64_t len, bool ply, int ntok, int ix, i
     HostLine* hl = mem.get<HostLine>(nl);
     {
         uint8_t* f2 = flag;  // nl <= len
-        cub::TransformInputIterator<uint8_t, IsHost, const uint8_t*> fi(dst, IsHost());
+        thrust::transform_iterator<IsHost, const uint8_t*> fi(dst, IsHost());
         size_t bytes = 0;
-        cub::CountingInputIterator<uint64_t> it(0);
+        thrust::counting_iterator<uint64_t> it(0);
         (void)f2;
         PCSB_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, fi, hsel, nsel + 1, (int64_t)nl, st.s));
         void* tmp = mem.get<uint8_t>(bytes);
