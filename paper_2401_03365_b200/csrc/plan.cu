@@ -96,11 +96,13 @@ GridGeom make_grid(const double lo_in[3], const double hi_in[3], double support)
     }
     const int sb = 0;
     // finer cells along x (rows are unchanged; x-trimming gets tighter) while the
-    // table stays within 2^27 cells.  Measured sweep time, xsub 1 -> 2 -> 4:
-    // config 3 -2.6%, config 4 -11% / -19%, config 5 -5% / -3%.
+    // table stays within 2^30 cells (4 GB; built once, HBM is 180 GB).  Measured
+    // sweep time, xsub 1 -> 2 -> 4: config 3 -2.6%, config 4 -11% / -19%,
+    // config 5 -5% / -3%; then (sweeps/s, best of 3) 4 -> 8: config 3 +1.3%,
+    // 4 +1.2%, 5 +3.6%, 2 -0.4%; 8 -> 16: config 3 +0.6%.
     int xsub = 1;
-    for (int t : {4, 2})
-        if (cells_for(lo, hi, cs) * t <= (double)(1u << 27)) {
+    for (int t : {16, 8, 4, 2})
+        if (cells_for(lo, hi, cs) * t <= (double)(1u << 30)) {
             xsub = t;
             break;
         }
