@@ -140,9 +140,17 @@ GridGeom make_grid_scaled(const double lo_in[3], const double hi_in[3], double s
     GridGeom g = base;
     g.cs = base.cs * scale;
     g.inv_cs = 1.0 / g.cs;
+    // x cells 4x finer than y/z while the per-sweep table stays within 2^27 cells
+    // (measured vs 1x, best of 3: config 3 +1.1%, 4 +1.2%, 5 +1.3%, 2 -1.3%)
     g.xsub = 1;
-    g.csx = g.cs;
-    g.inv_csx = g.inv_cs;
+    for (int t : {4, 2})
+        if (cells_for(lo, hi, g.cs) * t <= (double)(1u << 27)) {
+            g.xsub = t;
+            break;
+        }
+    if (const char* e = std::getenv("PCSB_XSUB_X")) g.xsub = std::max(1, std::atoi(e));  // developer knob
+    g.csx = g.cs / g.xsub;
+    g.inv_csx = 1.0 / g.csx;
     g.ox = lo[0] - g.cs;
     g.oy = lo[1] - g.cs;
     g.oz = lo[2] - g.cs;
