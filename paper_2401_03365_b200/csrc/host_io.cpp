@@ -71,6 +71,39 @@ void h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     PCSB_CUDA(cudaEventSynchronize(st.done[(k - 1) & 1]));
 }
 
+void h2d_staged_f32x4(void* dst_float4, const double* xyz, size_t n, float w, cudaStream_t s) {
+    if (!n) return;
+    Staging& st = staging();
+    std::lock_guard<std::mutex> lock(st.mu);
+    if (!st.ready) {
+        for (int i = 0; i < 2; ++i) {
+            PCSB_CUDA(cudaHostAlloc((void**)&st.buf[i], kChunk, cudaHostAllocPortable));
+            PCSB_CUDA(cudaEventCreateWithFlags(&st.done[i], cudaEventDisableTiming));
+        }
+        st.ready = true;
+    }
+    const int threads = std::max(1, std::min(8, omp_get_num_procs()));
+    const size_t per_chunk = kChunk / (4 * sizeof(float));
+    char* out = static_cast<char*>(dst_float4);
+    size_t k = 0;
+    for (size_t p0 = 0; p0 < n; p0 += per_chunk, ++k) {
+        const size_t np = std::min(per_chunk, n - p0);
+        float* b = reinterpret_cast<float*>(st.buf[k & 1]);
+        PCSB_CUDA(cudaEventSynchronize(st.done[k & 1]));
+#pragma omp parallel for num_threads(threads) schedule(static)
+        for (long long i = 0; i < (long long)np; ++i) {
+            const double* q = xyz + 3 * (p0 + (size_t)i);
+            b[4 * i] = (float)q[0];
+            b[4 * i + 1] = (float)q[1];
+            b[4 * i + 2] = (float)q[2];
+            b[4 * i + 3] = w;
+        }
+        PCSB_CUDA(cudaMemcpyAsync(out + p0 * 16, b, np * 16, cudaMemcpyHostToDevice, s));
+        PCSB_CUDA(cudaEventRecord(st.done[k & 1], s));
+    }
+    PCSB_CUDA(cudaEventSynchronize(st.done[(k - 1) & 1]));
+}
+
 void d2h_staged(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     if (!bytes) return;
     if (bytes < (2u << 20)) {

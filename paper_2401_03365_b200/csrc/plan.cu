@@ -394,15 +394,21 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     double *dP = nullptr, *dX0 = nullptr;
     V *Pv = nullptr, *X0v = nullptr;
     uint32_t *tk = nullptr, *tsk = nullptr;
-    dP = (decltype(dP))talloc(n * 3 * sizeof(double));
-    dX0 = (decltype(dX0))talloc((m ? m : 1) * 3 * sizeof(double));
     Pv = (decltype(Pv))talloc(n * sizeof(V));
     X0v = (decltype(X0v))talloc((m ? m : 1) * sizeof(V));
-    h2d_staged(dP, P, n * 3 * sizeof(double), stream_);
-    if (m) h2d_staged(dX0, X0, m * 3 * sizeof(double), stream_);
-    launch_convert_xyz<T>(dP, Pv, n, (T)1, stream_);
-    launch_convert_xyz<T>(dX0, X0v, m, (T)0, stream_);
-    launches_ += 2;
+    if (sizeof(T) == 4) {
+        // fp32 plans: rounded to fp32 while staging (16 instead of 24 bytes a point)
+        h2d_staged_f32x4(Pv, P, n, 1.0f, stream_);
+        h2d_staged_f32x4(X0v, X0, m, 0.0f, stream_);
+    } else {
+        dP = (decltype(dP))talloc(n * 3 * sizeof(double));
+        dX0 = (decltype(dX0))talloc((m ? m : 1) * 3 * sizeof(double));
+        h2d_staged(dP, P, n * 3 * sizeof(double), stream_);
+        if (m) h2d_staged(dX0, X0, m * 3 * sizeof(double), stream_);
+        launch_convert_xyz<T>(dP, Pv, n, (T)1, stream_);
+        launch_convert_xyz<T>(dX0, X0v, m, (T)0, stream_);
+        launches_ += 2;
+    }
 
     bbox_slots_ = (unsigned long long*)dalloc(8 * sizeof(unsigned long long));
     init_bbox_slots(bbox_slots_, stream_);
@@ -626,8 +632,8 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     RunState hs;
     PCSB_CUDA(cudaMemcpy(&hs, st_, sizeof(hs), cudaMemcpyDeviceToHost));
     setup_density_pairs_ = hs.density_pairs;
-    tfree(dP);
-    tfree(dX0);
+    if (dP) tfree(dP);
+    if (dX0) tfree(dX0);
     tfree(Pv);
     tfree(X0v);
     tfree(tk);
