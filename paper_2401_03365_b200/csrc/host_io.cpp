@@ -9,6 +9,7 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -26,6 +27,16 @@ struct Staging {
     cudaEvent_t done[2] = {nullptr, nullptr};
     bool ready = false;
 };
+
+// host threads filling / draining the pinned chunks (developer knob PCSB_IO_THREADS)
+int staging_threads() {
+    static const int t = [] {
+        const char* e = std::getenv("PCSB_IO_THREADS");
+        const int v = e ? std::atoi(e) : 16;  // e2e (config 3): 8 -> 16 threads +3%
+        return std::max(1, std::min(v, omp_get_num_procs()));
+    }();
+    return t;
+}
 
 Staging& staging() {
     static Staging s;  // never freed: pinned memory lives as long as the process
@@ -48,7 +59,7 @@ void h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t s) {
         }
         st.ready = true;
     }
-    const int threads = std::max(1, std::min(8, omp_get_num_procs()));
+    const int threads = staging_threads();
     const char* in = static_cast<const char*>(src);
     char* out = static_cast<char*>(dst);
     size_t k = 0;
@@ -82,7 +93,7 @@ void h2d_staged_f32x4(void* dst_float4, const double* xyz, size_t n, float w, cu
         }
         st.ready = true;
     }
-    const int threads = std::max(1, std::min(8, omp_get_num_procs()));
+    const int threads = staging_threads();
     const size_t per_chunk = kChunk / (4 * sizeof(float));
     char* out = static_cast<char*>(dst_float4);
     size_t k = 0;
@@ -120,7 +131,7 @@ void d2h_staged(void* dst, const void* src, size_t bytes, cudaStream_t s) {
         }
         st.ready = true;
     }
-    const int threads = std::max(1, std::min(8, omp_get_num_procs()));
+    const int threads = staging_threads();
     const char* in = static_cast<const char*>(src);
     char* out = static_cast<char*>(dst);
     const size_t nchunks = (bytes + kChunk - 1) / kChunk;
