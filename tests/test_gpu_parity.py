@@ -360,3 +360,31 @@ def test_mu0_skips_projected_grid_but_matches(pb, orc):
                         eta=orc.ETA_INV_CUBE, store_f32=True)
     assert s.interactions_attr == r.interactions_attr and s.interactions_rep == 0
     assert np.abs(out - r.points).max() <= 1e-5 * bbox_diag(P)
+
+
+@pytest.mark.parametrize("shape", ["line", "plane_grid", "clustered"])
+def test_fp32_degenerate_geometry_exact_neighbours(pb, orc, shape):
+    """Degenerate clouds through the fp32 plan (Hilbert order, bisected groups,
+    zero-extent axes, ties in every sort key): one sweep has the oracle's
+    neighbour sets exactly and agrees to fp32 rounding."""
+    rng = np.random.default_rng(41)
+    if shape == "line":
+        P = np.zeros((4000, 3))
+        P[:, 0] = rng.uniform(-1, 1, 4000)
+    elif shape == "plane_grid":
+        g = np.arange(60) * 0.02
+        P = np.stack(np.meshgrid(g, g, [0.5]), -1).reshape(-1, 3)
+    else:  # a few tight clusters with many coincident points
+        c = rng.uniform(-1, 1, (6, 3))
+        P = np.repeat(c, 500, axis=0) + rng.normal(scale=0.01, size=(3000, 3))
+        P[::7] = P[1::7]
+    P = r32(P)
+    X0 = P[rng.choice(P.shape[0], P.shape[0] // 10, replace=False)]
+    prm, c = pb.config_params(3, h=0.06)
+    prm.iterations = 1
+    out, s = pb.lop_project(P, X0, prm, eta=c["eta"], precision="fp32")
+    r = orc.lop_project(P, X0, prm.kernel.h, prm.kernel.cutoff_multiple, prm.mu, 1,
+                        eta=orc.ETA_NEG_LINEAR, store_f32=True)
+    assert (s.interactions_attr, s.interactions_rep) == (r.interactions_attr, r.interactions_rep)
+    assert (s.isolated_events, s.coincident_pairs) == (r.isolated_events, r.coincident_pairs)
+    assert np.abs(out - r.points).max() <= 4 * np.finfo(F32).eps * max(np.abs(P).max(), 1.0)
