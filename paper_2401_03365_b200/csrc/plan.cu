@@ -240,7 +240,7 @@ Plan::Plan(const pcs_lop_desc& d) : d_(d) {
     lanes_ = d_.lanes_per_point ? d_.lanes_per_point : 4;
     // repulsion over the sparser projected set: 16-query groups amortise the
     // per-row cost better (measured -1..2% sweep time on configs 3 and 4)
-    rep_lanes_ = d_.lanes_per_point ? lanes_ : 2;
+    rep_lanes_ = d_.lanes_per_point ? lanes_ : 4;  // measured with bisected groups: 4 >= 2 on configs 3, 4, 5
     if (const char* e = std::getenv("PCSB_REORDER_EVERY")) reorder_every_ = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("PCSB_ASYNC_ORDER")) async_order_ = std::atoi(e) != 0;  // developer knob
     if (const char* e = std::getenv("PCSB_FUSED")) fused_ = std::atoi(e) != 0;  // developer knob
