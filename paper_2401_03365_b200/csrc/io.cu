@@ -270,6 +270,10 @@ __device__ __forceinline__ LineSpan line_span(const char* t, uint64_t len, const
     return {b, e};
 }
 
+struct Widen {
+    __host__ __device__ __forceinline__ uint64_t operator()(uint8_t v) const { return v; }
+};
+
 struct IsHost {
     __host__ __device__ __forceinline__ uint8_t operator()(uint8_t s) const { return s == 2 ? 1 : 0; }
 };
@@ -481,8 +485,19 @@ DevParse device_parse(const char* t, uint64_t len, bool ply, int ntok, int ix, i
     uint8_t* flag = mem.get<uint8_t>(len);
     line_flag_kernel<<<grid_of(len), IO_THREADS, 0, st.s>>>(dt, len, flag);
     PCSB_CUDA(cudaGetLastError());
-    uint64_t* starts = mem.get<uint64_t>(len);
     uint64_t* nsel = mem.get<uint64_t>(2);
+    // count the lines first, so the start table is sized by lines, not bytes
+    {
+        thrust::transform_iterator<Widen, const uint8_t*> wf(flag, Widen());
+        size_t bytes = 0;
+        PCSB_CUDA(cub::DeviceReduce::Sum(nullptr, bytes, wf, nsel, (int64_t)len, st.s));
+        void* tmp = mem.get<uint8_t>(bytes);
+        PCSB_CUDA(cub::DeviceReduce::Sum(tmp, bytes, wf, nsel, (int64_t)len, st.s));
+    }
+    uint64_t nl_count = 0;
+    PCSB_CUDA(cudaMemcpyAsync(&nl_count, nsel, sizeof(uint64_t), cudaMemcpyDeviceToHost, st.s));
+    PCSB_CUDA(cudaStreamSynchronize(st.s));
+    uint64_t* starts = mem.get<uint64_t>(nl_count + 1);
     auto select = [&](const uint8_t* f, uint64_t n, uint64_t* outsel, uint64_t* count) {
         thrust::counting_iterator<uint64_t> it(0);
         size_t bytes = 0;
