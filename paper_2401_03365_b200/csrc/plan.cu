@@ -79,11 +79,14 @@ GridGeom make_grid(const double lo_in[3], const double hi_in[3], double support)
     double cs;
     // y/z cell side s/3 (measured sweeps/s vs s/4, with x cells up to 4x finer:
     // config 3 +3.3%, config 4 +5%, config 5 +11%; s/5 similar on config 3,
-    // worse on config 2), up to 2^28 cells (a 1 GB table); then s/2 (config 5
-    // at h = 0.01); then s
-    if (cells_for(lo, hi, support / 3.0) <= (double)(1u << 28)) {
+    // worse on config 2) when x cells 4x finer still fit the 2^30-cell table;
+    // else 0.4 s, else s/2 — x subdivision is worth more than finer y/z (config
+    // 5 at h = 0.01: 0.4 s with finer x +9% over s/3); then s
+    if (cells_for(lo, hi, support / 3.0) * 4 <= (double)(1u << 30)) {
         cs = support / 3.0;
-    } else if (cells_for(lo, hi, support * 0.5) <= (double)(1u << 28)) {
+    } else if (cells_for(lo, hi, support * 0.4) * 4 <= (double)(1u << 30)) {
+        cs = support * 0.4;
+    } else if (cells_for(lo, hi, support * 0.5) <= (double)(1u << 29)) {
         cs = support * 0.5;
     } else {
         cs = support;
@@ -92,7 +95,7 @@ GridGeom make_grid(const double lo_in[3], const double hi_in[3], double support)
     // developer knob (grid experiments): PCSB_CELL_FRAC = cell side / support
     if (const char* e = std::getenv("PCSB_CELL_FRAC")) {
         const double f = std::atof(e);
-        if (f > 0.0 && cells_for(lo, hi, support * f) <= (double)(1u << 28)) cs = support * f;
+        if (f > 0.0 && cells_for(lo, hi, support * f) <= (double)(1u << 30)) cs = support * f;
     }
     const int sb = 0;
     // finer cells along x (rows are unchanged; x-trimming gets tighter) while the
