@@ -4,18 +4,18 @@
 // (attraction :49-65, isolation/anchor :67-75, Weiszfeld quotient :77,
 // repulsion :79-97), with one persistent warp-cooperative kernel:
 //
-//  * Work unit = a RUN of the cell-sorted query list (consecutive queries in one
-//    grid row, x cells at most one apart; build_runs), fetched by an atomic
-//    counter so density imbalance self-schedules.  A warp walks its run in
-//    GROUPS of Q = 32/L queries (L lanes per query): a group's bounding box is
-//    a couple of cells wide at most.
-//  * Candidates: the cell rows (fixed y, z) that can hold a point within the
-//    support of the box, each trimmed to the x-interval allowed by the row's
-//    distance to the box (a per-row Minkowski sum of box and ball — no
-//    per-candidate cull).  Each row is one contiguous run of the sorted array;
-//    runs are streamed back to back with cp.async (4-byte copies straight into a
-//    pair-interleaved, bank-swizzled layout) into one half of a per-warp double
-//    buffer while the other half is evaluated.
+//  * Work unit = 16 (or 32) consecutive queries of the Hilbert-ordered query list
+//    (build_query_list), fetched by an atomic counter so density imbalance
+//    self-schedules; the pass ends on one-group units.  A warp splits its unit
+//    into GROUPS of Q = 32/L queries (L lanes per query): runs of the curve cut
+//    at curve blocks, or (single-GPU LOP) a recursive bisection of the unit
+//    along the longest axis (bisect_unit) — either way a compact box.
+//  * Candidates: the cell rows (fixed y, z) within the support of the box, each
+//    trimmed in x to the union of the group's queries' ball chords through the
+//    row (row_range; no per-candidate cull).  Each row is one contiguous range
+//    of 32-byte pair records; a warp streams its rows back to back into one half
+//    of a per-warp double buffer with one cp.async.bulk (TMA) per row piece
+//    while the other half is evaluated.
 //  * Evaluation: two candidates per lane with packed fp32x2 (FADD2/FMUL2/FFMA2),
 //    theta on MUFU.EX2, 1/d on MUFU.RSQ, predicated accumulation of
 //    sum w (c - q) relative to the query (fp32 error ~ support, not ~ |x|).
