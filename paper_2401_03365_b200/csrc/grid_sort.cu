@@ -11,6 +11,7 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "host_io.h"
 #include "kernels.cuh"
 
 namespace pcsb {
@@ -126,7 +127,7 @@ rs_hist_kernel(const uint32_t* __restrict__ keys, uint32_t n, int shift, uint32_
 // Exclusive scan of the digit-major block histograms, one block per digit row
 // (row d = the counts of digit d in every tile); the row totals land in
 // `totals` and are scanned by rs_scan_totals_kernel.
-constexpr int RS_ROW_THREADS = 256;
+constexpr int RS_ROW_THREADS = 1024;
 
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* sh, uint32_t* total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -160,13 +161,15 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
 __device__ __forceinline__ void scan_row(uint32_t* __restrict__ a, uint32_t ntiles,
                                          uint32_t* __restrict__ totals, uint32_t d, uint32_t* sh) {
     uint32_t* row = a + (size_t)d * ntiles;
-    const uint32_t chunk = (ntiles + RS_ROW_THREADS - 1) / RS_ROW_THREADS;
-    const uint32_t b = threadIdx.x * chunk;
+    const uint32_t chunk = (ntiles + blockDim.x - 1) / blockDim.x;
+    const uint32_t b = min(threadIdx.x * chunk, ntiles);
     const uint32_t e = min(b + chunk, ntiles);
     uint32_t s = 0;
+#pragma unroll 8
     for (uint32_t i = b; i < e; ++i) s += row[i];
     uint32_t tot = 0;
     uint32_t run = block_exclusive_scan(s, sh, &tot);
+#pragma unroll 8
     for (uint32_t i = b; i < e; ++i) {
         const uint32_t v = row[i];
         row[i] = run;
@@ -411,8 +414,10 @@ __global__ void morton_keys_kernel(const V* __restrict__ pts, uint32_t n, GridGe
 // ---- cell table: start[c] = #points with cell < c = a prefix maximum of marks ----
 // mark: for every boundary between two consecutive sorted points (and after the
 // last), start[cell(k) + 1] = k + 1; all other entries 0; then an inclusive
-// prefix-max over [0, ncells] fills every empty cell with the next start.  Work
-// is O(points + cells) in coalesced passes (no per-gap loops).
+// prefix-max over [0, ncells] fills every empty cell with the next start.  The
+// prefix entering each 4096-entry tile comes from a binary search over the keys
+// (cell_tile_prefix_kernel), so the table is read and written once after the
+// marks, through shared memory, in coalesced 16-byte accesses.
 constexpr int CS_THREADS = 256;
 constexpr int CS_ITEMS = 16;
 constexpr int CS_TILE = CS_THREADS * CS_ITEMS;
@@ -426,47 +431,28 @@ __global__ void cell_mark_kernel(const uint32_t* __restrict__ skeys, uint32_t n,
     }
 }
 
-__global__ void __launch_bounds__(CS_THREADS)
-cell_tile_max_kernel(const uint32_t* __restrict__ a, uint32_t count, uint32_t* __restrict__ tmax,
-                     const uint32_t* done) {
+// exclusive prefix max of the marks before each tile, without reading the table:
+// marks grow with the cell index (the keys are sorted), so the maximum over the
+// entries before tile b (indices <= T - 1, T = b * CS_TILE) is start[T - 1] =
+// #points with cell < T - 1, one binary search over the sorted keys per tile
+__global__ void cell_tile_prefix_kernel(const uint32_t* __restrict__ skeys, uint32_t n,
+                                        int sub_shift, uint32_t ntiles,
+                                        uint32_t* __restrict__ tprefix, const uint32_t* done) {
     if (done && *done) return;
-    __shared__ uint32_t sh[CS_THREADS / 32];
-    const size_t base = (size_t)blockIdx.x * CS_TILE;
-    uint32_t v = 0;
-#pragma unroll
-    for (int i = 0; i < CS_ITEMS; ++i) {
-        const size_t j = base + (size_t)i * CS_THREADS + threadIdx.x;
-        if (j < count) v = max(v, a[j]);
+    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= ntiles) return;
+    if (b == 0) {
+        tprefix[0] = 0;
+        return;
     }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t r = 0;
-        for (int w = 0; w < CS_THREADS / 32; ++w) r = max(r, sh[w]);
-        tmax[blockIdx.x] = r;
+    const uint32_t target = b * (uint32_t)CS_TILE - 1;
+    uint32_t lo = 0, hi = n;  // first k with cell(k) >= target
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if ((skeys[mid] >> sub_shift) < target) lo = mid + 1;
+        else hi = mid;
     }
-}
-
-// exclusive prefix max of the tile maxima (one block)
-__global__ void __launch_bounds__(CS_THREADS)
-cell_tiles_scan_kernel(uint32_t* __restrict__ tmax, uint32_t ntiles, const uint32_t* done) {
-    if (done && *done) return;
-    __shared__ uint32_t sh[CS_THREADS];
-    const uint32_t per = (ntiles + CS_THREADS - 1) / CS_THREADS;
-    const uint32_t b = threadIdx.x * per, e = min(b + per, ntiles);
-    uint32_t m = 0;
-    for (uint32_t i = b; i < e; ++i) m = max(m, tmax[i]);
-    sh[threadIdx.x] = m;
-    __syncthreads();
-    uint32_t run = 0;  // exclusive over the preceding threads
-    for (int t = 0; t < (int)threadIdx.x; ++t) run = max(run, sh[t]);
-    for (uint32_t i = b; i < e; ++i) {
-        const uint32_t v = tmax[i];
-        tmax[i] = run;
-        run = max(run, v);
-    }
+    tprefix[b] = lo;
 }
 
 __global__ void __launch_bounds__(CS_THREADS)
@@ -474,14 +460,39 @@ cell_apply_kernel(uint32_t* __restrict__ a, uint32_t count, const uint32_t* __re
                   const uint32_t* done) {
     if (done && *done) return;
     __shared__ uint32_t sh[CS_THREADS / 32];
+    // the tile passes through shared memory (one word of padding per 32) so that
+    // global loads and stores are coalesced while each thread scans CS_ITEMS
+    // consecutive entries without bank conflicts
+    __shared__ uint32_t tile[CS_TILE + CS_TILE / 32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t tbase = (size_t)blockIdx.x * CS_TILE;
+    const bool full = tbase + CS_TILE <= count;
+    if (full) {
+        const uint4* src = reinterpret_cast<const uint4*>(a + tbase);
+#pragma unroll
+        for (int i = 0; i < CS_ITEMS / 4; ++i) {
+            const int j = i * CS_THREADS + threadIdx.x;  // uint4 index in the tile
+            const uint4 q = src[j];
+            const int w = 4 * j;
+            tile[w + (w >> 5)] = q.x;
+            tile[w + 1 + (w >> 5)] = q.y;
+            tile[w + 2 + (w >> 5)] = q.z;
+            tile[w + 3 + (w >> 5)] = q.w;
+        }
+    } else {
+        for (int i = 0; i < CS_ITEMS; ++i) {
+            const int w = i * CS_THREADS + threadIdx.x;
+            tile[w + (w >> 5)] = (tbase + w < count) ? a[tbase + w] : 0u;
+        }
+    }
+    __syncthreads();
     // thread t owns CS_ITEMS consecutive entries of the tile
-    const size_t base = (size_t)blockIdx.x * CS_TILE + (size_t)threadIdx.x * CS_ITEMS;
+    const int own = threadIdx.x * CS_ITEMS;
     uint32_t v[CS_ITEMS];
     uint32_t run = 0;
 #pragma unroll
     for (int i = 0; i < CS_ITEMS; ++i) {
-        v[i] = (base + i < count) ? a[base + i] : 0u;
+        v[i] = tile[own + i + ((own + i) >> 5)];
         run = max(run, v[i]);
         v[i] = run;
     }
@@ -498,8 +509,23 @@ cell_apply_kernel(uint32_t* __restrict__ a, uint32_t count, const uint32_t* __re
     for (int w = 0; w < warp; ++w) pre = max(pre, sh[w]);
     if (lane > 0) pre = max(pre, left);
 #pragma unroll
-    for (int i = 0; i < CS_ITEMS; ++i)
-        if (base + i < count) a[base + i] = max(pre, v[i]);
+    for (int i = 0; i < CS_ITEMS; ++i) tile[own + i + ((own + i) >> 5)] = max(pre, v[i]);
+    __syncthreads();
+    if (full) {
+        uint4* dst = reinterpret_cast<uint4*>(a + tbase);
+#pragma unroll
+        for (int i = 0; i < CS_ITEMS / 4; ++i) {
+            const int j = i * CS_THREADS + threadIdx.x;
+            const int w = 4 * j;
+            dst[j] = make_uint4(tile[w + (w >> 5)], tile[w + 1 + (w >> 5)], tile[w + 2 + (w >> 5)],
+                                tile[w + 3 + (w >> 5)]);
+        }
+    } else {
+        for (int i = 0; i < CS_ITEMS; ++i) {
+            const int w = i * CS_THREADS + threadIdx.x;
+            if (tbase + w < count) a[tbase + w] = tile[w + (w >> 5)];
+        }
+    }
 }
 
 // ---- pair records (kernels.cuh) ----------------------------------------------
@@ -644,7 +670,7 @@ int radix_sort(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_
         rs_hist_kernel<<<nblocks, RS_THREADS, 0, s>>>(kin, n, shift, mask, scr.blockhist, nblocks,
                                                       done);
         uint32_t* totals = scr.blockhist + 256 * (size_t)nblocks;
-        rs_scan_rows_kernel<<<256, RS_ROW_THREADS, 0, s>>>(scr.blockhist, nblocks, totals, done);
+        rs_scan_rows_kernel<<<256, nblocks >= 16384 ? RS_ROW_THREADS : 256, 0, s>>>(scr.blockhist, nblocks, totals, done);
         rs_scatter_kernel<<<nblocks, RS_THREADS, 0, s>>>(kin, vin, ko, vo, n, shift, mask,
                                                          scr.blockhist, nblocks, totals, val_base,
                                                          done);
@@ -718,6 +744,19 @@ template int build_query_list<double4>(const double4*, uint32_t, const GridGeom&
                                        uint32_t*, int*, RadixScratch&, const uint32_t*, cudaStream_t,
                                        uint32_t);
 
+namespace {
+__global__ void widen_f32x3_kernel(const float* __restrict__ src, float4* __restrict__ dst,
+                                   uint64_t n, float w) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        dst[i] = make_float4(src[3 * i], src[3 * i + 1], src[3 * i + 2], w);
+}
+}  // namespace
+
+void launch_widen_f32x3(const float* src, float4* dst, size_t n, float w, cudaStream_t s) {
+    if (n) widen_f32x3_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n, w);
+}
+
 size_t cell_scan_scratch_entries(uint32_t ncells) {
     return ((size_t)ncells + 1 + CS_TILE - 1) / CS_TILE + 1;
 }
@@ -729,10 +768,10 @@ int build_cell_start(const uint32_t* sorted_keys, uint32_t n, int sub_shift, uin
     const uint32_t ntiles = (count + CS_TILE - 1) / CS_TILE;
     cudaMemsetAsync(cell_start, 0, (size_t)count * sizeof(uint32_t), s);
     if (n) cell_mark_kernel<<<grid_for(n, 256), 256, 0, s>>>(sorted_keys, n, sub_shift, cell_start, done);
-    cell_tile_max_kernel<<<ntiles, CS_THREADS, 0, s>>>(cell_start, count, scratch, done);
-    cell_tiles_scan_kernel<<<1, CS_THREADS, 0, s>>>(scratch, ntiles, done);
+    cell_tile_prefix_kernel<<<grid_for(ntiles, 256), 256, 0, s>>>(sorted_keys, n, sub_shift, ntiles,
+                                                                  scratch, done);
     cell_apply_kernel<<<ntiles, CS_THREADS, 0, s>>>(cell_start, count, scratch, done);
-    return 4;
+    return n ? 3 : 2;
 }
 
 size_t pairs_capacity(uint32_t n, const GridGeom& g) {

@@ -9,9 +9,11 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 namespace pcsb {
 
@@ -82,6 +84,19 @@ void h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     PCSB_CUDA(cudaEventSynchronize(st.done[(k - 1) & 1]));
 }
 
+// device-side landing chunks of h2d_staged_f32x4 (packed fp32 xyz), per device
+float* device_chunk(int k) {
+    static std::mutex mu;
+    static std::vector<std::array<float*, 2>> per_dev;
+    int dev = 0;
+    PCSB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    if ((int)per_dev.size() <= dev) per_dev.resize(dev + 1, {nullptr, nullptr});
+    float*& p = per_dev[dev][k & 1];
+    if (!p) PCSB_CUDA(cudaMalloc((void**)&p, kChunk));  // lives as long as the process
+    return p;
+}
+
 void h2d_staged_f32x4(void* dst_float4, const double* xyz, size_t n, float w, cudaStream_t s) {
     if (!n) return;
     Staging& st = staging();
@@ -94,22 +109,22 @@ void h2d_staged_f32x4(void* dst_float4, const double* xyz, size_t n, float w, cu
         st.ready = true;
     }
     const int threads = staging_threads();
-    const size_t per_chunk = kChunk / (4 * sizeof(float));
-    char* out = static_cast<char*>(dst_float4);
+    // 12 bytes per point cross PCIe (packed fp32 xyz); a kernel widens each
+    // landed chunk to float4 {x, y, z, w} in place in the destination
+    const size_t per_chunk = kChunk / (3 * sizeof(float));
+    float4* out = static_cast<float4*>(dst_float4);
     size_t k = 0;
     for (size_t p0 = 0; p0 < n; p0 += per_chunk, ++k) {
         const size_t np = std::min(per_chunk, n - p0);
         float* b = reinterpret_cast<float*>(st.buf[k & 1]);
+        float* d = device_chunk((int)k);
+        // the chunk's previous DMA and widening (two chunks ago) must have drained
         PCSB_CUDA(cudaEventSynchronize(st.done[k & 1]));
+        const double* q = xyz + 3 * p0;
 #pragma omp parallel for num_threads(threads) schedule(static)
-        for (long long i = 0; i < (long long)np; ++i) {
-            const double* q = xyz + 3 * (p0 + (size_t)i);
-            b[4 * i] = (float)q[0];
-            b[4 * i + 1] = (float)q[1];
-            b[4 * i + 2] = (float)q[2];
-            b[4 * i + 3] = w;
-        }
-        PCSB_CUDA(cudaMemcpyAsync(out + p0 * 16, b, np * 16, cudaMemcpyHostToDevice, s));
+        for (long long i = 0; i < (long long)(3 * np); ++i) b[i] = (float)q[i];
+        PCSB_CUDA(cudaMemcpyAsync(d, b, np * 12, cudaMemcpyHostToDevice, s));
+        launch_widen_f32x3(d, out + p0, np, w, s);
         PCSB_CUDA(cudaEventRecord(st.done[k & 1], s));
     }
     PCSB_CUDA(cudaEventSynchronize(st.done[(k - 1) & 1]));

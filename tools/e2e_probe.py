@@ -22,6 +22,15 @@ for rep in range(3):
     dev_ms = plan.last_run_ms()
     out, s = plan.download()
     t4 = time.perf_counter()
+    # the same download into pre-touched host buffers (no first-touch page faults)
+    import ctypes as C
+    from paper_2401_03365_b200 import _lib as L
+    o2 = np.ones((plan.m, 3)); i2 = np.ones(max(plan.m, 1), dtype=np.uint32); sc = L.LopSummaryC()
+    t6 = time.perf_counter()
+    L.lib().pcs_lop_plan_download(plan._h, o2.ctypes.data_as(C.POINTER(C.c_double)), C.byref(sc),
+                                  i2.ctypes.data_as(C.POINTER(C.c_uint32)), i2.size)
+    t7 = time.perf_counter()
+    print(f"download into touched buffers {1e3*(t7-t6):.1f} ms")
     plan.close()
     t5 = time.perf_counter()
     print(f"create {1e3*(t1-t0):.1f} ms upload {1e3*(t2-t1):.1f} ms (device setup {s.setup_ms:.1f}) "
