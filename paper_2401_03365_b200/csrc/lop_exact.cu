@@ -1,8 +1,9 @@
 #include <cstdlib>
 // lop_exact.cu — the exact-arithmetic path (fp64 math, reference predicate).
 //
-// One warp per query; lanes stride over the candidates of the cell rows that
-// can hold a point within the support.  Every decision follows the reference
+// One warp per query (a block per query for the fp32 path's deferred queries);
+// its threads stride over the candidates of the cell rows that can hold a point
+// within the support.  Every decision follows the reference
 // literally:
 //   membership   d2 = (dx*dx + dy*dy) + dz*dz <= r*r, no FMA  (spatial.cpp:89,100-101, core.hpp:28)
 //   distance     sqrt(d2)                                       (spatial.cpp:102)
@@ -11,8 +12,8 @@
 //   attraction   d == 0 -> anchor candidate (smallest index), else w = theta/d  (lop.cpp:54-65)
 //   isolation    !(sum w > 0): anchored -> anchor, else held + flagged         (lop.cpp:67-75)
 //   repulsion    skip self, d == 0 -> coincident++, w = theta*|eta'|/d         (lop.cpp:79-97)
-// Only the summation order differs from the reference (lane-strided partial sums
-// combined by a fixed xor tree — deterministic, but not index order), so the
+// Only the summation order differs from the reference (thread-strided partial
+// sums combined by a fixed xor tree and warp order — deterministic, but not index order), so the
 // result agrees to a few ulp rather than bit-for-bit.
 //
 // It is the whole computation in PCS_PREC_FP64 mode and the deferred-query path
@@ -48,6 +49,53 @@ __device__ __forceinline__ unsigned long long warp_min_u(unsigned long long v) {
     return v;
 }
 
+// A team of NW warps evaluates one query: NW = 1 (a warp per query: the fp64
+// path over all queries) or a whole block (the few deferred queries of the fp32
+// path, whose latency would otherwise end each sweep).  Team reductions combine
+// the warps' partial sums in a fixed order, so results stay deterministic.
+template <int NW>
+struct Team {
+    static constexpr int kSize = 32 * NW;
+    double* sh;  // NW words of block shared memory (NW > 1)
+    __device__ __forceinline__ int rank() const { return NW == 1 ? (int)(threadIdx.x & 31) : (int)threadIdx.x; }
+    __device__ __forceinline__ double sum(double v) const {
+        v = warp_sum_d(v);
+        if (NW == 1) return v;
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+        __syncthreads();
+        double r = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) r += sh[w];
+        return r;
+    }
+    __device__ __forceinline__ unsigned long long sum(unsigned long long v) const {
+        v = warp_sum_u(v);
+        if (NW == 1) return v;
+        unsigned long long* u = reinterpret_cast<unsigned long long*>(sh);
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) u[threadIdx.x >> 5] = v;
+        __syncthreads();
+        unsigned long long r = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) r += u[w];
+        return r;
+    }
+    __device__ __forceinline__ unsigned long long min(unsigned long long v) const {
+        v = warp_min_u(v);
+        if (NW == 1) return v;
+        unsigned long long* u = reinterpret_cast<unsigned long long*>(sh);
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) u[threadIdx.x >> 5] = v;
+        __syncthreads();
+        unsigned long long r = ~0ull;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) r = u[w] < r ? u[w] : r;
+        return r;
+    }
+};
+constexpr int EX_TEAM_WARPS = 8;  // deferred queries: one 256-thread block per query
+
 __device__ __forceinline__ double theta_ref(double d, double support, double h) {
     if (d > support) return 0.0;
     const double s = d / h;
@@ -78,32 +126,99 @@ __device__ __forceinline__ Rows rows_around(const GridGeom& g, double x, double 
     return r;
 }
 
-// Calls f(k) for every sorted position k of the rows, lane-strided.
+// Calls f(k) for every sorted position k of the rows, strided over `stride`
+// threads (a warp's lanes, or a team's threads).
 template <typename F>
 __device__ __forceinline__ void for_each_candidate(const uint32_t* __restrict__ start,
                                                    const GridGeom& g, const Rows& rw, int lane,
-                                                   F&& f) {
+                                                   F&& f, int stride = 32) {
     for (int r = 0; r < rw.nrows; ++r) {
         const int yy = rw.loy + r % rw.ny;
         const int zz = rw.loz + r / rw.ny;
         const uint32_t base = ((uint32_t)zz * (uint32_t)g.gy + (uint32_t)yy) * (uint32_t)g.gx;
         const uint32_t b = __ldg(&start[base + rw.lox]);
         const uint32_t e = __ldg(&start[base + rw.hix + 1]);
-        for (uint32_t k = b + lane; k < e; k += 32) f(k);
+        for (uint32_t k = b + lane; k < e; k += stride) f(k);
     }
 }
 
-template <typename T, bool kWlop>
-__global__ void __launch_bounds__(EX_THREADS) exact_kernel(const ExactArgs<T> a) {
+// Team version of for_each_candidate: for a block team the row bounds are
+// loaded in parallel and the candidates of all rows form one flat index space
+// (row found by binary search over the rows' prefix counts in shared memory),
+// so a query costs a few dependent loads instead of ~2 per row.
+constexpr int EX_TEAM_MAXR = 256;
+struct TeamRows {
+    uint32_t b[EX_TEAM_MAXR];
+    uint32_t pre[EX_TEAM_MAXR + 1];
+    uint32_t wtot[32];
+};
+
+template <int NW, typename F>
+__device__ __forceinline__ void team_for_each(const uint32_t* __restrict__ start, const GridGeom& g,
+                                              const Rows& rw, const Team<NW>& team, TeamRows* tr,
+                                              F&& f) {
+    if (NW == 1 || rw.nrows > EX_TEAM_MAXR || rw.nrows > Team<NW>::kSize) {
+        for_each_candidate(start, g, rw, team.rank(), f, Team<NW>::kSize);
+        return;
+    }
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    uint32_t cnt = 0;
+    if (t < rw.nrows) {
+        const int yy = rw.loy + t % rw.ny;
+        const int zz = rw.loz + t / rw.ny;
+        const uint32_t base = ((uint32_t)zz * (uint32_t)g.gy + (uint32_t)yy) * (uint32_t)g.gx;
+        const uint32_t b = __ldg(&start[base + rw.lox]);
+        cnt = __ldg(&start[base + rw.hix + 1]) - b;
+        tr->b[t] = b;
+    }
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    __syncthreads();  // the previous query's readers of tr are done
+    if (lane == 31) tr->wtot[w] = incl;
+    __syncthreads();
+    uint32_t before = 0;
+    for (int i = 0; i < w; ++i) before += tr->wtot[i];
+    if (t < rw.nrows) tr->pre[t] = before + incl - cnt;
+    if (t == rw.nrows - 1) tr->pre[rw.nrows] = before + incl;
+    __syncthreads();
+    const uint32_t total = tr->pre[rw.nrows];
+    for (uint32_t j = t; j < total; j += Team<NW>::kSize) {
+        int lo = 0, hi = rw.nrows - 1;  // last row with pre <= j
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (tr->pre[mid] <= j) lo = mid;
+            else hi = mid - 1;
+        }
+        f(tr->b[lo] + (j - tr->pre[lo]));
+    }
+}
+
+template <typename T, bool kWlop, int NW>
+__global__ void __launch_bounds__(NW == 1 ? EX_THREADS : 32 * NW) exact_kernel(const ExactArgs<T> a) {
     using V = typename Vec4<T>::type;
     if (a.done && *a.done) return;
-    const int lane = threadIdx.x & 31;
+    __shared__ double team_sh[NW];
+    __shared__ uint32_t team_q;
+    __shared__ TeamRows team_rows[1];
+    const Team<NW> team{team_sh};
+    const int lane = team.rank();  // this thread's rank in the query's team
     const uint32_t nq = a.nq_dev ? *a.nq_dev : a.nq;
     uint32_t* counter = &a.slot->exact_counter;
     for (;;) {
         uint32_t qn = 0;
-        if (lane == 0) qn = atomicAdd(counter, 1u);
-        qn = __shfl_sync(0xffffffffu, qn, 0);
+        if (NW == 1) {
+            if (lane == 0) qn = atomicAdd(counter, 1u);
+            qn = __shfl_sync(0xffffffffu, qn, 0);
+        } else {
+            __syncthreads();
+            if (threadIdx.x == 0) team_q = atomicAdd(counter, 1u);
+            __syncthreads();
+            qn = team_q;
+        }
         if (qn >= nq) break;
         const uint32_t q_int = a.qlist ? a.qlist[qn] : qn;  // internal index
         const V qv = a.Xq[q_int];
@@ -114,7 +229,7 @@ __global__ void __launch_bounds__(EX_THREADS) exact_kernel(const ExactArgs<T> a)
         double sw = 0.0, nx = 0.0, ny = 0.0, nz = 0.0;
         unsigned long long cnt = 0;
         unsigned long long anchor = ~0ull;  // (original index << 32) | sorted position
-        for_each_candidate(a.Pstart, a.g, rw, lane, [&](uint32_t k) {
+        team_for_each(a.Pstart, a.g, rw, team, team_rows, [&](uint32_t k) {
             const V p = a.P[k];
             const double px = (double)p.x, py = (double)p.y, pz = (double)p.z;
             const double d2 = exact_d2(px, py, pz, x, y, z);
@@ -134,12 +249,12 @@ __global__ void __launch_bounds__(EX_THREADS) exact_kernel(const ExactArgs<T> a)
             nz += w * pz;
             ++cnt;
         });
-        sw = warp_sum_d(sw);
-        nx = warp_sum_d(nx);
-        ny = warp_sum_d(ny);
-        nz = warp_sum_d(nz);
-        cnt = warp_sum_u(cnt);
-        anchor = warp_min_u(anchor);
+        sw = team.sum(sw);
+        nx = team.sum(nx);
+        ny = team.sum(ny);
+        nz = team.sum(nz);
+        cnt = team.sum(cnt);
+        anchor = team.min(anchor);
 
         double ux, uy, uz;
         bool isolated = false, attracted = sw > 0.0;
@@ -164,7 +279,7 @@ __global__ void __launch_bounds__(EX_THREADS) exact_kernel(const ExactArgs<T> a)
             if (a.mu > 0.0) {
                 double rs = 0.0, rx = 0.0, ry = 0.0, rz = 0.0;
                 const Rows rx_ = rows_around(a.gX, x, y, z, a.s_pad);
-                for_each_candidate(a.Xstart, a.gX, rx_, lane, [&](uint32_t k) {
+                team_for_each(a.Xstart, a.gX, rx_, team, team_rows, [&](uint32_t k) {
                     if (a.Xs_idx[k] == q_int) return;
                     const V c = a.Xs[k];
                     const double cx = (double)c.x, cy = (double)c.y, cz = (double)c.z;
@@ -183,12 +298,12 @@ __global__ void __launch_bounds__(EX_THREADS) exact_kernel(const ExactArgs<T> a)
                     rz += w * (z - cz);
                     ++rcnt;
                 });
-                rs = warp_sum_d(rs);
-                rx = warp_sum_d(rx);
-                ry = warp_sum_d(ry);
-                rz = warp_sum_d(rz);
-                rcnt = warp_sum_u(rcnt);
-                coinc = warp_sum_u(coinc);
+                rs = team.sum(rs);
+                rx = team.sum(rx);
+                ry = team.sum(ry);
+                rz = team.sum(rz);
+                rcnt = team.sum(rcnt);
+                coinc = team.sum(coinc);
                 if (rs > 0.0) {
                     ux += a.mu * (rx / rs);
                     uy += a.mu * (ry / rs);
@@ -366,8 +481,14 @@ int blocks_for(uint64_t n, int threads) {
 
 template <typename T>
 void launch_exact(const ExactArgs<T>& a, int grid_blocks, cudaStream_t s) {
-    if (a.wlop) exact_kernel<T, true><<<grid_blocks, EX_THREADS, 0, s>>>(a);
-    else exact_kernel<T, false><<<grid_blocks, EX_THREADS, 0, s>>>(a);
+    if (a.count_careful) {  // the fp32 path's deferred queries: a block per query
+        constexpr int NT = 32 * EX_TEAM_WARPS;
+        if (a.wlop) exact_kernel<T, true, EX_TEAM_WARPS><<<grid_blocks, NT, 0, s>>>(a);
+        else exact_kernel<T, false, EX_TEAM_WARPS><<<grid_blocks, NT, 0, s>>>(a);
+    } else {
+        if (a.wlop) exact_kernel<T, true, 1><<<grid_blocks, EX_THREADS, 0, s>>>(a);
+        else exact_kernel<T, false, 1><<<grid_blocks, EX_THREADS, 0, s>>>(a);
+    }
 }
 
 template <typename T>

@@ -708,6 +708,11 @@ fast_kernel(const FastArgs a) {
                           !isfinite(rp.z.x) || z != 1;
                 }
                 if (bad) {
+#ifdef PCSB_CAREFUL_DIAG  // developer diagnostic (tools/build_variant.sh)
+                    printf("careful q=%u (%.9g %.9g %.9g) w=%g sa=%g hits=%d zeros=%d rp.s=%g rz=%d\n",
+                           qint, q.x, q.y, q.z, q.w, sa, at.hneg, zeros, rp.s.x,
+                           rp.rneg - rp.hneg);
+#endif
                     const uint32_t pos = atomicAdd(&a.slot->careful_count, 1u);
                     a.careful_list[pos] = qint;
                 } else {
