@@ -267,8 +267,8 @@ Plan::Plan(const pcs_lop_desc& d) : d_(d) {
     fast_grid_ = sms * fast_blocks_per_sm(lanes_, d_.density_weights != 0, false, 2);
     density_grid_ = fast_grid_;
     {
-        // all block slots on one GPU (5 of 6 measured -1.4% .. -11% on configs 2-5);
-        // decided again at upload for sharded plans (set_attr_grid)
+        // all block slots on one GPU (one slot fewer: -1.5% .. -2.5% on configs 3-4);
+        // decided again at upload for small or sharded projected sets
         int per_sm = fast_grid_ / sms;
         if (const char* e = std::getenv("PCSB_ATTR_BLOCKS")) per_sm = std::atoi(e);  // developer knob
         attr_grid_ = sms * std::max(1, per_sm);
@@ -595,6 +595,14 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
         X_init_ = dalloc((size_t)std::max<uint32_t>(mpad_, 1) * sizeof(V));
         own_lo_ = 0;
         own_cnt_ = (uint32_t)m;
+        if (m < (1u << 18) && !std::getenv("PCSB_ATTR_BLOCKS")) {
+            // a short attraction pass would end before the side stream's grid
+            // rebuild got SM slots: leave it one per SM (config 2, 100k queries:
+            // sweep -13%; configs 4 / 3 with 400k / 1M queries: +2.5% / +1.5%)
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_);
+            attr_grid_ = sms * std::max(1, fast_grid_ / sms - 1);
+        }
         if (m)
             PCSB_CUDA(cudaMemcpyAsync(X_init_, X0v, m * sizeof(V), cudaMemcpyDeviceToDevice, stream_));
     }
