@@ -66,6 +66,10 @@ void cuda_check(cudaError_t e, const char* what) {
     }
 }
 
+#ifndef PCSB_MAX_CELLS
+#define PCSB_MAX_CELLS 1073741824.0  // 2^30 cells: a 4 GB data-grid table
+#endif
+
 GridGeom make_grid(const double lo_in[3], const double hi_in[3], double support) {
     double lo[3], hi[3];
     for (int a = 0; a < 3; ++a) {
@@ -77,16 +81,17 @@ GridGeom make_grid(const double lo_in[3], const double hi_in[3], double support)
     // keys are plain linear cells (x fastest): the query order comes from a
     // separate Morton sort of positions (build_query_list)
     double cs;
+    const double kMax = PCSB_MAX_CELLS;
     // y/z cell side s/3 (measured sweeps/s vs s/4, with x cells up to 4x finer:
     // config 3 +3.3%, config 4 +5%, config 5 +11%; s/5 similar on config 3,
     // worse on config 2) when x cells 4x finer still fit the 2^30-cell table;
     // else 0.4 s, else s/2 — x subdivision is worth more than finer y/z (config
     // 5 at h = 0.01: 0.4 s with finer x +9% over s/3); then s
-    if (cells_for(lo, hi, support / 3.0) * 4 <= (double)(1u << 30)) {
+    if (cells_for(lo, hi, support / 3.0) * 4 <= kMax) {
         cs = support / 3.0;
-    } else if (cells_for(lo, hi, support * 0.4) * 4 <= (double)(1u << 30)) {
+    } else if (cells_for(lo, hi, support * 0.4) * 4 <= kMax) {
         cs = support * 0.4;
-    } else if (cells_for(lo, hi, support * 0.5) <= (double)(1u << 29)) {
+    } else if (cells_for(lo, hi, support * 0.5) * 2 <= kMax) {
         cs = support * 0.5;
     } else {
         cs = support;
@@ -95,7 +100,7 @@ GridGeom make_grid(const double lo_in[3], const double hi_in[3], double support)
     // developer knob (grid experiments): PCSB_CELL_FRAC = cell side / support
     if (const char* e = std::getenv("PCSB_CELL_FRAC")) {
         const double f = std::atof(e);
-        if (f > 0.0 && cells_for(lo, hi, support * f) <= (double)(1u << 30)) cs = support * f;
+        if (f > 0.0 && cells_for(lo, hi, support * f) <= kMax) cs = support * f;
     }
     const int sb = 0;
     // finer cells along x (rows are unchanged; x-trimming gets tighter) while the
@@ -105,7 +110,7 @@ GridGeom make_grid(const double lo_in[3], const double hi_in[3], double support)
     // 4 +1.2%, 5 +3.6%, 2 -0.4%; 8 -> 16: config 3 +0.6%.
     int xsub = 1;
     for (int t : {16, 8, 4, 2})
-        if (cells_for(lo, hi, cs) * t <= (double)(1u << 30)) {
+        if (cells_for(lo, hi, cs) * t <= kMax) {
             xsub = t;
             break;
         }

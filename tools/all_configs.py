@@ -8,6 +8,9 @@ import paper_2401_03365_b200 as pb  # noqa: E402
 
 cases = [(1, None, 20), (2, None, 30), (3, None, 15), (4, None, 20), (5, 0.01, 10), (5, 0.02, 10),
          (5, 0.04, 5)]
+if len(sys.argv) > 1:  # subset: config numbers
+    keep = {int(a) for a in sys.argv[1:]}
+    cases = [c for c in cases if c[0] in keep]
 print("| config | h | precision | sweeps/s | interactions / sweep | interactions/s | lc/int |")
 print("|---|---:|---|---:|---:|---:|---:|")
 for cfg, h, k in cases:
