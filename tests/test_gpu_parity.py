@@ -388,3 +388,29 @@ def test_fp32_degenerate_geometry_exact_neighbours(pb, orc, shape):
     assert (s.interactions_attr, s.interactions_rep) == (r.interactions_attr, r.interactions_rep)
     assert (s.isolated_events, s.coincident_pairs) == (r.isolated_events, r.coincident_pairs)
     assert np.abs(out - r.points).max() <= 4 * np.finfo(F32).eps * max(np.abs(P).max(), 1.0)
+
+
+@pytest.mark.parametrize("wlop", [False, True])
+def test_deferred_queries_match_oracle(pb, orc, wlop):
+    """Projected points sitting exactly on a lonely data point stay anchored
+    there (lop.cpp:67-69); from sweep 2 on the fp32 kernel meets their exact
+    zero distance and defers them to the exact kernel (a block per query).
+    Their result, and everyone else's, must match the oracle."""
+    rng = np.random.default_rng(11)
+    # a well-conditioned surface sample (~350 neighbours per point: no iterate
+    # lands on a data sample, see test_fp32_full_trajectory) ...
+    dense = rng.uniform(-1, 1, (20000, 3)) * np.array([1.0, 1.0, 0.01])
+    g = np.arange(4) * 0.2                      # 64 points 0.2 > s apart, off the cloud
+    lonely = 1.3 + np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3)
+    P = r32(np.concatenate([dense, lonely]))
+    X0 = r32(np.concatenate([P[:300], P[20000:]]))   # ... and the lonely points
+    prm = pb.LopParams(kernel=pb.KernelParams(0.05, 3.0), mu=0.4, iterations=4)
+    eta = "neg_linear" if wlop else "inv_cube"
+    out, s = pb.lop_project(P, X0, prm, eta=eta, density_weights=wlop, precision="fp32")
+    r = orc.lop_project(P, X0, 0.05, 3.0, 0.4, 4, store_f32=True, wlop=wlop,
+                        eta=orc.ETA_NEG_LINEAR if wlop else orc.ETA_INV_CUBE)
+    assert s.careful_points >= 64 * 3          # the lonely points, sweeps 2..4
+    assert (s.interactions_attr, s.interactions_rep) == (r.interactions_attr, r.interactions_rep)
+    assert (s.isolated_events, s.coincident_pairs) == (r.isolated_events, r.coincident_pairs)
+    assert np.array_equal(out[300:], X0[300:])  # anchored on themselves
+    assert np.abs(out - r.points).max() <= 1e-5 * bbox_diag(P)
