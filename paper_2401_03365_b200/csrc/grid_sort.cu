@@ -187,11 +187,12 @@ rs_scan_rows_kernel(uint32_t* __restrict__ a, uint32_t nblocks, uint32_t* __rest
     scan_row(a, nblocks, totals, blockIdx.x, sh);
 }
 
-// Stable scatter: within a tile elements keep their order (round-major,
-// warp-major, lane-minor), ranks inside a warp come from __match_any_sync.  The
-// tile is first reordered by digit in shared memory, then written out as
-// contiguous digit runs (~8 keys = one 32-byte sector per run for 8-bit digits
-// and 2048-key tiles), instead of 4-byte writes scattered over 256 buckets.
+// Stable scatter: within a tile elements keep their order (warp-major, then
+// round, then lane: each warp owns 256 consecutive keys), ranks inside a warp
+// come from __match_any_sync and a per-warp running digit count.  The tile is
+// first reordered by digit in shared memory, then written out as contiguous
+// digit runs (~8 keys = one 32-byte sector per run for 8-bit digits and
+// 2048-key tiles), instead of 4-byte writes scattered over 256 buckets.
 struct ScatterSmem {
     uint32_t run[256];    // tile-local running offset per digit
     uint32_t gbase[256];  // global position = gbase[d] + tile-local position
@@ -202,6 +203,10 @@ struct ScatterSmem {
     uint32_t sh[33];
 };
 
+// kKeepVals: hold the tile's values in registers between ranking and placement
+// (the multi-kernel sort); else re-read them (the cooperative sort, which must
+// stay within 48 registers)
+template <bool kKeepVals>
 __device__ __forceinline__ void scatter_tile(const uint32_t* __restrict__ kin,
                                              const uint32_t* __restrict__ vin,
                                              uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
@@ -222,34 +227,48 @@ __device__ __forceinline__ void scatter_tile(const uint32_t* __restrict__ kin,
 #pragma unroll
     for (int w = 0; w < RS_WARPS; ++w) S.wcnt[w][d0] = 0;
     __syncthreads();
+    // warp w ranks the tile's keys [w*256, (w+1)*256) in rounds of 32 consecutive
+    // keys (so warp, round, lane is the input order), keeping a per-warp running
+    // count per digit: one block barrier for the whole tile
     const uint32_t base = tile * RS_TILE;
+    const uint32_t wbase = base + (uint32_t)warp * (RS_ITEMS * 32);
     const unsigned lt = (1u << lane) - 1u;
-    for (int r = 0; r < RS_ITEMS; ++r) {
-        const uint32_t i = base + r * RS_THREADS + threadIdx.x;
-        const bool valid = i < n;
-        const uint32_t key = valid ? kin[i] : 0u;
-        const uint32_t val = valid ? (vin ? vin[i] : val_base + i) : 0u;
-        const uint32_t d = valid ? ((key >> shift) & mask) : 256u;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
-        const uint32_t rank = __popc(peers & lt);
-        if (valid && (__ffs(peers) - 1) == lane) S.wcnt[warp][d] = __popc(peers);
-        __syncthreads();
-        {
-            uint32_t acc = S.run[d0];
+    uint32_t keys[RS_ITEMS], vals[RS_ITEMS], rk[RS_ITEMS];
 #pragma unroll
-            for (int w = 0; w < RS_WARPS; ++w) {
-                const uint32_t c = S.wcnt[w][d0];
-                S.woff[w][d0] = acc;
-                acc += c;
-                S.wcnt[w][d0] = 0;
-            }
-            S.run[d0] = acc;
+    for (int r = 0; r < RS_ITEMS; ++r) {
+        const uint32_t i = wbase + r * 32 + lane;
+        keys[r] = i < n ? kin[i] : 0u;
+        if (kKeepVals) vals[r] = i < n ? (vin ? vin[i] : val_base + i) : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < RS_ITEMS; ++r) {
+        const bool valid = wbase + r * 32 + lane < n;
+        const uint32_t d = valid ? ((keys[r] >> shift) & mask) : 256u;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t before = valid ? S.wcnt[warp][d] : 0u;
+        rk[r] = valid ? before + __popc(peers & lt) : 0xFFFFFFFFu;
+        __syncwarp();
+        if (valid && (__ffs(peers) - 1) == lane) S.wcnt[warp][d] = before + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    {
+        uint32_t acc = S.run[d0];
+#pragma unroll
+        for (int w = 0; w < RS_WARPS; ++w) {
+            const uint32_t c = S.wcnt[w][d0];
+            S.woff[w][d0] = acc;
+            acc += c;
         }
-        __syncthreads();
-        if (valid) {
-            const uint32_t pos = S.woff[warp][d] + rank;  // tile-local
-            S.skey[pos] = key;
-            S.sval[pos] = val;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < RS_ITEMS; ++r) {
+        if (rk[r] != 0xFFFFFFFFu) {
+            const uint32_t pos = S.woff[warp][(keys[r] >> shift) & mask] + rk[r];  // tile-local
+            const uint32_t i = wbase + r * 32 + lane;
+            S.skey[pos] = keys[r];
+            S.sval[pos] = kKeepVals ? vals[r] : (vin ? vin[i] : val_base + i);
         }
     }
     __syncthreads();
@@ -276,7 +295,7 @@ rs_scatter_kernel(const uint32_t* __restrict__ kin, const uint32_t* __restrict__
                   const uint32_t* done) {
     if (done && *done) return;
     __shared__ ScatterSmem S;
-    scatter_tile(kin, vin, kout, vout, n, shift, mask, blockoff, nblocks, digit_totals, val_base,
+    scatter_tile<true>(kin, vin, kout, vout, n, shift, mask, blockoff, nblocks, digit_totals, val_base,
                  blockIdx.x, S);
 }
 
@@ -284,7 +303,9 @@ rs_scatter_kernel(const uint32_t* __restrict__ kin, const uint32_t* __restrict__
 // scans, scatters, separated by grid-wide barriers; tiles and digit rows are
 // looped over the co-resident grid).  For the per-sweep sorts (<= a few M
 // keys) the multi-kernel version is launch/latency-bound.
-__global__ void __launch_bounds__(RS_THREADS)
+// (<= 48 registers: it must fit beside 5 blocks of the attraction pass, whose
+// SM slots it shares when it sorts the projected set on the side stream)
+__global__ void __launch_bounds__(RS_THREADS, 5)
 rs_coop_kernel(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
                uint32_t* vals_out, uint32_t* keys_alt, uint32_t* vals_alt, uint32_t n, int key_bits,
                uint32_t* blockhist, uint32_t ntiles, uint32_t val_base, const uint32_t* done) {
@@ -309,7 +330,7 @@ rs_coop_kernel(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_
         for (uint32_t d = blockIdx.x; d < 256; d += gridDim.x) scan_row(blockhist, ntiles, totals, d, S.sh);
         grid.sync();
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x)
-            scatter_tile(kin, vin, ko, vo, n, shift, mask, blockhist, ntiles, totals,
+            scatter_tile<false>(kin, vin, ko, vo, n, shift, mask, blockhist, ntiles, totals,
                          p == 0 ? val_base : 0u, t, S);
         grid.sync();
         kin = ko;
