@@ -149,14 +149,16 @@ void d2h_staged(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     const int threads = staging_threads();
     const char* in = static_cast<const char*>(src);
     char* out = static_cast<char*>(dst);
-    const size_t nchunks = (bytes + kChunk - 1) / kChunk;
-    // DMA chunk k+1 while the threads drain chunk k
-    PCSB_CUDA(cudaMemcpyAsync(st.buf[0], in, std::min(kChunk, bytes), cudaMemcpyDeviceToHost, s));
+    // DMA chunk k+1 while the threads drain chunk k; 4 MB chunks (of the 16 MB
+    // buffers) keep the first DMA and the last drain short
+    constexpr size_t kD2H = 4u << 20;
+    const size_t nchunks = (bytes + kD2H - 1) / kD2H;
+    PCSB_CUDA(cudaMemcpyAsync(st.buf[0], in, std::min(kD2H, bytes), cudaMemcpyDeviceToHost, s));
     PCSB_CUDA(cudaEventRecord(st.done[0], s));
     for (size_t k = 0; k < nchunks; ++k) {
-        const size_t off = k * kChunk, n = std::min(kChunk, bytes - off);
+        const size_t off = k * kD2H, n = std::min(kD2H, bytes - off);
         if (k + 1 < nchunks) {
-            const size_t off1 = off + kChunk, n1 = std::min(kChunk, bytes - off1);
+            const size_t off1 = off + kD2H, n1 = std::min(kD2H, bytes - off1);
             PCSB_CUDA(cudaMemcpyAsync(st.buf[(k + 1) & 1], in + off1, n1, cudaMemcpyDeviceToHost, s));
             PCSB_CUDA(cudaEventRecord(st.done[(k + 1) & 1], s));
         }
