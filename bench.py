@@ -42,6 +42,18 @@ WORKLOADS = {
 }
 
 
+# Parameters of the five configurations (h = support radius -> KernelParams{h/4, 4});
+# the same table as paper_2401_03365_b200.CONFIGS, repeated here so that the
+# reference arm does not import the product package.
+CONFIGS = {
+    1: dict(h=0.1, mu=0.45, eta="inv_cube", wlop=False, iterations=20, precision="fp64"),
+    2: dict(h=0.05, mu=0.45, eta="neg_linear", wlop=True, iterations=30, precision="fp32"),
+    3: dict(h=0.02, mu=0.40, eta="neg_linear", wlop=False, iterations=15, precision="fp32"),
+    4: dict(h=0.03, mu=0.45, eta="neg_linear", wlop=True, iterations=20, precision="fp32"),
+    5: dict(h=0.02, mu=0.45, eta="inv_cube", wlop=False, iterations=10, precision="fp32"),
+}
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -131,17 +143,21 @@ def sfu_peak(sm_mhz: float, sms: int = 148) -> dict:
 # ------------------------------------------------------------------------------
 # CPU baseline: the reference's own lop_project on the host cores
 # ------------------------------------------------------------------------------
-def cpu_baseline(cfg: int, P: np.ndarray, X0: np.ndarray, params, c: dict, repeats: int = 1,
-                 sweeps: int = 6) -> dict:
-    """The reference's own CPU path (oracle/_ref = the unmodified reference
-    compiled from /root/reference) on a bounded, seeded sample of the workload.
+def cpu_baseline(cfg: int, P: np.ndarray, X0: np.ndarray, c: dict, repeats: int = 3,
+                 sweeps: int = 11) -> dict:
+    """The reference's own CPU path on a bounded, seeded sample of the workload.
+
+    LOP configs run oracle/_ref — the unmodified reference compiled from
+    /root/reference (kind "reference"); for eta = -r the same objects with
+    lop.cpp's |eta'| call bound to 1 (oracle/ref_etar_wrap.cpp), so the
+    arithmetic per interaction is the configuration's.  WLOP configs (no
+    reference implementation) run the oracle port (kind "port").
 
     pcs::lop_project builds the kd-tree of the FULL data cloud inside the call
-    (lop.cpp:24), which alone takes seconds at 10M points.  The sweep rate is
-    therefore measured by differencing two calls on the same sample: one sweep
-    and `sweeps` sweeps (the index build cancels); the interactions of sweeps
-    2..K are counted by the oracle port on the same sample (counting is not
-    timed).  Medians over `repeats`."""
+    (lop.cpp:24), seconds at 10M points.  The sweep rate is therefore the
+    difference of a `sweeps`-sweep call and a 1-sweep call on the same sample
+    (the index build cancels), median of `repeats`; the interactions of sweeps
+    2..K are counted by the oracle port on the same sample (not timed)."""
     from oracle import oracle as O
 
     nthreads = os.cpu_count() or 1
@@ -150,13 +166,10 @@ def cpu_baseline(cfg: int, P: np.ndarray, X0: np.ndarray, params, c: dict, repea
     frac = 0.02 if X0.shape[0] >= 100000 else 1.0
     nsub = max(1, int(X0.shape[0] * frac))
     sub = np.sort(rng.choice(X0.shape[0], nsub, replace=False))
-    Xs = X0[sub]
-    h, cut, mu = params.kernel.h, params.kernel.cutoff_multiple, params.mu
+    Xs = np.ascontiguousarray(X0[sub])
+    h, cut, mu = c["h"] / 4.0, 4.0, c["mu"]
     eta_kind = O.ETA_NEG_LINEAR if c["eta"] == "neg_linear" else O.ETA_INV_CUBE
     use_ref = O.ref_available() and not c["wlop"]
-    if use_ref:
-        # the reference implements only eta = 1/(3r^3): count with that eta
-        eta_kind = O.ETA_INV_CUBE
     c1 = O.lop_project(P, Xs, h, cut, mu, 1, eta=eta_kind, wlop=c["wlop"])
     cK = O.lop_project(P, Xs, h, cut, mu, sweeps, eta=eta_kind, wlop=c["wlop"])
     inter = (cK.interactions_attr + cK.interactions_rep) - (c1.interactions_attr + c1.interactions_rep)
@@ -164,33 +177,63 @@ def cpu_baseline(cfg: int, P: np.ndarray, X0: np.ndarray, params, c: dict, repea
     def call(k):
         t = time.perf_counter()
         if use_ref:
-            O.ref_lop_project(P, Xs, h, cut, mu, k)
+            O.ref_lop_project(P, Xs, h, cut, mu, k, eta=eta_kind)
         else:
             O.lop_project(P, Xs, h, cut, mu, k, eta=eta_kind, wlop=c["wlop"])
         return time.perf_counter() - t
 
-    t1 = statistics.median(call(1) for _ in range(repeats))
-    tK = statistics.median(call(sweeps) for _ in range(repeats))
+    t1s, tKs = [], []
+    for _ in range(repeats):  # interleaved: drifts of the host affect both alike
+        t1s.append(call(1))
+        tKs.append(call(sweeps))
+    t1, tK = statistics.median(t1s), statistics.median(tKs)
     t_sweeps = max(1e-9, tK - t1)
+    lib = "oracle/_ref/libpcs_ref_etar.so" if eta_kind == O.ETA_NEG_LINEAR else "oracle/_ref/libpcs_ref.so"
     if use_ref:
         kind = "reference"
-        what = (f"reference pcs::lop_project (oracle/_ref, built from /root/reference) on a seeded "
-                f"{nsub}-point subset of X0 against the full P ({P.shape[0]} pts): time of a "
-                f"{sweeps}-sweep call minus a 1-sweep call (the in-call kd-tree build of P cancels), "
-                f"median of {repeats}; interactions of sweeps 2..{sweeps} counted by the oracle")
-        if c["eta"] != "inv_cube":
-            what += "; eta=1/(3r^3) (the only eta the reference implements; same neighbour work)"
+        what = (f"reference pcs::lop_project ({lib}, built from /root/reference"
+                f"{'; lop.cpp with |eta_prime| = 1 for eta = -r' if eta_kind == O.ETA_NEG_LINEAR else ''}) "
+                f"on a seeded {nsub}-point subset of X0 against the full P ({P.shape[0]} pts), "
+                f"{c['eta']} eta as configured: time of a {sweeps}-sweep call minus a 1-sweep call "
+                f"(the in-call kd-tree build of P cancels), median of {repeats}; interactions of "
+                f"sweeps 2..{sweeps} ({inter}) counted by the oracle port")
     else:
         kind = "port"
-        what = (f"oracle port (oracle/lop_oracle.c, OpenMP) on a seeded {nsub}-point subset of X0 "
-                f"against the full P ({P.shape[0]} pts): {sweeps}-sweep call minus 1-sweep call")
+        what = (f"oracle port (oracle/lop_oracle.c, OpenMP; the reference has no WLOP) on a seeded "
+                f"{nsub}-point subset of X0 against the full P ({P.shape[0]} pts): {sweeps}-sweep "
+                f"call minus 1-sweep call, median of {repeats}")
+    per = [max(1e-9, b - a) for a, b in zip(t1s, tKs)]
     return {"value": inter / t_sweeps, "unit": "interactions/s", "cores": int(os.environ.get(
         "OMP_NUM_THREADS", nthreads)), "kind": kind, "sample": what,
         "sample_interactions": int(inter), "sample_seconds": t_sweeps,
-        "seconds_per_sweep": t_sweeps / (sweeps - 1), "call_seconds": [t1, tK]}
+        "sweeps_timed": sweeps - 1, "repeats": repeats,
+        "rates_per_repeat": [inter / t for t in per],
+        "seconds_per_sweep": t_sweeps / (sweeps - 1), "call_seconds": {"1": t1s, str(sweeps): tKs}}
 
 
 # ------------------------------------------------------------------------------
+def self_launch(n: int) -> int:
+    """`python bench.py --gpus N` outside torchrun: re-executes itself as N ranks
+    (one process per GPU) under torch.distributed.run, exactly as the driver
+    launches it; fails loudly when fewer than N GPUs are visible."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        log(f"error: --gpus {n} requested but {have} CUDA device(s) are visible")
+        return 2
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    log("launching:", " ".join(cmd))
+    os.execv(sys.executable, cmd)
+    return 0  # not reached
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -203,6 +246,9 @@ def main():
     ap.add_argument("--lanes", type=int, default=0)
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "b200":
+        return self_launch(args.gpus)
+
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -210,34 +256,55 @@ def main():
         log(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}; using WORLD_SIZE")
     ngpu = world
 
-    import paper_2401_03365_b200 as pb
-
     cfg = args.config
-    params, c = pb.config_params(cfg)
+    c = dict(CONFIGS[cfg])
     precision = c["precision"]
 
     # ---------------- reference arm ----------------
     if args.impl == "reference":
+        # the reference's own CPU path only: inputs come from the oracle's restated
+        # generator (the same draws), so this process never loads the product library
         if rank != 0:
             return 0
-        P, X0 = pb.generate_config(cfg)
+        from oracle import oracle as O
+        t0 = time.perf_counter()
+        P, X0 = O.generate_config(cfg)
         if precision == "fp32":
             P = P.astype(np.float32).astype(np.float64)
             X0 = X0.astype(np.float32).astype(np.float64)
-        cb = cpu_baseline(cfg, P, X0, params, c, repeats=2)
+        cb = cpu_baseline(cfg, P, X0, c, repeats=3)
+        wall = time.perf_counter() - t0
+        try:  # evidence: the product library is not mapped in this process
+            maps = open("/proc/self/maps").read()
+            loaded = sorted({ln.split()[-1] for ln in maps.splitlines()
+                             if ln.endswith(".so") and ("/oracle/" in ln or "libpcs" in ln)})
+        except OSError:
+            loaded = None
         line = {
-            "impl": "reference", "metric": "neighbour interactions/sec (LOP sweep)",
-            "value": cb["value"], "unit": "interactions/s", "n_gpus": ngpu, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": cb["seconds_per_sweep"] * 1e3,
+            "impl": "reference", "libraries_mapped": loaded, "metric": "neighbour interactions/sec (LOP sweep)",
+            "value": cb["value"], "unit": "interactions/s", "n_gpus": ngpu,
+            "steps": cb["sweeps_timed"], "warmup": 1, "repeats": cb["repeats"],
+            "ms_per_step": cb["seconds_per_sweep"] * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded host generator, BASELINE.md §4)",
-            "config": {"workload": WORKLOADS[cfg], "sample": cb["sample"]},
+            "config": {"workload": WORKLOADS[cfg], "sample": cb["sample"],
+                       "note": f"--steps {args.steps} --warmup {args.warmup} requested; a step "
+                               f"here is one sweep of the bounded sample (steps = sweeps timed "
+                               f"per repeat: a {cb['sweeps_timed'] + 1}-sweep call minus a "
+                               f"1-sweep call)"},
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "rates_per_repeat": cb["rates_per_repeat"],
+            "timed_region_s": sum(cb["call_seconds"]["1"]) + sum(
+                cb["call_seconds"][str(cb["sweeps_timed"] + 1)]),
+            "wall_s": wall,
             "e2e": {"value": cb["value"], "unit": "interactions/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
         }
         print(json.dumps(line), flush=True)
         return 0
+
+    import paper_2401_03365_b200 as pb
+    params, c = pb.config_params(cfg)
 
     # ---------------- B200 arm ----------------
     import torch
@@ -383,7 +450,7 @@ def main():
             Pb = P.astype(np.float32).astype(np.float64)
             Xb = X0.astype(np.float32).astype(np.float64)
         try:
-            cbr = cpu_baseline(cfg, Pb, Xb, params, c)
+            cbr = cpu_baseline(cfg, Pb, Xb, c)
             cb = {k: cbr[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as e:  # pragma: no cover
             cb = {"value": None, "unit": "interactions/s", "cores": os.cpu_count(),

@@ -150,6 +150,24 @@ pcs_status pcs_lop_plan_download(pcs_lop_plan* p, double* X_out_xyz, pcs_lop_sum
 /* Number of this process's kernel launches issued by the plan so far. */
 uint64_t pcs_lop_plan_launches(const pcs_lop_plan* p);
 
+/* Per-query evidence of the fused path (parity facility; off by default, call
+ * after upload).  While enabled, every sweep records for each query of X^k:
+ * {attraction interactions (0 < d <= support), repulsion interactions,
+ * coincident pairs, flags} with flags 1 = isolated, 2 = anchored at a
+ * zero-distance sample, 4 = deferred to the exact fp64 kernel.  These are the
+ * per-point quantities of proj/src/lop.cpp:49-97 (hits of the two radius
+ * queries :49,80 after the zero-distance and self rules).
+ * pcs_lop_plan_query_counts returns the last sweep's records in original
+ * order (counts4: 4*m int32; -1 for queries another rank owns) and, in
+ * ever_flags (m bytes, may be NULL), the flags OR-ed over every sweep since
+ * the last reset. */
+pcs_status pcs_lop_plan_record_counts(pcs_lop_plan* p, int32_t enable);
+pcs_status pcs_lop_plan_query_counts(pcs_lop_plan* p, int32_t* counts4, uint8_t* ever_flags,
+                                     uint64_t m);
+/* Returns the device memory the library keeps reserved between calls (its
+ * stream-ordered pool on `device`, -1 = current) to the driver. */
+pcs_status pcs_trim_device_pool(int32_t device);
+
 /* ---- parity facilities ----------------------------------------------------
  * SpatialIndex::radius_query (proj/src/spatial.cpp:82-111) for every query, on
  * the device grid: CSR offsets (m+1) and hit indices ascending per query.

@@ -125,6 +125,186 @@ void orc_sphere(double* xyz, size_t n, uint64_t seed) {
 }
 
 /* ------------------------------------------------------------------------ */
+/* The benchmark configurations 1..5 (BASELINE.json "configs"; pinned readings */
+/* in BASELINE.md §4): a second statement of the product's host generator     */
+/* (paper_2401_03365_b200/csrc/generators.cpp), so that the reference arm of   */
+/* bench.py builds its inputs without loading the product library.  Same      */
+/* draws in the same order: surface stream seed 0, noise seed 1, outliers and */
+/* the X0 subset seed 2 (partial Fisher-Yates, j = i + gen() % (N - i)).       */
+/* ------------------------------------------------------------------------ */
+#define ORC_PI 3.141592653589793238462643383279502884
+
+static uint64_t cfg_scaled(uint64_t full, double scale) {
+    const double v = floor((double)full * scale + 0.5);
+    return v < 1.0 ? 1 : (uint64_t)v;
+}
+
+static int cfg_sizes(int cfg, double scale, uint64_t* surface, uint64_t* outliers, uint64_t* nx) {
+    static const uint64_t S[5] = {20000, 950000, 10000000, 4000000, 50000000};
+    static const uint64_t X[5] = {2000, 100000, 1000000, 400000, 5000000};
+    if (cfg < 1 || cfg > 5 || !(scale > 0.0)) return ORC_INVALID_PARAM;
+    *surface = cfg_scaled(S[cfg - 1], scale);
+    *outliers = cfg == 2 ? cfg_scaled(50000, scale) : 0;
+    *nx = cfg_scaled(X[cfg - 1], scale);
+    if (*nx > *surface + *outliers) *nx = *surface + *outliers;
+    return ORC_OK;
+}
+
+int orc_config_sizes(int cfg, double scale, uint64_t* n_p, uint64_t* n_x) {
+    uint64_t s, o, x;
+    if (cfg_sizes(cfg, scale, &s, &o, &x)) return ORC_INVALID_PARAM;
+    *n_p = s + o;
+    *n_x = x;
+    return ORC_OK;
+}
+
+static double ellipsoid_area(double a, double b, double c) {
+    const double p = 1.6075; /* Knud Thomsen's approximation */
+    const double ap = pow(a, p), bp = pow(b, p), cp = pow(c, p);
+    return 4.0 * ORC_PI * pow((ap * bp + ap * cp + bp * cp) / 3.0, 1.0 / p);
+}
+
+int orc_generate_config(int cfg, double scale, double* P, double* X0) {
+    uint64_t surface, outliers, nx;
+    if (cfg_sizes(cfg, scale, &surface, &outliers, &nx) || !P) return ORC_INVALID_PARAM;
+    const uint64_t n = surface + outliers;
+    mt64* gs = (mt64*)malloc(sizeof(mt64));
+    mt64* gx = (mt64*)malloc(sizeof(mt64));
+    if (!gs || !gx) {
+        free(gs);
+        free(gx);
+        return ORC_NO_MEMORY;
+    }
+    mt64_seed(gs, 0);
+    mt64_seed(gx, 2);
+    if (cfg == 1) {
+        for (uint64_t i = 0; i < surface; ++i) {
+            const double z = 1.0 - 2.0 * u01(gs);
+            const double phi = 2.0 * ORC_PI * u01(gs);
+            const double t = 1.0 - z * z;
+            const double rxy = sqrt(t > 0.0 ? t : 0.0);
+            P[3 * i] = rxy * cos(phi);
+            P[3 * i + 1] = rxy * sin(phi);
+            P[3 * i + 2] = z;
+        }
+        orc_add_noise(P, surface, 0.01, 1);
+    } else if (cfg == 2) {
+        const double R = 1.0, r = 0.3;
+        uint64_t k = 0;
+        while (k < surface) { /* area-uniform torus by rejection */
+            const double u = 2.0 * ORC_PI * u01(gs);
+            const double v = 2.0 * ORC_PI * u01(gs);
+            const double accept = (R + r * cos(u)) / (R + r);
+            if (u01(gs) > accept) continue;
+            const double ring = R + r * cos(u);
+            P[3 * k] = ring * cos(v);
+            P[3 * k + 1] = ring * sin(v);
+            P[3 * k + 2] = r * sin(u);
+            ++k;
+        }
+        orc_add_noise(P, surface, 0.005, 1);
+        double lo[3] = {P[0], P[1], P[2]}, hi[3] = {P[0], P[1], P[2]};
+        for (uint64_t i = 1; i < surface; ++i)
+            for (int a = 0; a < 3; ++a) {
+                const double w = P[3 * i + a];
+                if (w < lo[a]) lo[a] = w;
+                if (w > hi[a]) hi[a] = w;
+            }
+        for (uint64_t i = surface; i < n; ++i)
+            for (int a = 0; a < 3; ++a) P[3 * i + a] = lo[a] + (hi[a] - lo[a]) * u01(gx);
+    } else if (cfg == 3) {
+        for (uint64_t i = 0; i < n; ++i) {
+            const double x = 2.0 * u01(gs) - 1.0;
+            const double y = 2.0 * u01(gs) - 1.0;
+            P[3 * i] = x;
+            P[3 * i + 1] = y;
+            P[3 * i + 2] = 0.1 * sin(8.0 * x) * cos(8.0 * y);
+        }
+        mt64* gn = (mt64*)malloc(sizeof(mt64));
+        normal_t nm = {0.0, 0};
+        if (!gn) {
+            free(gs);
+            free(gx);
+            return ORC_NO_MEMORY;
+        }
+        mt64_seed(gn, 1);
+        for (uint64_t i = 0; i < n; ++i) P[3 * i + 2] = P[3 * i + 2] + 0.003 * normal_draw(&nm, gn);
+        free(gn);
+    } else if (cfg == 4) {
+        const double k = 3.9, ea = exp(-k), eb = exp(k);
+        for (uint64_t i = 0; i < n; ++i) {
+            const double u = u01(gs);
+            double z = log(ea + u * (eb - ea)) / k; /* inverse CDF of ~e^{kz} on [-1,1] */
+            z = z > 1.0 ? 1.0 : (z < -1.0 ? -1.0 : z);
+            const double phi = 2.0 * ORC_PI * u01(gs);
+            const double t = 1.0 - z * z;
+            const double rxy = sqrt(t > 0.0 ? t : 0.0);
+            P[3 * i] = rxy * cos(phi);
+            P[3 * i + 1] = rxy * sin(phi);
+            P[3 * i + 2] = z;
+        }
+        orc_add_noise(P, n, 0.005, 1);
+    } else {
+        double ax[8][3], ce[8][3], area[8], tot = 0.0;
+        for (int e = 0; e < 8; ++e) {
+            for (int a = 0; a < 3; ++a) ax[e][a] = 0.2 + 0.4 * u01(gs);
+            for (int a = 0; a < 3; ++a) ce[e][a] = -1.0 + 2.0 * u01(gs);
+            area[e] = ellipsoid_area(ax[e][0], ax[e][1], ax[e][2]);
+            tot += area[e];
+        }
+        uint64_t cnt[8], used = 0;
+        for (int e = 0; e < 8; ++e) {
+            cnt[e] = (uint64_t)floor((double)n * area[e] / tot);
+            used += cnt[e];
+        }
+        for (int e = 0; used < n; e = (e + 1) % 8, ++used) cnt[e]++;
+        uint64_t k = 0;
+        for (int e = 0; e < 8; ++e) {
+            const double a = ax[e][0], b = ax[e][1], c = ax[e][2];
+            double gmax = a * c > a * b ? a * c : a * b;
+            if (b * c > gmax) gmax = b * c;
+            uint64_t got = 0;
+            while (got < cnt[e]) {
+                const double z = 1.0 - 2.0 * u01(gs);
+                const double phi = 2.0 * ORC_PI * u01(gs);
+                const double t = 1.0 - z * z;
+                const double rr = sqrt(t > 0.0 ? t : 0.0);
+                const double x = rr * cos(phi), y = rr * sin(phi);
+                const double gl = sqrt((b * c * x) * (b * c * x) + (a * c * y) * (a * c * y) +
+                                       (a * b * z) * (a * b * z));
+                if (u01(gs) > gl / gmax) continue;
+                P[3 * k] = ce[e][0] + a * x;
+                P[3 * k + 1] = ce[e][1] + b * y;
+                P[3 * k + 2] = ce[e][2] + c * z;
+                ++k;
+                ++got;
+            }
+        }
+        orc_add_noise(P, n, 0.002, 1);
+    }
+    if (X0) {
+        uint32_t* idx = (uint32_t*)malloc((n ? n : 1) * sizeof(uint32_t));
+        if (!idx) {
+            free(gs);
+            free(gx);
+            return ORC_NO_MEMORY;
+        }
+        for (uint64_t i = 0; i < n; ++i) idx[i] = (uint32_t)i;
+        for (uint64_t i = 0; i < nx; ++i) {
+            const uint64_t j = i + mt64_next(gx) % (n - i);
+            const uint32_t t = idx[i];
+            idx[i] = idx[j];
+            idx[j] = t;
+            memcpy(X0 + 3 * i, P + 3 * (uint64_t)idx[i], 3 * sizeof(double));
+        }
+        free(idx);
+    }
+    free(gs);
+    free(gx);
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Weight kernels (proj/src/kernels.cpp)                                      */
 /* ------------------------------------------------------------------------ */
 
@@ -426,94 +606,121 @@ typedef struct {
     uint64_t attr, rep;
 } pair_counts;
 
+/* One point of a sweep (lop.cpp:43-100): x = cur[i] -> out; cnt (may be NULL)
+ * receives {attraction interactions, repulsion interactions, coincident
+ * pairs, flags (1 isolated, 2 anchored)}; isolated / coincident as the
+ * reference's per-point arrays (lop.cpp:28-29). */
+static void sweep_point(const grid_t* pg, const double* P, const double* v, const grid_t* xg,
+                        const double* cur, const double* w, size_t i, const orc_params* prm,
+                        hits_t* ht, double out[3], uint8_t* isolated, uint32_t* coincident,
+                        int32_t cnt[4]) {
+    const double support = prm->h * prm->cutoff_multiple;
+    const double mu = prm->mu;
+    const double* x = cur + 3 * i;
+    int32_t n_attr = 0, n_rep = 0;
+    *isolated = 0;
+    *coincident = 0;
+    if (cnt) cnt[0] = cnt[1] = cnt[2] = cnt[3] = 0;
+    /* Attraction (lop.cpp:49-65) */
+    grid_query(pg, x, support, ht);
+    double attr_wsum = 0.0;
+    double num[3] = {0.0, 0.0, 0.0};
+    int anchored = 0;
+    double anchor[3] = {0.0, 0.0, 0.0};
+    for (size_t k = 0; k < ht->n; ++k) {
+        const double dist = sqrt(ht->d2[k]);
+        const double* p = P + 3 * (size_t)ht->idx[k];
+        if (dist == 0.0) {
+            if (!anchored) {
+                anchored = 1;
+                anchor[0] = p[0];
+                anchor[1] = p[1];
+                anchor[2] = p[2];
+            }
+            continue;
+        }
+        double wgt = orc_theta(dist, prm->h, prm->cutoff_multiple) / dist;
+        if (v) wgt = wgt / v[ht->idx[k]];
+        attr_wsum += wgt;
+        num[0] += wgt * p[0];
+        num[1] += wgt * p[1];
+        num[2] += wgt * p[2];
+        ++n_attr;
+    }
+    /* Isolation / anchor (lop.cpp:67-75) */
+    if (!(attr_wsum > 0.0)) {
+        if (anchored) {
+            out[0] = anchor[0];
+            out[1] = anchor[1];
+            out[2] = anchor[2];
+            if (cnt) cnt[3] = 2 | 8;
+        } else {
+            *isolated = 1;
+            out[0] = x[0];
+            out[1] = x[1];
+            out[2] = x[2];
+            if (cnt) cnt[3] = 1;
+        }
+        return; /* n_attr is 0 here: every hit had d == 0 */
+    }
+    /* Weiszfeld quotient (lop.cpp:77) */
+    double upd[3] = {num[0] / attr_wsum, num[1] / attr_wsum, num[2] / attr_wsum};
+    /* Repulsion (lop.cpp:79-97) */
+    if (mu > 0.0) {
+        grid_query(xg, x, support, ht);
+        double rep_wsum = 0.0;
+        double rn[3] = {0.0, 0.0, 0.0};
+        for (size_t k = 0; k < ht->n; ++k) {
+            if (ht->idx[k] == (uint32_t)i) continue;
+            const double dist = sqrt(ht->d2[k]);
+            if (dist == 0.0) {
+                ++*coincident;
+                continue;
+            }
+            const double* xp = cur + 3 * (size_t)ht->idx[k];
+            double wgt = orc_theta(dist, prm->h, prm->cutoff_multiple) *
+                         etad(dist, prm->eta_kind) / dist;
+            if (w) wgt = wgt * w[ht->idx[k]];
+            rep_wsum += wgt;
+            rn[0] += wgt * (x[0] - xp[0]);
+            rn[1] += wgt * (x[1] - xp[1]);
+            rn[2] += wgt * (x[2] - xp[2]);
+            ++n_rep;
+        }
+        if (rep_wsum > 0.0) {
+            upd[0] += mu * (rn[0] / rep_wsum);
+            upd[1] += mu * (rn[1] / rep_wsum);
+            upd[2] += mu * (rn[2] / rep_wsum);
+        }
+    }
+    out[0] = upd[0];
+    out[1] = upd[1];
+    out[2] = upd[2];
+    if (cnt) {
+        cnt[0] = n_attr;
+        cnt[1] = n_rep;
+        cnt[2] = (int32_t)*coincident;
+        cnt[3] = anchored ? 8 : 0; /* a zero-distance sample was skipped (lop.cpp:55-61) */
+    }
+}
+
 /* One Jacobi sweep from cur to next. */
 static void sweep(const grid_t* pg, const double* P, const double* v, const grid_t* xg,
                   const double* cur, const double* w, size_t m, const orc_params* prm,
-                  double* next, uint8_t* isolated, uint32_t* coincident, pair_counts* pc) {
-    const double support = prm->h * prm->cutoff_multiple;
-    const double mu = prm->mu;
+                  double* next, uint8_t* isolated, uint32_t* coincident, pair_counts* pc,
+                  uint8_t* flags_or) {
     uint64_t n_attr = 0, n_rep = 0;
 #pragma omp parallel reduction(+ : n_attr, n_rep)
     {
         hits_t ht = {0};
+        int32_t cnt[4];
 #pragma omp for schedule(static)
         for (size_t i = 0; i < m; ++i) {
-            const double* x = cur + 3 * i;
-            isolated[i] = 0;
-            coincident[i] = 0;
-            /* Attraction (lop.cpp:49-65) */
-            grid_query(pg, x, support, &ht);
-            double attr_wsum = 0.0;
-            double num[3] = {0.0, 0.0, 0.0};
-            int anchored = 0;
-            double anchor[3] = {0.0, 0.0, 0.0};
-            for (size_t k = 0; k < ht.n; ++k) {
-                const double dist = sqrt(ht.d2[k]);
-                const double* p = P + 3 * (size_t)ht.idx[k];
-                if (dist == 0.0) {
-                    if (!anchored) {
-                        anchored = 1;
-                        anchor[0] = p[0];
-                        anchor[1] = p[1];
-                        anchor[2] = p[2];
-                    }
-                    continue;
-                }
-                double wgt = orc_theta(dist, prm->h, prm->cutoff_multiple) / dist;
-                if (v) wgt = wgt / v[ht.idx[k]];
-                attr_wsum += wgt;
-                num[0] += wgt * p[0];
-                num[1] += wgt * p[1];
-                num[2] += wgt * p[2];
-                ++n_attr;
-            }
-            /* Isolation / anchor (lop.cpp:67-75) */
-            if (!(attr_wsum > 0.0)) {
-                if (anchored) {
-                    next[3 * i + 0] = anchor[0];
-                    next[3 * i + 1] = anchor[1];
-                    next[3 * i + 2] = anchor[2];
-                } else {
-                    isolated[i] = 1;
-                    next[3 * i + 0] = x[0];
-                    next[3 * i + 1] = x[1];
-                    next[3 * i + 2] = x[2];
-                }
-                continue;
-            }
-            /* Weiszfeld quotient (lop.cpp:77) */
-            double upd[3] = {num[0] / attr_wsum, num[1] / attr_wsum, num[2] / attr_wsum};
-            /* Repulsion (lop.cpp:79-97) */
-            if (mu > 0.0) {
-                grid_query(xg, x, support, &ht);
-                double rep_wsum = 0.0;
-                double rn[3] = {0.0, 0.0, 0.0};
-                for (size_t k = 0; k < ht.n; ++k) {
-                    if (ht.idx[k] == (uint32_t)i) continue;
-                    const double dist = sqrt(ht.d2[k]);
-                    if (dist == 0.0) {
-                        ++coincident[i];
-                        continue;
-                    }
-                    const double* xp = cur + 3 * (size_t)ht.idx[k];
-                    double wgt = orc_theta(dist, prm->h, prm->cutoff_multiple) *
-                                 etad(dist, prm->eta_kind) / dist;
-                    if (w) wgt = wgt * w[ht.idx[k]];
-                    rep_wsum += wgt;
-                    rn[0] += wgt * (x[0] - xp[0]);
-                    rn[1] += wgt * (x[1] - xp[1]);
-                    rn[2] += wgt * (x[2] - xp[2]);
-                    ++n_rep;
-                }
-                if (rep_wsum > 0.0) {
-                    upd[0] += mu * (rn[0] / rep_wsum);
-                    upd[1] += mu * (rn[1] / rep_wsum);
-                    upd[2] += mu * (rn[2] / rep_wsum);
-                }
-            }
-            next[3 * i + 0] = upd[0];
-            next[3 * i + 1] = upd[1];
-            next[3 * i + 2] = upd[2];
+            sweep_point(pg, P, v, xg, cur, w, i, prm, &ht, next + 3 * i, isolated + i,
+                        coincident + i, cnt);
+            n_attr += (uint64_t)cnt[0];
+            n_rep += (uint64_t)cnt[1];
+            if (flags_or) flags_or[i] |= (uint8_t)cnt[3];
         }
         hits_free(&ht);
     }
@@ -521,6 +728,109 @@ static void sweep(const grid_t* pg, const double* P, const double* v, const grid
         pc->attr += n_attr;
         pc->rep += n_rep;
     }
+}
+
+/* WLOP density of the points `need` marks (all when need == NULL), summed in
+ * grid order (no per-point sort: the order only moves the last fp64 bits). */
+static void density_marked(const grid_t* gr, double h, double cutoff, const uint8_t* need,
+                           double* v, size_t n) {
+    const double support = h * cutoff;
+    const double r2 = support * support;
+    const double rp = support * (1.0 + 1e-6);
+#pragma omp parallel for schedule(dynamic, 256)
+    for (size_t j = 0; j < n; ++j) {
+        if (need && !need[j]) continue;
+        const double* c = gr->pts + 3 * j;
+        int64_t lo[3], hi[3];
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = cell_of(gr, a, c[a] - rp);
+            hi[a] = cell_of(gr, a, c[a] + rp);
+        }
+        double acc = 1.0;
+        for (int64_t z = lo[2]; z <= hi[2]; ++z)
+            for (int64_t y = lo[1]; y <= hi[1]; ++y) {
+                const uint64_t row = (uint64_t)(gr->g[0] * (y + gr->g[1] * z));
+                const uint64_t b = gr->start[row + (uint64_t)lo[0]];
+                const uint64_t e = gr->start[row + (uint64_t)hi[0] + 1];
+                for (uint64_t k = b; k < e; ++k) {
+                    const uint32_t idx = gr->order[k];
+                    if (idx == (uint32_t)j) continue;
+                    const double* p = gr->pts + 3 * (size_t)idx;
+                    const double dx = p[0] - c[0], dy = p[1] - c[1], dz = p[2] - c[2];
+                    const double d2 = dx * dx + dy * dy + dz * dz;
+                    if (d2 <= r2) acc += orc_theta(sqrt(d2), h, cutoff);
+                }
+            }
+        v[j] = acc;
+    }
+}
+
+int orc_lop_sweep_rows(const double* P, size_t n, const double* X, size_t m,
+                       const orc_params* prm, const uint32_t* rows, size_t nrows,
+                       double* Xnext_rows, int32_t* counts, int threads) {
+    int rc = validate(prm);
+    if (rc) return rc;
+    if (n == 0) return ORC_EMPTY_CLOUD;
+    for (size_t r = 0; r < nrows; ++r)
+        if (rows[r] >= m) return ORC_INVALID_PARAM;
+    if (nrows == 0) return ORC_OK;
+    set_threads(threads);
+    const double support = prm->h * prm->cutoff_multiple;
+    grid_t pg, xg;
+    if (grid_build(&pg, P, n, support)) return ORC_NO_MEMORY;
+    if (grid_build(&xg, X, m, support)) {
+        grid_free(&pg);
+        return ORC_NO_MEMORY;
+    }
+    double* v = NULL;
+    double* w = NULL;
+    if (prm->density_weights) {
+        /* v_j only for the data points some row query can see; w_i for every
+         * projected point a row query can see (its repulsion candidates) */
+        v = (double*)malloc(n * sizeof(double));
+        w = (double*)malloc(m * sizeof(double));
+        uint8_t* needP = (uint8_t*)calloc(n, 1);
+        uint8_t* needX = (uint8_t*)calloc(m, 1);
+        if (!v || !w || !needP || !needX) {
+            free(v); free(w); free(needP); free(needX);
+            grid_free(&pg);
+            grid_free(&xg);
+            return ORC_NO_MEMORY;
+        }
+#pragma omp parallel
+        {
+            hits_t ht = {0};
+#pragma omp for schedule(dynamic, 16)
+            for (size_t r = 0; r < nrows; ++r) {
+                const double* x = X + 3 * (size_t)rows[r];
+                grid_query(&pg, x, support, &ht);
+                for (size_t k = 0; k < ht.n; ++k) needP[ht.idx[k]] = 1;
+                grid_query(&xg, x, support, &ht);
+                for (size_t k = 0; k < ht.n; ++k) needX[ht.idx[k]] = 1;
+            }
+            hits_free(&ht);
+        }
+        density_marked(&pg, prm->h, prm->cutoff_multiple, needP, v, n);
+        density_marked(&xg, prm->h, prm->cutoff_multiple, needX, w, m);
+        free(needP);
+        free(needX);
+    }
+#pragma omp parallel
+    {
+        hits_t ht = {0};
+        uint8_t iso;
+        uint32_t co;
+#pragma omp for schedule(dynamic, 16)
+        for (size_t r = 0; r < nrows; ++r)
+            sweep_point(&pg, P, v, &xg, X, w, rows[r], prm, &ht, Xnext_rows + 3 * r, &iso, &co,
+                        counts ? counts + 4 * r : NULL);
+        hits_free(&ht);
+    }
+    free(v);
+    free(w);
+    grid_free(&pg);
+    grid_free(&xg);
+    return ORC_OK;
 }
 
 static double max_displacement(const double* a, const double* b, size_t m) {
@@ -560,7 +870,7 @@ int orc_lop_sweep(const double* P, size_t n, const double* X, size_t m, const or
         density_on_grid(&pg, prm->h, prm->cutoff_multiple, v, n);
         density_on_grid(&xg, prm->h, prm->cutoff_multiple, w, m);
     }
-    sweep(&pg, P, v, &xg, X, w, m, prm, Xnext, iso, co, NULL);
+    sweep(&pg, P, v, &xg, X, w, m, prm, Xnext, iso, co, NULL, NULL);
     if (max_disp) *max_disp = max_displacement(Xnext, X, m);
     if (!isolated) free(iso);
     if (!coincident) free(co);
@@ -574,6 +884,12 @@ int orc_lop_sweep(const double* P, size_t n, const double* X, size_t m, const or
 int orc_lop_project(const double* P, size_t n, const double* X0, size_t m,
                     const orc_params* prm, double* out, orc_summary* sum,
                     uint32_t* isolated_out, int threads) {
+    return orc_lop_project_flags(P, n, X0, m, prm, out, sum, isolated_out, NULL, threads);
+}
+
+int orc_lop_project_flags(const double* P, size_t n, const double* X0, size_t m,
+                          const orc_params* prm, double* out, orc_summary* sum,
+                          uint32_t* isolated_out, uint8_t* flags_out, int threads) {
     /* Semantics order (lop.cpp:13-20): validate, empty data, empty initial. */
     int rc = validate(prm);
     if (rc) return rc;
@@ -606,6 +922,7 @@ int orc_lop_project(const double* P, size_t n, const double* X0, size_t m,
         return ORC_NO_MEMORY;
     }
     memcpy(cur, X0, 3 * m * sizeof(double));
+    if (flags_out) memset(flags_out, 0, m);
     if (v) density_on_grid(&pg, prm->h, prm->cutoff_multiple, v, n);
     pair_counts pc = {0, 0};
     for (int it = 1; it <= prm->iterations; ++it) {
@@ -616,7 +933,8 @@ int orc_lop_project(const double* P, size_t n, const double* X0, size_t m,
             break;
         }
         if (w) density_on_grid(&xg, prm->h, prm->cutoff_multiple, w, m);
-        sweep(&pg, P, v, &xg, cur, w, m, prm, nxt, iso, co, &pc);
+        sweep(&pg, P, v, &xg, cur, w, m, prm, nxt, iso, co, &pc,
+              flags_out && it >= 2 ? flags_out : NULL);
         if (prm->store_f32)
             for (size_t i = 0; i < 3 * m; ++i) nxt[i] = (double)(float)nxt[i];
         grid_free(&xg);

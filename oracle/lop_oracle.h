@@ -72,12 +72,29 @@ int orc_lop_project(const double* P, size_t n, const double* X0, size_t m,
                     const orc_params* prm, double* out, orc_summary* sum,
                     uint32_t* isolated_out, int threads);
 
+/* Same, and flags_out (m bytes, may be NULL) = per point, OR over sweeps >= 2 of
+ * 1 isolated, 2 anchored, 8 a zero-distance data sample skipped (lop.cpp:55-61):
+ * the discontinuities of the reference's update. */
+int orc_lop_project_flags(const double* P, size_t n, const double* X0, size_t m,
+                          const orc_params* prm, double* out, orc_summary* sum,
+                          uint32_t* isolated_out, uint8_t* flags_out, int threads);
+
 /* One sweep only, from X (m*3) to Xnext (m*3); per-point outputs optional.
  * Used by the per-sweep parity tests.  v (n, may be NULL) are data density
  * weights for WLOP (computed internally when NULL and density_weights). */
 int orc_lop_sweep(const double* P, size_t n, const double* X, size_t m,
                   const orc_params* prm, double* Xnext, uint8_t* isolated,
                   uint32_t* coincident, double* max_disp, int threads);
+
+/* One sweep from X evaluated for the queries rows[0..nrows) only (the whole X
+ * is the repulsion candidate set): Xnext_rows (nrows*3) and, when counts is
+ * not NULL, 4 int32 per row: attraction interactions (0 < d <= s), repulsion
+ * interactions, coincident pairs, flags (1 isolated, 2 anchored, 8 a
+ * zero-distance data sample was skipped).  Used by the
+ * full-size per-query parity tests. */
+int orc_lop_sweep_rows(const double* P, size_t n, const double* X, size_t m,
+                       const orc_params* prm, const uint32_t* rows, size_t nrows,
+                       double* Xnext_rows, int32_t* counts, int threads);
 
 /* SpatialIndex::radius_query for every query: CSR output, hits ascending by
  * index.  offsets has m+1 entries.  If idx is NULL only offsets are filled.
@@ -95,6 +112,10 @@ void orc_add_noise(double* xyz, size_t n, double sigma, uint64_t seed);
 void orc_plane(double* xyz, size_t n, uint64_t seed);
 void orc_sphere(double* xyz, size_t n, uint64_t seed);
 double orc_theta(double d, double h, double cutoff);
+/* The benchmark configurations (same draws as pcs_generate_config): sizes, then
+ * P (n_p*3) and X0 (n_x*3, may be NULL). */
+int orc_config_sizes(int cfg, double scale, uint64_t* n_p, uint64_t* n_x);
+int orc_generate_config(int cfg, double scale, double* P, double* X0);
 
 /* Deviation metrics: proj/src/spatial.cpp:119-158 (nearest),
  * proj/src/metrics.cpp:11-133 (aggregate, deviation, point_triangle_distance,

@@ -17,6 +17,9 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORC_PATH = os.path.join(HERE, "liborc.so")
 REF_PATH = os.path.join(HERE, "_ref", "libpcs_ref.so")
+# the same unmodified reference objects with lop.cpp's |eta'| call bound to 1
+# (eta = -r; oracle/ref_etar_wrap.cpp, linked with -Wl,--wrap)
+REF_ETAR_PATH = os.path.join(HERE, "_ref", "libpcs_ref_etar.so")
 
 ETA_INV_CUBE = 0
 ETA_NEG_LINEAR = 1
@@ -76,6 +79,7 @@ class Result:
     interactions_attr: int = 0
     interactions_rep: int = 0
     last_max_disp: float = 0.0
+    flags: np.ndarray = None
 
 
 def build(reference: bool = True) -> None:
@@ -103,9 +107,15 @@ def orc():
         lib.orc_lop_project.argtypes = [_c_dbl_p, C.c_size_t, _c_dbl_p, C.c_size_t,
                                         C.POINTER(OrcParams), _c_dbl_p, C.POINTER(OrcSummary),
                                         _c_u32_p, C.c_int]
+        lib.orc_lop_project_flags.argtypes = [_c_dbl_p, C.c_size_t, _c_dbl_p, C.c_size_t,
+                                              C.POINTER(OrcParams), _c_dbl_p,
+                                              C.POINTER(OrcSummary), _c_u32_p, _c_u8_p, C.c_int]
         lib.orc_lop_sweep.argtypes = [_c_dbl_p, C.c_size_t, _c_dbl_p, C.c_size_t,
                                       C.POINTER(OrcParams), _c_dbl_p, _c_u8_p, _c_u32_p,
                                       _c_dbl_p, C.c_int]
+        lib.orc_lop_sweep_rows.argtypes = [_c_dbl_p, C.c_size_t, _c_dbl_p, C.c_size_t,
+                                           C.POINTER(OrcParams), _c_u32_p, C.c_size_t, _c_dbl_p,
+                                           C.POINTER(C.c_int32), C.c_int]
         lib.orc_radius_query_all.argtypes = [_c_dbl_p, C.c_size_t, _c_dbl_p, C.c_size_t,
                                              C.c_double, _c_u64_p, _c_u32_p, _c_dbl_p, C.c_int]
         lib.orc_density_weights.argtypes = [_c_dbl_p, C.c_size_t, C.c_double, C.c_double,
@@ -113,6 +123,8 @@ def orc():
         lib.orc_add_noise.argtypes = [_c_dbl_p, C.c_size_t, C.c_double, C.c_uint64]
         lib.orc_plane.argtypes = [_c_dbl_p, C.c_size_t, C.c_uint64]
         lib.orc_sphere.argtypes = [_c_dbl_p, C.c_size_t, C.c_uint64]
+        lib.orc_config_sizes.argtypes = [C.c_int, C.c_double, _c_u64_p, _c_u64_p]
+        lib.orc_generate_config.argtypes = [C.c_int, C.c_double, _c_dbl_p, _c_dbl_p]
         lib.orc_theta.argtypes = [C.c_double, C.c_double, C.c_double]
         lib.orc_theta.restype = C.c_double
         lib.orc_nearest_all.argtypes = [_c_dbl_p, C.c_size_t, _c_dbl_p, C.c_size_t, _c_u32_p,
@@ -131,12 +143,28 @@ def ref_available() -> bool:
     return os.path.exists(REF_PATH)
 
 
-def ref():
-    global _ref
+_ref_etar = None
+
+
+def ref(eta: int = ETA_INV_CUBE):
+    """The reference build: eta = 1/(3r^3) as the reference ships it, or (eta =
+    ETA_NEG_LINEAR) the same objects with |eta'| bound to 1."""
+    global _ref, _ref_etar
+    if eta == ETA_NEG_LINEAR:
+        if _ref_etar is None:
+            if not os.path.exists(REF_ETAR_PATH):
+                raise FileNotFoundError(REF_ETAR_PATH)
+            _ref_etar = _bind_ref(C.CDLL(REF_ETAR_PATH))
+        return _ref_etar
     if _ref is None:
         if not ref_available():
             raise FileNotFoundError(REF_PATH)
-        lib = C.CDLL(REF_PATH)
+        _ref = _bind_ref(C.CDLL(REF_PATH))
+    return _ref
+
+
+def _bind_ref(lib):
+    if True:
         lib.ref_lop_project.argtypes = [_c_dbl_p, C.c_uint64, _c_dbl_p, C.c_uint64, C.c_double,
                                         C.c_double, C.c_double, C.c_int, C.c_double, _c_dbl_p,
                                         C.POINTER(RefSummary), _c_u32_p]
@@ -161,8 +189,7 @@ def ref():
                                         _c_u64_p, C.POINTER(C.c_int64)]
         lib.ref_point_triangle_distance.argtypes = [_c_dbl_p, _c_dbl_p]
         lib.ref_point_triangle_distance.restype = C.c_double
-        _ref = lib
-    return _ref
+    return lib
 
 
 def _xyz(a) -> np.ndarray:
@@ -181,23 +208,31 @@ class OracleError(RuntimeError):
 
 
 def lop_project(P, X0, h, cutoff=3.0, mu=0.4, iterations=30, tol=1e-7,
-                eta=ETA_INV_CUBE, wlop=False, threads=0, store_f32=False) -> Result:
-    """orc_lop_project — the C restatement of pcs::lop_project (+eta/WLOP)."""
+                eta=ETA_INV_CUBE, wlop=False, threads=0, store_f32=False,
+                flags=False) -> Result:
+    """orc_lop_project — the C restatement of pcs::lop_project (+eta/WLOP).
+    flags=True also returns per-point event flags (Result.flags, OR over sweeps
+    >= 2: 1 isolated, 2 anchored, 8 a zero-distance data sample skipped)."""
     P = _xyz(P)
     X0 = _xyz(X0)
     m = X0.shape[0]
     out = np.empty_like(X0)
     iso = np.empty(max(m, 1), dtype=np.uint32)
+    fl = np.zeros(max(m, 1), dtype=np.uint8)
     prm = OrcParams(h, cutoff, mu, iterations, tol, eta, 1 if wlop else 0, 1 if store_f32 else 0)
     s = OrcSummary()
-    rc = orc().orc_lop_project(_ptr(P, _c_dbl_p), P.shape[0], _ptr(X0, _c_dbl_p), m,
-                               C.byref(prm), _ptr(out, _c_dbl_p), C.byref(s),
-                               _ptr(iso, _c_u32_p), threads)
+    rc = orc().orc_lop_project_flags(_ptr(P, _c_dbl_p), P.shape[0], _ptr(X0, _c_dbl_p), m,
+                                     C.byref(prm), _ptr(out, _c_dbl_p), C.byref(s),
+                                     _ptr(iso, _c_u32_p), _ptr(fl, _c_u8_p) if flags else None,
+                                     threads)
     if rc:
         raise OracleError(rc)
-    return Result(out, s.iterations_run, bool(s.converged), s.isolated_events,
-                  s.coincident_pairs, iso[: s.n_isolated].copy(), s.interactions_attr,
-                  s.interactions_rep, s.last_max_disp)
+    r = Result(out, s.iterations_run, bool(s.converged), s.isolated_events,
+               s.coincident_pairs, iso[: s.n_isolated].copy(), s.interactions_attr,
+               s.interactions_rep, s.last_max_disp)
+    if flags:
+        r.flags = fl[:m].copy()
+    return r
 
 
 def lop_sweep(P, X, h, cutoff=3.0, mu=0.4, eta=ETA_INV_CUBE, wlop=False, threads=0):
@@ -216,6 +251,25 @@ def lop_sweep(P, X, h, cutoff=3.0, mu=0.4, eta=ETA_INV_CUBE, wlop=False, threads
     if rc:
         raise OracleError(rc)
     return nxt, iso[:m], co[:m], md.value
+
+
+def lop_sweep_rows(P, X, rows, h, cutoff=3.0, mu=0.4, eta=ETA_INV_CUBE, wlop=False, threads=0):
+    """One sweep from X for the query rows only (orc_lop_sweep_rows): returns
+    (X_next[rows], counts[rows, 4]) with counts = (attraction interactions,
+    repulsion interactions, coincident pairs, flags: 1 isolated, 2 anchored)."""
+    P = _xyz(P)
+    X = _xyz(X)
+    rows = np.ascontiguousarray(rows, dtype=np.uint32)
+    nr = rows.shape[0]
+    nxt = np.empty((max(nr, 1), 3), dtype=np.float64)
+    cnt = np.zeros((max(nr, 1), 4), dtype=np.int32)
+    prm = OrcParams(h, cutoff, mu, 1, 1e-7, eta, 1 if wlop else 0, 0)
+    rc = orc().orc_lop_sweep_rows(_ptr(P, _c_dbl_p), P.shape[0], _ptr(X, _c_dbl_p), X.shape[0],
+                                  C.byref(prm), _ptr(rows, _c_u32_p), nr, _ptr(nxt, _c_dbl_p),
+                                  cnt.ctypes.data_as(C.POINTER(C.c_int32)), threads)
+    if rc:
+        raise OracleError(rc)
+    return nxt[:nr], cnt[:nr]
 
 
 def radius_query_all(C_pts, Q, r, threads=0):
@@ -268,20 +322,40 @@ def sphere(n, seed):
     return a
 
 
+def generate_config(cfg: int, scale: float = 1.0):
+    """(P, X0) of benchmark configuration cfg (orc_generate_config: the same draws
+    as the product's pcs_generate_config, restated in the oracle so that the
+    reference arm never loads the product library)."""
+    n_p = np.zeros(1, dtype=np.uint64)
+    n_x = np.zeros(1, dtype=np.uint64)
+    lib = orc()
+    if lib.orc_config_sizes(cfg, scale, _ptr(n_p, _c_u64_p), _ptr(n_x, _c_u64_p)):
+        raise OracleError(1, f"config {cfg}")
+    P = np.empty((int(n_p[0]), 3), dtype=np.float64)
+    X0 = np.empty((int(n_x[0]), 3), dtype=np.float64)
+    rc = lib.orc_generate_config(cfg, scale, _ptr(P, _c_dbl_p), _ptr(X0, _c_dbl_p))
+    if rc:
+        raise OracleError(rc)
+    return P, X0
+
+
 def theta(d, h, cutoff=3.0):
     return orc().orc_theta(d, h, cutoff)
 
 
 # --- the unmodified reference (oracle/_ref) ------------------------------------
 
-def ref_lop_project(P, X0, h, cutoff=3.0, mu=0.4, iterations=30, tol=1e-7) -> Result:
+def ref_lop_project(P, X0, h, cutoff=3.0, mu=0.4, iterations=30, tol=1e-7,
+                    eta=ETA_INV_CUBE) -> Result:
+    """pcs::lop_project of the reference build (eta = ETA_NEG_LINEAR: the
+    reference's lop.cpp with |eta'| = 1, see REF_ETAR_PATH)."""
     P = _xyz(P)
     X0 = _xyz(X0)
     m = X0.shape[0]
     out = np.empty_like(X0)
     iso = np.empty(max(m, 1), dtype=np.uint32)
     s = RefSummary()
-    lib = ref()
+    lib = ref(eta)
     rc = lib.ref_lop_project(_ptr(P, _c_dbl_p), P.shape[0], _ptr(X0, _c_dbl_p), m, h, cutoff,
                              mu, iterations, tol, _ptr(out, _c_dbl_p), C.byref(s),
                              _ptr(iso, _c_u32_p))

@@ -9,7 +9,7 @@ from .lop import (  # noqa: F401
     NumericalFailure, DeviceUnavailable, add_noise, config_params, config_sizes, density_weights, generate_config,
     generate_surface, grid_sort, lop_project, radius_query_all, shard_layout,
     nearest_all, deviation, deviation_to_mesh, ParseError, format_from_path, format_cloud,
-    parse_cloud, read_cloud, write_cloud, parse_mesh, format_double,
+    parse_cloud, read_cloud, write_cloud, parse_mesh, format_double, trim_device_pool,
 )
 
 __all__ = [
@@ -19,5 +19,5 @@ __all__ = [
     "config_sizes", "density_weights", "generate_config", "generate_surface", "grid_sort", "lop_project",
     "radius_query_all", "shard_layout", "DeviationReport", "EmptyMesh", "nearest_all",
     "deviation", "deviation_to_mesh", "ParseError", "format_from_path", "format_cloud",
-    "parse_cloud", "read_cloud", "write_cloud", "parse_mesh", "format_double",
+    "parse_cloud", "read_cloud", "write_cloud", "parse_mesh", "format_double", "trim_device_pool",
 ]

@@ -42,7 +42,8 @@ EXPORTED = [
     "pcs_loopback_group_create", "pcs_loopback_group_destroy", "pcs_lop_plan_set_loopback",
     "pcs_shard_layout_weighted", "pcs_nearest_all", "pcs_deviation", "pcs_deviation_to_mesh",
     "pcs_format_cloud", "pcs_parse_cloud", "pcs_parse_mesh", "pcs_format_double",
-    "pcs_format_cloud_alloc", "pcs_free_buffer",
+    "pcs_format_cloud_alloc", "pcs_free_buffer", "pcs_lop_plan_record_counts",
+    "pcs_lop_plan_query_counts", "pcs_trim_device_pool",
 ]
 
 
@@ -140,6 +141,9 @@ def lib():
                                             C.c_uint64]
         L.pcs_lop_plan_launches.argtypes = [C.c_void_p]
         L.pcs_lop_plan_launches.restype = C.c_uint64
+        L.pcs_lop_plan_record_counts.argtypes = [C.c_void_p, C.c_int32]
+        L.pcs_lop_plan_query_counts.argtypes = [C.c_void_p, C.POINTER(C.c_int32), _u8p, C.c_uint64]
+        L.pcs_trim_device_pool.argtypes = [C.c_int32]
         L.pcs_radius_query_all.argtypes = [C.POINTER(LopDesc), _dp, C.c_uint64, _dp, C.c_uint64,
                                            C.c_double, _u64p, _u32p, C.c_uint64]
         L.pcs_density_weights.argtypes = [C.POINTER(LopDesc), _dp, C.c_uint64, _dp]

@@ -134,6 +134,25 @@ pcs_status pcs_lop_plan_upload(pcs_lop_plan* p, const double* P_xyz, uint64_t n,
 
 pcs_status pcs_nccl_unique_id(uint8_t id_out[128]);
 
+pcs_status pcs_lop_plan_record_counts(pcs_lop_plan* p, int32_t enable) {
+    return guarded([&] {
+        PLAN(p);
+        plan.record_counts(enable != 0);
+    });
+}
+
+pcs_status pcs_lop_plan_query_counts(pcs_lop_plan* p, int32_t* counts4, uint8_t* ever_flags,
+                                     uint64_t m) {
+    return guarded([&] {
+        PLAN(p);
+        plan.query_counts(counts4, ever_flags, m);
+    });
+}
+
+pcs_status pcs_trim_device_pool(int32_t device) {
+    return guarded([&] { pcsb::trim_device_pool(pcsb::select_device(device)); });
+}
+
 pcs_status pcs_lop_plan_set_comm(pcs_lop_plan* p, const uint8_t id[128], int32_t nranks,
                                  int32_t rank) {
     return guarded([&] {

@@ -2,6 +2,7 @@
 // radix sort of (key, index), the gather into sorted order and the cell
 // lower-bound table.  Replaces the reference's kd-tree build + radius query
 // (proj/src/spatial.cpp:32-111) with integer work that is HBM/L2-bound.
+#include "dev_knobs.h"
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -643,7 +644,7 @@ int radix_sort(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_
         cudaDeviceGetAttribute(&ok, cudaDevAttrCooperativeLaunch, dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rs_coop_kernel, RS_THREADS, 0);
-        if (const char* e = std::getenv("PCSB_COOP_SORT"))  // developer knob: 0 disables
+        if (const char* e = dev_knob("PCSB_COOP_SORT"))  // developer knob: 0 disables
             if (std::atoi(e) == 0) ok = 0;
         return ok ? sms * per : 0;
     }();
@@ -651,7 +652,7 @@ int radix_sort(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_
     // measured: one cooperative launch wins for small sorts (config 2's 100K keys:
     // 0.14 -> 0.10 ms per query order) and loses from ~1M keys on
     static const uint32_t coop_max = [] {
-        const char* e = std::getenv("PCSB_COOP_MAX");  // developer knob (keys)
+        const char* e = dev_knob("PCSB_COOP_MAX");  // developer knob (keys)
         return e ? (uint32_t)std::atol(e) : (256u << 10);
     }();
     if (coop_blocks > 0 && n <= coop_max) {
@@ -731,7 +732,7 @@ int build_query_list(const V* sorted_pts, uint32_t n, const GridGeom& g, double 
     // query curve: Hilbert (measured tighter groups than the Z-curve) unless the
     // developer knob PCSB_CURVE=morton
     static const int hilbert = [] {
-        const char* e = std::getenv("PCSB_CURVE");
+        const char* e = dev_knob("PCSB_CURVE");
         return (e && std::string(e) == "morton") ? 0 : 1;
     }();
     ax.hilbert = hilbert;
@@ -741,7 +742,7 @@ int build_query_list(const V* sorted_pts, uint32_t n, const GridGeom& g, double 
     // the height-field config: fuller groups outweigh their larger boxes)
     const double unit = 0.5 * g.cs * std::ldexp(1.0, ax.shift);
     int k = (int)std::floor(std::log2(2.0 * support / unit) + 0.5);
-    if (const char* e = std::getenv("PCSB_BLOCK_ADJ")) k += std::atoi(e);  // developer knob
+    if (const char* e = dev_knob("PCSB_BLOCK_ADJ")) k += std::atoi(e);  // developer knob
     k = std::max(0, std::min(k, 10));
     *block_shift = 0;
     if (ax.hilbert) *block_shift = 3 * std::min(k, hb);

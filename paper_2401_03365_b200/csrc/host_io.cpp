@@ -4,6 +4,7 @@
 // through its own pinned buffer with one thread).  Here the copy goes through a
 // process-wide pool of two pinned 16 MB chunks filled by OpenMP threads while
 // the DMA of the previous chunk runs: ~24 GB/s measured (tools/h2d_probe.cu).
+#include "dev_knobs.h"
 #include "host_io.h"
 
 #include <omp.h>
@@ -33,7 +34,7 @@ struct Staging {
 // host threads filling / draining the pinned chunks (developer knob PCSB_IO_THREADS)
 int staging_threads() {
     static const int t = [] {
-        const char* e = std::getenv("PCSB_IO_THREADS");
+        const char* e = dev_knob("PCSB_IO_THREADS");
         const int v = e ? std::atoi(e) : 16;  // e2e (config 3): 8 -> 16 threads +3%
         return std::max(1, std::min(v, omp_get_num_procs()));
     }();

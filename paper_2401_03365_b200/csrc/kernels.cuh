@@ -108,10 +108,16 @@ struct FastArgs {
     float4* attr;             // PH_ATTR -> PH_REP: per list position (sum w, sum w d)
     int2* attr_n;             //   (hits, zero-distance candidates)
     uint8_t* ever_isolated;   // internal index
+    int4* qcounts;            // parity facility (nullptr = off), internal index: per query
+                              // {attraction hits, repulsion hits, coincident, flags}
+    uint8_t* qever;           // with qcounts: OR of the flags over all sweeps
     RunState* st;
     SweepSlot* slot;
     const uint32_t* done;
 };
+
+// flags of FastArgs::qcounts / ExactArgs::qcounts (pcs_lop_plan_query_counts)
+enum : int { QC_ISOLATED = 1, QC_ANCHORED = 2, QC_DEFERRED = 4 };
 
 // rep_mode: 0 = attraction only (mu == 0), 1 = inv-cube repulsion, 2 = neg-linear.
 // phase: 0 = fused, 1 = attraction pass (writes attr), 2 = repulsion + update.
@@ -162,6 +168,8 @@ struct ExactArgs {
     int wlop;
     V* Xnext;
     uint8_t* ever_isolated;
+    int4* qcounts;            // as FastArgs::qcounts (nullptr = off)
+    uint8_t* qever;
     RunState* st;
     SweepSlot* slot;
     const uint32_t* done;
@@ -190,7 +198,8 @@ void launch_radius_dump(const typename Vec4<T>::type* C, const uint32_t* Corder,
                         cudaStream_t s);
 
 // ---- sweep bookkeeping --------------------------------------------------------
-void launch_finalize_sweep(RunState* st, SweepSlot* slot, int sweep, double tol, cudaStream_t s);
+void launch_finalize_sweep(RunState* st, SweepSlot* slot, SweepSlot* next, int sweep, double tol,
+                           cudaStream_t s);
 template <typename T>
 void launch_unpermute(const typename Vec4<T>::type* X, const uint32_t* orig_of_internal,
                       uint32_t mpad, double* out_xyz, cudaStream_t s);

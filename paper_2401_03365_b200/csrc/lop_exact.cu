@@ -1,3 +1,4 @@
+#include "dev_knobs.h"
 #include <cstdlib>
 // lop_exact.cu — the exact-arithmetic path (fp64 math, reference predicate).
 //
@@ -331,6 +332,13 @@ __global__ void __launch_bounds__(NW == 1 ? EX_THREADS : 32 * NW) exact_kernel(c
                 if (coinc) atomicAdd(&a.st->coincident_pairs, coinc);
             }
             if (a.count_careful) atomicAdd(&a.st->careful_points, 1ull);
+            if (a.qcounts) {
+                const int fl = (isolated ? QC_ISOLATED : (attracted ? 0 : QC_ANCHORED)) |
+                               (a.count_careful ? QC_DEFERRED : 0);
+                a.qcounts[q_int] = make_int4(attracted ? (int)cnt : 0, attracted ? (int)rcnt : 0,
+                                             attracted ? (int)coinc : 0, fl);
+                a.qever[q_int] |= (uint8_t)fl;
+            }
         }
     }
 }
@@ -414,8 +422,10 @@ radius_dump_kernel(const typename Vec4<T>::type* __restrict__ C, const uint32_t*
     }
 }
 
-__global__ void finalize_kernel(RunState* st, SweepSlot* slot, int sweep, double tol) {
+__global__ void finalize_kernel(RunState* st, SweepSlot* slot, SweepSlot* next, int sweep,
+                                double tol) {
     if (st->done) return;
+    if (next != slot) *next = SweepSlot{};  // recycled slot of the next sweep
     const unsigned long long b = slot->max_disp_bits;
     const double md = __longlong_as_double((long long)b);
     st->iterations_run = sweep;
@@ -514,8 +524,9 @@ void launch_radius_dump(const typename Vec4<T>::type* C, const uint32_t* Corder,
         C, Corder, Cstart, g, Q, m, r2, s_pad, offsets_or_counts, idx);
 }
 
-void launch_finalize_sweep(RunState* st, SweepSlot* slot, int sweep, double tol, cudaStream_t s) {
-    finalize_kernel<<<1, 1, 0, s>>>(st, slot, sweep, tol);
+void launch_finalize_sweep(RunState* st, SweepSlot* slot, SweepSlot* next, int sweep, double tol,
+                           cudaStream_t s) {
+    finalize_kernel<<<1, 1, 0, s>>>(st, slot, next, sweep, tol);
 }
 
 template <typename T>
@@ -589,7 +600,7 @@ void launch_shard_work(const typename Vec4<T>::type* X0, uint32_t m, const GridG
                        double s_pad, const uint32_t* Pstart, float* w, cudaStream_t s) {
     if (!m) return;
     static const float per_query = [] {  // developer knob: per-query constant of the estimate
-        const char* e = std::getenv("PCSB_SHARD_C");
+        const char* e = dev_knob("PCSB_SHARD_C");
         return e ? (float)std::atof(e) : 64.0f;
     }();
     shard_work_kernel<typename Vec4<T>::type><<<blocks_for(m, 256), 256, 0, s>>>(

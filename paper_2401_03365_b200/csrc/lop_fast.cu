@@ -26,6 +26,7 @@
 //    meet an exact zero distance in the attraction (sweeps >= 2), a coincident
 //    projected pair or a non-finite sum are deferred to the exact fp64 kernel
 //    (lop_exact.cu).  The neighbour SET is always the reference's.
+#include "dev_knobs.h"
 #include <cfloat>
 #include <cstdlib>
 
@@ -714,7 +715,7 @@ fast_kernel(const FastArgs a) {
                            rp.rneg - rp.hneg);
 #endif
                     const uint32_t pos = atomicAdd(&a.slot->careful_count, 1u);
-                    a.careful_list[pos] = qint;
+                    a.careful_list[pos] = qint;  // counts: written by the exact kernel
                 } else {
                     float nx = q.x, ny = q.y, nz = q.z;
                     bool isolated = false;
@@ -739,6 +740,11 @@ fast_kernel(const FastArgs a) {
                         }
                     }
                     a.Xnext[qint] = make_float4(nx, ny, nz, 0.f);
+                    if (a.qcounts) {
+                        const int fl = isolated ? QC_ISOLATED : (attracted ? 0 : QC_ANCHORED);
+                        a.qcounts[qint] = make_int4((int)n_attr, (int)n_rep, 0, fl);
+                        a.qever[qint] |= (uint8_t)fl;
+                    }
                     const float ddx = nx - q.x, ddy = ny - q.y, ddz = nz - q.z;
                     disp = sqrtf(fmaf(ddz, ddz, fmaf(ddy, ddy, ddx * ddx)));
                     if (isolated) {
@@ -882,7 +888,7 @@ uint32_t work_unit_queries(uint32_t nq, int total_warps) {
     (void)nq;
     (void)total_warps;
     static const uint32_t u = [] {
-        const char* e = std::getenv("PCSB_UNIT");  // developer knob (1..32)
+        const char* e = dev_knob("PCSB_UNIT");  // developer knob (1..32)
         const int v = e ? std::atoi(e) : 16;
         return (uint32_t)(v >= 1 && v <= 32 ? v : 16);
     }();

@@ -20,6 +20,7 @@
 // smaller index can remain.  Distances are the reference's exactly
 // (`norm2(c - q)` with every fp64 operation individually rounded, then sqrt);
 // the aggregate is summed on the host in index order, as the reference does.
+#include "dev_knobs.h"
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -52,7 +53,7 @@ GridGeom nn_grid(const double lo[3], const double hi[3], uint64_t n) {
     for (int a = 0; a < 3; ++a) ext = std::max(ext, hi[a] - lo[a]);
     if (!(ext > 0.0)) ext = 1.0;
     double target = std::min(8.0 * (double)n, (double)(1u << 26));
-    if (const char* e = std::getenv("PCSB_NN_CELLS_PER_POINT"))  // developer knob
+    if (const char* e = dev_knob("PCSB_NN_CELLS_PER_POINT"))  // developer knob
         target = std::min(std::atof(e) * (double)n, (double)(1u << 26));
     target = std::max(target, 1.0);
     // largest-first bisection on the cell side: cells_for is non-increasing in cs

@@ -2,6 +2,7 @@
 // pcs::lop_project (proj/src/lop.cpp:10-127): validate, build the data index
 // once (:24), then per sweep rebuild the index over the moving set (:39),
 // update every point (:41-100), aggregate (:102-113) and stop early (:116-119).
+#include "dev_knobs.h"
 #include "plan.cuh"
 
 #include <algorithm>
@@ -70,7 +71,7 @@ void cuda_check(cudaError_t e, const char* what) {
 #define PCSB_MAX_CELLS 1073741824.0  // 2^30 cells: a 4 GB data-grid table
 #endif
 
-GridGeom make_grid(const double lo_in[3], const double hi_in[3], double support) {
+GridGeom make_grid(const double lo_in[3], const double hi_in[3], double support, uint64_t npts) {
     double lo[3], hi[3];
     for (int a = 0; a < 3; ++a) {
         lo[a] = lo_in[a];
@@ -81,7 +82,9 @@ GridGeom make_grid(const double lo_in[3], const double hi_in[3], double support)
     // keys are plain linear cells (x fastest): the query order comes from a
     // separate Morton sort of positions (build_query_list)
     double cs;
-    const double kMax = PCSB_MAX_CELLS;
+    // the table is O(points): at most 64 cells per point (>= 2^24 cells), so a
+    // small cloud in a large box never reserves a multi-GB table
+    const double kMax = std::min((double)PCSB_MAX_CELLS, std::max(16777216.0, 64.0 * (double)npts));
     // y/z cell side s/3 (measured sweeps/s vs s/4, with x cells up to 4x finer:
     // config 3 +3.3%, config 4 +5%, config 5 +11%; s/5 similar on config 3,
     // worse on config 2) when x cells 4x finer still fit the 2^30-cell table;
@@ -98,7 +101,7 @@ GridGeom make_grid(const double lo_in[3], const double hi_in[3], double support)
         while (cells_for(lo, hi, cs) > (double)(1u << 27)) cs *= 1.25;
     }
     // developer knob (grid experiments): PCSB_CELL_FRAC = cell side / support
-    if (const char* e = std::getenv("PCSB_CELL_FRAC")) {
+    if (const char* e = dev_knob("PCSB_CELL_FRAC")) {
         const double f = std::atof(e);
         if (f > 0.0 && cells_for(lo, hi, support * f) <= kMax) cs = support * f;
     }
@@ -114,7 +117,7 @@ GridGeom make_grid(const double lo_in[3], const double hi_in[3], double support)
             xsub = t;
             break;
         }
-    if (const char* e = std::getenv("PCSB_XSUB")) xsub = std::max(1, std::atoi(e));  // developer knob
+    if (const char* e = dev_knob("PCSB_XSUB")) xsub = std::max(1, std::atoi(e));  // developer knob
     g.cs = cs;
     g.inv_cs = 1.0 / cs;
     g.xsub = xsub;
@@ -156,7 +159,7 @@ GridGeom make_grid_scaled(const double lo_in[3], const double hi_in[3], double s
             g.xsub = t;
             break;
         }
-    if (const char* e = std::getenv("PCSB_XSUB_X")) g.xsub = std::max(1, std::atoi(e));  // developer knob
+    if (const char* e = dev_knob("PCSB_XSUB_X")) g.xsub = std::max(1, std::atoi(e));  // developer knob
     g.csx = g.cs / g.xsub;
     g.inv_csx = 1.0 / g.csx;
     g.ox = lo[0] - g.cs;
@@ -182,7 +185,7 @@ double x_cell_scale(uint64_t n, uint64_t m, const GridGeom& g) {
     (void)n;
     (void)m;
     (void)g;
-    if (const char* e = std::getenv("PCSB_XCELL")) return std::atof(e);
+    if (const char* e = dev_knob("PCSB_XCELL")) return std::atof(e);
     return 2.0;
 }
 
@@ -249,11 +252,11 @@ Plan::Plan(const pcs_lop_desc& d) : d_(d) {
     // repulsion over the sparser projected set: 16-query groups amortise the
     // per-row cost better (measured -1..2% sweep time on configs 3 and 4)
     rep_lanes_ = d_.lanes_per_point ? lanes_ : 4;  // measured with bisected groups: 4 >= 2 on configs 3, 4, 5
-    if (const char* e = std::getenv("PCSB_REORDER_EVERY")) reorder_every_ = std::max(1, std::atoi(e));
-    if (const char* e = std::getenv("PCSB_ASYNC_ORDER")) async_order_ = std::atoi(e) != 0;  // developer knob
-    if (const char* e = std::getenv("PCSB_FUSED")) fused_ = std::atoi(e) != 0;  // developer knob
-    if (const char* e = std::getenv("PCSB_BISECT")) bisect_ = std::atoi(e) != 0;  // developer knob
-    if (const char* e = std::getenv("PCSB_REP_LANES")) rep_lanes_ = std::atoi(e);  // developer knob
+    if (const char* e = dev_knob("PCSB_REORDER_EVERY")) reorder_every_ = std::max(1, std::atoi(e));
+    if (const char* e = dev_knob("PCSB_ASYNC_ORDER")) async_order_ = std::atoi(e) != 0;  // developer knob
+    if (const char* e = dev_knob("PCSB_FUSED")) fused_ = std::atoi(e) != 0;  // developer knob
+    if (const char* e = dev_knob("PCSB_BISECT")) bisect_ = std::atoi(e) != 0;  // developer knob
+    if (const char* e = dev_knob("PCSB_REP_LANES")) rep_lanes_ = std::atoi(e);  // developer knob
     device_ = select_device(d_.device);
     PCSB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     {
@@ -275,13 +278,13 @@ Plan::Plan(const pcs_lop_desc& d) : d_(d) {
         // all block slots on one GPU (one slot fewer: -1.5% .. -2.5% on configs 3-4);
         // decided again at upload for small or sharded projected sets
         int per_sm = fast_grid_ / sms;
-        if (const char* e = std::getenv("PCSB_ATTR_BLOCKS")) per_sm = std::atoi(e);  // developer knob
+        if (const char* e = dev_knob("PCSB_ATTR_BLOCKS")) per_sm = std::atoi(e);  // developer knob
         attr_grid_ = sms * std::max(1, per_sm);
     }
     exact_grid_ = sms * 8;
     support_ = d_.h * d_.cutoff_multiple;
     r2_ = support_ * support_;
-    if (const char* e = std::getenv("PCSB_EMULATE_RANK")) {  // developer knob "N:r"
+    if (const char* e = dev_knob("PCSB_EMULATE_RANK")) {  // developer knob "N:r"
         int n = 0, r = 0;
         if (std::sscanf(e, "%d:%d", &n, &r) == 2 && n >= 1 && r >= 0 && r < n) {
             nranks_ = n;
@@ -325,12 +328,21 @@ cudaMemPool_t device_pool(int dev) {
         props.location.type = cudaMemLocationTypeDevice;
         props.location.id = dev;
         PCSB_CUDA(cudaMemPoolCreate(&pools[dev], &props));
-        uint64_t keep = ~0ull;
+        // keep up to 16 GB reserved between calls (warm repeated calls: the plan's
+        // buffers are sub-allocations); beyond that, memory returns to the
+        // device at each synchronisation; pcs_trim_device_pool releases it all
+        uint64_t keep = 16ull << 30;
         PCSB_CUDA(cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep));
     }
     return pools[dev];
 }
 }  // namespace
+
+void trim_device_pool(int dev) {
+    PCSB_CUDA(cudaSetDevice(dev));
+    PCSB_CUDA(cudaDeviceSynchronize());
+    PCSB_CUDA(cudaMemPoolTrimTo(device_pool(dev), 0));
+}
 
 void* Plan::talloc(size_t bytes) {
     void* p = nullptr;
@@ -391,6 +403,9 @@ template <typename T>
 void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     using V = typename Vec4<T>::type;
     free_all();
+    qcounts_ = nullptr;
+    qever_ = nullptr;
+    record_counts_ = false;
     n_ = n;
     m_ = m;
     cudaEvent_t e0, e1;
@@ -434,7 +449,7 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
             throw Failure(PCS_ERR_INVALID_PARAM, "clouds must have finite coordinates");
         maxabs = std::max(maxabs, std::max(std::fabs(lo[a]), std::fabs(hi[a])));
     }
-    g_ = make_grid(lo, hi, support_);
+    g_ = make_grid(lo, hi, support_, n);
     gX_ = make_grid_scaled(lo, hi, support_, x_cell_scale(n, m, g_), g_);
     s_pad_ = support_ * (1.0 + std::ldexp(1.0, -10)) + 1e-12 * maxabs;
     maxabs_ = maxabs;
@@ -573,7 +588,7 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
             }
         }
         X_init_ = dalloc((size_t)std::max<uint32_t>(mpad_, 1) * sizeof(V));
-        if (nranks_ >= 4 && !std::getenv("PCSB_ATTR_BLOCKS")) {
+        if (nranks_ >= 4 && !dev_knob("PCSB_ATTR_BLOCKS")) {
             // with a quarter of the queries or less the attraction pass is short and
             // the side stream's grid rebuild (latency-bound) would be exposed after
             // it: leave it one block slot per SM (8-GPU emulation: -4% per sweep)
@@ -600,7 +615,7 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
         X_init_ = dalloc((size_t)std::max<uint32_t>(mpad_, 1) * sizeof(V));
         own_lo_ = 0;
         own_cnt_ = (uint32_t)m;
-        if (m < (1u << 18) && !std::getenv("PCSB_ATTR_BLOCKS")) {
+        if (m < (1u << 18) && !dev_knob("PCSB_ATTR_BLOCKS")) {
             // a short attraction pass would end before the side stream's grid
             // rebuild got SM slots: leave it one per SM (config 2, 100k queries:
             // sweep -13%; configs 4 / 3 with 400k / 1M queries: +2.5% / +1.5%)
@@ -666,6 +681,7 @@ void Plan::reset() {
     PCSB_CUDA(cudaMemsetAsync(st_, 0, sizeof(RunState), stream_));
     PCSB_CUDA(cudaMemsetAsync(slots_, 0, (size_t)slot_cap_ * sizeof(SweepSlot), stream_));
     PCSB_CUDA(cudaMemsetAsync(ever_iso_, 0, std::max<uint32_t>(mpad_, 1), stream_));
+    if (qever_) PCSB_CUDA(cudaMemsetAsync(qever_, 0, std::max<uint32_t>(mpad_, 1), stream_));
     PCSB_CUDA(cudaStreamSynchronize(stream_));
     sweeps_issued_ = 0;
     q_stale_ = true;
@@ -675,8 +691,6 @@ void Plan::reset() {
 void Plan::run(int sweeps, bool sync) {
     if (!uploaded_) throw Failure(PCS_ERR_INVALID_PARAM, "plan has no data (upload first)");
     if (sweeps <= 0) sweeps = d_.iterations;
-    if (sweeps_issued_ + sweeps > slot_cap_)
-        throw Failure(PCS_ERR_INVALID_PARAM, "too many sweeps for one plan run (reset the plan)");
     PCSB_CUDA(cudaSetDevice(device_));
     synchronize();
     PCSB_CUDA(cudaEventRecord(run_ev_[0], stream_));
@@ -713,7 +727,7 @@ void Plan::synchronize() {
         const float exposed = tg > ta ? tg - ta : 0.f;
         sort_ms_ += q + exposed;
         kernel_ms_ += tk - q - exposed;
-        static const bool dbg = std::getenv("PCSB_DEBUG_TIMES") != nullptr;  // developer knob
+        static const bool dbg = dev_knob("PCSB_DEBUG_TIMES") != nullptr;  // developer knob
         if (dbg) {
             float te = 0.f;
             PCSB_CUDA(cudaEventElapsedTime(&te, se.e[0], se.e[5]));
@@ -756,7 +770,7 @@ template <typename T>
 void Plan::density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur) {
     using V = typename Vec4<T>::type;
     const bool multi = sharded();
-    SweepSlot* slot = slots_ + (sweeps_issued_ - 1);
+    SweepSlot* slot = slots_ + (sweeps_issued_ - 1) % slot_cap_;
     if (fp32_) {
         DensityArgs da{};
         da.C = (const float4*)Xcur;
@@ -801,7 +815,10 @@ void Plan::density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur) {
 template <typename T>
 void Plan::enqueue_sweep(int k) {
     using V = typename Vec4<T>::type;
-    SweepSlot* slot = slots_ + (k - 1);
+    // sweep slots are recycled modulo slot_cap_: finalize of sweep k clears the
+    // slot of sweep k + 1 (any iteration count, LopParams::iterations >= 1)
+    SweepSlot* slot = slots_ + (k - 1) % slot_cap_;
+    SweepSlot* next_slot = slots_ + k % slot_cap_;
     void* cur = X_[(k - 1) & 1];
     void* nxt = X_[k & 1];
     const uint32_t* done = &st_->done;
@@ -815,6 +832,9 @@ void Plan::enqueue_sweep(int k) {
         for (auto& e : se.e) PCSB_CUDA(cudaEventCreate(&e));
     }
     PCSB_CUDA(cudaEventRecord(se.e[0], stream_));
+    if (record_counts_)  // queries this rank does not own stay -1
+        PCSB_CUDA(cudaMemsetAsync(qcounts_, 0xFF, (size_t)std::max<uint32_t>(mpad_, 1) * sizeof(int4),
+                                  stream_));
     const int rep = d_.mu > 0.0 ? (d_.eta_kind == PCS_ETA_INV_CUBE ? 1 : 2) : 0;
     // the projected set's grid is needed by the repulsion (and WLOP w_i) only
     const bool xgrid = rep != 0;
@@ -857,9 +877,12 @@ void Plan::enqueue_sweep(int k) {
     // previous sweep's readers of the alternate buffers completed before X^k was
     // ready, which stream2_ waited for
     if (xgrid && async_order_ && sweeps_since_order_ >= reorder_every_ && k < last_sweep_) {
+        // done == nullptr: this chain runs beside the main stream, whose
+        // finalize kernel may set the flag mid-launch; a cooperative sort whose
+        // blocks read the flag at different times would deadlock in grid.sync
         launches_ += build_query_list((const V*)cur + own_lo_, own_cnt_, g_, support_, nullptr, 0, 0,
                                       q_keys_alt_, q_skeys_alt_, q_list_alt_, &block_shift_alt_, rs2_,
-                                      done, stream2_, own_lo_);
+                                      nullptr, stream2_, own_lo_);
         PCSB_CUDA(cudaEventRecord(ev_qready_, stream2_));
         q_next_ready_ = true;
     }
@@ -890,13 +913,13 @@ void Plan::enqueue_sweep(int k) {
         // (emulated 8-rank sweep: slowest rank 1.03 ms bisected vs 0.72 ms cut).
         const bool bis = bisect_ && !multi;
         a.bisect = bis ? 1 : 0;
-        a.unit = bis && !std::getenv("PCSB_UNIT") && !d_.density_weights
+        a.unit = bis && !dev_knob("PCSB_UNIT") && !d_.density_weights
                      ? 32u
                      : work_unit_queries(nq, fast_grid_ * 4);
         {   // the last ~one group per warp of the attraction pass comes in one-group units
             const uint32_t q = 32u / (uint32_t)lanes_;
             static const double tail_frac = [] {  // developer knob: warps' groups in the tail
-                const char* e = std::getenv("PCSB_TAIL");
+                const char* e = dev_knob("PCSB_TAIL");
                 return e ? std::atof(e) : 2.0;  // ~2 groups per warp: emulated 8-rank -3%, 1 GPU neutral
             }();
             const uint64_t tail = (uint64_t)(tail_frac * attr_grid_ * 4u * q);
@@ -919,6 +942,8 @@ void Plan::enqueue_sweep(int k) {
         a.attr = attr_;
         a.attr_n = attr_n_;
         a.ever_isolated = ever_iso_;
+        a.qcounts = record_counts_ ? qcounts_ : nullptr;
+        a.qever = qever_;
         a.st = st_;
         a.slot = slot;
         a.done = done;
@@ -967,6 +992,8 @@ void Plan::enqueue_sweep(int k) {
         e.wlop = d_.density_weights;
         e.Xnext = (V*)nxt;
         e.ever_isolated = ever_iso_;
+        e.qcounts = record_counts_ ? qcounts_ : nullptr;
+        e.qever = qever_;
         e.st = st_;
         e.slot = slot;
         e.done = done;
@@ -990,10 +1017,61 @@ void Plan::enqueue_sweep(int k) {
         coll_->allreduce(&slot->max_disp_bits, 1, CDType::U64, COp::Max, stream_);
         coll_->group_end();
     }
-    launch_finalize_sweep(st_, slot, k, d_.convergence_tol, stream_);
+    launch_finalize_sweep(st_, slot, next_slot, k, d_.convergence_tol, stream_);
     launches_ += 1;
     PCSB_CUDA(cudaEventRecord(se.e[5], stream_));
     pending_.push_back(se);
+}
+
+void Plan::record_counts(bool on) {
+    if (!uploaded_) throw Failure(PCS_ERR_INVALID_PARAM, "record_counts needs an uploaded plan");
+    PCSB_CUDA(cudaSetDevice(device_));
+    synchronize();
+    const size_t mp = std::max<uint32_t>(mpad_, 1);
+    if (on && !qcounts_) {
+        qcounts_ = (int4*)dalloc(mp * sizeof(int4));
+        qever_ = (uint8_t*)dalloc(mp);
+        PCSB_CUDA(cudaMemsetAsync(qcounts_, 0xFF, mp * sizeof(int4), stream_));
+        PCSB_CUDA(cudaMemsetAsync(qever_, 0, mp, stream_));
+        PCSB_CUDA(cudaStreamSynchronize(stream_));
+    }
+    record_counts_ = on;
+}
+
+// Per query (original order) of the last sweep: {attraction interactions,
+// repulsion interactions, coincident pairs, flags (QC_*)}; -1 for queries this
+// rank did not own (sharded plans); ever_flags = the flags OR-ed over the run.
+void Plan::query_counts(int32_t* counts4, uint8_t* ever_flags, uint64_t m) {
+    if (!record_counts_ || !qcounts_)
+        throw Failure(PCS_ERR_INVALID_PARAM, "per-query counts were not recorded (record_counts)");
+    if (m != m_) throw Failure(PCS_ERR_INVALID_PARAM, "query_counts: m must equal the plan's m");
+    PCSB_CUDA(cudaSetDevice(device_));
+    synchronize();
+    std::vector<int4> c(mpad_);
+    std::vector<uint8_t> ev(mpad_);
+    std::vector<uint32_t> ooi;
+    if (mpad_) {
+        PCSB_CUDA(cudaMemcpyAsync(c.data(), qcounts_, (size_t)mpad_ * sizeof(int4),
+                                  cudaMemcpyDeviceToHost, stream_));
+        PCSB_CUDA(cudaMemcpyAsync(ev.data(), qever_, mpad_, cudaMemcpyDeviceToHost, stream_));
+        if (orig_of_internal_) {
+            ooi.resize(mpad_);
+            PCSB_CUDA(cudaMemcpyAsync(ooi.data(), orig_of_internal_, (size_t)mpad_ * sizeof(uint32_t),
+                                      cudaMemcpyDeviceToHost, stream_));
+        }
+        PCSB_CUDA(cudaStreamSynchronize(stream_));
+    }
+    for (uint32_t i = 0; i < mpad_; ++i) {
+        const uint32_t o = ooi.empty() ? i : ooi[i];
+        if (o >= m) continue;
+        if (counts4) {
+            counts4[4 * (size_t)o] = c[i].x;
+            counts4[4 * (size_t)o + 1] = c[i].y;
+            counts4[4 * (size_t)o + 2] = c[i].z;
+            counts4[4 * (size_t)o + 3] = c[i].w;
+        }
+        if (ever_flags) ever_flags[o] = ev[i];
+    }
 }
 
 void Plan::download(double* X_out, pcs_lop_summary* s, uint32_t* iso, uint64_t cap) {
@@ -1009,7 +1087,7 @@ void Plan::download(double* X_out, pcs_lop_summary* s, uint32_t* iso, uint64_t c
         unsigned long long hv[7] = {hs.isolated_events, hs.coincident_pairs, hs.interactions_attr,
                                     hs.interactions_rep, hs.density_pairs, hs.careful_points,
                                     hs.lane_candidates};
-        PCSB_CUDA(cudaMemcpy(tmp, hv, sizeof(hv), cudaMemcpyHostToDevice));
+        PCSB_CUDA(cudaMemcpyAsync(tmp, hv, sizeof(hv), cudaMemcpyHostToDevice, stream_));
         coll_->allreduce(tmp, 7, CDType::U64, COp::Sum, stream_);
         PCSB_CUDA(cudaMemcpyAsync(hv, tmp, sizeof(hv), cudaMemcpyDeviceToHost, stream_));
         PCSB_CUDA(cudaStreamSynchronize(stream_));
@@ -1121,7 +1199,7 @@ struct TmpGrid {
                 throw Failure(PCS_ERR_INVALID_PARAM, "clouds must have finite coordinates");
             maxabs = std::max(maxabs, std::max(std::fabs(lo[a]), std::fabs(hi[a])));
         }
-        g = make_grid(lo, hi, support);
+        g = make_grid(lo, hi, support, n);
         s_pad = support * (1.0 + std::ldexp(1.0, -10)) + 1e-12 * maxabs;
         this->maxabs = maxabs;
         uint32_t* keys = (uint32_t*)alloc(nn * sizeof(uint32_t));

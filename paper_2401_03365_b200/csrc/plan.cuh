@@ -31,7 +31,9 @@ void cuda_check(cudaError_t e, const char* what);
 #define PCSB_CUDA(x) ::pcsb::cuda_check((x), #x)
 
 // Derives the shared grid for a bounding box and a support radius.
-GridGeom make_grid(const double lo[3], const double hi[3], double support);
+GridGeom make_grid(const double lo[3], const double hi[3], double support, uint64_t npts);
+// releases the reserved memory of the library's stream-ordered pool on `dev`
+void trim_device_pool(int dev);
 GridGeom make_grid_scaled(const double lo[3], const double hi[3], double support, double scale,
                           const GridGeom& base);
 double x_cell_scale(uint64_t n, uint64_t m, const GridGeom& g);
@@ -56,6 +58,9 @@ public:
     double last_run_ms() const { return last_run_ms_; }
     void download(double* X_out, pcs_lop_summary* s, uint32_t* iso, uint64_t cap);
     uint64_t launches() const { return launches_; }
+    // Parity facility: per-query counts of every sweep (pcs_lop_plan_query_counts).
+    void record_counts(bool on);
+    void query_counts(int32_t* counts4, uint8_t* ever_flags, uint64_t m);
 
 private:
     template <typename T> void upload_t(const double* P, uint64_t n, const double* X0, uint64_t m);
@@ -132,6 +137,9 @@ private:
     uint32_t* careful_list_ = nullptr;
     uint8_t* ever_iso_ = nullptr;
     uint32_t* orig_of_internal_ = nullptr;  // multi-GPU only
+    bool record_counts_ = false;      // parity facility (record_counts)
+    int4* qcounts_ = nullptr;         // last sweep, internal index
+    uint8_t* qever_ = nullptr;        // flags OR-ed over the run
     RadixScratch rs_{};
     RadixScratch rs2_{};              // stream2_'s sorts
     float4* attr_ = nullptr;          // attraction sums per query-list position (PH_ATTR -> PH_REP)

@@ -253,6 +253,20 @@ class LopPlan:
     def launches(self) -> int:
         return int(L.lib().pcs_lop_plan_launches(self._h))
 
+    def record_counts(self, enable: bool = True) -> None:
+        """Parity facility: record per-query counts every sweep (after upload)."""
+        _check(L.lib().pcs_lop_plan_record_counts(self._h, 1 if enable else 0))
+
+    def query_counts(self) -> Tuple[np.ndarray, np.ndarray]:
+        """(counts[m, 4], ever_flags[m]) of the last sweep: attraction and repulsion
+        interactions, coincident pairs, flags (1 isolated, 2 anchored, 4 deferred to
+        the exact kernel); ever_flags = flags OR-ed over the run."""
+        cnt = np.zeros((max(self.m, 1), 4), dtype=np.int32)
+        ev = np.zeros(max(self.m, 1), dtype=np.uint8)
+        _check(L.lib().pcs_lop_plan_query_counts(self._h, cnt.ctypes.data_as(C.POINTER(C.c_int32)),
+                                                 _ptr(ev, L._u8p), self.m))
+        return cnt[: self.m], ev[: self.m]
+
     def download(self) -> Tuple[np.ndarray, LopSummary]:
         out = np.empty((self.m, 3), dtype=np.float64)
         iso = np.zeros(max(self.m, 1), dtype=np.uint32)
@@ -538,3 +552,8 @@ def config_params(config: int, h: Optional[float] = None) -> Tuple[LopParams, di
         c["h"] = h
     p = LopParams(kernel=KernelParams(c["h"] / 4.0, 4.0), mu=c["mu"], iterations=c["iterations"])
     return p, c
+
+
+def trim_device_pool(device: int = -1) -> None:
+    """Returns the device memory the library keeps reserved between calls."""
+    _check(L.lib().pcs_trim_device_pool(int(device)))

@@ -160,18 +160,43 @@ def test_fp32_full_trajectory(pb, orc, cfg, scale, h, its):
     P, X0, prm, c = scaled_case(pb, cfg, scale, h)
     prm.iterations = its
     eta = orc.ETA_NEG_LINEAR if c["eta"] == "neg_linear" else orc.ETA_INV_CUBE
-    out, s = pb.lop_project(P, X0, prm, eta=c["eta"], density_weights=c["wlop"], precision="fp32")
+    plan = pb.LopPlan(prm, eta=c["eta"], density_weights=c["wlop"], precision="fp32")
+    plan.upload(P, X0)
+    plan.record_counts(True)
+    plan.run(its)
+    out, s = plan.download()
+    _, gpu_ever = plan.query_counts()
+    plan.close()
     kw = dict(eta=eta, wlop=c["wlop"])
-    r = orc.lop_project(P, X0, prm.kernel.h, 4.0, prm.mu, its, store_f32=True, **kw)
+    r = orc.lop_project(P, X0, prm.kernel.h, 4.0, prm.mu, its, store_f32=True, flags=True, **kw)
     r64 = orc.lop_project(P, X0, prm.kernel.h, 4.0, prm.mu, its, **kw)
     tol = 1e-5 * bbox_diag(P)
     own = np.abs(r.points - r64.points).max(axis=1) > tol     # the oracle against itself
     err = np.abs(out - r.points).max(axis=1)
-    print(f"cfg{cfg}: max err {err.max():.2e}, beyond tol {(err > tol).sum()}/{len(err)}, "
-          f"oracle fp32-vs-fp64 storage beyond tol {own.sum()}")
-    # the B200 run disagrees with the oracle no more often than the oracle
-    # disagrees with itself when only its storage precision changes
-    assert (err > tol).mean() <= max(0.005, 2.0 * own.mean())
+    bad = err > tol
+    # Attribution: every point beyond the bar must be explained by a
+    # discontinuity of the reference's update (lop.cpp:55-69: a zero-distance
+    # data sample is skipped, an isolated-by-weight point is anchored) met in
+    # either run — the B200 run's deferred / anchored queries (fp32 zero
+    # distance -> exact kernel) or the oracle's anchored / zero-distance
+    # points — or lie within one support of such a point (its repulsion moved
+    # it).  Any other outlier fails.
+    event = ((gpu_ever & 6) != 0) | ((r.flags & (2 | 8)) != 0)
+    near = np.zeros_like(bad)
+    if bad.any() and event.any():
+        from scipy.spatial import cKDTree
+        s_sup = prm.kernel.support()
+        t_ev = cKDTree(np.concatenate([r.points[event], out[event]]))
+        d_ev = t_ev.query(np.concatenate([r.points[bad], out[bad]]))[0]
+        nb = int(bad.sum())
+        near[np.nonzero(bad)[0]] = np.minimum(d_ev[:nb], d_ev[nb:]) <= s_sup
+    unexplained = bad & ~event & ~near
+    print(f"cfg{cfg}: max err {err.max():.2e}, beyond tol {bad.sum()}/{len(err)} (events "
+          f"{int((bad & event).sum())}, near events {int((bad & ~event & near).sum())}, "
+          f"unexplained {int(unexplained.sum())}); events: gpu {int(((gpu_ever & 6) != 0).sum())} "
+          f"oracle {int(((r.flags & 10) != 0).sum())}; oracle fp32-vs-fp64 storage beyond tol "
+          f"{own.sum()}")
+    assert unexplained.sum() == 0, np.nonzero(unexplained)[0][:10]
     if cfg in (3, 5):
         assert err.max() <= tol
     # and the projected sets are statistically the same surface sample: mean fit

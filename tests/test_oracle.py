@@ -121,3 +121,78 @@ def test_density_weights_count_coincident_duplicates(orc):
     C = np.array([[0.0, 0, 0], [0.0, 0, 0], [1.0, 0, 0]])
     v = orc.density_weights(C, 0.2, 3.0)  # support 0.6: the far point is alone
     assert v[0] == 2.0 and v[1] == 2.0 and v[2] == 1.0  # theta(0) = 1 for the duplicate
+
+
+# ----------------------------------------------------------------------------
+# eta = -r: pinned to the reference's own lop.cpp (|eta'| bound to 1 at link
+# time, oracle/ref_etar_wrap.cpp) — fixture and live build
+# ----------------------------------------------------------------------------
+ETAR = ["height", "sphere", "duplicates", "random_isolated"]
+
+
+@pytest.fixture(scope="module")
+def golden_etar():
+    import os
+    return np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_etar.npz"))
+
+
+@pytest.mark.parametrize("name", ETAR)
+def test_neg_linear_bit_exact_vs_reference_fixture(orc, golden_etar, name):
+    g = golden_etar
+    h, cut, mu, it = g[f"lop_{name}_params"]
+    r = orc.lop_project(g[f"lop_{name}_P"], g[f"lop_{name}_X0"], h, cut, mu, int(it),
+                        eta=orc.ETA_NEG_LINEAR)
+    assert np.array_equal(r.points, g[f"lop_{name}_out"])
+    assert (r.iterations_run, int(r.converged), r.isolated_events, r.coincident_pairs) == \
+        tuple(g[f"lop_{name}_summary"])
+    assert np.array_equal(np.asarray(r.isolated_indices, dtype=np.int64),
+                          g[f"lop_{name}_isolated"])
+    if name == "duplicates":
+        assert r.coincident_pairs > 0
+    if name == "random_isolated":
+        assert r.isolated_events > 0
+
+
+def test_neg_linear_bit_exact_vs_live_reference(orc):
+    if not orc.ref_available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(77)
+    for k in range(3):
+        P = rng.uniform(-1, 1, (800, 3))
+        X0 = np.concatenate([P[rng.choice(800, 60, replace=False)], P[:3]])  # coincident pairs
+        a = orc.lop_project(P, X0, 0.1, 4.0, 0.45, 5, eta=orc.ETA_NEG_LINEAR)
+        b = orc.ref_lop_project(P, X0, 0.1, 4.0, 0.45, 5, eta=orc.ETA_NEG_LINEAR)
+        assert np.array_equal(a.points, b.points)
+        assert (a.isolated_events, a.coincident_pairs) == (b.isolated_events, b.coincident_pairs)
+        # and the wrap really changed eta: the shipped eta = 1/(3r^3) differs
+        c = orc.ref_lop_project(P, X0, 0.1, 4.0, 0.45, 5)
+        assert np.abs(c.points - b.points).max() > 1e-6
+
+
+@pytest.mark.parametrize("cfg,scale", [(1, 0.1), (2, 0.01), (3, 0.002), (4, 0.003), (5, 0.0005)])
+def test_oracle_config_generator_matches_product(orc, pb, cfg, scale):
+    """The oracle's restated config generator (used by bench.py's reference arm
+    so that it never loads the product library) draws exactly what the
+    product's host generator draws (host code, no device needed)."""
+    P, X0 = orc.generate_config(cfg, scale)
+    P2, X2 = pb.generate_config(cfg, scale)
+    assert np.array_equal(P, P2) and np.array_equal(X0, X2)
+
+
+def test_sweep_rows_matches_full_sweep(orc):
+    rng = np.random.default_rng(3)
+    P = rng.uniform(-1, 1, (6000, 3)) * np.array([1, 1, 0.05])
+    X = np.concatenate([P[rng.choice(6000, 600, replace=False)], P[:2], [[9.0, 9.0, 9.0]]])
+    rows = np.array([0, 5, 600, 601, 602, 77], dtype=np.uint32)
+    for eta in (orc.ETA_INV_CUBE, orc.ETA_NEG_LINEAR):
+        for wlop in (False, True):
+            full, iso, co, _ = orc.lop_sweep(P, X, 0.08, 3.0, 0.45, eta=eta, wlop=wlop)
+            nxt, cnt = orc.lop_sweep_rows(P, X, rows, 0.08, 3.0, 0.45, eta=eta, wlop=wlop)
+            assert np.abs(nxt - full[rows]).max() <= 1e-15
+            assert np.array_equal(cnt[:, 2], co[rows])
+            assert np.array_equal(cnt[:, 3] & 1, iso[rows])
+    r = orc.lop_project(P, X, 0.08, 3.0, 0.45, 1, eta=orc.ETA_NEG_LINEAR)
+    _, cnt = orc.lop_sweep_rows(P, X, np.arange(X.shape[0]), 0.08, 3.0, 0.45,
+                                eta=orc.ETA_NEG_LINEAR)
+    assert (cnt[:, 0].sum(), cnt[:, 1].sum()) == (r.interactions_attr, r.interactions_rep)
+    assert cnt[602, 3] == 1  # the far point is isolated
