@@ -180,6 +180,25 @@ __device__ __forceinline__ void scan_row(uint32_t* __restrict__ a, uint32_t ntil
     __syncthreads();
 }
 
+// Exclusive scan of digit row d by ONE thread (rows of a few tiles).
+constexpr uint32_t kSerialScanTiles = 16;
+__device__ __forceinline__ void serial_scan_row(uint32_t* __restrict__ a, uint32_t ntiles,
+                                                uint32_t* __restrict__ totals, uint32_t d) {
+    uint32_t* row = a + (size_t)d * ntiles;
+    uint32_t run = 0;
+    for (uint32_t t0 = 0; t0 < ntiles; t0 += 16) {
+        uint32_t v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = t0 + i < ntiles ? row[t0 + i] : 0u;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            if (t0 + i < ntiles) row[t0 + i] = run;
+            run += v[i];
+        }
+    }
+    totals[d] = run;
+}
+
 __global__ void __launch_bounds__(RS_ROW_THREADS)
 rs_scan_rows_kernel(uint32_t* __restrict__ a, uint32_t nblocks, uint32_t* __restrict__ totals,
                     const uint32_t* done) {
@@ -328,7 +347,14 @@ rs_coop_kernel(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x)
             hist_tile(kin, n, shift, mask, blockhist, ntiles, t, h);
         grid.sync();
-        for (uint32_t d = blockIdx.x; d < 256; d += gridDim.x) scan_row(blockhist, ntiles, totals, d, S.sh);
+        if (ntiles <= kSerialScanTiles) {
+            // few tiles (the grid is then only a few blocks): one thread per digit
+            // row, 16 entries per L2 round trip, no block barriers (a 1-tile sort
+            // spent 430 us here scanning 256 rows one after another)
+            if (blockIdx.x == 0) serial_scan_row(blockhist, ntiles, totals, threadIdx.x);
+        } else {
+            for (uint32_t d = blockIdx.x; d < 256; d += gridDim.x) scan_row(blockhist, ntiles, totals, d, S.sh);
+        }
         grid.sync();
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x)
             scatter_tile<false>(kin, vin, ko, vo, n, shift, mask, blockhist, ntiles, totals,
