@@ -19,6 +19,7 @@
 //
 // It is the whole computation in PCS_PREC_FP64 mode and the deferred-query path
 // of the fp32 fused kernel.
+#include <algorithm>
 #include <cfloat>
 
 #include "common.cuh"
@@ -495,6 +496,13 @@ void launch_exact(const ExactArgs<T>& a, int grid_blocks, cudaStream_t s) {
         constexpr int NT = 32 * EX_TEAM_WARPS;
         if (a.wlop) exact_kernel<T, true, EX_TEAM_WARPS><<<grid_blocks, NT, 0, s>>>(a);
         else exact_kernel<T, false, EX_TEAM_WARPS><<<grid_blocks, NT, 0, s>>>(a);
+    } else if (a.nq <= 32768u) {
+        // few queries (config 1: 2,000): a 128-thread team per query with its
+        // rows' bounds loaded at once and the candidates flattened — the latency of
+        // a few dependent loads per query instead of ~2 per cell row
+        const int blocks = (int)std::min<uint32_t>(std::max(a.nq, 1u), (uint32_t)grid_blocks * 2u);
+        if (a.wlop) exact_kernel<T, true, 4><<<blocks, 128, 0, s>>>(a);
+        else exact_kernel<T, false, 4><<<blocks, 128, 0, s>>>(a);
     } else {
         if (a.wlop) exact_kernel<T, true, 1><<<grid_blocks, EX_THREADS, 0, s>>>(a);
         else exact_kernel<T, false, 1><<<grid_blocks, EX_THREADS, 0, s>>>(a);
