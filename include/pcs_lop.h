@@ -219,6 +219,79 @@ pcs_status pcs_deviation_to_mesh(const pcs_lop_desc* d, const double* cloud_xyz,
                                  const double* tri_xyz, uint64_t ntri,
                                  pcs_deviation_report* report, double* distances_out);
 
+/* ---- MLS projection ------------------------------------
+ * Replaces the reference's per-point MLS solver (proj/src/wls.cpp:53-222,
+ * proj/src/mls.cpp:28-93) and the spatial index it queries
+ * (proj/include/pcs/spatial.hpp).  An index keeps a cloud resident on the
+ * device; the grid for a query radius is built on first use and cached. */
+typedef struct pcs_mls_index pcs_mls_index;
+
+/* MlsParams (proj/include/pcs/mls.hpp:14-30) + the device. */
+typedef struct pcs_mls_desc {
+    uint32_t struct_size;      /* sizeof(pcs_mls_desc) */
+    double h;                  /* KernelParams::h */
+    double cutoff_multiple;    /* KernelParams::cutoff_multiple (support = h * cutoff) */
+    int32_t degree;            /* polynomial degree in [1, 4] */
+    double plane_tol;          /* plane fixed-point tolerance (> 0) */
+    int32_t plane_max_iter;    /* >= 1 */
+    int32_t device;            /* CUDA device, -1 = current */
+} pcs_mls_desc;
+void pcs_mls_desc_default(pcs_mls_desc* d); /* MlsParams defaults: h 1, cutoff 3, degree 2, 1e-10, 50 */
+
+/* Mode of pcs_mls_project. */
+typedef enum pcs_mls_mode {
+    PCS_MLS_PROJECT = 0,  /* project_point_guarded without a guard (mls.cpp:28-69) */
+    PCS_MLS_PLANE = 1,    /* fit_reference_plane (wls.cpp:53-147) */
+    PCS_MLS_POLY = 2      /* fit_local_polynomial of degree d->degree over a given frame (wls.cpp:149-222) */
+} pcs_mls_mode;
+
+/* One query's outcome.  Status codes follow the reference enums:
+ * status = ProjectionStatus (0 Full, 1 DegradedDegree, 2 PlaneOnly, 3 Skipped),
+ * plane_status = PlaneFitStatus (0 Ok, 1 TooFewNeighbors, 2 DegenerateNeighborhood,
+ * 3 NoConvergence), poly_status = PolyFitStatus of the last polynomial fit
+ * (0 Ok, 1 TooFewNeighbors, 2 SingularSystem).  cmin/cmax bound every query
+ * centre the computation used (plane iterates, frame origin) — a slab guard
+ * (parallel_smooth) is decided from them exactly. */
+typedef struct pcs_mls_result {
+    double projected[3];
+    double origin[3], normal[3], u[3], v[3];  /* LocalFrame */
+    double coeffs[15];                        /* polynomial of degree_used (POLY: of d->degree) */
+    double cmin[3], cmax[3];
+    int32_t status;
+    int32_t degree_used;
+    int32_t iterations;
+    int32_t plane_status;
+    int32_t poly_status;
+    int32_t pad;
+} pcs_mls_result;
+
+pcs_status pcs_mls_index_create(const double* xyz, uint64_t n, int32_t device, pcs_mls_index** out);
+void pcs_mls_index_destroy(pcs_mls_index* index);
+/* SpatialIndex::radius_query for m centres (proj/src/spatial.cpp:82-111): CSR of
+ * the hits, ascending point index per centre, distances sqrt(norm2(p - c)) as
+ * the reference computes them.  Query the total with idx/dist NULL first
+ * (offsets[m] = total); PCS_ERR_CAPACITY when cap < total.  r must be finite > 0. */
+pcs_status pcs_mls_index_radius(pcs_mls_index* index, const double* centers_xyz, uint64_t m,
+                                double r, uint64_t* offsets, uint32_t* idx, double* dist,
+                                uint64_t cap);
+/* Per query: the projection / plane fit / polynomial fit, one warp per query.
+ * frames (POLY only): 12 doubles per query, origin, normal, u, v.  centers_out
+ * (may be NULL): (plane_max_iter + 1) x 3 doubles per query — the plane
+ * iterates q_1..q_iterations, then the frame origin — so that a host-side
+ * coverage predicate can be replayed in the reference's order. */
+pcs_status pcs_mls_project(pcs_mls_index* index, const pcs_mls_desc* d, const double* q_xyz,
+                           uint64_t m, int32_t mode, const double* frames, pcs_mls_result* out,
+                           double* centers_out);
+/* smooth_cloud (proj/src/mls.cpp:75-93) in one call: every point of the cloud
+ * projected against the cloud itself; out_xyz (3n) and per-point results
+ * (may be NULL). */
+pcs_status pcs_mls_smooth(const pcs_mls_desc* d, const double* xyz, uint64_t n, double* out_xyz,
+                          pcs_mls_result* results);
+/* partition (proj/src/parallel.cpp:64-127), host only: axis, W-1 cuts, and the
+ * worker of every point (counts differ by at most one). */
+pcs_status pcs_mls_partition(const double* xyz, uint64_t n, uint64_t workers, double support,
+                             int32_t* axis, double* cuts, uint32_t* worker_of);
+
 /* ---- cloud IO (the data format either side of the path) -----
  * CloudFormat (proj/include/pcs/io.hpp): XYZ, or ASCII PLY. */
 typedef enum pcs_cloud_format { PCS_FMT_XYZ = 0, PCS_FMT_PLY_ASCII = 1 } pcs_cloud_format;

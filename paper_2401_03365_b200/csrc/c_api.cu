@@ -262,6 +262,76 @@ pcs_status pcs_deviation_to_mesh(const pcs_lop_desc* d, const double* cloud_xyz,
     });
 }
 
+// ---- MLS projection -----------------------------------------------------------
+struct pcs_mls_index {
+    pcsb::MlsIndex* ix;
+};
+
+namespace {
+const pcs_mls_desc& checked_mls(const pcs_mls_desc* d) {
+    if (!d) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null descriptor");
+    if (d->struct_size != sizeof(pcs_mls_desc))
+        throw pcsb::Failure(PCS_ERR_INVALID_PARAM,
+                            "pcs_mls_desc.struct_size mismatch (initialise with pcs_mls_desc_default)");
+    return *d;
+}
+}  // namespace
+
+void pcs_mls_desc_default(pcs_mls_desc* d) {
+    if (!d) return;
+    std::memset(d, 0, sizeof(*d));
+    d->struct_size = sizeof(pcs_mls_desc);
+    d->h = 1.0;
+    d->cutoff_multiple = 3.0;
+    d->degree = 2;
+    d->plane_tol = 1e-10;
+    d->plane_max_iter = 50;
+    d->device = -1;
+}
+
+pcs_status pcs_mls_index_create(const double* xyz, uint64_t n, int32_t device, pcs_mls_index** out) {
+    return guarded([&] {
+        if (!out) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null handle");
+        *out = nullptr;
+        pcsb::MlsIndex* ix = pcsb::mls_index_create(xyz, n, device);
+        *out = new pcs_mls_index{ix};
+    });
+}
+
+void pcs_mls_index_destroy(pcs_mls_index* index) {
+    if (!index) return;
+    pcsb::mls_index_destroy(index->ix);
+    delete index;
+}
+
+pcs_status pcs_mls_index_radius(pcs_mls_index* index, const double* centers_xyz, uint64_t m,
+                                double r, uint64_t* offsets, uint32_t* idx, double* dist,
+                                uint64_t cap) {
+    return guarded([&] {
+        if (!index) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null index");
+        pcsb::mls_index_radius(index->ix, centers_xyz, m, r, offsets, idx, dist, cap);
+    });
+}
+
+pcs_status pcs_mls_project(pcs_mls_index* index, const pcs_mls_desc* d, const double* q_xyz,
+                           uint64_t m, int32_t mode, const double* frames, pcs_mls_result* out,
+                           double* centers_out) {
+    return guarded([&] {
+        if (!index) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null index");
+        pcsb::mls_project(index->ix, checked_mls(d), q_xyz, m, mode, frames, out, centers_out);
+    });
+}
+
+pcs_status pcs_mls_smooth(const pcs_mls_desc* d, const double* xyz, uint64_t n, double* out_xyz,
+                          pcs_mls_result* results) {
+    return guarded([&] { pcsb::mls_smooth(checked_mls(d), xyz, n, out_xyz, results); });
+}
+
+pcs_status pcs_mls_partition(const double* xyz, uint64_t n, uint64_t workers, double support,
+                             int32_t* axis, double* cuts, uint32_t* worker_of) {
+    return guarded([&] { pcsb::mls_partition(xyz, n, workers, support, axis, cuts, worker_of); });
+}
+
 pcs_status pcs_format_cloud(const pcs_lop_desc* d, const double* xyz, uint64_t n, int32_t format,
                             char* out, uint64_t cap, uint64_t* len) {
     return guarded([&] {

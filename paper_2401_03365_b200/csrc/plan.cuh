@@ -179,4 +179,18 @@ void deviation(const pcs_lop_desc& d, const double* cloud, uint64_t m, const dou
 void deviation_to_mesh(const pcs_lop_desc& d, const double* cloud, uint64_t m, const double* tri,
                        uint64_t ntri, pcs_deviation_report* rep, double* distances_out);
 
+
+// MLS projection (mls.cu)
+struct MlsIndex;
+MlsIndex* mls_index_create(const double* xyz, uint64_t n, int device);
+void mls_index_destroy(MlsIndex* ix);
+void mls_index_radius(MlsIndex* ix, const double* centers, uint64_t m, double r, uint64_t* offsets,
+                      uint32_t* idx, double* dist, uint64_t cap);
+void mls_project(MlsIndex* ix, const pcs_mls_desc& d, const double* q, uint64_t m, int mode,
+                 const double* frames, pcs_mls_result* out, double* centers_out);
+void mls_smooth(const pcs_mls_desc& d, const double* xyz, uint64_t n, double* out_xyz,
+                pcs_mls_result* results);
+void mls_partition(const double* xyz, uint64_t n, uint64_t workers, double support, int32_t* axis,
+                   double* cuts, uint32_t* worker_of);
+
 }  // namespace pcsb

@@ -1,7 +1,7 @@
 // Minimal doctest-compatible test shim (our own code; the reference's vendored
 // doctest is not shipped, proj/.gitignore:2).  Supports exactly what the
 // reference's LOP / metrics / IO tests use: TEST_CASE, CHECK, CHECK_FALSE,
-// REQUIRE, FAIL, CHECK_THROWS_AS, doctest::Approx(..).epsilon(..), and
+// REQUIRE, FAIL, CHECK_THROWS_AS, doctest::Approx(..).epsilon(..).scale(..), and
 // DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN.  Prints one line per failed check and a
 // summary; exit status = number of failed test cases (capped at 255).
 #pragma once
@@ -21,10 +21,15 @@ struct Approx {
         eps = e;
         return *this;
     }
+    Approx& scale(double s) {
+        scl = s;
+        return *this;
+    }
     double value;
     double eps = 1.192092896e-07 * 100;
+    double scl = 1.0;
     friend bool operator==(double lhs, const Approx& a) {
-        return std::fabs(lhs - a.value) <= a.eps * (1.0 + std::fmax(std::fabs(lhs), std::fabs(a.value)));
+        return std::fabs(lhs - a.value) <= a.eps * (a.scl + std::fmax(std::fabs(lhs), std::fabs(a.value)));
     }
     friend bool operator==(const Approx& a, double rhs) { return rhs == a; }
     friend bool operator!=(double lhs, const Approx& a) { return !(lhs == a); }

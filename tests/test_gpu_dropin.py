@@ -47,3 +47,33 @@ def test_reference_test_io_passes_unmodified():
     bad lines), byte-stable writing (device shortest round-trip formatter),
     meshes, format inference and file-level errors."""
     _run("test_io", "13 passed | 0 failed")
+
+
+def test_reference_test_spatial_passes_unmodified():
+    """proj/tests/test_spatial.cpp: SpatialIndex radius / nearest queries (device
+    grid of the MLS index, nearest-neighbour kernel) against the reference's
+    linear-scan oracles, bit for bit, incl. boundary radii and duplicates."""
+    _run("test_spatial", "10 passed | 0 failed")
+
+
+def test_reference_test_wls_passes_unmodified():
+    """proj/tests/test_wls.cpp: the device plane fit (weighted-PCA fixed point,
+    orientation and frame rules, degenerate and thin neighbourhoods) and the
+    device polynomial fit (normal equations through a Jacobi eigen-
+    decomposition) against the reference's dense long-double oracle, the
+    objective grid search and its gradient checks."""
+    _run("test_wls", "15 passed | 0 failed")
+
+
+def test_reference_test_mls_passes_unmodified():
+    """proj/tests/test_mls.cpp: project_point / smooth_cloud on the device —
+    exact planes, the dense sphere, noise reduction, input-order independence,
+    idempotence, Skipped pass-through, summary counts, validation."""
+    _run("test_mls", "11 passed | 0 failed")
+
+
+def test_reference_test_parallel_passes_unmodified():
+    """proj/tests/test_parallel.cpp: partition / exchange_borders (host slab
+    layout) and parallel_smooth bit-identical to smooth_cloud for 1-8 and 16
+    workers."""
+    _run("test_parallel", "12 passed | 0 failed")

@@ -6,12 +6,12 @@ set -e
 name=$1; shift
 d="tools/bin/${name:?name}"
 mkdir -p "$d"
-for f in grid_sort lop_fast lop_exact plan comm c_api nn io; do
+for f in grid_sort lop_fast lop_exact plan comm c_api nn io mls; do
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC \
     -I include -I paper_2401_03365_b200/csrc --expt-relaxed-constexpr -DPCSB_DEV_KNOBS "$@" \
     -c paper_2401_03365_b200/csrc/$f.cu -o "$d/$f.o" &
 done
 wait
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$d/libpcs_lop_b200.so" \
-  "$d"/{grid_sort,lop_fast,lop_exact,plan,comm,c_api,nn,io}.o \
-  paper_2401_03365_b200/build/{nccl_dl,generators,pcs_api,shard,host_io}.o -ldl -lgomp
+  "$d"/{grid_sort,lop_fast,lop_exact,plan,comm,c_api,nn,io,mls}.o \
+  paper_2401_03365_b200/build/{nccl_dl,generators,pcs_api,shard,host_io,mls_api}.o -ldl -lgomp
