@@ -1115,3 +1115,345 @@ int orc_deviation_to_mesh(const double* cloud, size_t m, const double* tri, size
     if (!dist_out) free(d);
     return st;
 }
+
+/* ------------------------------------------------------------------------ */
+/* MLS projection (proj/src/wls.cpp:53-222, proj/src/mls.cpp:28-69)          */
+/* ------------------------------------------------------------------------ */
+
+/* theta(d) (proj/src/kernels.cpp:8-15) */
+static double mls_theta(double d, double support, double h) {
+    if (d > support) return 0.0;
+    const double s = d / h;
+    return exp(-s * s);
+}
+
+/* Eigenvalues (ascending) of a symmetric 3x3 matrix by the trigonometric
+ * solution of its characteristic cubic; the eigenvector of the smallest one as
+ * the largest cross product of two rows of A - l0 I. */
+static void eig3_small(const double A[3][3], double ev[3], double vec[3]) {
+    const double p1 = A[0][1] * A[0][1] + A[0][2] * A[0][2] + A[1][2] * A[1][2];
+    if (p1 == 0.0) {
+        int idx[3] = {0, 1, 2};
+        for (int i = 0; i < 3; ++i)
+            for (int j = i + 1; j < 3; ++j)
+                if (A[idx[j]][idx[j]] < A[idx[i]][idx[i]]) {
+                    const int t = idx[i];
+                    idx[i] = idx[j];
+                    idx[j] = t;
+                }
+        for (int i = 0; i < 3; ++i) ev[i] = A[idx[i]][idx[i]];
+        vec[0] = vec[1] = vec[2] = 0.0;
+        vec[idx[0]] = 1.0;
+        return;
+    }
+    const double q = (A[0][0] + A[1][1] + A[2][2]) / 3.0;
+    const double p2 = (A[0][0] - q) * (A[0][0] - q) + (A[1][1] - q) * (A[1][1] - q) +
+                      (A[2][2] - q) * (A[2][2] - q) + 2.0 * p1;
+    const double p = sqrt(p2 / 6.0);
+    double B[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) B[i][j] = (A[i][j] - (i == j ? q : 0.0)) / p;
+    double r = 0.5 * (B[0][0] * (B[1][1] * B[2][2] - B[1][2] * B[2][1]) -
+                      B[0][1] * (B[1][0] * B[2][2] - B[1][2] * B[2][0]) +
+                      B[0][2] * (B[1][0] * B[2][1] - B[1][1] * B[2][0]));
+    if (r < -1.0) r = -1.0;
+    if (r > 1.0) r = 1.0;
+    const double phi = acos(r) / 3.0;
+    const double big = q + 2.0 * p * cos(phi);
+    const double small = q + 2.0 * p * cos(phi + 2.0943951023931954923);
+    ev[0] = small;
+    ev[2] = big;
+    ev[1] = 3.0 * q - big - small;
+    double R[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) R[i][j] = A[i][j] - (i == j ? small : 0.0);
+    double best = -1.0;
+    const int pairs[3][2] = {{0, 1}, {0, 2}, {1, 2}};
+    for (int k = 0; k < 3; ++k) {
+        const double* a = R[pairs[k][0]];
+        const double* b = R[pairs[k][1]];
+        const double c[3] = {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2],
+                             a[0] * b[1] - a[1] * b[0]};
+        const double nn = c[0] * c[0] + c[1] * c[1] + c[2] * c[2];
+        if (nn > best) {
+            best = nn;
+            vec[0] = c[0];
+            vec[1] = c[1];
+            vec[2] = c[2];
+        }
+    }
+}
+
+/* Cyclic Jacobi (long double) of a symmetric K x K matrix: ascending
+ * eigenvalues ev[K], eigenvectors as the columns of V (row-major, stride K). */
+static void jacobi_ld(long double* A, int K, long double* ev, long double* V) {
+    for (int i = 0; i < K * K; ++i) V[i] = (i / K == i % K) ? 1.0L : 0.0L;
+    for (int sweep = 0; sweep < 100; ++sweep) {
+        long double off = 0.0L, dia = 0.0L;
+        for (int i = 0; i < K; ++i)
+            for (int j = 0; j < K; ++j) {
+                const long double v = A[i * K + j];
+                if (i == j) dia += v * v;
+                else off += v * v;
+            }
+        if (!(off > 1e-38L * dia)) break;
+        for (int p = 0; p < K - 1; ++p)
+            for (int q = p + 1; q < K; ++q) {
+                const long double apq = A[p * K + q];
+                if (apq == 0.0L) continue;
+                const long double tau = (A[q * K + q] - A[p * K + p]) / (2.0L * apq);
+                const long double t = (tau >= 0.0L ? 1.0L : -1.0L) / (fabsl(tau) + sqrtl(1.0L + tau * tau));
+                const long double c = 1.0L / sqrtl(1.0L + t * t), s = t * c;
+                for (int k = 0; k < K; ++k) {
+                    const long double akp = A[k * K + p], akq = A[k * K + q];
+                    A[k * K + p] = c * akp - s * akq;
+                    A[k * K + q] = s * akp + c * akq;
+                    const long double vkp = V[k * K + p], vkq = V[k * K + q];
+                    V[k * K + p] = c * vkp - s * vkq;
+                    V[k * K + q] = s * vkp + c * vkq;
+                }
+                for (int k = 0; k < K; ++k) {
+                    const long double apk = A[p * K + k], aqk = A[q * K + k];
+                    A[p * K + k] = c * apk - s * aqk;
+                    A[q * K + k] = s * apk + c * aqk;
+                }
+                A[p * K + q] = A[q * K + p] = 0.0L;
+            }
+    }
+    int idx[15];
+    for (int i = 0; i < K; ++i) idx[i] = i;
+    for (int i = 0; i < K; ++i)
+        for (int j = i + 1; j < K; ++j)
+            if (A[idx[j] * K + idx[j]] < A[idx[i] * K + idx[i]]) {
+                const int t = idx[i];
+                idx[i] = idx[j];
+                idx[j] = t;
+            }
+    long double W[225];
+    for (int i = 0; i < K; ++i) {
+        ev[i] = A[idx[i] * K + idx[i]];
+        for (int k = 0; k < K; ++k) W[k * K + i] = V[k * K + idx[i]];
+    }
+    memcpy(V, W, sizeof(long double) * (size_t)(K * K));
+}
+
+enum { MLS_FULL = 0, MLS_DEGRADED = 1, MLS_PLANE_ONLY = 2, MLS_SKIPPED = 3 };
+enum { PLN_OK = 0, PLN_TOO_FEW = 1, PLN_DEGENERATE = 2, PLN_NO_CONV = 3 };
+enum { POLY_OK = 0, POLY_TOO_FEW = 1, POLY_SINGULAR = 2 };
+
+/* fit_reference_plane (wls.cpp:53-147) without a guard. */
+static int mls_plane(const grid_t* gr, const double r[3], const orc_mls_params* prm, hits_t* hits,
+                     double o[3], double nrm[3], double u[3], double v[3], int* iters) {
+    const double support = prm->h * prm->cutoff;
+    double q[3] = {r[0], r[1], r[2]};
+    double n[3] = {0.0, 0.0, 0.0};
+    double t = 0.0;
+    int converged = 0;
+    for (int iter = 1; iter <= prm->max_iter; ++iter) {
+        *iters = iter;
+        grid_query(gr, q, support, hits);
+        if (hits->n < 3) return PLN_TOO_FEW;
+        double wsum = 0.0, c[3] = {0.0, 0.0, 0.0};
+        for (size_t k = 0; k < hits->n; ++k) {
+            const double w = mls_theta(sqrt(hits->d2[k]), support, prm->h);
+            const double* p = gr->pts + 3 * (size_t)hits->idx[k];
+            wsum += w;
+            for (int a = 0; a < 3; ++a) c[a] += w * p[a];
+        }
+        if (!(wsum > 0.0)) return PLN_TOO_FEW;
+        for (int a = 0; a < 3; ++a) c[a] /= wsum;
+        double C[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+        for (size_t k = 0; k < hits->n; ++k) {
+            const double w = mls_theta(sqrt(hits->d2[k]), support, prm->h);
+            const double* p = gr->pts + 3 * (size_t)hits->idx[k];
+            const double d[3] = {p[0] - c[0], p[1] - c[1], p[2] - c[2]};
+            C[0][0] += w * d[0] * d[0];
+            C[0][1] += w * d[0] * d[1];
+            C[0][2] += w * d[0] * d[2];
+            C[1][1] += w * d[1] * d[1];
+            C[1][2] += w * d[1] * d[2];
+            C[2][2] += w * d[2] * d[2];
+        }
+        C[1][0] = C[0][1];
+        C[2][0] = C[0][2];
+        C[2][1] = C[1][2];
+        double ev[3], ve[3];
+        eig3_small(C, ev, ve);
+        if (ev[1] - ev[0] <= 1e-12 * ev[2]) return PLN_DEGENERATE;
+        const double nn = sqrt(ve[0] * ve[0] + ve[1] * ve[1] + ve[2] * ve[2]);
+        for (int a = 0; a < 3; ++a) n[a] = ve[a] / nn;
+        t = n[0] * (c[0] - r[0]) + n[1] * (c[1] - r[1]) + n[2] * (c[2] - r[2]);
+        const double qn[3] = {r[0] + t * n[0], r[1] + t * n[1], r[2] + t * n[2]};
+        const double dq[3] = {qn[0] - q[0], qn[1] - q[1], qn[2] - q[2]};
+        const double step = sqrt(dq[0] * dq[0] + dq[1] * dq[1] + dq[2] * dq[2]);
+        for (int a = 0; a < 3; ++a) q[a] = qn[a];
+        if (step < prm->tol) {
+            converged = 1;
+            break;
+        }
+    }
+    if (t > 0.0) {
+        for (int a = 0; a < 3; ++a) n[a] = -n[a];
+    } else if (t == 0.0) {
+        const int flip = n[2] != 0.0 ? n[2] < 0.0 : (n[1] != 0.0 ? n[1] < 0.0 : n[0] < 0.0);
+        if (flip)
+            for (int a = 0; a < 3; ++a) n[a] = -n[a];
+    }
+    for (int a = 0; a < 3; ++a) {
+        o[a] = q[a];
+        nrm[a] = n[a];
+    }
+    const double ax = fabs(n[0]), ay = fabs(n[1]), az = fabs(n[2]);
+    double e[3] = {1.0, 0.0, 0.0}, best = ax;
+    if (ay < best) {
+        e[0] = 0.0; e[1] = 1.0; e[2] = 0.0;
+        best = ay;
+    }
+    if (az < best) {
+        e[0] = 0.0; e[1] = 0.0; e[2] = 1.0;
+    }
+    const double en = e[0] * n[0] + e[1] * n[1] + e[2] * n[2];
+    for (int a = 0; a < 3; ++a) u[a] = e[a] - en * n[a];
+    const double un = sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+    for (int a = 0; a < 3; ++a) u[a] /= un;
+    v[0] = n[1] * u[2] - n[2] * u[1];
+    v[1] = n[2] * u[0] - n[0] * u[2];
+    v[2] = n[0] * u[1] - n[1] * u[0];
+    return converged ? PLN_OK : PLN_NO_CONV;
+}
+
+/* fit_local_polynomial (wls.cpp:149-222) without a guard. */
+static int mls_poly(const grid_t* gr, const double o[3], const double n[3], const double u[3],
+                    const double v[3], const orc_mls_params* prm, int degree, hits_t* hits,
+                    double coeffs[15]) {
+    const double support = prm->h * prm->cutoff;
+    grid_query(gr, o, support, hits);
+    const int K = (degree + 1) * (degree + 2) / 2;
+    if (hits->n < (size_t)K) return POLY_TOO_FEW;
+    double M[225], b[15];
+    memset(M, 0, sizeof(M));
+    memset(b, 0, sizeof(b));
+    for (size_t k = 0; k < hits->n; ++k) {
+        const double* p = gr->pts + 3 * (size_t)hits->idx[k];
+        const double d[3] = {p[0] - o[0], p[1] - o[1], p[2] - o[2]};
+        const double ui = d[0] * u[0] + d[1] * u[1] + d[2] * u[2];
+        const double vi = d[0] * v[0] + d[1] * v[1] + d[2] * v[2];
+        const double fi = d[0] * n[0] + d[1] * n[1] + d[2] * n[2];
+        const double w = mls_theta(sqrt(hits->d2[k]), support, prm->h);
+        double up[5] = {1, 0, 0, 0, 0}, vp[5] = {1, 0, 0, 0, 0}, basis[15];
+        for (int i = 1; i <= degree; ++i) {
+            up[i] = up[i - 1] * ui;
+            vp[i] = vp[i - 1] * vi;
+        }
+        int kk = 0;
+        for (int s = 0; s <= degree; ++s)
+            for (int a = s; a >= 0; --a) basis[kk++] = up[a] * vp[s - a];
+        for (int row = 0; row < K; ++row) {
+            const double wb = w * basis[row];
+            for (int col = 0; col < K; ++col) M[row * K + col] += wb * basis[col];
+            b[row] += wb * fi;
+        }
+    }
+    long double A[225], V[225], ev[15];
+    for (int i = 0; i < K * K; ++i) A[i] = M[i];
+    jacobi_ld(A, K, ev, V);
+    const long double lmax = ev[K - 1];
+    if (!(lmax > 0.0L) || ev[0] <= 1e-12L * lmax) return POLY_SINGULAR;
+    long double x[15], y[15], res[15];
+    for (int j = 0; j < K; ++j) {
+        long double s = 0.0L;
+        for (int k = 0; k < K; ++k) s += V[k * K + j] * b[k];
+        y[j] = s / ev[j];
+    }
+    for (int i = 0; i < K; ++i) {
+        long double s = 0.0L;
+        for (int j = 0; j < K; ++j) s += V[i * K + j] * y[j];
+        x[i] = s;
+    }
+    for (int i = 0; i < K; ++i) {  /* one refinement, as the reference does */
+        long double s = 0.0L;
+        for (int j = 0; j < K; ++j) s += (long double)M[i * K + j] * x[j];
+        res[i] = b[i] - s;
+    }
+    for (int j = 0; j < K; ++j) {
+        long double s = 0.0L;
+        for (int k = 0; k < K; ++k) s += V[k * K + j] * res[k];
+        y[j] = s / ev[j];
+    }
+    for (int i = 0; i < K; ++i) {
+        long double s = 0.0L;
+        for (int j = 0; j < K; ++j) s += V[i * K + j] * y[j];
+        coeffs[i] = (double)(x[i] + s);
+    }
+    return POLY_OK;
+}
+
+int orc_mls_project(const double* C, size_t n, const double* Q, size_t m, const orc_mls_params* prm,
+                    int mode, const double* frames, orc_mls_result* out, int threads) {
+    if (!prm || !(prm->h > 0.0) || !(prm->cutoff > 0.0) || prm->degree < 1 || prm->degree > 4 ||
+        !(prm->tol > 0.0) || prm->max_iter < 1 || mode < 0 || mode > 2)
+        return ORC_INVALID_PARAM;
+    if (m == 0) return ORC_OK;
+    if (mode == ORC_MLS_POLY && !frames) return ORC_INVALID_PARAM;
+    grid_t gr;
+    if (grid_build(&gr, C, n, prm->h * prm->cutoff) != ORC_OK) return ORC_NO_MEMORY;
+    set_threads(threads);
+#pragma omp parallel
+    {
+        hits_t hits;
+        memset(&hits, 0, sizeof(hits));
+#pragma omp for schedule(dynamic, 16)
+        for (size_t i = 0; i < m; ++i) {
+            orc_mls_result R;
+            memset(&R, 0, sizeof(R));
+            const double* r = Q + 3 * i;
+            for (int a = 0; a < 3; ++a) R.projected[a] = r[a];
+            R.status = MLS_SKIPPED;
+            double o[3], nn[3], u[3], v[3];
+            int have = 0;
+            if (mode == ORC_MLS_POLY) {
+                const double* f = frames + 12 * i;
+                for (int a = 0; a < 3; ++a) {
+                    o[a] = f[a];
+                    nn[a] = f[3 + a];
+                    u[a] = f[6 + a];
+                    v[a] = f[9 + a];
+                }
+                have = 1;
+            } else {
+                R.plane_status = mls_plane(&gr, r, prm, &hits, o, nn, u, v, &R.iterations);
+                have = R.plane_status == PLN_OK || R.plane_status == PLN_NO_CONV;
+            }
+            if (have) {
+                for (int a = 0; a < 3; ++a) {
+                    R.origin[a] = o[a];
+                    R.normal[a] = nn[a];
+                    R.u[a] = u[a];
+                    R.v[a] = v[a];
+                }
+                if (mode == ORC_MLS_POLY) {
+                    R.poly_status = mls_poly(&gr, o, nn, u, v, prm, prm->degree, &hits, R.coeffs);
+                    if (R.poly_status == POLY_OK) R.degree_used = prm->degree;
+                } else if (mode == ORC_MLS_PROJECT) {
+                    for (int a = 0; a < 3; ++a) R.projected[a] = o[a];
+                    R.status = MLS_PLANE_ONLY;
+                    for (int deg = prm->degree; deg >= 1; --deg) {
+                        R.poly_status = mls_poly(&gr, o, nn, u, v, prm, deg, &hits, R.coeffs);
+                        if (R.poly_status == POLY_OK) {
+                            const double hgt = R.coeffs[0];  /* evaluate_polynomial(poly, 0, 0) */
+                            for (int a = 0; a < 3; ++a) R.projected[a] = o[a] + hgt * nn[a];
+                            R.status = deg == prm->degree ? MLS_FULL : MLS_DEGRADED;
+                            R.degree_used = deg;
+                            break;
+                        }
+                        memset(R.coeffs, 0, sizeof(R.coeffs));
+                    }
+                }
+            }
+            out[i] = R;
+        }
+        hits_free(&hits);
+    }
+    grid_free(&gr);
+    return ORC_OK;
+}

@@ -128,6 +128,32 @@ double orc_point_triangle_distance(const double p[3], const double tri[9]);
 int orc_deviation_to_mesh(const double* cloud, size_t m, const double* tri, size_t ntri,
                           double out[4], double* dist_out, int threads);
 
+/* MLS projection: proj/src/wls.cpp:53-222 (fit_reference_plane,
+ * fit_local_polynomial), proj/src/mls.cpp:28-69 (project_point_guarded without
+ * a guard).  Hits in ascending index order, weighted sums in that order (as the
+ * reference); the eigen-solvers are restated, not Eigen's: the 3x3 covariance by
+ * the closed form (trigonometric roots of the characteristic cubic, eigenvector
+ * as the largest cross product of rows of A - l I), the K x K normal matrix by
+ * cyclic Jacobi in long double.  Parity with the reference is pinned by the
+ * reference's own tests (test_wls / test_mls properties), not by golden vectors:
+ * Eigen is absent here, so the reference's MLS cannot be built. */
+typedef struct orc_mls_params {
+    double h, cutoff;
+    int degree;
+    double tol;
+    int max_iter;
+} orc_mls_params;
+typedef struct orc_mls_result {
+    double projected[3];
+    double origin[3], normal[3], u[3], v[3];
+    double coeffs[15];
+    int status, degree_used, iterations, plane_status, poly_status;
+} orc_mls_result;
+enum { ORC_MLS_PROJECT = 0, ORC_MLS_PLANE = 1, ORC_MLS_POLY = 2 };
+/* mode POLY: frames = 12 doubles per query (origin, normal, u, v). */
+int orc_mls_project(const double* C, size_t n, const double* Q, size_t m, const orc_mls_params* prm,
+                    int mode, const double* frames, orc_mls_result* out, int threads);
+
 #ifdef __cplusplus
 }
 #endif

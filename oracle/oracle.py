@@ -135,8 +135,45 @@ def orc():
         lib.orc_point_triangle_distance.restype = C.c_double
         lib.orc_deviation_to_mesh.argtypes = [_c_dbl_p, C.c_size_t, _c_dbl_p, C.c_size_t,
                                               _c_dbl_p, _c_dbl_p, C.c_int]
+        lib.orc_mls_project.argtypes = [_c_dbl_p, C.c_size_t, _c_dbl_p, C.c_size_t,
+                                        C.POINTER(OrcMlsParams), C.c_int, _c_dbl_p, C.c_void_p,
+                                        C.c_int]
         _orc = lib
     return _orc
+
+
+class OrcMlsParams(C.Structure):
+    _fields_ = [("h", C.c_double), ("cutoff", C.c_double), ("degree", C.c_int),
+                ("tol", C.c_double), ("max_iter", C.c_int)]
+
+
+# orc_mls_result (lop_oracle.h)
+MLS_DTYPE = np.dtype([("projected", "f8", 3), ("origin", "f8", 3), ("normal", "f8", 3),
+                      ("u", "f8", 3), ("v", "f8", 3), ("coeffs", "f8", 15), ("status", "i4"),
+                      ("degree_used", "i4"), ("iterations", "i4"), ("plane_status", "i4"),
+                      ("poly_status", "i4"), ("pad", "i4")])
+MLS_PROJECT, MLS_PLANE, MLS_POLY = 0, 1, 2
+
+
+def mls_project(C_pts, Q, h, cutoff=3.0, degree=2, tol=1e-10, max_iter=50, mode=MLS_PROJECT,
+                frames=None, threads=0) -> np.ndarray:
+    """orc_mls_project — the C restatement of project_point / fit_reference_plane /
+    fit_local_polynomial (proj/src/mls.cpp:28-69, wls.cpp:53-222) per query;
+    returns a structured array (MLS_DTYPE)."""
+    Cc = _xyz(C_pts)
+    Qq = _xyz(Q)
+    m = Qq.shape[0]
+    out = np.zeros(max(m, 1), dtype=MLS_DTYPE)
+    fr = None
+    if mode == MLS_POLY:
+        fr = np.ascontiguousarray(frames, dtype=np.float64).reshape(m, 12)
+    prm = OrcMlsParams(h, cutoff, degree, tol, max_iter)
+    rc = orc().orc_mls_project(_ptr(Cc, _c_dbl_p), Cc.shape[0], _ptr(Qq, _c_dbl_p), m,
+                               C.byref(prm), mode, _ptr(fr, _c_dbl_p) if fr is not None else None,
+                               out.ctypes.data_as(C.c_void_p), threads)
+    if rc:
+        raise OracleError(rc)
+    return out[:m]
 
 
 def ref_available() -> bool:

@@ -11,6 +11,10 @@ from .lop import (  # noqa: F401
     nearest_all, deviation, deviation_to_mesh, ParseError, format_from_path, format_cloud,
     parse_cloud, read_cloud, write_cloud, parse_mesh, format_double, trim_device_pool,
 )
+from .mls import (  # noqa: F401
+    MlsIndex, MlsParams, MlsResults, PlaneFitStatus, PolyFitStatus, ProjectionStatus, partition,
+    smooth_cloud,
+)
 
 __all__ = [
     "CONFIGS", "EmptyCloud", "Error", "InvalidParam", "KernelParams", "LopParams", "LopPlan",
@@ -20,4 +24,6 @@ __all__ = [
     "radius_query_all", "shard_layout", "DeviationReport", "EmptyMesh", "nearest_all",
     "deviation", "deviation_to_mesh", "ParseError", "format_from_path", "format_cloud",
     "parse_cloud", "read_cloud", "write_cloud", "parse_mesh", "format_double", "trim_device_pool",
+    "MlsIndex", "MlsParams", "MlsResults", "PlaneFitStatus", "PolyFitStatus", "ProjectionStatus",
+    "partition", "smooth_cloud",
 ]

@@ -44,7 +44,13 @@ EXPORTED = [
     "pcs_format_cloud", "pcs_parse_cloud", "pcs_parse_mesh", "pcs_format_double",
     "pcs_format_cloud_alloc", "pcs_free_buffer", "pcs_lop_plan_record_counts",
     "pcs_lop_plan_query_counts", "pcs_trim_device_pool",
+    "pcs_mls_desc_default", "pcs_mls_index_create", "pcs_mls_index_destroy", "pcs_mls_index_radius",
+    "pcs_mls_project", "pcs_mls_smooth", "pcs_mls_partition",
 ]
+
+PCS_MLS_PROJECT = 0
+PCS_MLS_PLANE = 1
+PCS_MLS_POLY = 2
 
 
 class LopDesc(C.Structure):
@@ -62,6 +68,22 @@ class LopDesc(C.Structure):
         ("lanes_per_point", C.c_int32),
         ("reserved", C.c_int32 * 7),
     ]
+
+
+class MlsDesc(C.Structure):
+    """pcs_mls_desc (MlsParams, proj/include/pcs/mls.hpp:14-30, + the device)."""
+    _fields_ = [("struct_size", C.c_uint32), ("h", C.c_double), ("cutoff_multiple", C.c_double),
+                ("degree", C.c_int32), ("plane_tol", C.c_double), ("plane_max_iter", C.c_int32),
+                ("device", C.c_int32)]
+
+
+class MlsResultC(C.Structure):
+    """pcs_mls_result: one query's projection / plane frame / polynomial."""
+    _fields_ = [("projected", C.c_double * 3), ("origin", C.c_double * 3),
+                ("normal", C.c_double * 3), ("u", C.c_double * 3), ("v", C.c_double * 3),
+                ("coeffs", C.c_double * 15), ("cmin", C.c_double * 3), ("cmax", C.c_double * 3),
+                ("status", C.c_int32), ("degree_used", C.c_int32), ("iterations", C.c_int32),
+                ("plane_status", C.c_int32), ("poly_status", C.c_int32), ("pad", C.c_int32)]
 
 
 class DeviationReportC(C.Structure):
@@ -171,11 +193,25 @@ def lib():
                                              C.POINTER(C.c_void_p), _u64p]
         L.pcs_free_buffer.argtypes = [C.c_void_p]
         L.pcs_free_buffer.restype = None
+        L.pcs_mls_desc_default.argtypes = [C.POINTER(MlsDesc)]
+        L.pcs_mls_desc_default.restype = None
+        L.pcs_mls_index_create.argtypes = [_dp, C.c_uint64, C.c_int32, C.POINTER(C.c_void_p)]
+        L.pcs_mls_index_destroy.argtypes = [C.c_void_p]
+        L.pcs_mls_index_destroy.restype = None
+        L.pcs_mls_index_radius.argtypes = [C.c_void_p, _dp, C.c_uint64, C.c_double, _u64p, _u32p,
+                                           _dp, C.c_uint64]
+        L.pcs_mls_project.argtypes = [C.c_void_p, C.POINTER(MlsDesc), _dp, C.c_uint64, C.c_int32,
+                                      _dp, C.POINTER(MlsResultC), _dp]
+        L.pcs_mls_smooth.argtypes = [C.POINTER(MlsDesc), _dp, C.c_uint64, _dp,
+                                     C.POINTER(MlsResultC)]
+        L.pcs_mls_partition.argtypes = [_dp, C.c_uint64, C.c_uint64, C.c_double,
+                                        C.POINTER(C.c_int32), _dp, _u32p]
         L.pcs_format_double.argtypes = [C.c_double, C.c_char_p]
         L.pcs_format_double.restype = C.c_int32
         for name in EXPORTED:
             fn = getattr(L, name)
-            if name in ("pcs_format_double", "pcs_free_buffer"):
+            if name in ("pcs_format_double", "pcs_free_buffer", "pcs_mls_desc_default",
+                        "pcs_mls_index_destroy"):
                 continue
             if fn.restype is C.c_int:  # default restype -> pcs_status
                 fn.restype = C.c_int
