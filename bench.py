@@ -397,11 +397,15 @@ def main():
         "frac_at_measured_clock": kernel_rate / (pk["per_sm_clk"] * 148 * sm_mhz * 1e6),
         "traffic": None,
     }
-    prof = os.path.join(HERE, "profiles", "fast_kernel_ncu.json")
-    if os.path.exists(prof):
+    # the latest ncu --set full capture of the two passes (profiles/rNN_fast_kernel_ncu.json)
+    cands = sorted(f for f in os.listdir(os.path.join(HERE, "profiles"))
+                   if f.endswith("fast_kernel_ncu.json")) if os.path.isdir(os.path.join(HERE, "profiles")) else []
+    prof = os.path.join(HERE, "profiles", cands[-1]) if cands else ""
+    if prof and os.path.exists(prof):
         try:
             # DRAM bytes of one sweep's attraction + repulsion launches (ncu --set full)
             roofline["traffic"] = json.load(open(prof)).get("dram_bytes_per_launch")
+            roofline["traffic_source"] = os.path.relpath(prof, HERE)
         except Exception:
             pass
 
