@@ -11,6 +11,24 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Checked builds (-DPCSB_CHECKS, tools/build_variant.sh checked ...): device-
+// side bounds / invariant assertions that trap the kernel (the launch then
+// fails loudly); compiled out of the shipped library.
+#ifdef PCSB_CHECKS
+#include <cstdio>
+#define PCSB_DCHECK(c)                                                                     \
+    do {                                                                                   \
+        if (!(c)) {                                                                        \
+            printf("PCSB_CHECKS failed at %s:%d: %s\n", __FILE__, __LINE__, #c);          \
+            __trap();                                                                      \
+        }                                                                                  \
+    } while (0)
+#else
+#define PCSB_DCHECK(c) \
+    do {               \
+    } while (0)
+#endif
+
 namespace pcsb {
 
 // Uniform grid shared by the data and the projected set.  Cells are cubes of

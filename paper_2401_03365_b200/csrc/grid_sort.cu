@@ -660,9 +660,44 @@ size_t radix_blockhist_entries(uint32_t n) {
     return 256 * (nb ? nb : 1) + 256;  // + the digit totals / bases
 }
 
+#ifdef PCSB_CHECKS
+// Checked builds: the lower-bound table is non-decreasing and ends at n; the
+// radix sort's output keys are non-decreasing in the sorted bits.
+__global__ void check_cell_table_kernel(const uint32_t* start, uint32_t ncells, uint32_t n,
+                                        const uint32_t* done) {
+    if (done && *done) return;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ncells; i += gridDim.x * blockDim.x)
+        PCSB_DCHECK(start[i] <= start[i + 1]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) PCSB_DCHECK(start[0] == 0 && start[ncells] == n);
+}
+__global__ void check_sorted_kernel(const uint32_t* keys, uint32_t n, uint32_t mask,
+                                    const uint32_t* done) {
+    if (done && *done) return;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i + 1 < n; i += gridDim.x * blockDim.x)
+        PCSB_DCHECK((keys[i] & mask) <= (keys[i + 1] & mask));
+}
+#endif
+
+static int radix_sort_impl(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
+                           uint32_t* vals_out, uint32_t n, int key_bits, RadixScratch& scr,
+                           const uint32_t* done, cudaStream_t s, uint32_t val_base);
+
 int radix_sort(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
                uint32_t* vals_out, uint32_t n, int key_bits, RadixScratch& scr,
                const uint32_t* done, cudaStream_t s, uint32_t val_base) {
+    const int k = radix_sort_impl(keys_in, vals_in, keys_out, vals_out, n, key_bits, scr, done, s, val_base);
+#ifdef PCSB_CHECKS
+    if (n > 1) {
+        const uint32_t mask = key_bits >= 32 ? 0xFFFFFFFFu : ((1u << (key_bits > 0 ? key_bits : 1)) - 1u);
+        check_sorted_kernel<<<grid_for(n, 256), 256, 0, s>>>(keys_out, n, mask, done);
+    }
+#endif
+    return k;
+}
+
+static int radix_sort_impl(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out,
+                           uint32_t* vals_out, uint32_t n, int key_bits, RadixScratch& scr,
+                           const uint32_t* done, cudaStream_t s, uint32_t val_base) {
     if (n == 0) return 0;
     static const int coop_blocks = [] {
         int dev = 0, sms = 0, per = 0, ok = 0;
@@ -819,6 +854,9 @@ int build_cell_start(const uint32_t* sorted_keys, uint32_t n, int sub_shift, uin
     cell_tile_prefix_kernel<<<grid_for(ntiles, 256), 256, 0, s>>>(sorted_keys, n, sub_shift, ntiles,
                                                                   scratch, done);
     cell_apply_kernel<<<ntiles, CS_THREADS, 0, s>>>(cell_start, count, scratch, done);
+#ifdef PCSB_CHECKS
+    check_cell_table_kernel<<<grid_for(count, 256), 256, 0, s>>>(cell_start, ncells, n, done);
+#endif
     return n ? 3 : 2;
 }
 

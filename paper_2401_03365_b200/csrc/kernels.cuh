@@ -82,9 +82,11 @@ int build_pairs(const float4* src, const uint32_t* idx, float4* sorted_out,
 // ---- fused fp32 kernels (lop_fast.cu) ---------------------------------------
 struct FastArgs {
     const float4* Ppairs;     // data, pair records; w = 1/v_j (WLOP) or 1
+    size_t Ppairs_cap;        // float4 elements of Ppairs (checked builds)
     const uint32_t* Pstart;   // cell table of the sorted data (+ row delta = record slot)
     const float4* Xq;         // projected set X^k, internal index order (queries)
     const float4* Xpairs;     // projected set, pair records; w = w_i (WLOP)
+    size_t Xpairs_cap;        // float4 elements of Xpairs (checked builds)
     const uint32_t* Xstart;   // cell table of the sorted projected set
     const uint32_t* qlist;    // queries (internal indices, build_query_list order)
     const uint32_t* qcodes;   // their Morton codes
@@ -128,6 +130,7 @@ int fast_blocks_per_sm(int lanes_per_point, bool wlop, bool check_zero, int rep_
 struct DensityArgs {
     const float4* C;          // cloud, sorted (queries)
     const float4* Cpairs;     // cloud, pair records (candidates)
+    size_t Cpairs_cap;        // float4 elements of Cpairs (checked builds)
     const uint32_t* Cstart;   // cell table of the sorted cloud
     const uint32_t* qlist;    // queries (sorted slots, build_query_list order)
     const uint32_t* qcodes;

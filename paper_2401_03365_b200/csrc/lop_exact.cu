@@ -138,8 +138,10 @@ __device__ __forceinline__ void for_each_candidate(const uint32_t* __restrict__ 
         const int yy = rw.loy + r % rw.ny;
         const int zz = rw.loz + r / rw.ny;
         const uint32_t base = ((uint32_t)zz * (uint32_t)g.gy + (uint32_t)yy) * (uint32_t)g.gx;
+        PCSB_DCHECK((uint64_t)base + (uint64_t)rw.hix + 1 <= (uint64_t)g.ncells);
         const uint32_t b = __ldg(&start[base + rw.lox]);
         const uint32_t e = __ldg(&start[base + rw.hix + 1]);
+        PCSB_DCHECK(b <= e);
         for (uint32_t k = b + lane; k < e; k += stride) f(k);
     }
 }
@@ -169,8 +171,10 @@ __device__ __forceinline__ void team_for_each(const uint32_t* __restrict__ start
         const int yy = rw.loy + t % rw.ny;
         const int zz = rw.loz + t / rw.ny;
         const uint32_t base = ((uint32_t)zz * (uint32_t)g.gy + (uint32_t)yy) * (uint32_t)g.gx;
+        PCSB_DCHECK((uint64_t)base + (uint64_t)rw.hix + 1 <= (uint64_t)g.ncells);
         const uint32_t b = __ldg(&start[base + rw.lox]);
         cnt = __ldg(&start[base + rw.hix + 1]) - b;
+        PCSB_DCHECK(cnt <= 0x7FFFFFFFu);
         tr->b[t] = b;
     }
     uint32_t incl = cnt;

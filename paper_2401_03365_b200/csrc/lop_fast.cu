@@ -133,6 +133,21 @@ __device__ __forceinline__ void fence_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
+// Checked builds poison a half with far records once it has been evaluated:
+// a later evaluation that reads the half before its bulk copies landed then
+// sees points that are never hits, and the exact per-query interaction counts
+// of the parity tests expose the missing neighbours.
+__device__ __forceinline__ void poison_half(float4* half, int lane) {
+#ifdef PCSB_CHECKS
+    for (int t = lane; t < 2 * HR; t += 32)
+        half[t] = (t & 1) ? make_float4(kFar, kFar, 0.f, 0.f) : make_float4(kFar, kFar, kFar, kFar);
+    __syncwarp();
+#else
+    (void)half;
+    (void)lane;
+#endif
+}
+
 struct Stage {
     float4* ring;     // 2 halves x HR records x 2 float4
     uint32_t ring_s;  // its shared-window address
@@ -146,6 +161,8 @@ __device__ __forceinline__ Stage make_stage(float4* ring, uint64_t* bars, int la
     S.ring_s = (uint32_t)__cvta_generic_to_shared(ring);
     S.bar_s = (uint32_t)__cvta_generic_to_shared(bars);
     S.phase = 0;
+    poison_half(ring, lane);
+    poison_half(ring + 2 * HR, lane);
     if (lane == 0) {
         mbar_init(S.bar_s, 1);
         mbar_init(S.bar_s + 8, 1);
@@ -223,9 +240,11 @@ __device__ __forceinline__ void row_range(const uint32_t* __restrict__ start, co
     const int hix = cell_coord((double)hi, g.ox, g.inv_csx, g.gx);
     const uint32_t row = (uint32_t)zz * (uint32_t)g.gy + (uint32_t)yy;
     const uint32_t base = row * (uint32_t)g.gx;
+    PCSB_DCHECK(lox <= hix && (uint64_t)base + (uint64_t)hix + 1 <= (uint64_t)g.ncells);
     const uint32_t delta = pair_row_delta(start, row, (uint32_t)g.gx);  // record-slot shift
     rb = __ldg(&start[base + lox]) + delta;
     re = __ldg(&start[base + hix + 1]) + delta;
+    PCSB_DCHECK(rb <= re);
 }
 
 // Streams every record of the trimmed rows through the double buffer and calls
@@ -237,18 +256,23 @@ __device__ __forceinline__ void row_range(const uint32_t* __restrict__ start, co
 // the half is full.  A half is evaluated after the other half has been filled,
 // so its copies had that long to land.
 template <typename Eval>
-__device__ __forceinline__ void gather_eval(const float4* __restrict__ pairs,
+__device__ __forceinline__ void gather_eval(const float4* __restrict__ pairs, size_t pairs_cap,
                                             const uint32_t* __restrict__ start, const GridGeom& g,
                                             const Box& b, double s_pad, const GroupQ& G, Stage& S,
                                             int lane, Eval&& eval) {
+    (void)pairs_cap;
     const RowSpan rs = row_span(g, b, s_pad);
     uint32_t cur = 0, fill = 0;
     int pending = -1;
     auto finish = [&](uint32_t h, int nrec) {
+        PCSB_DCHECK(nrec >= 0 && nrec <= HR && nrec % STEP == 0);
+#ifndef PCSB_MUTATE_NO_WAIT  // detector self-test only (tools/gpu_checked.sh): a missing wait
         mbar_wait(S.bar_s + 8u * h, (S.phase >> h) & 1u);
+#endif
         S.phase ^= 1u << h;
         eval(S.ring + h * (2 * HR), nrec);
         __syncwarp();
+        poison_half(S.ring + h * (2 * HR), lane);
     };
     for (int r0 = 0; r0 < rs.nrows; r0 += 32) {
         uint32_t rb, re;
@@ -267,6 +291,8 @@ __device__ __forceinline__ void gather_eval(const float4* __restrict__ pairs,
             const uint32_t w1 = min(total, w0 + (uint32_t)HR - fill);
             const uint32_t lo = max(mine0, w0), hi = min(incl, w1);
             if (lo < hi) {
+                PCSB_DCHECK(fill + (lo - w0) + (hi - lo) <= (uint32_t)HR);
+                PCSB_DCHECK(2 * ((size_t)rec0 + (hi - mine0)) <= pairs_cap);
                 const uint32_t bar = S.bar_s + 8u * cur;
                 mbar_expect_tx(bar, (hi - lo) * 32u);
                 bulk_g2s(S.ring_s + (cur * HR + fill + (lo - w0)) * 32u,
@@ -648,7 +674,7 @@ fast_kernel(const FastArgs a) {
             // ---------------- attraction: data candidates (lop.cpp:49-65) ----------------
             Acc at = acc_zero();
             if (kAttr) {
-                gather_eval(a.Ppairs, a.Pstart, a.gP, box, a.s_pad, G, S, lane,
+                gather_eval(a.Ppairs, a.Ppairs_cap, a.Pstart, a.gP, box, a.s_pad, G, S, lane,
                             [&](const float4* half, int nrec) {
                                 eval_half<L, K_ATTR, kWlop, kCheckZero>(half, nrec, sub, q, ec,
                                                                       a.band, a.r2, at);
@@ -678,7 +704,7 @@ fast_kernel(const FastArgs a) {
             // ---------------- repulsion: projected-set candidates (lop.cpp:79-97) ----------------
             Acc rp = acc_zero();
             if (kRepul) {
-                gather_eval(a.Xpairs, a.Xstart, a.gX, box, a.s_pad, G, S, lane,
+                gather_eval(a.Xpairs, a.Xpairs_cap, a.Xstart, a.gX, box, a.s_pad, G, S, lane,
                             [&](const float4* half, int nrec) {
                                 eval_half<L, KREP, kWlop, true>(half, nrec, sub, q, ec, a.band,
                                                                 a.r2, rp);
@@ -808,7 +834,7 @@ density_kernel(const DensityArgs a) {
             __syncwarp();
             const GroupQ G{qsh[warp], (int)(g1 - g0), a.scull2};
             Acc A = acc_zero();
-            gather_eval(a.Cpairs, a.Cstart, a.g, box, a.s_pad, G, S, lane,
+            gather_eval(a.Cpairs, a.Cpairs_cap, a.Cstart, a.g, box, a.s_pad, G, S, lane,
                         [&](const float4* half, int nrec) {
                             eval_half<DL, K_DENSITY, false, true>(half, nrec, sub, q, ec, a.band,
                                                                  a.r2, A);

@@ -61,6 +61,7 @@ enum : int { YF_OK = 0, YF_TOO_FEW = 1, YF_SINGULAR = 2 };
 struct MlsArgs {
     const double4* pts;      // cloud in cell order
     const uint32_t* start;   // cell lower-bound table
+    uint32_t n;              // cloud size (checked builds)
     GridGeom g;
     double s_pad, r2, support, h;
     const double* q;         // queries, xyz
@@ -123,8 +124,10 @@ __device__ __forceinline__ void for_candidates(const MlsArgs& a, double cx, doub
         if (r < nrows) {
             const int yy = loy + r % ny, zz = loz + r / ny;
             const uint32_t base = ((uint32_t)zz * (uint32_t)g.gy + (uint32_t)yy) * (uint32_t)g.gx;
+            PCSB_DCHECK((uint64_t)base + (uint64_t)hix + 1 <= (uint64_t)g.ncells);
             b = __ldg(&a.start[base + lox]);
             cnt = __ldg(&a.start[base + hix + 1]) - b;
+            PCSB_DCHECK((uint64_t)b + cnt <= (uint64_t)a.n);
         }
         uint32_t incl = cnt;
 #pragma unroll
@@ -793,6 +796,7 @@ void mls_project(MlsIndex* ix, const pcs_mls_desc& d, const double* q, uint64_t 
     MlsArgs a{};
     a.pts = ix->sorted;
     a.start = ix->start;
+    a.n = (uint32_t)ix->n;
     a.g = ix->g;
     a.support = support;
     a.r2 = support * support;

@@ -490,7 +490,8 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     launches_ += build_cell_start(tsk, nn, 3 * g_.sub_bits, g_.ncells, P_start_, cell_scratch_,
                                   nullptr, stream_);
     if (fp32_) {
-        P_pairs_ = (float4*)dalloc(pairs_capacity(nn, g_) * sizeof(float4));
+        P_pairs_cap_ = pairs_capacity(nn, g_);
+        P_pairs_ = (float4*)dalloc(P_pairs_cap_ * sizeof(float4));
         launches_ += build_pairs((const float4*)P_sorted_, nullptr, nullptr, tsk, nn, g_, P_start_,
                                  P_pairs_, nullptr, stream_);
     }
@@ -510,6 +511,7 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
                                           pf, pfs, pq, &bsh, rs_, nullptr, stream_);
             da.C = (const float4*)P_sorted_;
             da.Cpairs = P_pairs_;
+            da.Cpairs_cap = P_pairs_cap_;
             da.Cstart = P_start_;
             da.qlist = pq;
             da.qcodes = pfs;
@@ -635,7 +637,8 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     X_sidx_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
     X_start_ = (uint32_t*)dalloc(((size_t)gX_.ncells + 1) * sizeof(uint32_t));
     if (fp32_) {
-        X_pairs_ = (float4*)dalloc(pairs_capacity((uint32_t)mp, gX_) * sizeof(float4));
+        X_pairs_cap_ = pairs_capacity((uint32_t)mp, gX_);
+        X_pairs_ = (float4*)dalloc(X_pairs_cap_ * sizeof(float4));
     }
     careful_list_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
     attr_ = (float4*)dalloc(mp * sizeof(float4));
@@ -775,6 +778,7 @@ void Plan::density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur) {
         DensityArgs da{};
         da.C = (const float4*)Xcur;
         da.Cpairs = X_pairs_;
+        da.Cpairs_cap = X_pairs_cap_;
         da.Cstart = X_start_;
         da.qlist = qlist;
         da.qcodes = q_skeys_;
@@ -894,9 +898,11 @@ void Plan::enqueue_sweep(int k) {
     if (fp32_) {
         FastArgs a{};
         a.Ppairs = P_pairs_;
+        a.Ppairs_cap = P_pairs_cap_;
         a.Pstart = P_start_;
         a.Xq = (const float4*)cur;
         a.Xpairs = X_pairs_;
+        a.Xpairs_cap = X_pairs_cap_;
         a.Xstart = X_start_;
         a.qlist = qlist;
         a.qcodes = q_skeys_;
@@ -1313,11 +1319,13 @@ void density_weights_t(const pcs_lop_desc& d, const double* C, uint64_t n, doubl
         int bsh = 0;
         build_query_list((const float4*)tg.sorted, (uint32_t)n, tg.g, support, nullptr, 0, 0, pf, pfs,
                          pq, &bsh, rs, nullptr, s);
-        float4* cp = (float4*)tg.alloc(pairs_capacity((uint32_t)n, tg.g) * sizeof(float4));
+        const size_t cp_cap = pairs_capacity((uint32_t)n, tg.g);
+        float4* cp = (float4*)tg.alloc(cp_cap * sizeof(float4));
         build_pairs((const float4*)tg.sorted, nullptr, nullptr, tg.skeys, (uint32_t)n, tg.g, tg.start, cp,
                     nullptr, s);
         da.C = (const float4*)tg.sorted;
         da.Cpairs = cp;
+        da.Cpairs_cap = cp_cap;
         da.Cstart = tg.start;
         da.qlist = pq;
         da.qcodes = pfs;

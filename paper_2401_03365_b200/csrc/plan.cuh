@@ -129,6 +129,7 @@ private:
     uint32_t* q_list_alt_ = nullptr;
     int block_shift_alt_ = 0;
     bool q_next_ready_ = false;
+    size_t P_pairs_cap_ = 0, X_pairs_cap_ = 0;  // float4 elements of the pair records
     bool fused_ = false;              // one pass (attraction + repulsion) after the X grid
     bool bisect_ = true;              // query groups by recursive bisection of 32-query units
     bool async_order_ = true;         // developer knob PCSB_ASYNC_ORDER=0: build in line
