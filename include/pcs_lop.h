@@ -74,7 +74,9 @@ typedef struct pcs_lop_desc {
     int32_t precision;         /* pcs_precision */
     int32_t device;            /* CUDA ordinal; -1 = current device */
     int32_t lanes_per_point;   /* fp32 kernel tuning: 0 = auto, else 2, 4, 8 */
-    int32_t reserved[7];
+    int32_t no_graphs;         /* 1: enqueue every sweep's launches; 0 (default): sweeps 2.. are
+                                  replayed as CUDA graphs of 8 sweeps (single-process plans) */
+    int32_t reserved[6];
 } pcs_lop_desc;
 
 /* LopSummary (proj/include/pcs/lop.hpp:29-35) + measured counters. */
@@ -149,6 +151,12 @@ pcs_status pcs_lop_plan_download(pcs_lop_plan* p, double* X_out_xyz, pcs_lop_sum
                                  uint32_t* isolated_out, uint64_t isolated_cap);
 /* Number of this process's kernel launches issued by the plan so far. */
 uint64_t pcs_lop_plan_launches(const pcs_lop_plan* p);
+/* CUDA-graph replay of the sweeps on (1, the descriptor default unless
+ * no_graphs) or off (0).  With graphs on, sweeps 2, 3, ... run as replays of one
+ * captured graph of 8 sweeps (kernel_ms / sort_ms then cover only the sweeps
+ * enqueued one by one); pcs_lop_plan_graph_launches counts the replays. */
+pcs_status pcs_lop_plan_set_graphs(pcs_lop_plan* p, int32_t enable);
+uint64_t pcs_lop_plan_graph_launches(const pcs_lop_plan* p);
 
 /* Per-query evidence of the fused path (parity facility; off by default, call
  * after upload).  While enabled, every sweep records for each query of X^k:

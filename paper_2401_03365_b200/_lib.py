@@ -45,7 +45,8 @@ EXPORTED = [
     "pcs_format_cloud_alloc", "pcs_free_buffer", "pcs_lop_plan_record_counts",
     "pcs_lop_plan_query_counts", "pcs_trim_device_pool",
     "pcs_mls_desc_default", "pcs_mls_index_create", "pcs_mls_index_destroy", "pcs_mls_index_radius",
-    "pcs_mls_project", "pcs_mls_smooth", "pcs_mls_partition",
+    "pcs_mls_project", "pcs_mls_smooth", "pcs_mls_partition", "pcs_lop_plan_set_graphs",
+    "pcs_lop_plan_graph_launches",
 ]
 
 PCS_MLS_PROJECT = 0
@@ -66,7 +67,8 @@ class LopDesc(C.Structure):
         ("precision", C.c_int32),
         ("device", C.c_int32),
         ("lanes_per_point", C.c_int32),
-        ("reserved", C.c_int32 * 7),
+        ("no_graphs", C.c_int32),
+        ("reserved", C.c_int32 * 6),
     ]
 
 
@@ -163,6 +165,9 @@ def lib():
                                             C.c_uint64]
         L.pcs_lop_plan_launches.argtypes = [C.c_void_p]
         L.pcs_lop_plan_launches.restype = C.c_uint64
+        L.pcs_lop_plan_set_graphs.argtypes = [C.c_void_p, C.c_int32]
+        L.pcs_lop_plan_graph_launches.argtypes = [C.c_void_p]
+        L.pcs_lop_plan_graph_launches.restype = C.c_uint64
         L.pcs_lop_plan_record_counts.argtypes = [C.c_void_p, C.c_int32]
         L.pcs_lop_plan_query_counts.argtypes = [C.c_void_p, C.POINTER(C.c_int32), _u8p, C.c_uint64]
         L.pcs_trim_device_pool.argtypes = [C.c_int32]

@@ -220,6 +220,17 @@ uint64_t pcs_lop_plan_launches(const pcs_lop_plan* p) {
     return p ? reinterpret_cast<const pcsb::Plan*>(p)->launches() : 0;
 }
 
+pcs_status pcs_lop_plan_set_graphs(pcs_lop_plan* p, int32_t enable) {
+    return guarded([&] {
+        if (!p) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null plan");
+        reinterpret_cast<pcsb::Plan*>(p)->set_graphs(enable != 0);
+    });
+}
+
+uint64_t pcs_lop_plan_graph_launches(const pcs_lop_plan* p) {
+    return p ? reinterpret_cast<const pcsb::Plan*>(p)->graph_launches() : 0;
+}
+
 pcs_status pcs_radius_query_all(const pcs_lop_desc* d, const double* C_xyz, uint64_t n,
                                 const double* Q_xyz, uint64_t m, double r, uint64_t* offsets,
                                 uint32_t* idx, uint64_t idx_cap) {

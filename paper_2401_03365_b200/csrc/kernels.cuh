@@ -201,7 +201,7 @@ void launch_radius_dump(const typename Vec4<T>::type* C, const uint32_t* Corder,
                         cudaStream_t s);
 
 // ---- sweep bookkeeping --------------------------------------------------------
-void launch_finalize_sweep(RunState* st, SweepSlot* slot, SweepSlot* next, int sweep, double tol,
+void launch_finalize_sweep(RunState* st, SweepSlot* slot, SweepSlot* next, double tol,
                            cudaStream_t s);
 template <typename T>
 void launch_unpermute(const typename Vec4<T>::type* X, const uint32_t* orig_of_internal,

@@ -427,13 +427,15 @@ radius_dump_kernel(const typename Vec4<T>::type* __restrict__ C, const uint32_t*
     }
 }
 
-__global__ void finalize_kernel(RunState* st, SweepSlot* slot, SweepSlot* next, int sweep,
-                                double tol) {
+// Sweep epilogue (lop.cpp:102-119).  The sweep count lives on the device
+// (iterations_run += 1 per executed sweep), so the launch has no per-sweep
+// argument and replays identically inside a CUDA graph.
+__global__ void finalize_kernel(RunState* st, SweepSlot* slot, SweepSlot* next, double tol) {
     if (st->done) return;
     if (next != slot) *next = SweepSlot{};  // recycled slot of the next sweep
     const unsigned long long b = slot->max_disp_bits;
     const double md = __longlong_as_double((long long)b);
-    st->iterations_run = sweep;
+    st->iterations_run += 1;
     st->last_max_disp = md;
     if (md < tol) {  // lop.cpp:116-119
         st->converged = 1;
@@ -536,9 +538,9 @@ void launch_radius_dump(const typename Vec4<T>::type* C, const uint32_t* Corder,
         C, Corder, Cstart, g, Q, m, r2, s_pad, offsets_or_counts, idx);
 }
 
-void launch_finalize_sweep(RunState* st, SweepSlot* slot, SweepSlot* next, int sweep, double tol,
+void launch_finalize_sweep(RunState* st, SweepSlot* slot, SweepSlot* next, double tol,
                            cudaStream_t s) {
-    finalize_kernel<<<1, 1, 0, s>>>(st, slot, next, sweep, tol);
+    finalize_kernel<<<1, 1, 0, s>>>(st, slot, next, tol);
 }
 
 template <typename T>

@@ -18,7 +18,11 @@
 namespace pcsb {
 
 namespace {
-constexpr int kSlotCap = 4096;
+// sweep slots are recycled (finalize of sweep k clears the slot of sweep k + 1);
+// kSlotCap = the CUDA-graph period, so a captured period maps sweeps to the same
+// slots on every replay
+constexpr int kSlotCap = 8;
+constexpr int kGraphPeriod = 8;
 
 int bit_width_u64(uint64_t v) {
     int b = 0;
@@ -252,6 +256,8 @@ Plan::Plan(const pcs_lop_desc& d) : d_(d) {
     // repulsion over the sparser projected set: 16-query groups amortise the
     // per-row cost better (measured -1..2% sweep time on configs 3 and 4)
     rep_lanes_ = d_.lanes_per_point ? lanes_ : 4;  // measured with bisected groups: 4 >= 2 on configs 3, 4, 5
+    use_graphs_ = d_.no_graphs == 0;
+    if (const char* e = dev_knob("PCSB_GRAPHS")) use_graphs_ = std::atoi(e) != 0;  // developer knob
     if (const char* e = dev_knob("PCSB_REORDER_EVERY")) reorder_every_ = std::max(1, std::atoi(e));
     if (const char* e = dev_knob("PCSB_ASYNC_ORDER")) async_order_ = std::atoi(e) != 0;  // developer knob
     if (const char* e = dev_knob("PCSB_FUSED")) fused_ = std::atoi(e) != 0;  // developer knob
@@ -297,6 +303,7 @@ Plan::Plan(const pcs_lop_desc& d) : d_(d) {
 Plan::~Plan() {
     if (stream2_) cudaStreamSynchronize(stream2_);
     if (stream_) cudaStreamSynchronize(stream_);
+    drop_graph();
     free_all();
     for (auto& se : event_pool_)
         for (auto e : se.e) cudaEventDestroy(e);
@@ -386,6 +393,7 @@ void Plan::set_loopback(LoopbackGroup* g, int rank) {
     delete coll_;
     coll_ = nullptr;
     coll_ = make_loopback_collectives(g, rank);
+    loopback_ = true;  // host rendezvous: not capturable
 }
 
 void Plan::upload(const double* P, uint64_t n, const double* X0, uint64_t m) {
@@ -402,6 +410,7 @@ void Plan::upload(const double* P, uint64_t n, const double* X0, uint64_t m) {
 template <typename T>
 void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     using V = typename Vec4<T>::type;
+    drop_graph();
     free_all();
     qcounts_ = nullptr;
     qever_ = nullptr;
@@ -698,14 +707,127 @@ void Plan::run(int sweeps, bool sync) {
     synchronize();
     PCSB_CUDA(cudaEventRecord(run_ev_[0], stream_));
     last_sweep_ = sweeps_issued_ + sweeps;
-    for (int i = 0; i < sweeps; ++i) {
-        const int k = ++sweeps_issued_;
-        if (fp32_) enqueue_sweep<float>(k);
-        else enqueue_sweep<double>(k);
+    while (sweeps_issued_ < last_sweep_) {
+        const int k = sweeps_issued_ + 1;
+        // whole periods k0 = 2 (mod kGraphPeriod) run as one captured graph
+        if (use_graphs_ && !loopback_ && k >= 2 && (k - 2) % kGraphPeriod == 0 &&
+            last_sweep_ - k + 1 >= kGraphPeriod && !q_stale_) {
+            enqueue_period(k);
+            continue;
+        }
+        ++sweeps_issued_;
+        enqueue_one(k);
     }
     PCSB_CUDA(cudaEventRecord(run_ev_[1], stream_));
     run_pending_ = true;
     if (sync) synchronize();
+}
+
+void Plan::enqueue_one(int k) {
+    if (fp32_) enqueue_sweep<float>(k);
+    else enqueue_sweep<double>(k);
+}
+
+void Plan::drop_graph() {
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+    if (graph_) cudaGraphDestroy(graph_);
+    graph_exec_ = nullptr;
+    graph_ = nullptr;
+}
+
+void Plan::set_graphs(bool on) {
+    synchronize();
+    use_graphs_ = on;
+    if (!on) drop_graph();
+}
+
+// Sweeps k0 .. k0 + kGraphPeriod - 1 as one CUDA graph: captured the first time
+// (and whenever the query-list buffers or the per-query count facility differ
+// from the captured ones), replayed afterwards.  A capture that fails (e.g. a
+// launch type the driver cannot capture) switches the plan back to enqueueing
+// every launch.
+void Plan::enqueue_period(int k0) {
+    (void)k0;
+    const void* key[3] = {q_list_, q_skeys_, record_counts_ ? (const void*)qcounts_ : nullptr};
+    const int shift[2] = {block_shift_, block_shift_alt_};
+    const bool same = graph_exec_ && key[0] == graph_key_[0] && key[1] == graph_key_[1] &&
+                      key[2] == graph_key_[2] && shift[0] == graph_shift_[0] &&
+                      shift[1] == graph_shift_[1];
+    if (same) {
+        sweeps_issued_ += kGraphPeriod;
+        launches_ += graph_period_launches_;
+        PCSB_CUDA(cudaGraphLaunch(graph_exec_, stream_));
+        ++graph_launches_;
+        return;
+    }
+    drop_graph();
+    // host state the period's enqueue mutates (restored if the capture fails)
+    struct Snap {
+        uint32_t *qs, *ql, *qsa, *qla;
+        int bs, bsa, since, issued;
+        bool stale, next_ready;
+        uint64_t launches;
+    } snap{q_skeys_, q_list_, q_skeys_alt_, q_list_alt_, block_shift_, block_shift_alt_,
+           sweeps_since_order_, sweeps_issued_, q_stale_, q_next_ready_, launches_};
+    PCSB_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    capturing_ = true;
+    bool ok = true;
+    try {
+        for (int j = 0; j < kGraphPeriod; ++j) {
+            ++sweeps_issued_;
+            enqueue_one(sweeps_issued_);
+        }
+    } catch (const Failure&) {
+        ok = false;
+    }
+    capturing_ = false;
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(stream_, &g);
+    for (auto& se : capture_events_) event_pool_.push_back(se);
+    capture_events_.clear();
+    ok = ok && e == cudaSuccess && g != nullptr;
+    if (ok && cudaGraphInstantiate(&graph_exec_, g, 0) != cudaSuccess) ok = false;
+    if (ok) {
+        graph_ = g;
+    } else if (g) {
+        cudaGraphDestroy(g);
+    }
+    cudaGetLastError();
+    if (!ok) {
+        // a launch the driver cannot capture: enqueue every launch from now on
+        graph_exec_ = nullptr;
+        use_graphs_ = false;
+        q_skeys_ = snap.qs;
+        q_list_ = snap.ql;
+        q_skeys_alt_ = snap.qsa;
+        q_list_alt_ = snap.qla;
+        block_shift_ = snap.bs;
+        block_shift_alt_ = snap.bsa;
+        sweeps_since_order_ = snap.since;
+        sweeps_issued_ = snap.issued;
+        q_stale_ = snap.stale;
+        q_next_ready_ = snap.next_ready;
+        launches_ = snap.launches;
+        for (int j = 0; j < kGraphPeriod; ++j) {
+            ++sweeps_issued_;
+            enqueue_one(sweeps_issued_);
+        }
+        return;
+    }
+    graph_period_launches_ = launches_ - snap.launches;
+    PCSB_CUDA(cudaGraphLaunch(graph_exec_, stream_));
+    ++graph_launches_;
+    // replayable only if the period left the host state where it started
+    // (two query-order swaps: the buffers are back in place)
+    if (q_list_ == snap.ql && q_skeys_ == snap.qs && block_shift_ == snap.bs &&
+        block_shift_alt_ == snap.bsa && sweeps_since_order_ == snap.since &&
+        q_next_ready_ == snap.next_ready && q_stale_ == snap.stale) {
+        for (int i = 0; i < 3; ++i) graph_key_[i] = key[i];
+        graph_shift_[0] = shift[0];
+        graph_shift_[1] = shift[1];
+    } else {
+        graph_key_[0] = graph_key_[1] = graph_key_[2] = nullptr;  // never matches: recapture
+    }
 }
 
 void Plan::synchronize() {
@@ -1023,10 +1145,13 @@ void Plan::enqueue_sweep(int k) {
         coll_->allreduce(&slot->max_disp_bits, 1, CDType::U64, COp::Max, stream_);
         coll_->group_end();
     }
-    launch_finalize_sweep(st_, slot, next_slot, k, d_.convergence_tol, stream_);
+    launch_finalize_sweep(st_, slot, next_slot, d_.convergence_tol, stream_);
     launches_ += 1;
     PCSB_CUDA(cudaEventRecord(se.e[5], stream_));
-    pending_.push_back(se);
+    // timing events exist only for sweeps enqueued one by one (a captured record
+    // is a dependency edge, not a timestamp of the replays)
+    if (capturing_) capture_events_.push_back(se);
+    else pending_.push_back(se);
 }
 
 void Plan::record_counts(bool on) {

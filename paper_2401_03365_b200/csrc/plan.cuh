@@ -58,6 +58,9 @@ public:
     double last_run_ms() const { return last_run_ms_; }
     void download(double* X_out, pcs_lop_summary* s, uint32_t* iso, uint64_t cap);
     uint64_t launches() const { return launches_; }
+    // CUDA-graph replay of sweeps 2, 3, ... in periods of kGraphPeriod (run()).
+    void set_graphs(bool on);
+    uint64_t graph_launches() const { return graph_launches_; }
     // Parity facility: per-query counts of every sweep (pcs_lop_plan_query_counts).
     void record_counts(bool on);
     void query_counts(int32_t* counts4, uint8_t* ever_flags, uint64_t m);
@@ -65,6 +68,9 @@ public:
 private:
     template <typename T> void upload_t(const double* P, uint64_t n, const double* X0, uint64_t m);
     template <typename T> void enqueue_sweep(int k);
+    void enqueue_one(int k);
+    void enqueue_period(int k0);  // capture (or replay) sweeps k0 .. k0 + kGraphPeriod - 1
+    void drop_graph();
     template <typename T> void density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur);
     template <typename T> void grid_rebuild(const void* Xcur, cudaStream_t st);
     void allgather_x(void* X, bool fp32);
@@ -163,6 +169,20 @@ private:
     };
     std::vector<SweepEvents> pending_;  // per issued sweep in the current run
     std::vector<SweepEvents> event_pool_;
+    // CUDA graph of kGraphPeriod sweeps.  A period starting at k0 = 2 (mod
+    // kGraphPeriod) returns the host state (query-list buffers, reorder count) to
+    // where it started and uses sweep slots 1..kGraphPeriod (mod kGraphPeriod),
+    // so one capture is replayed for every later period with the same buffers.
+    bool use_graphs_ = true;
+    bool loopback_ = false;
+    bool capturing_ = false;
+    cudaGraph_t graph_ = nullptr;
+    cudaGraphExec_t graph_exec_ = nullptr;
+    uint64_t graph_period_launches_ = 0;  // kernels in one period
+    uint64_t graph_launches_ = 0;         // replays (incl. the capture's own launch)
+    const void* graph_key_[3] = {nullptr, nullptr, nullptr};  // q_list_, q_skeys_, qcounts state
+    int graph_shift_[2] = {0, 0};
+    std::vector<SweepEvents> capture_events_;
 };
 
 // Parity facilities (stateless).

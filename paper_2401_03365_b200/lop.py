@@ -253,6 +253,13 @@ class LopPlan:
     def launches(self) -> int:
         return int(L.lib().pcs_lop_plan_launches(self._h))
 
+    def set_graphs(self, enable: bool) -> None:
+        """CUDA-graph replay of the sweeps (default on; off = every launch enqueued)."""
+        _check(L.lib().pcs_lop_plan_set_graphs(self._h, 1 if enable else 0))
+
+    def graph_launches(self) -> int:
+        return int(L.lib().pcs_lop_plan_graph_launches(self._h))
+
     def record_counts(self, enable: bool = True) -> None:
         """Parity facility: record per-query counts every sweep (after upload)."""
         _check(L.lib().pcs_lop_plan_record_counts(self._h, 1 if enable else 0))
