@@ -74,8 +74,8 @@ typedef struct pcs_lop_desc {
     int32_t precision;         /* pcs_precision */
     int32_t device;            /* CUDA ordinal; -1 = current device */
     int32_t lanes_per_point;   /* fp32 kernel tuning: 0 = auto, else 2, 4, 8 */
-    int32_t no_graphs;         /* 1: enqueue every sweep's launches; 0 (default): sweeps 2.. are
-                                  replayed as CUDA graphs of 8 sweeps (single-process plans) */
+    int32_t no_graphs;         /* 1: enqueue every sweep's launches; 0 (default): sweeps 2.. of
+                                  unsharded plans are replayed as CUDA graphs of 8 sweeps */
     int32_t reserved[6];
 } pcs_lop_desc;
 

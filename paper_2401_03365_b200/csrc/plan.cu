@@ -658,6 +658,10 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     q_keys_alt_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
     q_skeys_alt_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
     q_list_alt_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
+    q_home_[0] = q_skeys_;
+    q_home_[1] = q_list_;
+    q_home_[2] = q_skeys_alt_;
+    q_home_[3] = q_list_alt_;
     q_next_ready_ = false;
     ever_iso_ = (uint8_t*)dalloc(mp);
     slots_ = (SweepSlot*)dalloc(kSlotCap * sizeof(SweepSlot));
@@ -697,6 +701,16 @@ void Plan::reset() {
     PCSB_CUDA(cudaStreamSynchronize(stream_));
     sweeps_issued_ = 0;
     q_stale_ = true;
+    // the query-order buffers back in their upload-time roles (the order is
+    // rebuilt by sweep 1 anyway): every run then meets a captured CUDA graph in
+    // the same host state, whatever the parity of the previous run's swaps
+    q_skeys_ = q_home_[0];
+    q_list_ = q_home_[1];
+    q_skeys_alt_ = q_home_[2];
+    q_list_alt_ = q_home_[3];
+    block_shift_alt_ = 0;
+    q_next_ready_ = false;
+    sweeps_since_order_ = 0;
     sweeps_ms_ = kernel_ms_ = sort_ms_ = 0.0;
 }
 
@@ -707,18 +721,30 @@ void Plan::run(int sweeps, bool sync) {
     synchronize();
     PCSB_CUDA(cudaEventRecord(run_ev_[0], stream_));
     last_sweep_ = sweeps_issued_ + sweeps;
+    // single-process plans only: captured kernel nodes do not keep the side
+    // stream's high priority, which sharded plans need for the projected-set
+    // rebuild to take the SM slots their short attraction pass leaves (emulated
+    // 8-rank sweep 0.67 -> 0.69 ms with graphs; 1 GPU config 1 +34%, config 3 +0.7%)
+    const bool graphs = use_graphs_ && !loopback_ && !sharded();
     while (sweeps_issued_ < last_sweep_) {
         const int k = sweeps_issued_ + 1;
-        // whole periods k0 = 2 (mod kGraphPeriod) run as one captured graph
-        if (use_graphs_ && !loopback_ && k >= 2 && (k - 2) % kGraphPeriod == 0 &&
-            last_sweep_ - k + 1 >= kGraphPeriod && !q_stale_) {
-            enqueue_period(k);
+        // whole periods k0 = 2 (mod kGraphPeriod) replay the captured graph
+        if (graphs && k >= 2 && (k - 2) % kGraphPeriod == 0 && last_sweep_ - k + 1 >= kGraphPeriod &&
+            !q_stale_ && graph_matches()) {
+            replay_period();
             continue;
         }
         ++sweeps_issued_;
         enqueue_one(k);
+        if (graphs && !have_snap_ && (k - 1) % kGraphPeriod == 0 && !q_stale_ && !graph_matches()) {
+            period_snap_ = snapshot();  // the host state at the start of a period
+            have_snap_ = true;
+        }
     }
     PCSB_CUDA(cudaEventRecord(run_ev_[1], stream_));
+    // capture the period off the critical path: the sweeps above are executing
+    if (graphs && use_graphs_ && have_snap_) capture_period(period_snap_);
+    have_snap_ = false;
     run_pending_ = true;
     if (sync) synchronize();
 }
@@ -738,6 +764,7 @@ void Plan::drop_graph() {
 void Plan::set_graphs(bool on) {
     synchronize();
     use_graphs_ = on;
+    have_snap_ = false;
     if (!on) drop_graph();
 }
 
@@ -746,29 +773,56 @@ void Plan::set_graphs(bool on) {
 // from the captured ones), replayed afterwards.  A capture that fails (e.g. a
 // launch type the driver cannot capture) switches the plan back to enqueueing
 // every launch.
-void Plan::enqueue_period(int k0) {
-    (void)k0;
-    const void* key[3] = {q_list_, q_skeys_, record_counts_ ? (const void*)qcounts_ : nullptr};
-    const int shift[2] = {block_shift_, block_shift_alt_};
-    const bool same = graph_exec_ && key[0] == graph_key_[0] && key[1] == graph_key_[1] &&
-                      key[2] == graph_key_[2] && shift[0] == graph_shift_[0] &&
-                      shift[1] == graph_shift_[1];
-    if (same) {
-        sweeps_issued_ += kGraphPeriod;
-        launches_ += graph_period_launches_;
-        PCSB_CUDA(cudaGraphLaunch(graph_exec_, stream_));
-        ++graph_launches_;
-        return;
-    }
+Plan::HostSnap Plan::snapshot() const {
+    return HostSnap{q_skeys_,          q_list_,         q_skeys_alt_, q_list_alt_,  block_shift_,
+                    block_shift_alt_,  sweeps_since_order_, sweeps_issued_, last_sweep_, q_stale_,
+                    q_next_ready_,     launches_,
+                    record_counts_ ? (const void*)qcounts_ : nullptr};
+}
+
+void Plan::restore(const HostSnap& h) {
+    q_skeys_ = h.qs;
+    q_list_ = h.ql;
+    q_skeys_alt_ = h.qsa;
+    q_list_alt_ = h.qla;
+    block_shift_ = h.bs;
+    block_shift_alt_ = h.bsa;
+    sweeps_since_order_ = h.since;
+    sweeps_issued_ = h.issued;
+    last_sweep_ = h.last;
+    q_stale_ = h.stale;
+    q_next_ready_ = h.next_ready;
+    launches_ = h.launches;
+}
+
+bool Plan::graph_matches() const {
+    if (!graph_exec_) return false;
+    const HostSnap& g = graph_snap_;
+    // (block_shift_alt_ is not part of the state: the period's own re-ordering
+    // builds overwrite it before it is read)
+    return g.qs == q_skeys_ && g.ql == q_list_ && g.qsa == q_skeys_alt_ && g.qla == q_list_alt_ &&
+           g.bs == block_shift_ && g.since == sweeps_since_order_ &&
+           g.stale == q_stale_ && g.next_ready == q_next_ready_ &&
+           g.counts == (record_counts_ ? (const void*)qcounts_ : nullptr);
+}
+
+void Plan::replay_period() {
+    sweeps_issued_ += kGraphPeriod;
+    launches_ += graph_period_launches_;
+    PCSB_CUDA(cudaGraphLaunch(graph_exec_, stream_));
+    ++graph_launches_;
+}
+
+// Records (does not execute) the kGraphPeriod sweeps that start from host state
+// `at` as a CUDA graph, then puts the host state back.  The period returns the
+// query-list buffers and reorder count to where they started (two swaps), so
+// the graph replays every later period from the same state.  A capture the
+// driver rejects switches the plan to enqueueing every launch.
+void Plan::capture_period(const HostSnap& at) {
+    const HostSnap now = snapshot();
     drop_graph();
-    // host state the period's enqueue mutates (restored if the capture fails)
-    struct Snap {
-        uint32_t *qs, *ql, *qsa, *qla;
-        int bs, bsa, since, issued;
-        bool stale, next_ready;
-        uint64_t launches;
-    } snap{q_skeys_, q_list_, q_skeys_alt_, q_list_alt_, block_shift_, block_shift_alt_,
-           sweeps_since_order_, sweeps_issued_, q_stale_, q_next_ready_, launches_};
+    restore(at);
+    last_sweep_ = 1 << 30;  // the period's own re-orderings are built inside it
     PCSB_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
     capturing_ = true;
     bool ok = true;
@@ -786,48 +840,30 @@ void Plan::enqueue_period(int k0) {
     for (auto& se : capture_events_) event_pool_.push_back(se);
     capture_events_.clear();
     ok = ok && e == cudaSuccess && g != nullptr;
-    if (ok && cudaGraphInstantiate(&graph_exec_, g, 0) != cudaSuccess) ok = false;
+    const HostSnap after = snapshot();
+    // replayable only if the period left the host state where it started
+    ok = ok && after.qs == at.qs && after.ql == at.ql && after.bs == at.bs &&
+         after.since == at.since && after.next_ready == at.next_ready && after.stale == at.stale;
+    if (ok && cudaGraphInstantiate(&graph_exec_, g, 0) != cudaSuccess) {
+        graph_exec_ = nullptr;
+        ok = false;
+    }
+    static const bool dbg = dev_knob("PCSB_DEBUG_GRAPH") != nullptr;  // developer knob
+    if (dbg)
+        std::fprintf(stderr, "[pcsb] graph capture: ok=%d end=%s state %d%d%d%d%d%d%d\n", (int)ok,
+                     cudaGetErrorString(e), after.qs == at.qs, after.ql == at.ql, after.bs == at.bs,
+                     after.bsa == at.bsa, after.since == at.since, after.next_ready == at.next_ready,
+                     after.stale == at.stale);
     if (ok) {
         graph_ = g;
-    } else if (g) {
-        cudaGraphDestroy(g);
+        graph_period_launches_ = after.launches - at.launches;
+        graph_snap_ = at;
+    } else {
+        if (g) cudaGraphDestroy(g);
+        use_graphs_ = false;
     }
     cudaGetLastError();
-    if (!ok) {
-        // a launch the driver cannot capture: enqueue every launch from now on
-        graph_exec_ = nullptr;
-        use_graphs_ = false;
-        q_skeys_ = snap.qs;
-        q_list_ = snap.ql;
-        q_skeys_alt_ = snap.qsa;
-        q_list_alt_ = snap.qla;
-        block_shift_ = snap.bs;
-        block_shift_alt_ = snap.bsa;
-        sweeps_since_order_ = snap.since;
-        sweeps_issued_ = snap.issued;
-        q_stale_ = snap.stale;
-        q_next_ready_ = snap.next_ready;
-        launches_ = snap.launches;
-        for (int j = 0; j < kGraphPeriod; ++j) {
-            ++sweeps_issued_;
-            enqueue_one(sweeps_issued_);
-        }
-        return;
-    }
-    graph_period_launches_ = launches_ - snap.launches;
-    PCSB_CUDA(cudaGraphLaunch(graph_exec_, stream_));
-    ++graph_launches_;
-    // replayable only if the period left the host state where it started
-    // (two query-order swaps: the buffers are back in place)
-    if (q_list_ == snap.ql && q_skeys_ == snap.qs && block_shift_ == snap.bs &&
-        block_shift_alt_ == snap.bsa && sweeps_since_order_ == snap.since &&
-        q_next_ready_ == snap.next_ready && q_stale_ == snap.stale) {
-        for (int i = 0; i < 3; ++i) graph_key_[i] = key[i];
-        graph_shift_[0] = shift[0];
-        graph_shift_[1] = shift[1];
-    } else {
-        graph_key_[0] = graph_key_[1] = graph_key_[2] = nullptr;  // never matches: recapture
-    }
+    restore(now);
 }
 
 void Plan::synchronize() {

@@ -69,7 +69,19 @@ private:
     template <typename T> void upload_t(const double* P, uint64_t n, const double* X0, uint64_t m);
     template <typename T> void enqueue_sweep(int k);
     void enqueue_one(int k);
-    void enqueue_period(int k0);  // capture (or replay) sweeps k0 .. k0 + kGraphPeriod - 1
+    // host state that enqueueing sweeps mutates (CUDA-graph capture / replay)
+    struct HostSnap {
+        uint32_t *qs, *ql, *qsa, *qla;
+        int bs, bsa, since, issued, last;
+        bool stale, next_ready;
+        uint64_t launches;
+        const void* counts;
+    };
+    HostSnap snapshot() const;
+    void restore(const HostSnap& h);
+    bool graph_matches() const;
+    void replay_period();
+    void capture_period(const HostSnap& at);
     void drop_graph();
     template <typename T> void density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur);
     template <typename T> void grid_rebuild(const void* Xcur, cudaStream_t st);
@@ -179,9 +191,11 @@ private:
     cudaGraph_t graph_ = nullptr;
     cudaGraphExec_t graph_exec_ = nullptr;
     uint64_t graph_period_launches_ = 0;  // kernels in one period
-    uint64_t graph_launches_ = 0;         // replays (incl. the capture's own launch)
-    const void* graph_key_[3] = {nullptr, nullptr, nullptr};  // q_list_, q_skeys_, qcounts state
-    int graph_shift_[2] = {0, 0};
+    uint64_t graph_launches_ = 0;         // replays
+    HostSnap graph_snap_{};               // host state the captured period starts from
+    HostSnap period_snap_{};              // a period start seen in the current run
+    bool have_snap_ = false;
+    uint32_t* q_home_[4] = {nullptr, nullptr, nullptr, nullptr};  // q_skeys_, q_list_, alts at upload
     std::vector<SweepEvents> capture_events_;
 };
 

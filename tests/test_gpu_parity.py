@@ -464,3 +464,41 @@ def test_deferred_queries_match_oracle(pb, orc, wlop):
     assert (s.isolated_events, s.coincident_pairs) == (r.isolated_events, r.coincident_pairs)
     assert np.array_equal(out[300:], X0[300:])  # anchored on themselves
     assert np.abs(out - r.points).max() <= 1e-5 * bbox_diag(P)
+
+
+@pytest.mark.parametrize("cfg,scale,h,prec", [(3, 0.01, 0.2, "fp32"), (2, 0.02, 0.3, "fp32"),
+                                              (1, 1.0, None, "fp64")])
+def test_cuda_graph_replay_is_bit_identical(pb, cfg, scale, h, prec):
+    """Sweeps 2.. replayed as captured CUDA graphs of 8 sweeps give exactly the
+    positions and summary of enqueuing every launch (deterministic kernels, same
+    launch order).  The first run with graphs on enqueues every launch and
+    captures the period at its end (off the critical path); the next run
+    replays it (graph launches counted)."""
+    P, X0 = pb.generate_config(cfg, scale)
+    if prec == "fp32":
+        P, X0 = r32(P), r32(X0)
+    prm, c = pb.config_params(cfg, h=h)
+    prm.iterations = 21
+    prm.convergence_tol = 1e-30
+    plan = pb.LopPlan(prm, eta=c["eta"], density_weights=c["wlop"], precision=prec)
+    try:
+        plan.upload(P, X0)
+        res = {}
+        for on in (False, True, True):
+            plan.set_graphs(on)
+            plan.reset()
+            g0 = plan.graph_launches()
+            plan.run(21)
+            out, s = plan.download()
+            res.setdefault(on, []).append((out, s, plan.graph_launches() - g0))
+        (o0, s0, g_off), = res[False]
+        assert [g for _, _, g in res[True]] == [0, 2]  # then sweeps 2-9 and 10-17 replayed
+        for out, s, g in res[True]:
+            assert np.array_equal(out, o0)
+            assert (s.iterations_run, s.interactions_attr, s.interactions_rep, s.isolated_events,
+                    s.coincident_pairs, s.careful_points) == \
+                   (s0.iterations_run, s0.interactions_attr, s0.interactions_rep,
+                    s0.isolated_events, s0.coincident_pairs, s0.careful_points)
+        assert g_off == 0
+    finally:
+        plan.close()
