@@ -253,9 +253,96 @@ struct Frame {
     double o[3], n[3], u[3], v[3];
 };
 
-// fit_local_polynomial (wls.cpp:149-222) of `degree` over frame F; coefficients
-// in S.x on success.
-__device__ int poly_fit(const MlsArgs& a, WarpSmem& S, const Frame& F, int degree, int lane) {
+// Entry e of the packed normal system of a K-coefficient fit: the upper
+// triangle of M row by row, then the right-hand side b (col -1).
+__host__ __device__ constexpr int entry_row(int K, int e) {
+    if (e >= K * (K + 1) / 2) return e - K * (K + 1) / 2;
+    int r = 0;
+    while (e >= K - r) {
+        e -= K - r;
+        ++r;
+    }
+    return r;
+}
+__host__ __device__ constexpr int entry_col(int K, int e) {
+    if (e >= K * (K + 1) / 2) return -1;
+    int r = 0;
+    while (e >= K - r) {
+        e -= K - r;
+        ++r;
+    }
+    return r + e;
+}
+
+// The hit of candidate k for the frame F: local coordinates and weight
+// (wls.cpp:183-188; distance = sqrt(norm2(p - origin))).
+__device__ __forceinline__ bool frame_hit(const MlsArgs& a, const Frame& F, uint32_t k, double& ui,
+                                          double& vi, double& fi, double& w) {
+    if (k == 0xFFFFFFFFu) return false;
+    const double4 p = a.pts[k];
+    const double d2 = exact_d2(p.x, p.y, p.z, F.o[0], F.o[1], F.o[2]);
+    if (!(d2 <= a.r2)) return false;
+    const double dx = p.x - F.o[0], dy = p.y - F.o[1], dz = p.z - F.o[2];
+    ui = __dadd_rn(__dadd_rn(__dmul_rn(dx, F.u[0]), __dmul_rn(dy, F.u[1])), __dmul_rn(dz, F.u[2]));
+    vi = __dadd_rn(__dadd_rn(__dmul_rn(dx, F.v[0]), __dmul_rn(dy, F.v[1])), __dmul_rn(dz, F.v[2]));
+    fi = __dadd_rn(__dadd_rn(__dmul_rn(dx, F.n[0]), __dmul_rn(dy, F.n[1])), __dmul_rn(dz, F.n[2]));
+    w = theta_k(__dsqrt_rn(d2), a.support, a.h);
+    return true;
+}
+
+// Normal system of degree D <= 2 (K <= 6, 27 entries): every lane accumulates
+// ITS hits into registers (entries fully unrolled), then one fixed xor-tree
+// reduction per entry — no per-hit broadcast.  Returns the hit count.
+template <int D>
+__device__ int accum_lane(const MlsArgs& a, WarpSmem& S, const Frame& F, int lane) {
+    constexpr int K = (D + 1) * (D + 2) / 2;
+    constexpr int NE = K * (K + 1) / 2 + K;
+    double acc[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) acc[e] = 0.0;
+    int cnt = 0;
+    for_candidates(a, F.o[0], F.o[1], F.o[2], lane, [&](uint32_t k) {
+        double ui, vi, fi, w;
+        if (!frame_hit(a, F, k, ui, vi, fi, w)) return;
+        ++cnt;
+        double up[D + 1], vp[D + 1], bs[K];
+        up[0] = vp[0] = 1.0;
+#pragma unroll
+        for (int i = 1; i <= D; ++i) {
+            up[i] = up[i - 1] * ui;
+            vp[i] = vp[i - 1] * vi;
+        }
+        int kk = 0;
+#pragma unroll
+        for (int s = 0; s <= D; ++s)
+#pragma unroll
+            for (int e = s; e >= 0; --e) bs[kk++] = up[e] * vp[s - e];
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+            const int r = entry_row(K, e), c = entry_col(K, e);
+            const double wb = w * bs[r];
+            acc[e] += c >= 0 ? wb * bs[c] : wb * fi;
+        }
+    });
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+        const double v = wsum(acc[e]);
+        const int r = entry_row(K, e), c = entry_col(K, e);
+        if (lane == 0) {
+            if (c >= 0) {
+                S.M[r * KS + c] = v;
+                S.M[c * KS + r] = v;
+            } else {
+                S.b[r] = v;
+            }
+        }
+    }
+    return wsumi(cnt);
+}
+
+// Normal system of degree 3 or 4 (K = 10, 15: up to 135 entries): each hit is
+// broadcast to the warp and every lane accumulates the entries it owns.
+__device__ int accum_bcast(const MlsArgs& a, WarpSmem& S, const Frame& F, int degree, int lane) {
     const int K = (degree + 1) * (degree + 2) / 2;
     const int NE = K * (K + 1) / 2 + K;  // packed upper triangle of M, then b
     // the entries this lane owns (e = lane + 32 t), as (row, col); col = -1: b[row]
@@ -263,40 +350,14 @@ __device__ int poly_fit(const MlsArgs& a, WarpSmem& S, const Frame& F, int degre
 #pragma unroll
     for (int t = 0; t < 5; ++t) {
         const int e = lane + 32 * t;
-        er[t] = -1;
-        ec[t] = -1;
-        if (e < NE) {
-            if (e < K * (K + 1) / 2) {
-                int r = 0, rem = e;
-                while (rem >= K - r) {
-                    rem -= K - r;
-                    ++r;
-                }
-                er[t] = r;
-                ec[t] = r + rem;
-            } else {
-                er[t] = e - K * (K + 1) / 2;
-                ec[t] = -1;
-            }
-        }
+        er[t] = e < NE ? entry_row(K, e) : -1;
+        ec[t] = e < NE ? entry_col(K, e) : -1;
     }
     double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     int cnt = 0;
     for_candidates(a, F.o[0], F.o[1], F.o[2], lane, [&](uint32_t k) {
         double ui = 0.0, vi = 0.0, fi = 0.0, w = 0.0;
-        bool hit = false;
-        if (k != 0xFFFFFFFFu) {
-            const double4 p = a.pts[k];
-            const double d2 = exact_d2(p.x, p.y, p.z, F.o[0], F.o[1], F.o[2]);
-            if (d2 <= a.r2) {
-                hit = true;
-                const double dx = p.x - F.o[0], dy = p.y - F.o[1], dz = p.z - F.o[2];
-                ui = __dadd_rn(__dadd_rn(__dmul_rn(dx, F.u[0]), __dmul_rn(dy, F.u[1])), __dmul_rn(dz, F.u[2]));
-                vi = __dadd_rn(__dadd_rn(__dmul_rn(dx, F.v[0]), __dmul_rn(dy, F.v[1])), __dmul_rn(dz, F.v[2]));
-                fi = __dadd_rn(__dadd_rn(__dmul_rn(dx, F.n[0]), __dmul_rn(dy, F.n[1])), __dmul_rn(dz, F.n[2]));
-                w = theta_k(__dsqrt_rn(d2), a.support, a.h);
-            }
-        }
+        const bool hit = frame_hit(a, F, k, ui, vi, fi, w);
         cnt += hit ? 1 : 0;
         unsigned mask = __ballot_sync(0xffffffffu, hit);
         while (mask) {
@@ -323,8 +384,6 @@ __device__ int poly_fit(const MlsArgs& a, WarpSmem& S, const Frame& F, int degre
             }
         }
     });
-    cnt = wsumi(cnt);
-    if (cnt < K) return YF_TOO_FEW;
 #pragma unroll
     for (int t = 0; t < 5; ++t) {
         if (er[t] < 0) continue;
@@ -335,6 +394,17 @@ __device__ int poly_fit(const MlsArgs& a, WarpSmem& S, const Frame& F, int degre
             S.b[er[t]] = acc[t];
         }
     }
+    return wsumi(cnt);
+}
+
+// fit_local_polynomial (wls.cpp:149-222) of `degree` over frame F; coefficients
+// in S.x on success.
+__device__ int poly_fit(const MlsArgs& a, WarpSmem& S, const Frame& F, int degree, int lane) {
+    const int K = (degree + 1) * (degree + 2) / 2;
+    const int cnt = degree == 1 ? accum_lane<1>(a, S, F, lane)
+                  : degree == 2 ? accum_lane<2>(a, S, F, lane)
+                                : accum_bcast(a, S, F, degree, lane);
+    if (cnt < K) return YF_TOO_FEW;
     __syncwarp();
     for (int i = lane; i < K * KS; i += 32) S.A[i] = S.M[i];
     __syncwarp();
@@ -367,7 +437,7 @@ __device__ int poly_fit(const MlsArgs& a, WarpSmem& S, const Frame& F, int degre
     return YF_OK;
 }
 
-__global__ void __launch_bounds__(MLS_THREADS) mls_kernel(const MlsArgs a) {
+__global__ void __launch_bounds__(MLS_THREADS, 5) mls_kernel(const MlsArgs a) {
     __shared__ WarpSmem smem[MLS_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpSmem& S = smem[warp];
