@@ -15,4 +15,6 @@ plan.run(3)
 plan.reset()
 plan.run(6)
 _, s = plan.download()
-print(f"cfg {cfg}: {s.sweeps_ms / 6:.4f} ms/sweep")
+inter = s.interactions_attr + s.interactions_rep
+print(f"cfg {cfg}: {s.sweeps_ms / 6:.4f} ms/sweep, kernel {s.kernel_ms / 6:.4f} ms, interactions/sweep "
+      f"{inter / 6:.4e}, lc/int {s.lane_candidates / max(1, inter):.3f}")
