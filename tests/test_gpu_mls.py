@@ -96,3 +96,25 @@ def test_degenerate_thin_and_empty_inputs(pb):
     assert (res.plane_status == 2).all() and (res.status == 3).all()
     with pytest.raises(pb.InvalidParam):
         pb.smooth_cloud(iso, pb.MlsParams(degree=0))
+
+
+@pytest.mark.parametrize("n,h,deg", [(200, 0.05, 2), (500, 0.03, 3), (400, 0.05, 4)])
+def test_sparse_clouds_degrade_like_the_oracle(pb, orc, n, h, deg):
+    """Sparse random clouds: thin neighbourhoods step the degree down
+    (DegradedDegree, mls.cpp:48-60) or pass the point through (Skipped,
+    TooFewNeighbors); statuses, degrees used, plane statuses and iteration
+    counts must be the oracle's, positions within rounding."""
+    seen = np.zeros(4, dtype=int)
+    for seed in range(4):
+        P = np.random.default_rng(seed).uniform(-1, 1, (n, 3))
+        out, res = pb.smooth_cloud(P, pb.MlsParams(kernel=pb.KernelParams(h), degree=deg))
+        r = orc.mls_project(P, P, h, degree=deg)
+        assert np.array_equal(res.status, r["status"])
+        assert np.array_equal(res.degree_used, r["degree_used"])
+        assert np.array_equal(res.plane_status, r["plane_status"])
+        assert np.array_equal(res.iterations, r["iterations"])
+        assert np.abs(out - r["projected"]).max() <= 1e-9
+        skipped = res.status == 3
+        assert np.array_equal(out[skipped], P[skipped])
+        seen += np.bincount(res.status, minlength=4)
+    assert seen[1] > 0 and seen[3] > 0, seen  # degraded and skipped points occur
