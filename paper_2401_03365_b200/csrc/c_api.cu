@@ -103,6 +103,8 @@ pcs_status pcs_lop_run(const pcs_lop_desc* d, const double* P_xyz, uint64_t n,
         if (!P_xyz || !X0_xyz || !X_out_xyz)
             throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null point buffer");
         pcsb::Plan plan(desc);
+        // one run: a captured CUDA graph would never be replayed
+        plan.set_graphs(false);
         plan.upload(P_xyz, n, X0_xyz, m);
         plan.run(desc.iterations, true);
         plan.download(X_out_xyz, summary, isolated_out, isolated_cap);
