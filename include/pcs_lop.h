@@ -151,6 +151,10 @@ pcs_status pcs_lop_plan_download(pcs_lop_plan* p, double* X_out_xyz, pcs_lop_sum
                                  uint32_t* isolated_out, uint64_t isolated_cap);
 /* Number of this process's kernel launches issued by the plan so far. */
 uint64_t pcs_lop_plan_launches(const pcs_lop_plan* p);
+/* Restart from the given positions (m points, original order; unsharded plans):
+ * the next run starts its sweep 1 from X instead of X0.  The data grid and the
+ * grid box of the upload are kept; positions may lie anywhere. */
+pcs_status pcs_lop_plan_set_positions(pcs_lop_plan* p, const double* X_xyz, uint64_t m);
 /* CUDA-graph replay of the sweeps on (1, the descriptor default unless
  * no_graphs) or off (0).  With graphs on, sweeps 2, 3, ... run as replays of one
  * captured graph of 8 sweeps (kernel_ms / sort_ms then cover only the sweeps

@@ -46,7 +46,7 @@ EXPORTED = [
     "pcs_lop_plan_query_counts", "pcs_trim_device_pool",
     "pcs_mls_desc_default", "pcs_mls_index_create", "pcs_mls_index_destroy", "pcs_mls_index_radius",
     "pcs_mls_project", "pcs_mls_smooth", "pcs_mls_partition", "pcs_lop_plan_set_graphs",
-    "pcs_lop_plan_graph_launches",
+    "pcs_lop_plan_graph_launches", "pcs_lop_plan_set_positions",
 ]
 
 PCS_MLS_PROJECT = 0
@@ -166,6 +166,7 @@ def lib():
         L.pcs_lop_plan_launches.argtypes = [C.c_void_p]
         L.pcs_lop_plan_launches.restype = C.c_uint64
         L.pcs_lop_plan_set_graphs.argtypes = [C.c_void_p, C.c_int32]
+        L.pcs_lop_plan_set_positions.argtypes = [C.c_void_p, _dp, C.c_uint64]
         L.pcs_lop_plan_graph_launches.argtypes = [C.c_void_p]
         L.pcs_lop_plan_graph_launches.restype = C.c_uint64
         L.pcs_lop_plan_record_counts.argtypes = [C.c_void_p, C.c_int32]

@@ -222,6 +222,13 @@ uint64_t pcs_lop_plan_launches(const pcs_lop_plan* p) {
     return p ? reinterpret_cast<const pcsb::Plan*>(p)->launches() : 0;
 }
 
+pcs_status pcs_lop_plan_set_positions(pcs_lop_plan* p, const double* X_xyz, uint64_t m) {
+    return guarded([&] {
+        if (!p) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null plan");
+        reinterpret_cast<pcsb::Plan*>(p)->set_positions(X_xyz, m);
+    });
+}
+
 pcs_status pcs_lop_plan_set_graphs(pcs_lop_plan* p, int32_t enable) {
     return guarded([&] {
         if (!p) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null plan");

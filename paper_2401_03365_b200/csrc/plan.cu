@@ -687,6 +687,30 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     tfree(tsk);
 }
 
+// Restart point of the run (unsharded plans): X_init_ <- X (m points, original
+// order = internal order), then reset().  The grids keep the upload-time box:
+// positions may lie anywhere (boundary cells are unbounded outward).
+void Plan::set_positions(const double* X, uint64_t m) {
+    if (!uploaded_) throw Failure(PCS_ERR_INVALID_PARAM, "plan has no data (upload first)");
+    if (sharded()) throw Failure(PCS_ERR_INVALID_PARAM, "set_positions: unsharded plans only");
+    if (m != m_) throw Failure(PCS_ERR_INVALID_PARAM, "set_positions: m must equal the plan's m");
+    if (m && !X) throw Failure(PCS_ERR_INVALID_PARAM, "null buffer");
+    PCSB_CUDA(cudaSetDevice(device_));
+    synchronize();
+    if (m) {
+        if (fp32_) {
+            h2d_staged_f32x4(X_init_, X, m, 0.0f, stream_);
+        } else {
+            double* dX = (double*)talloc(m * 3 * sizeof(double));
+            h2d_staged(dX, X, m * 3 * sizeof(double), stream_);
+            launch_convert_xyz<double>(dX, (double4*)X_init_, m, 0.0, stream_);
+            launches_ += 1;
+            tfree(dX);
+        }
+    }
+    reset();
+}
+
 void Plan::reset() {
     if (!n_) throw Failure(PCS_ERR_INVALID_PARAM, "plan has no data (upload first)");
     PCSB_CUDA(cudaSetDevice(device_));

@@ -53,6 +53,7 @@ public:
     void set_loopback(LoopbackGroup* g, int rank);
     void upload(const double* P, uint64_t n, const double* X0, uint64_t m);
     void reset();
+    void set_positions(const double* X, uint64_t m);
     void run(int sweeps, bool sync);
     void synchronize();
     double last_run_ms() const { return last_run_ms_; }

@@ -253,6 +253,11 @@ class LopPlan:
     def launches(self) -> int:
         return int(L.lib().pcs_lop_plan_launches(self._h))
 
+    def set_positions(self, X) -> None:
+        """Restart point: the next run starts from X (m points) instead of X0."""
+        Xc = _cloud(X)
+        _check(L.lib().pcs_lop_plan_set_positions(self._h, _ptr(Xc), Xc.shape[0]))
+
     def set_graphs(self, enable: bool) -> None:
         """CUDA-graph replay of the sweeps (default on; off = every launch enqueued)."""
         _check(L.lib().pcs_lop_plan_set_graphs(self._h, 1 if enable else 0))

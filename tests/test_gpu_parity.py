@@ -502,3 +502,49 @@ def test_cuda_graph_replay_is_bit_identical(pb, cfg, scale, h, prec):
         assert g_off == 0
     finally:
         plan.close()
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_positions_outside_the_upload_box(pb, orc, prec):
+    """Projected points may leave the box the grids were built over (repulsion
+    pushes boundary points outward; an isolated point holds its position): out-
+    of-range cells clamp into the boundary cells, which are unbounded outward,
+    so no neighbour is lost (SURVEY §8(a') item 7).  The plan restarts from
+    positions placed outside the upload-time box — far away (isolated), and
+    just outside, within one support of the data — and one sweep must equal the
+    reference map per query (counts exact, positions within rounding)."""
+    P, X0 = pb.generate_config(3, 0.01)
+    if prec == "fp32":
+        P, X0 = r32(P), r32(X0)
+    prm, c = pb.config_params(3, h=0.2)
+    s = prm.kernel.support()
+    lo, hi = np.minimum(P.min(0), X0.min(0)), np.maximum(P.max(0), X0.max(0))
+    X = X0.copy()
+    X[:40] += np.array([3.0, 0.0, 0.0])                       # far beyond +x: isolated
+    X[40:80] += np.array([0.0, -2.5, 0.7])                    # far beyond -y, +z
+    edge = np.argsort(P[:, 0])[-40:]                          # data points at the +x edge
+    X[80:120] = P[edge] + np.array([0.6 * s, 0.0, 0.25 * s])  # outside the box, data within s
+    edge = np.argsort(P[:, 1])[:40]
+    X[120:160] = P[edge] - np.array([0.0, 0.45 * s, 0.0])
+    if prec == "fp32":
+        X = r32(X)
+    assert ((X[:160] < lo) | (X[:160] > hi)).any(axis=1).all()
+    plan = pb.LopPlan(prm, eta=c["eta"], precision=prec)
+    try:
+        plan.upload(P, X0)
+        plan.set_positions(X)
+        plan.record_counts(True)
+        plan.run(1)
+        Xn, _ = plan.download()
+        cnt, _ = plan.query_counts()
+    finally:
+        plan.close()
+    eta = orc.ETA_NEG_LINEAR
+    rows = np.arange(X.shape[0], dtype=np.uint32)
+    nxt, oc = orc.lop_sweep_rows(P, X, rows, prm.kernel.h, prm.kernel.cutoff_multiple, prm.mu,
+                                 eta=eta)
+    assert np.array_equal(cnt[:, :3], oc[:, :3])
+    assert np.array_equal(cnt[:, 3] & 3, oc[:, 3] & 3)
+    assert (oc[:80, 3] & 1).all() and (oc[80:160, 0] > 0).all()  # isolated far; edge ones attracted
+    tol = 4 * np.finfo(np.float32).eps * np.abs(X).max() if prec == "fp32" else 1e-12
+    assert np.abs(Xn - nxt).max() <= tol
