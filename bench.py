@@ -143,7 +143,7 @@ def sfu_peak(sm_mhz: float, sms: int = 148) -> dict:
 # ------------------------------------------------------------------------------
 # CPU baseline: the reference's own lop_project on the host cores
 # ------------------------------------------------------------------------------
-def cpu_baseline(cfg: int, P: np.ndarray, X0: np.ndarray, c: dict, repeats: int = 3,
+def cpu_baseline(cfg: int, P: np.ndarray, X0: np.ndarray, c: dict, repeats: int = 5,
                  sweeps: int = 11) -> dict:
     """The reference's own CPU path on a bounded, seeded sample of the workload.
 
@@ -272,7 +272,7 @@ def main():
         if precision == "fp32":
             P = P.astype(np.float32).astype(np.float64)
             X0 = X0.astype(np.float32).astype(np.float64)
-        cb = cpu_baseline(cfg, P, X0, c, repeats=3)
+        cb = cpu_baseline(cfg, P, X0, c, repeats=5)
         wall = time.perf_counter() - t0
         try:  # evidence: the product library is not mapped in this process
             maps = open("/proc/self/maps").read()
