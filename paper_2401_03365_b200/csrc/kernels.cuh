@@ -150,6 +150,13 @@ struct DensityArgs {
     const uint32_t* done;
 };
 void launch_density(const DensityArgs& a, int grid_blocks, cudaStream_t s);
+// Query groups of the curve-ordered list qin[0, nq) (internal indices into Xq):
+// bisected 8-query groups of every 32-position unit, cut where consecutive
+// queries are farther apart than sqrt(jump2); writes the permuted list to qout
+// and, per position, the first position of its group to codes (the fused
+// kernels then group by equal codes, block_shift = 0).
+void launch_group_order(const uint32_t* qin, const float4* Xq, uint32_t nq, float jump2,
+                        uint32_t* qout, uint32_t* codes, const uint32_t* done, cudaStream_t s);
 
 // ---- exact fp64 path (lop_exact.cu) -----------------------------------------
 template <typename T>

@@ -27,6 +27,7 @@
 //    projected pair or a non-finite sum are deferred to the exact fp64 kernel
 //    (lop_exact.cu).  The neighbour SET is always the reference's.
 #include "dev_knobs.h"
+#include <algorithm>
 #include <cfloat>
 #include <cstdlib>
 
@@ -803,6 +804,48 @@ fast_kernel(const FastArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Query groups, computed once per query-order rebuild (every few sweeps) rather
+// than by the fused passes of every sweep: each 32-position unit of the curve-
+// ordered list is cut where the curve jumps (farther than sqrt(jump2) between
+// consecutive queries: the curve leaving a rank's slab or a cluster), and every
+// piece is bisected recursively along its longest axis (bisect_unit).  The list
+// is permuted into that order and the code of every position becomes the first
+// position of its group, so the fused kernels' curve-run grouping
+// (group_breaks / group_end with block_shift = 0) reproduces the bisected groups.
+// ---------------------------------------------------------------------------
+template <int Q>
+__global__ void __launch_bounds__(128)
+group_order_kernel(const uint32_t* __restrict__ qin, const float4* __restrict__ Xq, uint32_t nq,
+                   float jump2, uint32_t* __restrict__ qout, uint32_t* __restrict__ codes,
+                   const uint32_t* done) {
+    if (done && *done) return;
+    const int lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t u = warp; (uint64_t)u * 32 < nq; u += nw) {
+        const uint32_t r0 = u * 32, r1 = min(nq, r0 + 32);
+        for (uint32_t s0 = r0, s1; s0 < r1; s0 = s1) {
+            const uint32_t pos = s0 + (uint32_t)lane;
+            float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (pos < r1) p = __ldg(&Xq[__ldg(&qin[pos])]);
+            const float px = __shfl_up_sync(0xffffffffu, p.x, 1);
+            const float py = __shfl_up_sync(0xffffffffu, p.y, 1);
+            const float pz = __shfl_up_sync(0xffffffffu, p.z, 1);
+            const float dx = p.x - px, dy = p.y - py, dz = p.z - pz;
+            const bool jump = lane > 0 && pos < r1 && fmaf(dz, dz, fmaf(dy, dy, dx * dx)) > jump2;
+            const unsigned m = __ballot_sync(0xffffffffu, jump);
+            s1 = m ? s0 + (uint32_t)(__ffs(m) - 1) : r1;
+            const uint32_t n = s1 - s0;
+            const uint32_t slot = bisect_unit<Q>(qin, Xq, s0, n, lane);
+            if ((uint32_t)lane < n) {
+                qout[s0 + lane] = __ldg(&qin[s0 + slot]);
+                codes[s0 + lane] = s0 + ((uint32_t)lane / Q) * Q;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // WLOP density pass: dens_i = 1 + sum_{i' != i, d <= s} theta(d)  (fp32,
 // exact neighbour set via the same fp64 re-decision of guard-band pairs).
 // ---------------------------------------------------------------------------
@@ -919,6 +962,14 @@ uint32_t work_unit_queries(uint32_t nq, int total_warps) {
         return (uint32_t)(v >= 1 && v <= 32 ? v : 16);
     }();
     return u;
+}
+
+void launch_group_order(const uint32_t* qin, const float4* Xq, uint32_t nq, float jump2,
+                        uint32_t* qout, uint32_t* codes, const uint32_t* done, cudaStream_t s) {
+    if (!nq) return;
+    const uint32_t units = (nq + 31) / 32;
+    const int blocks = (int)std::min<uint32_t>((units + 3) / 4, 148u * 16u);
+    group_order_kernel<8><<<blocks, 128, 0, s>>>(qin, Xq, nq, jump2, qout, codes, done);
 }
 
 void launch_density(const DensityArgs& a, int grid_blocks, cudaStream_t s) {

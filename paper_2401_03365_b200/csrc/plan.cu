@@ -262,6 +262,8 @@ Plan::Plan(const pcs_lop_desc& d) : d_(d) {
     if (const char* e = dev_knob("PCSB_ASYNC_ORDER")) async_order_ = std::atoi(e) != 0;  // developer knob
     if (const char* e = dev_knob("PCSB_FUSED")) fused_ = std::atoi(e) != 0;  // developer knob
     if (const char* e = dev_knob("PCSB_BISECT")) bisect_ = std::atoi(e) != 0;  // developer knob
+    group_order_ = fp32_ && bisect_;
+    if (const char* e = dev_knob("PCSB_GROUP_ORDER")) group_order_ = fp32_ && std::atoi(e) != 0;  // developer knob
     if (const char* e = dev_knob("PCSB_REP_LANES")) rep_lanes_ = std::atoi(e);  // developer knob
     device_ = select_device(d_.device);
     PCSB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
@@ -964,7 +966,7 @@ void Plan::density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur) {
         da.Cstart = X_start_;
         da.qlist = qlist;
         da.qcodes = q_skeys_;
-        da.block_shift = block_shift_;
+        da.block_shift = group_order_ ? 0 : block_shift_;
         da.nq = nq;
         da.unit = work_unit_queries(nq, density_grid_ * 4);
         da.g = gX_;
@@ -1052,6 +1054,7 @@ void Plan::enqueue_sweep(int k) {
             launches_ += build_query_list((const V*)cur + own_lo_, own_cnt_, g_, support_, nullptr, 0,
                                           0, q_keys_, q_skeys_, q_list_, &block_shift_, rs_, done,
                                           stream_, own_lo_);
+            group_order(cur, q_list_, q_skeys_, q_keys_, done, stream_);
         }
         sweeps_since_order_ = 0;
         q_stale_ = false;
@@ -1069,6 +1072,7 @@ void Plan::enqueue_sweep(int k) {
         launches_ += build_query_list((const V*)cur + own_lo_, own_cnt_, g_, support_, nullptr, 0, 0,
                                       q_keys_alt_, q_skeys_alt_, q_list_alt_, &block_shift_alt_, rs2_,
                                       nullptr, stream2_, own_lo_);
+        group_order(cur, q_list_alt_, q_skeys_alt_, q_keys_alt_, nullptr, stream2_);
         PCSB_CUDA(cudaEventRecord(ev_qready_, stream2_));
         q_next_ready_ = true;
     }
@@ -1099,8 +1103,12 @@ void Plan::enqueue_sweep(int k) {
         // consecutive positions of the whole domain's curve can lie far apart, and
         // a 32-query unit spanning two such pieces bisects into straddling groups
         // (emulated 8-rank sweep: slowest rank 1.03 ms bisected vs 0.72 ms cut).
-        const bool bis = bisect_ && !multi;
+        // groups: precomputed by group_order (bisected, cut at curve jumps) and
+        // read back from the codes (block_shift 0), or in-kernel bisection
+        // (PCSB_GROUP_ORDER=0 builds), or curve runs cut at blocks
+        const bool bis = bisect_ && !multi && !group_order_;
         a.bisect = bis ? 1 : 0;
+        if (group_order_) a.block_shift = 0;
         a.unit = bis && !dev_knob("PCSB_UNIT") && !d_.density_weights
                      ? 32u
                      : work_unit_queries(nq, fast_grid_ * 4);
@@ -1212,6 +1220,18 @@ void Plan::enqueue_sweep(int k) {
     // is a dependency edge, not a timestamp of the replays)
     if (capturing_) capture_events_.push_back(se);
     else pending_.push_back(se);
+}
+
+// Precomputed query groups (launch_group_order) for the fused fp32 kernels:
+// the list is permuted through `tmp` (the order build's free key buffer).
+void Plan::group_order(const void* cur, uint32_t* qlist, uint32_t* codes, uint32_t* tmp,
+                       const uint32_t* done, cudaStream_t st) {
+    if (!group_order_ || !own_cnt_) return;
+    launch_group_order(qlist, (const float4*)cur, own_cnt_, (float)(4.0 * support_ * support_), tmp,
+                       codes, done, st);
+    PCSB_CUDA(cudaMemcpyAsync(qlist, tmp, (size_t)own_cnt_ * sizeof(uint32_t),
+                              cudaMemcpyDeviceToDevice, st));
+    launches_ += 1;
 }
 
 void Plan::record_counts(bool on) {

@@ -87,6 +87,8 @@ private:
     template <typename T> void density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur);
     template <typename T> void grid_rebuild(const void* Xcur, cudaStream_t st);
     void allgather_x(void* X, bool fp32);
+    void group_order(const void* cur, uint32_t* qlist, uint32_t* codes, uint32_t* tmp,
+                     const uint32_t* done, cudaStream_t st);
     void free_all();
     void* dalloc(size_t bytes);
     void* talloc(size_t bytes);  // stream-ordered, from the device pool
@@ -151,6 +153,7 @@ private:
     size_t P_pairs_cap_ = 0, X_pairs_cap_ = 0;  // float4 elements of the pair records
     bool fused_ = false;              // one pass (attraction + repulsion) after the X grid
     bool bisect_ = true;              // query groups by recursive bisection of 32-query units
+    bool group_order_ = false;        // groups precomputed at each query-order rebuild (fp32)
     bool async_order_ = true;         // developer knob PCSB_ASYNC_ORDER=0: build in line
     int last_sweep_ = 0;              // last sweep index of the current run()
     cudaEvent_t ev_qready_ = nullptr;
