@@ -95,6 +95,8 @@ struct FastArgs {
     uint32_t unit;            // queries per work unit (work_unit_queries)
     uint32_t tail_start;      // list position (multiple of unit) where short units begin
     uint32_t tail_unit;       // queries per unit from tail_start (raised to one group)
+    uint32_t tail_parts;      // attraction pass: warps sharing a tail unit's candidate rows (1 = off)
+    uint32_t tail_cap;        // entries per plane of attr_x / attr_nx (positions from tail_start)
     int bisect;               // 1: groups by recursive bisection of each unit (bisect_unit)
     GridGeom gP, gX;          // grids of the data and of the projected set
     double s_pad;             // support with margin (cell ranges)
@@ -109,6 +111,8 @@ struct FastArgs {
     uint32_t* careful_list;   // deferred queries (internal indices)
     float4* attr;             // PH_ATTR -> PH_REP: per list position (sum w, sum w d)
     int2* attr_n;             //   (hits, zero-distance candidates)
+    float4* attr_x;           // parts 1.. of row-split tail units: tail_parts - 1 planes
+    int2* attr_nx;
     uint8_t* ever_isolated;   // internal index
     int4* qcounts;            // parity facility (nullptr = off), internal index: per query
                               // {attraction hits, repulsion hits, coincident, flags}

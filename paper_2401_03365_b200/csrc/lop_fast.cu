@@ -260,7 +260,7 @@ template <typename Eval>
 __device__ __forceinline__ void gather_eval(const float4* __restrict__ pairs, size_t pairs_cap,
                                             const uint32_t* __restrict__ start, const GridGeom& g,
                                             const Box& b, double s_pad, const GroupQ& G, Stage& S,
-                                            int lane, Eval&& eval) {
+                                            int lane, int rfirst, int rstride, Eval&& eval) {
     (void)pairs_cap;
     const RowSpan rs = row_span(g, b, s_pad);
     uint32_t cur = 0, fill = 0;
@@ -275,9 +275,11 @@ __device__ __forceinline__ void gather_eval(const float4* __restrict__ pairs, si
         __syncwarp();
         poison_half(S.ring + h * (2 * HR), lane);
     };
-    for (int r0 = 0; r0 < rs.nrows; r0 += 32) {
+    // rows rfirst, rfirst + rstride, ...: all of them (0, 1), or this warp's share
+    // of a tail group whose rows are dealt round robin to rstride warps
+    for (int r0 = rfirst; r0 < rs.nrows; r0 += 32 * rstride) {
         uint32_t rb, re;
-        row_range(start, g, G, rs, r0 + lane, rb, re);
+        row_range(start, g, G, rs, r0 + lane * rstride, rb, re);
         const uint32_t rec0 = rb >> 1;
         const uint32_t nrec = re > rb ? ((re + 1) >> 1) - rec0 : 0u;
         uint32_t incl = nrec;
@@ -530,18 +532,26 @@ __device__ __forceinline__ EvalConsts make_consts(const float4& q, float kneg, f
 // The next work unit for this warp: [r0, r1) positions in the query list.
 // Units of `unit` queries up to tail_start, then units of tail_unit (one query
 // group) so that the pass ends on short units (the tail of a persistent pass).
+//
+// With parts > 1 every tail unit is handed out `parts` times: part p takes the
+// candidate rows p, p + parts, ... of the unit's groups (the attraction pass
+// of a short query list ends on fractions of a group; the partial sums are
+// combined in part order by the repulsion pass).
 __device__ __forceinline__ bool next_unit(uint32_t* counter, uint32_t nq, uint32_t unit,
-                                          uint32_t tail_start, uint32_t tail_unit, int lane,
-                                          uint32_t& r0, uint32_t& r1) {
+                                          uint32_t tail_start, uint32_t tail_unit, uint32_t parts,
+                                          int lane, uint32_t& r0, uint32_t& r1, uint32_t& part) {
     uint32_t u = 0;
     if (lane == 0) u = atomicAdd(counter, 1u);
     u = __shfl_sync(0xffffffffu, u, 0);
     const uint32_t n1 = tail_start / unit;  // tail_start is a multiple of unit
     uint32_t len = unit;
+    part = 0;
     if (u < n1) {
         r0 = u * unit;
     } else {
-        r0 = tail_start + (u - n1) * tail_unit;
+        const uint32_t t = u - n1;
+        r0 = tail_start + (t / parts) * tail_unit;
+        part = t % parts;
         len = tail_unit;
     }
     if (r0 >= nq) return false;
@@ -649,9 +659,12 @@ fast_kernel(const FastArgs a) {
     const int qi = lane / L, sub = lane % L;
     uint32_t* counter = PH == PH_REP ? &a.slot->group_counter2 : &a.slot->group_counter;
 
-    uint32_t r0, r1;
+    uint32_t r0, r1, part;
     const uint32_t tail_unit = max(a.tail_unit, (uint32_t)Q);
-    while (next_unit(counter, a.nq, a.unit, a.tail_start, tail_unit, lane, r0, r1)) {
+    // only the attraction pass splits its tail units by rows (FastArgs::tail_parts)
+    const uint32_t parts = PH == PH_ATTR ? max(a.tail_parts, 1u) : 1u;
+    while (next_unit(counter, a.nq, a.unit, a.tail_start, tail_unit, parts, lane, r0, r1, part)) {
+        const int rfirst = (int)part, rstride = r0 >= a.tail_start ? (int)parts : 1;
         const bool bis = a.bisect != 0;
         const unsigned brk = bis ? 0u : group_breaks(a.qcodes, a.block_shift, r0, r1, lane);
         const uint32_t slotpos = bis ? bisect_unit<Q>(a.qlist, a.Xq, r0, r1 - r0, lane) : (uint32_t)lane;
@@ -676,7 +689,7 @@ fast_kernel(const FastArgs a) {
             Acc at = acc_zero();
             if (kAttr) {
                 gather_eval(a.Ppairs, a.Ppairs_cap, a.Pstart, a.gP, box, a.s_pad, G, S, lane,
-                            [&](const float4* half, int nrec) {
+                            rfirst, rstride, [&](const float4* half, int nrec) {
                                 eval_half<L, K_ATTR, kWlop, kCheckZero>(half, nrec, sub, q, ec,
                                                                       a.band, a.r2, at);
                                 evals += 2 * nrec;
@@ -685,15 +698,33 @@ fast_kernel(const FastArgs a) {
             }
             if (PH == PH_ATTR) {
                 if (member && sub == 0) {
-                    a.attr[qpos] = make_float4(at.s.x, at.x.x, at.y.x, at.z.x);
-                    a.attr_n[qpos] = make_int2(at.hneg, kCheckZero ? at.rneg - at.hneg : 0);
+                    // part p > 0 of a row-split tail unit: plane p - 1 of the extra sums
+                    const size_t o = part == 0 ? (size_t)qpos
+                                               : (size_t)(part - 1) * a.tail_cap + (qpos - a.tail_start);
+                    (part == 0 ? a.attr : a.attr_x)[o] = make_float4(at.s.x, at.x.x, at.y.x, at.z.x);
+                    (part == 0 ? a.attr_n : a.attr_nx)[o] =
+                        make_int2(at.hneg, kCheckZero ? at.rneg - at.hneg : 0);
                 }
                 if (lane == 0) atomicAdd(&a.st->lane_candidates, (unsigned long long)evals * Q);
                 continue;
             }
             if (PH == PH_REP && member && sub == 0) {
-                const float4 v = a.attr[qpos];
-                const int2 c = a.attr_n[qpos];
+                float4 v = a.attr[qpos];
+                int2 c = a.attr_n[qpos];
+                if (a.tail_parts > 1 && qpos >= a.tail_start) {
+                    // row-split tail units of the attraction pass: partial sums in part order
+                    for (uint32_t p = 1; p < a.tail_parts; ++p) {
+                        const size_t o = (size_t)(p - 1) * a.tail_cap + (qpos - a.tail_start);
+                        const float4 w = a.attr_x[o];
+                        const int2 d = a.attr_nx[o];
+                        v.x += w.x;
+                        v.y += w.y;
+                        v.z += w.z;
+                        v.w += w.w;
+                        c.x += d.x;
+                        c.y += d.y;
+                    }
+                }
                 at.s.x = v.x;
                 at.x.x = v.y;
                 at.y.x = v.z;
@@ -705,7 +736,7 @@ fast_kernel(const FastArgs a) {
             // ---------------- repulsion: projected-set candidates (lop.cpp:79-97) ----------------
             Acc rp = acc_zero();
             if (kRepul) {
-                gather_eval(a.Xpairs, a.Xpairs_cap, a.Xstart, a.gX, box, a.s_pad, G, S, lane,
+                gather_eval(a.Xpairs, a.Xpairs_cap, a.Xstart, a.gX, box, a.s_pad, G, S, lane, 0, 1,
                             [&](const float4* half, int nrec) {
                                 eval_half<L, KREP, kWlop, true>(half, nrec, sub, q, ec, a.band,
                                                                 a.r2, rp);
@@ -862,7 +893,8 @@ density_kernel(const DensityArgs a) {
     Stage S = make_stage(smem + warp * 4 * HR, bars + 2 * warp, lane);
     const int qi = lane / DL, sub = lane % DL;
     uint32_t r0, r1;
-    while (next_unit(a.counter, a.nq, a.unit, a.nq / a.unit * a.unit, a.unit, lane, r0, r1)) {
+    uint32_t part;
+    while (next_unit(a.counter, a.nq, a.unit, a.nq / a.unit * a.unit, a.unit, 1u, lane, r0, r1, part)) {
         const unsigned brk = group_breaks(a.qcodes, a.block_shift, r0, r1, lane);
         for (uint32_t g0 = r0, g1; g0 < r1; g0 = g1) {
             g1 = group_end(brk, r0, r1, g0, Q);
@@ -877,7 +909,7 @@ density_kernel(const DensityArgs a) {
             __syncwarp();
             const GroupQ G{qsh[warp], (int)(g1 - g0), a.scull2};
             Acc A = acc_zero();
-            gather_eval(a.Cpairs, a.Cpairs_cap, a.Cstart, a.g, box, a.s_pad, G, S, lane,
+            gather_eval(a.Cpairs, a.Cpairs_cap, a.Cstart, a.g, box, a.s_pad, G, S, lane, 0, 1,
                         [&](const float4* half, int nrec) {
                             eval_half<DL, K_DENSITY, false, true>(half, nrec, sub, q, ec, a.band,
                                                                  a.r2, A);

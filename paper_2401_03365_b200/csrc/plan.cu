@@ -654,6 +654,13 @@ void Plan::upload_t(const double* P, uint64_t n, const double* X0, uint64_t m) {
     careful_list_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
     attr_ = (float4*)dalloc(mp * sizeof(float4));
     attr_n_ = (int2*)dalloc(mp * sizeof(int2));
+    attr_x_ = nullptr;
+    attr_nx_ = nullptr;
+    if (fp32_) {  // partial attraction sums of row-split tail units (enqueue_sweep)
+        tail_cap_ = (uint32_t)std::min<uint64_t>(mp, (uint64_t)4 * fast_grid_ * 4u * 16u + 64u);
+        attr_x_ = (float4*)dalloc((size_t)kTailPlanes * tail_cap_ * sizeof(float4));
+        attr_nx_ = (int2*)dalloc((size_t)kTailPlanes * tail_cap_ * sizeof(int2));
+    }
     q_keys_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
     q_skeys_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
     q_list_ = (uint32_t*)dalloc(mp * sizeof(uint32_t));
@@ -1118,9 +1125,30 @@ void Plan::enqueue_sweep(int k) {
                 const char* e = dev_knob("PCSB_TAIL");
                 return e ? std::atof(e) : 2.0;  // ~2 groups per warp: emulated 8-rank -3%, 1 GPU neutral
             }();
-            const uint64_t tail = (uint64_t)(tail_frac * attr_grid_ * 4u * q);
+            uint64_t tail = (uint64_t)(tail_frac * attr_grid_ * 4u * q);
+            // short lists (a rank of a sharded plan, a small projected set): the
+            // pass is a few groups per warp, so the tail units' candidate rows are
+            // dealt to two warps each (partial sums combined in part order).
+            // Measured (tools/gpu_tail_parts.sh): slowest emulated rank of 8 on
+            // config 3 0.664 -> 0.621 ms (4 parts 0.612), of 4 1.098 -> 1.059 ms
+            // (10 groups per warp), config 2 -1.7%; with 14 groups per warp (config
+            // 4) it costs 0.7%, with 20 (2 ranks) nothing changes
+            static const int parts_knob = [] {  // developer knob: 1, 2 or 4
+                const char* e = dev_knob("PCSB_TAIL_PARTS");
+                return e ? std::atoi(e) : 0;
+            }();
+            const uint64_t groups_per_warp = nq / ((uint64_t)attr_grid_ * 4u * q);
+            uint32_t parts = parts_knob ? (uint32_t)parts_knob : (groups_per_warp < 12 ? 2u : 1u);
+            if (!(xgrid && !fused_) || !attr_x_ || tail_cap_ <= a.unit) parts = 1;  // split pass only
+            parts = std::min(parts, kTailPlanes + 1u);
+            if (parts > 1) tail = std::min<uint64_t>(tail, tail_cap_ - a.unit);
             a.tail_start = nq > tail ? (uint32_t)((nq - tail) / a.unit * a.unit) : 0u;
             a.tail_unit = q;
+            if (parts > 1 && nq - a.tail_start > tail_cap_) parts = 1;
+            a.tail_parts = parts;
+            a.tail_cap = tail_cap_;
+            a.attr_x = attr_x_;
+            a.attr_nx = attr_nx_;
         }
         a.gP = g_;
         a.gX = gX_;

@@ -167,6 +167,10 @@ private:
     RadixScratch rs2_{};              // stream2_'s sorts
     float4* attr_ = nullptr;          // attraction sums per query-list position (PH_ATTR -> PH_REP)
     int2* attr_n_ = nullptr;
+    static constexpr uint32_t kTailPlanes = 3;  // row-split tail units: up to 4 parts
+    float4* attr_x_ = nullptr;  // kTailPlanes planes of tail_cap_ partial sums
+    int2* attr_nx_ = nullptr;
+    uint32_t tail_cap_ = 0;
     RunState* st_ = nullptr;
     SweepSlot* slots_ = nullptr;
     int slot_cap_ = 0;
