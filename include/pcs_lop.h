@@ -299,6 +299,20 @@ pcs_status pcs_mls_project(pcs_mls_index* index, const pcs_mls_desc* d, const do
  * (may be NULL). */
 pcs_status pcs_mls_smooth(const pcs_mls_desc* d, const double* xyz, uint64_t n, double* out_xyz,
                           pcs_mls_result* results);
+/* ProjectionOutcome without the point (proj/include/pcs/mls.hpp:38-44): what
+ * smooth_cloud's SmoothingSummary::add consumes (proj/src/mls.cpp:5-16). */
+typedef struct pcs_mls_outcome {
+    int8_t status;        /* ProjectionStatus */
+    int8_t degree_used;
+    int8_t plane_status;  /* PlaneFitStatus */
+    int8_t poly_status;   /* PolyFitStatus of the last fit tried */
+    int32_t iterations;   /* plane-fit iterations */
+} pcs_mls_outcome;
+/* smooth_cloud as the reference returns it (the projected cloud and what the
+ * summary needs): 32 bytes per point cross PCIe instead of the 312-byte
+ * records of pcs_mls_smooth; the queries are the device index's own points. */
+pcs_status pcs_mls_smooth_outcomes(const pcs_mls_desc* d, const double* xyz, uint64_t n,
+                                   double* out_xyz, pcs_mls_outcome* outcomes);
 /* partition (proj/src/parallel.cpp:64-127), host only: axis, W-1 cuts, and the
  * worker of every point (counts differ by at most one). */
 pcs_status pcs_mls_partition(const double* xyz, uint64_t n, uint64_t workers, double support,

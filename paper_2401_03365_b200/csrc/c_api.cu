@@ -347,6 +347,11 @@ pcs_status pcs_mls_smooth(const pcs_mls_desc* d, const double* xyz, uint64_t n, 
     return guarded([&] { pcsb::mls_smooth(checked_mls(d), xyz, n, out_xyz, results); });
 }
 
+pcs_status pcs_mls_smooth_outcomes(const pcs_mls_desc* d, const double* xyz, uint64_t n,
+                                   double* out_xyz, pcs_mls_outcome* outcomes) {
+    return guarded([&] { pcsb::mls_smooth_outcomes(checked_mls(d), xyz, n, out_xyz, outcomes); });
+}
+
 pcs_status pcs_mls_partition(const double* xyz, uint64_t n, uint64_t workers, double support,
                              int32_t* axis, double* cuts, uint32_t* worker_of) {
     return guarded([&] { pcsb::mls_partition(xyz, n, workers, support, axis, cuts, worker_of); });

@@ -74,6 +74,12 @@ struct MlsArgs {
     pcs_mls_result* out;
     double* centers;         // optional, (max_iter + 1) * 3 per query
     uint32_t* counter;
+    // smooth_cloud (pcs_mls_smooth_outcomes): query i is the cloud's own sorted
+    // point i (spatially coherent warps), results land at the point's original
+    // index order[i] as xyz + the 8-byte outcome instead of the full record
+    const uint32_t* order;
+    double* lean_xyz;
+    pcs_mls_outcome* lean_out;
 };
 
 struct WarpSmem {
@@ -446,8 +452,17 @@ __global__ void __launch_bounds__(MLS_THREADS, 5) mls_kernel(const MlsArgs a) {
         if (lane == 0) qi = atomicAdd(a.counter, 1u);
         qi = __shfl_sync(0xffffffffu, qi, 0);
         if (qi >= a.m) break;
-        const double rx = a.q[3 * (size_t)qi], ry = a.q[3 * (size_t)qi + 1],
-                     rz = a.q[3 * (size_t)qi + 2];
+        double rx, ry, rz;
+        if (a.lean_out) {
+            const double4 self = a.pts[qi];
+            rx = self.x;
+            ry = self.y;
+            rz = self.z;
+        } else {
+            rx = a.q[3 * (size_t)qi];
+            ry = a.q[3 * (size_t)qi + 1];
+            rz = a.q[3 * (size_t)qi + 2];
+        }
         pcs_mls_result R;
         memset(&R, 0, sizeof(R));
         R.projected[0] = rx;
@@ -630,7 +645,23 @@ __global__ void __launch_bounds__(MLS_THREADS, 5) mls_kernel(const MlsArgs a) {
             R.cmin[i] = cmn[i];
             R.cmax[i] = cmx[i];
         }
-        if (lane == 0) a.out[qi] = R;
+        if (lane == 0) {
+            if (a.lean_out) {
+                const size_t oi = a.order[qi];
+                a.lean_xyz[3 * oi] = R.projected[0];
+                a.lean_xyz[3 * oi + 1] = R.projected[1];
+                a.lean_xyz[3 * oi + 2] = R.projected[2];
+                pcs_mls_outcome o;
+                o.status = (int8_t)R.status;
+                o.degree_used = (int8_t)R.degree_used;
+                o.plane_status = (int8_t)R.plane_status;
+                o.poly_status = (int8_t)R.poly_status;
+                o.iterations = R.iterations;
+                a.lean_out[oi] = o;
+            } else {
+                a.out[qi] = R;
+            }
+        }
         __syncwarp();
     }
 }
@@ -900,6 +931,53 @@ void mls_project(MlsIndex* ix, const pcs_mls_desc& d, const double* q, uint64_t 
     if (centers_out)
         PCSB_CUDA(cudaMemcpyAsync(centers_out, a.centers, ncen * sizeof(double), cudaMemcpyDeviceToHost,
                                   ix->s));
+    PCSB_CUDA(cudaStreamSynchronize(ix->s));
+    PCSB_CUDA(cudaGetLastError());
+}
+
+// smooth_cloud without the per-point records: the queries are the index's own
+// sorted points (no second upload; consecutive warps work on neighbouring
+// points), 32 bytes per point come back instead of 312.
+void mls_smooth_outcomes(const pcs_mls_desc& d, const double* xyz, uint64_t n, double* out_xyz,
+                         pcs_mls_outcome* outcomes) {
+    if (n == 0) return;
+    if (!xyz || !out_xyz || !outcomes) throw Failure(PCS_ERR_INVALID_PARAM, "null buffer");
+    // parameter checks of mls_project (same messages): a zero-query call validates only
+    mls_project(nullptr, d, nullptr, 0, PCS_MLS_PROJECT, nullptr, nullptr, nullptr);
+    std::unique_ptr<MlsIndex> ix(mls_index_create(xyz, n, d.device));
+    std::lock_guard<std::mutex> lk(ix->mu);
+    PCSB_CUDA(cudaSetDevice(ix->device));
+    const double support = d.h * d.cutoff_multiple;
+    ix->ensure_grid(support);
+    DevTmp t;
+    MlsArgs a{};
+    a.pts = ix->sorted;
+    a.start = ix->start;
+    a.n = (uint32_t)ix->n;
+    a.g = ix->g;
+    a.support = support;
+    a.r2 = support * support;
+    a.s_pad = support * (1.0 + 1e-12) + 4.0 * std::ldexp(ix->maxabs + support + 1.0, -52);
+    a.h = d.h;
+    a.m = (uint32_t)n;
+    a.mode = PCS_MLS_PROJECT;
+    a.degree = d.degree;
+    a.tol = d.plane_tol;
+    a.max_iter = d.plane_max_iter;
+    a.order = ix->order;
+    a.lean_xyz = t.get<double>(n * 3);
+    a.lean_out = t.get<pcs_mls_outcome>(n);
+    a.counter = t.get<uint32_t>(1);
+    PCSB_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(uint32_t), ix->s));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
+    const uint64_t want = (n + MLS_WARPS - 1) / MLS_WARPS;
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)sms * 8));
+    mls_kernel<<<grid, MLS_THREADS, 0, ix->s>>>(a);
+    PCSB_CUDA(cudaGetLastError());
+    PCSB_CUDA(cudaMemcpyAsync(out_xyz, a.lean_xyz, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, ix->s));
+    PCSB_CUDA(cudaMemcpyAsync(outcomes, a.lean_out, n * sizeof(pcs_mls_outcome), cudaMemcpyDeviceToHost,
+                              ix->s));
     PCSB_CUDA(cudaStreamSynchronize(ix->s));
     PCSB_CUDA(cudaGetLastError());
 }

@@ -279,8 +279,20 @@ std::pair<PointCloud, SmoothingSummary> smooth_cloud(const PointCloud& cloud,
     PointCloud out;
     SmoothingSummary summary;
     if (cloud.empty()) return {out, summary};
-    const std::vector<pcs_mls_result> res = smooth_device(cloud, params, out);
-    for (const pcs_mls_result& R : res) summary.add(outcome_of(R));
+    // the summary needs only each point's outcome (SmoothingSummary::add)
+    const pcs_mls_desc d = mls_desc(params.kernel, params.degree, params.plane_tol, params.plane_max_iter);
+    std::vector<pcs_mls_outcome> oc(cloud.size());
+    out.points.resize(cloud.size());
+    check(pcs_mls_smooth_outcomes(&d, xyz_of(cloud), cloud.size(), &out.points[0].x, oc.data()));
+    for (std::size_t i = 0; i < oc.size(); ++i) {
+        ProjectionOutcome o;
+        o.projected = out.points[i];
+        o.status = projection_status_of(oc[i].status);
+        o.degree_used = oc[i].degree_used;
+        o.iterations_used = oc[i].iterations;
+        o.plane_status = plane_status_of(oc[i].plane_status);
+        summary.add(o);
+    }
     return {out, summary};
 }
 

@@ -176,18 +176,43 @@ class MlsIndex:
         return _results(out[:m])
 
 
-def smooth_cloud(cloud, params: MlsParams, device: int = -1) -> Tuple[np.ndarray, MlsResults]:
+# pcs_mls_outcome: ProjectionOutcome without the point (proj/include/pcs/mls.hpp:38-44)
+OUTCOME_DTYPE = np.dtype([("status", "i1"), ("degree_used", "i1"), ("plane_status", "i1"),
+                          ("poly_status", "i1"), ("iterations", "i4")])
+assert OUTCOME_DTYPE.itemsize == 8
+
+
+def smooth_cloud(cloud, params: MlsParams, device: int = -1,
+                 full_records: bool = False) -> Tuple[np.ndarray, MlsResults]:
     """smooth_cloud (proj/src/mls.cpp:75-93): every point projected against the
-    untouched input cloud, one device launch; output order = input order."""
+    untouched input cloud, one device launch; output order = input order.
+
+    As the reference, the call returns the projected cloud and the per-point
+    outcome (status, degree used, plane-fit iterations and status); the frames,
+    coefficients and centre bounds of ``MlsResults`` are filled only with
+    ``full_records=True`` (312 instead of 32 bytes per point cross PCIe)."""
     params.validate()
     P = _cloud(cloud)
     n = P.shape[0]
     out = np.zeros((n, 3), dtype=np.float64)
-    res = np.zeros(max(n, 1), dtype=RESULT_DTYPE)
+    if full_records:
+        res = np.zeros(max(n, 1), dtype=RESULT_DTYPE)
+        if n:
+            d = _desc(params, device)
+            _check(L.lib().pcs_mls_smooth(C.byref(d), _ptr(P), n, _ptr(out), _rptr(res)))
+        return out, _results(res[:n])
+    oc = np.zeros(max(n, 1), dtype=OUTCOME_DTYPE)
+    oc["status"] = 3  # Skipped
     if n:
         d = _desc(params, device)
-        _check(L.lib().pcs_mls_smooth(C.byref(d), _ptr(P), n, _ptr(out), _rptr(res)))
-    return out, _results(res[:n])
+        _check(L.lib().pcs_mls_smooth_outcomes(C.byref(d), _ptr(P), n, _ptr(out),
+                                               oc.ctypes.data_as(C.c_void_p)))
+    oc = oc[:n]
+    i4 = lambda k: oc[k].astype(np.int32)  # noqa: E731
+    return out, MlsResults(projected=out, origin=None, normal=None, u=None, v=None, coeffs=None,
+                           cmin=None, cmax=None, status=i4("status"),
+                           degree_used=i4("degree_used"), iterations=i4("iterations"),
+                           plane_status=i4("plane_status"), poly_status=i4("poly_status"))
 
 
 def partition(cloud, workers: int, support: float) -> Tuple[int, np.ndarray, np.ndarray]:

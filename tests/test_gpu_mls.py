@@ -118,3 +118,19 @@ def test_sparse_clouds_degrade_like_the_oracle(pb, orc, n, h, deg):
         assert np.array_equal(out[skipped], P[skipped])
         seen += np.bincount(res.status, minlength=4)
     assert seen[1] > 0 and seen[3] > 0, seen  # degraded and skipped points occur
+
+
+@pytest.mark.parametrize("kind,n,seed,sigma,h,deg", CASES[:4])
+def test_smooth_outcomes_equal_full_records(pb, kind, n, seed, sigma, h, deg):
+    """pcs_mls_smooth_outcomes (queries = the index's own sorted points, 32 bytes
+    per point back) against pcs_mls_smooth (312-byte records): the projected
+    cloud is bit-identical and every outcome field equal; sparse clouds too."""
+    for P in (cloud(pb, kind, n, seed, sigma),
+              np.random.default_rng(seed).uniform(-1.0, 1.0, (300, 3))):
+        prm = pb.MlsParams(kernel=pb.KernelParams(h), degree=deg)
+        lean, ro = pb.smooth_cloud(P, prm)
+        full, rf = pb.smooth_cloud(P, prm, full_records=True)
+        assert np.array_equal(lean, full)
+        assert np.array_equal(lean, ro.projected) and ro.coeffs is None
+        for k in ("status", "degree_used", "iterations", "plane_status", "poly_status"):
+            assert np.array_equal(getattr(ro, k), getattr(rf, k)), k
