@@ -90,12 +90,12 @@ struct WarpSmem {
     int perm[KS];
 };
 
-__device__ __forceinline__ double wsum(double v) {
+__device__ __noinline__ double wsum(double v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
-__device__ __forceinline__ int wsumi(int v) {
+__device__ __noinline__ int wsumi(int v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
@@ -162,7 +162,7 @@ __device__ __forceinline__ void for_candidates(const MlsArgs& a, double cx, doub
 // Cyclic Jacobi eigen-decomposition of the symmetric K x K matrix in S.A
 // (destroyed; its diagonal ends as the eigenvalues); eigenvectors -> S.V
 // columns; sorted ascending into S.ev with S.V permuted accordingly.
-__device__ void jacobi_eigen(WarpSmem& S, int K, int lane) {
+__device__ __noinline__ void jacobi_eigen(WarpSmem& S, int K, int lane) {
     for (int i = lane; i < K * KS; i += 32) {
         const int r = i / KS, c = i % KS;
         if (c < K) S.V[i] = r == c ? 1.0 : 0.0;
@@ -300,7 +300,7 @@ __device__ __forceinline__ bool frame_hit(const MlsArgs& a, const Frame& F, uint
 // ITS hits into registers (entries fully unrolled), then one fixed xor-tree
 // reduction per entry — no per-hit broadcast.  Returns the hit count.
 template <int D>
-__device__ int accum_lane(const MlsArgs& a, WarpSmem& S, const Frame& F, int lane) {
+__device__ __noinline__ int accum_lane(const MlsArgs& a, WarpSmem& S, const Frame& F, int lane) {
     constexpr int K = (D + 1) * (D + 2) / 2;
     constexpr int NE = K * (K + 1) / 2 + K;
     double acc[NE];
@@ -348,7 +348,7 @@ __device__ int accum_lane(const MlsArgs& a, WarpSmem& S, const Frame& F, int lan
 
 // Normal system of degree 3 or 4 (K = 10, 15: up to 135 entries): each hit is
 // broadcast to the warp and every lane accumulates the entries it owns.
-__device__ int accum_bcast(const MlsArgs& a, WarpSmem& S, const Frame& F, int degree, int lane) {
+__device__ __noinline__ int accum_bcast(const MlsArgs& a, WarpSmem& S, const Frame& F, int degree, int lane) {
     const int K = (degree + 1) * (degree + 2) / 2;
     const int NE = K * (K + 1) / 2 + K;  // packed upper triangle of M, then b
     // the entries this lane owns (e = lane + 32 t), as (row, col); col = -1: b[row]
@@ -405,7 +405,7 @@ __device__ int accum_bcast(const MlsArgs& a, WarpSmem& S, const Frame& F, int de
 
 // fit_local_polynomial (wls.cpp:149-222) of `degree` over frame F; coefficients
 // in S.x on success.
-__device__ int poly_fit(const MlsArgs& a, WarpSmem& S, const Frame& F, int degree, int lane) {
+__device__ __noinline__ int poly_fit(const MlsArgs& a, WarpSmem& S, const Frame& F, int degree, int lane) {
     const int K = (degree + 1) * (degree + 2) / 2;
     const int cnt = degree == 1 ? accum_lane<1>(a, S, F, lane)
                   : degree == 2 ? accum_lane<2>(a, S, F, lane)
@@ -443,7 +443,10 @@ __device__ int poly_fit(const MlsArgs& a, WarpSmem& S, const Frame& F, int degre
     return YF_OK;
 }
 
-__global__ void __launch_bounds__(MLS_THREADS, 5) mls_kernel(const MlsArgs a) {
+#ifndef PCSB_MLS_MINB
+#define PCSB_MLS_MINB 8  // 64 registers: 233 -> 196 ms on the 1M-point sphere (6: 209, 5: 233)
+#endif
+__global__ void __launch_bounds__(MLS_THREADS, PCSB_MLS_MINB) mls_kernel(const MlsArgs a) {
     __shared__ WarpSmem smem[MLS_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpSmem& S = smem[warp];
@@ -491,30 +494,13 @@ __global__ void __launch_bounds__(MLS_THREADS, 5) mls_kernel(const MlsArgs a) {
             for (int iter = 1; iter <= a.max_iter; ++iter) {
                 R.iterations = iter;
                 record_center(a, qi, iter - 1, qx, qy, qz, cmn, cmx, lane);
+                // one pass over the neighbourhood: weight, first and second moments
+                // about the iterate q; the covariance about the centroid c follows as
+                // sum w (p-q)(p-q)^T - sw (c-q)(c-q)^T  (|c - q| is of the order of
+                // the neighbourhood's spread, so nothing cancels beyond a few ulps;
+                // wls.cpp:70-101 makes a centroid pass and a covariance pass)
                 int cnt = 0;
                 double sw = 0.0, sx = 0.0, sy = 0.0, sz = 0.0;
-                for_candidates(a, qx, qy, qz, lane, [&](uint32_t k) {
-                    if (k == 0xFFFFFFFFu) return;
-                    const double4 p = a.pts[k];
-                    const double d2 = exact_d2(p.x, p.y, p.z, qx, qy, qz);
-                    if (!(d2 <= a.r2)) return;
-                    const double w = theta_k(__dsqrt_rn(d2), a.support, a.h);
-                    ++cnt;
-                    sw += w;
-                    sx += w * p.x;
-                    sy += w * p.y;
-                    sz += w * p.z;
-                });
-                cnt = wsumi(cnt);
-                sw = wsum(sw);
-                sx = wsum(sx);
-                sy = wsum(sy);
-                sz = wsum(sz);
-                if (cnt < 3 || !(sw > 0.0)) {
-                    pstatus = PF_TOO_FEW;
-                    break;
-                }
-                const double cx = sx / sw, cy = sy / sw, cz = sz / sw;
                 double c00 = 0.0, c01 = 0.0, c02 = 0.0, c11 = 0.0, c12 = 0.0, c22 = 0.0;
                 for_candidates(a, qx, qy, qz, lane, [&](uint32_t k) {
                     if (k == 0xFFFFFFFFu) return;
@@ -522,20 +508,34 @@ __global__ void __launch_bounds__(MLS_THREADS, 5) mls_kernel(const MlsArgs a) {
                     const double d2 = exact_d2(p.x, p.y, p.z, qx, qy, qz);
                     if (!(d2 <= a.r2)) return;
                     const double w = theta_k(__dsqrt_rn(d2), a.support, a.h);
-                    const double dx = p.x - cx, dy = p.y - cy, dz = p.z - cz;
-                    c00 += w * dx * dx;
-                    c01 += w * dx * dy;
-                    c02 += w * dx * dz;
-                    c11 += w * dy * dy;
-                    c12 += w * dy * dz;
-                    c22 += w * dz * dz;
+                    const double dx = p.x - qx, dy = p.y - qy, dz = p.z - qz;
+                    const double wx = w * dx, wy = w * dy, wz = w * dz;
+                    ++cnt;
+                    sw += w;
+                    sx += wx;
+                    sy += wy;
+                    sz += wz;
+                    c00 += wx * dx;
+                    c01 += wx * dy;
+                    c02 += wx * dz;
+                    c11 += wy * dy;
+                    c12 += wy * dz;
+                    c22 += wz * dz;
                 });
-                c00 = wsum(c00);
-                c01 = wsum(c01);
-                c02 = wsum(c02);
-                c11 = wsum(c11);
-                c12 = wsum(c12);
-                c22 = wsum(c22);
+                cnt = wsumi(cnt);
+                sw = wsum(sw);
+                if (cnt < 3 || !(sw > 0.0)) {
+                    pstatus = PF_TOO_FEW;
+                    break;
+                }
+                const double ox = wsum(sx) / sw, oy = wsum(sy) / sw, oz = wsum(sz) / sw;  // c - q
+                const double cx = qx + ox, cy = qy + oy, cz = qz + oz;
+                c00 = wsum(c00) - sw * ox * ox;
+                c01 = wsum(c01) - sw * ox * oy;
+                c02 = wsum(c02) - sw * ox * oz;
+                c11 = wsum(c11) - sw * oy * oy;
+                c12 = wsum(c12) - sw * oy * oz;
+                c22 = wsum(c22) - sw * oz * oz;
                 if (lane == 0) {
                     S.A[0] = c00; S.A[1] = c01; S.A[2] = c02;
                     S.A[KS] = c01; S.A[KS + 1] = c11; S.A[KS + 2] = c12;
