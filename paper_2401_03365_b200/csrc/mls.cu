@@ -238,6 +238,66 @@ __device__ __noinline__ void jacobi_eigen(WarpSmem& S, int K, int lane) {
     __syncwarp();
 }
 
+// Symmetric 3 x 3 eigenproblem of the plane fit, every lane redundantly in
+// registers (no shared memory, no warp barriers): cyclic Jacobi with the same
+// rotation and stopping rule as jacobi_eigen.  a = {a00, a01, a02, a11, a12,
+// a22}; returns the ascending eigenvalues and the eigenvector of the smallest.
+struct Eig3 {
+    double ev[3];
+    double n[3];
+};
+template <int P, int Q, int R>
+__device__ __forceinline__ void rot3(double (&A)[3][3], double (&V)[3][3]) {
+    const double apq = A[P][Q];
+    if (apq == 0.0) return;
+    const double tau = (A[Q][Q] - A[P][P]) / (2.0 * apq);
+    const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+    const double c = 1.0 / sqrt(1.0 + t * t), s = t * c;
+    A[P][P] -= t * apq;
+    A[Q][Q] += t * apq;
+    A[P][Q] = A[Q][P] = 0.0;
+    const double arp = A[R][P], arq = A[R][Q];
+    A[R][P] = A[P][R] = c * arp - s * arq;
+    A[R][Q] = A[Q][R] = s * arp + c * arq;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double vkp = V[k][P], vkq = V[k][Q];
+        V[k][P] = c * vkp - s * vkq;
+        V[k][Q] = s * vkp + c * vkq;
+    }
+}
+__device__ __noinline__ Eig3 eig3(double a00, double a01, double a02, double a11, double a12,
+                                  double a22) {
+    double A[3][3] = {{a00, a01, a02}, {a01, a11, a12}, {a02, a12, a22}};
+    double V[3][3] = {{1.0, 0.0, 0.0}, {0.0, 1.0, 0.0}, {0.0, 0.0, 1.0}};
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        const double off = 2.0 * (A[0][1] * A[0][1] + A[0][2] * A[0][2] + A[1][2] * A[1][2]);
+        const double dia = A[0][0] * A[0][0] + A[1][1] * A[1][1] + A[2][2] * A[2][2];
+        if (!(off > 1e-32 * dia)) break;
+        rot3<0, 1, 2>(A, V);
+        rot3<0, 2, 1>(A, V);
+        rot3<1, 2, 0>(A, V);
+    }
+    // ascending eigenvalues, stable (ties keep the lower index first)
+    int i0 = 0, i1 = 1, i2 = 2;
+    if (A[1][1] < A[i0][i0]) i0 = 1;
+    if (A[2][2] < A[i0][i0]) i0 = 2;
+    i1 = i0 == 0 ? 1 : 0;
+    i2 = 3 - i0 - i1;
+    if (A[i2][i2] < A[i1][i1]) {
+        const int t = i1;
+        i1 = i2;
+        i2 = t;
+    }
+    Eig3 e;
+    e.ev[0] = A[i0][i0];
+    e.ev[1] = A[i1][i1];
+    e.ev[2] = A[i2][i2];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) e.n[k] = i0 == 0 ? V[k][0] : (i0 == 1 ? V[k][1] : V[k][2]);
+    return e;
+}
+
 __device__ __forceinline__ void record_center(const MlsArgs& a, uint32_t qi, int slot, double x,
                                               double y, double z, double* cmn, double* cmx,
                                               int lane) {
@@ -536,20 +596,14 @@ __global__ void __launch_bounds__(MLS_THREADS, PCSB_MLS_MINB) mls_kernel(const M
                 c11 = wsum(c11) - sw * oy * oy;
                 c12 = wsum(c12) - sw * oy * oz;
                 c22 = wsum(c22) - sw * oz * oz;
-                if (lane == 0) {
-                    S.A[0] = c00; S.A[1] = c01; S.A[2] = c02;
-                    S.A[KS] = c01; S.A[KS + 1] = c11; S.A[KS + 2] = c12;
-                    S.A[2 * KS] = c02; S.A[2 * KS + 1] = c12; S.A[2 * KS + 2] = c22;
-                }
-                __syncwarp();
-                jacobi_eigen(S, 3, lane);
-                if (S.ev[1] - S.ev[0] <= 1e-12 * S.ev[2]) {
+                const Eig3 e3 = eig3(c00, c01, c02, c11, c12, c22);
+                if (e3.ev[1] - e3.ev[0] <= 1e-12 * e3.ev[2]) {
                     pstatus = PF_DEGENERATE;
                     break;
                 }
-                nx = S.V[0];
-                ny = S.V[KS];
-                nz = S.V[2 * KS];
+                nx = e3.n[0];
+                ny = e3.n[1];
+                nz = e3.n[2];
                 const double nn = sqrt(nx * nx + ny * ny + nz * nz);
                 nx /= nn;
                 ny /= nn;
