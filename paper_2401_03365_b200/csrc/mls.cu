@@ -278,21 +278,19 @@ __device__ __noinline__ Eig3 eig3(double a00, double a01, double a02, double a11
         rot3<0, 2, 1>(A, V);
         rot3<1, 2, 0>(A, V);
     }
-    // ascending eigenvalues, stable (ties keep the lower index first)
-    int i0 = 0, i1 = 1, i2 = 2;
-    if (A[1][1] < A[i0][i0]) i0 = 1;
-    if (A[2][2] < A[i0][i0]) i0 = 2;
-    i1 = i0 == 0 ? 1 : 0;
-    i2 = 3 - i0 - i1;
-    if (A[i2][i2] < A[i1][i1]) {
-        const int t = i1;
-        i1 = i2;
-        i2 = t;
-    }
+    // ascending eigenvalues, stable (ties keep the lower index first); selects, not
+    // indexed reads, so that A and V stay in registers
+    const double d0 = A[0][0], d1 = A[1][1], d2 = A[2][2];
+    int i0 = 0;
+    if (d1 < d0) i0 = 1;
+    if (d2 < (i0 == 0 ? d0 : d1)) i0 = 2;
+    const double lo = i0 == 0 ? d0 : (i0 == 1 ? d1 : d2);
+    const double ra = i0 == 0 ? d1 : d0;  // the other two, lower index first
+    const double rb = i0 == 2 ? d1 : d2;
     Eig3 e;
-    e.ev[0] = A[i0][i0];
-    e.ev[1] = A[i1][i1];
-    e.ev[2] = A[i2][i2];
+    e.ev[0] = lo;
+    e.ev[1] = rb < ra ? rb : ra;
+    e.ev[2] = rb < ra ? ra : rb;
 #pragma unroll
     for (int k = 0; k < 3; ++k) e.n[k] = i0 == 0 ? V[k][0] : (i0 == 1 ? V[k][1] : V[k][2]);
     return e;
