@@ -80,6 +80,13 @@ struct MlsArgs {
     const uint32_t* order;
     double* lean_xyz;
     pcs_mls_outcome* lean_out;
+    struct MlsMid* mid;      // plane-fit results between the two launches of the lean path
+};
+
+// What the polynomial launch of the lean path needs from the plane launch.
+struct MlsMid {
+    double o[3], n[3], u[3], v[3];
+    int32_t iterations, plane_status, have_frame, pad;
 };
 
 struct WarpSmem {
@@ -504,6 +511,11 @@ __device__ __noinline__ int poly_fit(const MlsArgs& a, WarpSmem& S, const Frame&
 #ifndef PCSB_MLS_MINB
 #define PCSB_MLS_MINB 8  // 64 registers: 233 -> 196 ms on the 1M-point sphere (6: 209, 5: 233)
 #endif
+// PH = 0: the whole projection in one launch.  The lean smooth_cloud path runs it
+// as two launches — PH = 1: the plane fit (results to a.mid), PH = 2: the degree
+// ladder over the stored frames — so that each launch's warps walk a code body
+// half the size (the kernel's dominant stall is instruction fetch).
+template <int PH>
 __global__ void __launch_bounds__(MLS_THREADS, PCSB_MLS_MINB) mls_kernel(const MlsArgs a) {
     __shared__ WarpSmem smem[MLS_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -534,7 +546,18 @@ __global__ void __launch_bounds__(MLS_THREADS, PCSB_MLS_MINB) mls_kernel(const M
         Frame F;
         bool have_frame = false;
 
-        if (a.mode == PCS_MLS_POLY) {
+        if (PH == 2) {
+            const MlsMid& M = a.mid[qi];
+            for (int i = 0; i < 3; ++i) {
+                F.o[i] = M.o[i];
+                F.n[i] = M.n[i];
+                F.u[i] = M.u[i];
+                F.v[i] = M.v[i];
+            }
+            R.iterations = M.iterations;
+            R.plane_status = M.plane_status;
+            have_frame = M.have_frame != 0;
+        } else if (a.mode == PCS_MLS_POLY) {
             const double* fr = a.frames + 12 * (size_t)qi;
             for (int i = 0; i < 3; ++i) {
                 F.o[i] = fr[i];
@@ -651,6 +674,24 @@ __global__ void __launch_bounds__(MLS_THREADS, PCSB_MLS_MINB) mls_kernel(const M
                 R.plane_status = converged ? PF_OK : PF_NO_CONV;
                 have_frame = true;
             }
+        }
+        if (PH == 1) {
+            if (lane == 0) {
+                MlsMid M;
+                for (int i = 0; i < 3; ++i) {
+                    M.o[i] = have_frame ? F.o[i] : 0.0;
+                    M.n[i] = have_frame ? F.n[i] : 0.0;
+                    M.u[i] = have_frame ? F.u[i] : 0.0;
+                    M.v[i] = have_frame ? F.v[i] : 0.0;
+                }
+                M.iterations = R.iterations;
+                M.plane_status = R.plane_status;
+                M.have_frame = have_frame ? 1 : 0;
+                M.pad = 0;
+                a.mid[qi] = M;
+            }
+            __syncwarp();
+            continue;
         }
         if (have_frame) {
             for (int i = 0; i < 3; ++i) {
@@ -771,21 +812,24 @@ struct MlsIndex {
 
     void* galloc(size_t b) {
         void* p = nullptr;
-        PCSB_CUDA(cudaMalloc(&p, b ? b : 16));
+        p = pool_alloc(device, b, s);
         allocs.push_back(p);
         return p;
     }
     void free_grid() {
-        for (void* p : allocs) cudaFree(p);
+        for (void* p : allocs) pool_free(p, s);
         allocs.clear();
         grid_support = -1.0;
     }
     ~MlsIndex() {
         if (s) cudaStreamSynchronize(s);
         free_grid();
-        if (xyz) cudaFree(xyz);
-        if (pts) cudaFree(pts);
-        if (s) cudaStreamDestroy(s);
+        pool_free(xyz, s);
+        pool_free(pts, s);
+        if (s) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
     }
     // the grid for radius `support` (built on first use, then cached)
     void ensure_grid(double support) {
@@ -822,18 +866,18 @@ MlsIndex* mls_index_create(const double* xyz, uint64_t n, int device) {
     ix->n = n;
     PCSB_CUDA(cudaStreamCreateWithFlags(&ix->s, cudaStreamNonBlocking));
     if (n) {
-        PCSB_CUDA(cudaMalloc(&ix->xyz, n * 3 * sizeof(double)));
-        PCSB_CUDA(cudaMalloc(&ix->pts, n * sizeof(double4)));
+        ix->xyz = (double*)pool_alloc(ix->device, n * 3 * sizeof(double), ix->s);
+        ix->pts = (double4*)pool_alloc(ix->device, n * sizeof(double4), ix->s);
         h2d_staged(ix->xyz, xyz, n * 3 * sizeof(double), ix->s);
         launch_convert_xyz<double>(ix->xyz, ix->pts, n, 1.0, ix->s);
-        unsigned long long* slots = nullptr;
-        PCSB_CUDA(cudaMalloc(&slots, 8 * sizeof(unsigned long long)));
+        unsigned long long* slots =
+            (unsigned long long*)pool_alloc(ix->device, 8 * sizeof(unsigned long long), ix->s);
         init_bbox_slots(slots, ix->s);
         launch_bbox<double>(ix->pts, n, slots, ix->s);
         unsigned long long hb[6];
         PCSB_CUDA(cudaMemcpyAsync(hb, slots, sizeof(hb), cudaMemcpyDeviceToHost, ix->s));
         PCSB_CUDA(cudaStreamSynchronize(ix->s));
-        cudaFree(slots);
+        pool_free(slots, ix->s);
         for (int a = 0; a < 3; ++a) {
             ix->lo[a] = ordered_to_double(hb[a]);
             ix->hi[a] = ordered_to_double(hb[3 + a]);
@@ -848,15 +892,17 @@ MlsIndex* mls_index_create(const double* xyz, uint64_t n, int device) {
 void mls_index_destroy(MlsIndex* ix) { delete ix; }
 
 namespace {
-struct DevTmp {
+struct DevTmp {  // stream-ordered temporaries of one call (library pool)
+    int dev;
+    cudaStream_t s;
     std::vector<void*> p;
+    DevTmp(int dev_, cudaStream_t s_) : dev(dev_), s(s_) {}
     ~DevTmp() {
-        for (void* x : p) cudaFree(x);
+        for (void* x : p) pool_free(x, s);
     }
     template <typename X>
     X* get(size_t count) {
-        void* x = nullptr;
-        PCSB_CUDA(cudaMalloc(&x, std::max<size_t>(count * sizeof(X), 16)));
+        void* x = pool_alloc(dev, std::max<size_t>(count * sizeof(X), 16), s);
         p.push_back(x);
         return (X*)x;
     }
@@ -876,7 +922,7 @@ void mls_index_radius(MlsIndex* ix, const double* centers, uint64_t m, double r,
     }
     if (m > 0xFFFFFFFEull) throw Failure(PCS_ERR_INVALID_PARAM, "radius_query: too many centres");
     ix->ensure_grid(r);
-    DevTmp t;
+    DevTmp t(ix->device, ix->s);
     double* dQ = t.get<double>(m * 3);
     PCSB_CUDA(cudaMemcpyAsync(dQ, centers, m * 3 * sizeof(double), cudaMemcpyHostToDevice, ix->s));
     uint64_t* cnt = t.get<uint64_t>(m + 1);
@@ -945,7 +991,7 @@ void mls_project(MlsIndex* ix, const pcs_mls_desc& d, const double* q, uint64_t 
         return;
     }
     ix->ensure_grid(support);
-    DevTmp t;
+    DevTmp t(ix->device, ix->s);
     MlsArgs a{};
     a.pts = ix->sorted;
     a.start = ix->start;
@@ -977,7 +1023,7 @@ void mls_project(MlsIndex* ix, const pcs_mls_desc& d, const double* q, uint64_t 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
     const uint64_t want = (m + MLS_WARPS - 1) / MLS_WARPS;
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)sms * 8));
-    mls_kernel<<<grid, MLS_THREADS, 0, ix->s>>>(a);
+    mls_kernel<0><<<grid, MLS_THREADS, 0, ix->s>>>(a);
     PCSB_CUDA(cudaGetLastError());
     PCSB_CUDA(cudaMemcpyAsync(out, a.out, m * sizeof(pcs_mls_result), cudaMemcpyDeviceToHost, ix->s));
     if (centers_out)
@@ -1001,7 +1047,7 @@ void mls_smooth_outcomes(const pcs_mls_desc& d, const double* xyz, uint64_t n, d
     PCSB_CUDA(cudaSetDevice(ix->device));
     const double support = d.h * d.cutoff_multiple;
     ix->ensure_grid(support);
-    DevTmp t;
+    DevTmp t(ix->device, ix->s);
     MlsArgs a{};
     a.pts = ix->sorted;
     a.start = ix->start;
@@ -1025,7 +1071,10 @@ void mls_smooth_outcomes(const pcs_mls_desc& d, const double* xyz, uint64_t n, d
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
     const uint64_t want = (n + MLS_WARPS - 1) / MLS_WARPS;
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)sms * 8));
-    mls_kernel<<<grid, MLS_THREADS, 0, ix->s>>>(a);
+    a.mid = t.get<MlsMid>(n);
+    mls_kernel<1><<<grid, MLS_THREADS, 0, ix->s>>>(a);
+    PCSB_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(uint32_t), ix->s));
+    mls_kernel<2><<<grid, MLS_THREADS, 0, ix->s>>>(a);
     PCSB_CUDA(cudaGetLastError());
     PCSB_CUDA(cudaMemcpyAsync(out_xyz, a.lean_xyz, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, ix->s));
     PCSB_CUDA(cudaMemcpyAsync(outcomes, a.lean_out, n * sizeof(pcs_mls_outcome), cudaMemcpyDeviceToHost,

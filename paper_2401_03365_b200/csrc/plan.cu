@@ -347,6 +347,19 @@ cudaMemPool_t device_pool(int dev) {
 }
 }  // namespace
 
+// Stream-ordered allocations from the library's pool for the other operators
+// (MLS index and temporaries): sub-allocations after the first call in a
+// process, freed without a device synchronisation.
+void* pool_alloc(int dev, size_t bytes, cudaStream_t s) {
+    void* p = nullptr;
+    PCSB_CUDA(cudaMallocFromPoolAsync(&p, bytes ? bytes : 16, device_pool(dev), s));
+    return p;
+}
+
+void pool_free(void* p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
 void trim_device_pool(int dev) {
     PCSB_CUDA(cudaSetDevice(dev));
     PCSB_CUDA(cudaDeviceSynchronize());

@@ -34,6 +34,8 @@ void cuda_check(cudaError_t e, const char* what);
 GridGeom make_grid(const double lo[3], const double hi[3], double support, uint64_t npts);
 // releases the reserved memory of the library's stream-ordered pool on `dev`
 void trim_device_pool(int dev);
+void* pool_alloc(int dev, size_t bytes, cudaStream_t s);
+void pool_free(void* p, cudaStream_t s);
 GridGeom make_grid_scaled(const double lo[3], const double hi[3], double support, double scale,
                           const GridGeom& base);
 double x_cell_scale(uint64_t n, uint64_t m, const GridGeom& g);

@@ -7,6 +7,6 @@ for v in ${VARIANTS:-default}; do
   for deg in ${DEGS:-1 2}; do
     PCS_LOP_LIB=$lib timeout 600 /usr/local/cuda/bin/ncu --metrics gpu__time_duration.sum --clock-control none -k mls_kernel --csv \
       --log-file gpurun_out/mlsk.csv python tools/mls_probe.py ${MLS_N:-1000000} ${MLS_H:-0.01} $deg > gpurun_out/mlsk.log 2>&1
-    echo "$v degree $deg: $(grep mls_kernel gpurun_out/mlsk.csv | awk -F'","' '{print $NF}' | tr -d '"' | tail -1) ns; $(grep -o 'max |dev - oracle| [0-9.e+-]*' gpurun_out/mlsk.log)"
+    echo "$v degree $deg: $(grep mls_kernel gpurun_out/mlsk.csv | awk -F'","' '{print $NF}' | tr -d '"' | tr '\n' ' ') ns; $(grep -o 'max |dev - oracle| [0-9.e+-]*' gpurun_out/mlsk.log)"
   done
 done

