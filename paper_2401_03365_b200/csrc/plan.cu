@@ -746,6 +746,7 @@ void Plan::reset() {
     if (qever_) PCSB_CUDA(cudaMemsetAsync(qever_, 0, std::max<uint32_t>(mpad_, 1), stream_));
     PCSB_CUDA(cudaStreamSynchronize(stream_));
     sweeps_issued_ = 0;
+    gather_pending_ = false;
     q_stale_ = true;
     // the query-order buffers back in their upload-time roles (the order is
     // rebuilt by sweep 1 anyway): every run then meets a captured CUDA graph in
@@ -966,8 +967,8 @@ void Plan::grid_rebuild(const void* Xcur, cudaStream_t st) {
     }
 }
 
-void Plan::allgather_x(void* X, bool f32) {
-    coll_->allgather(X, (size_t)chunk_ * 4, f32 ? CDType::F32 : CDType::F64, stream_);
+void Plan::allgather_x(void* X, bool f32, cudaStream_t st) {
+    coll_->allgather(X, (size_t)chunk_ * 4, f32 ? CDType::F32 : CDType::F64, st ? st : stream_);
 }
 
 // WLOP w_i of the owned queries on X^k (internal indices in qlist), written to
@@ -1053,6 +1054,13 @@ void Plan::enqueue_sweep(int k) {
         PCSB_CUDA(cudaEventRecord(ev_xready_, stream_));
         PCSB_CUDA(cudaStreamWaitEvent(stream2_, ev_xready_, 0));
         PCSB_CUDA(cudaEventRecord(se.e[1], stream2_));
+        if (multi && gather_pending_) {
+            // the previous sweep's exchange, deferred to here: the other ranks'
+            // positions are needed by the grid rebuild only, so the all-gather
+            // runs beside the attraction pass (which reads the owned slots)
+            allgather_x(cur, fp32_, stream2_);
+            gather_pending_ = false;
+        }
         grid_rebuild<T>(cur, stream2_);
         PCSB_CUDA(cudaEventRecord(se.e[2], stream2_));
     } else {
@@ -1249,8 +1257,12 @@ void Plan::enqueue_sweep(int k) {
     }
     // (4) exchange + aggregation (lop.cpp:102-119)
     if (multi) {
+        // the all-gather of X^{k+1} moves to the side stream of the next sweep
+        // (above) unless this is the run's last sweep or no grid is rebuilt
+        const bool defer = xgrid && k < last_sweep_ && !capturing_;
         coll_->group_start();
-        allgather_x(nxt, fp32_);
+        if (defer) gather_pending_ = true;
+        else allgather_x(nxt, fp32_);
         coll_->allreduce(&slot->max_disp_bits, 1, CDType::U64, COp::Max, stream_);
         coll_->group_end();
     }

@@ -88,7 +88,8 @@ private:
     void drop_graph();
     template <typename T> void density_pass_x(const uint32_t* qlist, uint32_t nq, void* Xcur);
     template <typename T> void grid_rebuild(const void* Xcur, cudaStream_t st);
-    void allgather_x(void* X, bool fp32);
+    void allgather_x(void* X, bool fp32, cudaStream_t st = nullptr);
+    bool gather_pending_ = false;  // sharded: X^k's all-gather runs at the start of sweep k
     void group_order(const void* cur, uint32_t* qlist, uint32_t* codes, uint32_t* tmp,
                      const uint32_t* done, cudaStream_t st);
     void free_all();
