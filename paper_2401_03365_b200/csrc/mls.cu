@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(MLS_THREADS, PCSB_MLS_MINB) mls_kernel(const M
         qi = __shfl_sync(0xffffffffu, qi, 0);
         if (qi >= a.m) break;
         double rx, ry, rz;
-        if (a.lean_out) {
+        if (PH != 0) {  // the lean path's launches: the cloud's own sorted points
             const double4 self = a.pts[qi];
             rx = self.x;
             ry = self.y;
@@ -694,13 +694,15 @@ __global__ void __launch_bounds__(MLS_THREADS, PCSB_MLS_MINB) mls_kernel(const M
             continue;
         }
         if (have_frame) {
-            for (int i = 0; i < 3; ++i) {
-                R.origin[i] = F.o[i];
-                R.normal[i] = F.n[i];
-                R.u[i] = F.u[i];
-                R.v[i] = F.v[i];
+            if (PH != 2) {
+                for (int i = 0; i < 3; ++i) {
+                    R.origin[i] = F.o[i];
+                    R.normal[i] = F.n[i];
+                    R.u[i] = F.u[i];
+                    R.v[i] = F.v[i];
+                }
             }
-            if (a.mode == PCS_MLS_POLY) {
+            if (PH != 2 && a.mode == PCS_MLS_POLY) {
                 record_center(a, qi, 0, F.o[0], F.o[1], F.o[2], cmn, cmx, lane);
                 const int st = poly_fit(a, S, F, a.degree, lane);
                 R.poly_status = st;
@@ -709,7 +711,7 @@ __global__ void __launch_bounds__(MLS_THREADS, PCSB_MLS_MINB) mls_kernel(const M
                     const int K = (a.degree + 1) * (a.degree + 2) / 2;
                     for (int k = 0; k < K; ++k) R.coeffs[k] = S.x[k];
                 }
-            } else if (a.mode == PCS_MLS_PROJECT) {
+            } else if (PH == 2 || a.mode == PCS_MLS_PROJECT) {
                 // ---------------- degree ladder (mls.cpp:48-68) ----------------
                 record_center(a, qi, R.iterations, F.o[0], F.o[1], F.o[2], cmn, cmx, lane);
                 R.projected[0] = F.o[0];
@@ -720,8 +722,10 @@ __global__ void __launch_bounds__(MLS_THREADS, PCSB_MLS_MINB) mls_kernel(const M
                     const int st = poly_fit(a, S, F, deg, lane);
                     R.poly_status = st;
                     if (st == YF_OK) {
-                        const int K = (deg + 1) * (deg + 2) / 2;
-                        for (int k = 0; k < K; ++k) R.coeffs[k] = S.x[k];
+                        if (PH != 2) {
+                            const int K = (deg + 1) * (deg + 2) / 2;
+                            for (int k = 0; k < K; ++k) R.coeffs[k] = S.x[k];
+                        }
                         // evaluate_polynomial(poly, 0, 0) = c0 + c1*0 + ... = c0
                         const double hgt = S.x[0];
                         R.projected[0] = __dadd_rn(F.o[0], __dmul_rn(hgt, F.n[0]));
@@ -739,7 +743,7 @@ __global__ void __launch_bounds__(MLS_THREADS, PCSB_MLS_MINB) mls_kernel(const M
             R.cmax[i] = cmx[i];
         }
         if (lane == 0) {
-            if (a.lean_out) {
+            if (PH == 2) {  // (R never leaves the registers in this launch)
                 const size_t oi = a.order[qi];
                 a.lean_xyz[3 * oi] = R.projected[0];
                 a.lean_xyz[3 * oi + 1] = R.projected[1];
