@@ -63,7 +63,7 @@ struct MlsArgs {
     const uint32_t* start;   // cell lower-bound table
     uint32_t n;              // cloud size (checked builds)
     GridGeom g;
-    double s_pad, r2, support, h;
+    double s_pad, r2, support, h, inv_h;
     const double* q;         // queries, xyz
     uint32_t m;
     int mode;                // PCS_MLS_*
@@ -108,9 +108,11 @@ __device__ __noinline__ int wsumi(int v) {
     return v;
 }
 
-__device__ __forceinline__ double theta_k(double d, double support, double h) {
+// theta(d) = exp(-(d/h)^2) inside the support (proj/src/kernels.cpp:8-14); d/h as
+// d * (1/h): one rounding apart from the reference's quotient
+__device__ __forceinline__ double theta_k(double d, double support, double inv_h) {
     if (d > support) return 0.0;
-    const double s = d / h;
+    const double s = d * inv_h;
     return exp(-s * s);
 }
 
@@ -273,10 +275,23 @@ __device__ __forceinline__ void rot3(double (&A)[3][3], double (&V)[3][3]) {
         V[k][Q] = s * vkp + c * vkq;
     }
 }
+// V: in, an orthonormal basis close to the eigenvectors (the previous plane
+// iterate's; the identity at first) — the matrix is rotated into it, so the
+// sweeps start from a nearly diagonal matrix (1-2 instead of ~5); out, the
+// eigenvectors (columns).
 __device__ __noinline__ Eig3 eig3(double a00, double a01, double a02, double a11, double a12,
-                                  double a22) {
-    double A[3][3] = {{a00, a01, a02}, {a01, a11, a12}, {a02, a12, a22}};
-    double V[3][3] = {{1.0, 0.0, 0.0}, {0.0, 1.0, 0.0}, {0.0, 0.0, 1.0}};
+                                  double a22, double (&V)[3][3]) {
+    const double S[3][3] = {{a00, a01, a02}, {a01, a11, a12}, {a02, a12, a22}};
+    double T[3][3], A[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)  // T = S V
+#pragma unroll
+        for (int j = 0; j < 3; ++j) T[i][j] = S[i][0] * V[0][j] + S[i][1] * V[1][j] + S[i][2] * V[2][j];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)  // A = V^T T, symmetrised
+#pragma unroll
+        for (int j = i; j < 3; ++j)
+            A[i][j] = A[j][i] = V[0][i] * T[0][j] + V[1][i] * T[1][j] + V[2][i] * T[2][j];
     for (int sweep = 0; sweep < 60; ++sweep) {
         const double off = 2.0 * (A[0][1] * A[0][1] + A[0][2] * A[0][2] + A[1][2] * A[1][2]);
         const double dia = A[0][0] * A[0][0] + A[1][1] * A[1][1] + A[2][2] * A[2][2];
@@ -357,7 +372,7 @@ __device__ __forceinline__ bool frame_hit(const MlsArgs& a, const Frame& F, uint
     ui = __dadd_rn(__dadd_rn(__dmul_rn(dx, F.u[0]), __dmul_rn(dy, F.u[1])), __dmul_rn(dz, F.u[2]));
     vi = __dadd_rn(__dadd_rn(__dmul_rn(dx, F.v[0]), __dmul_rn(dy, F.v[1])), __dmul_rn(dz, F.v[2]));
     fi = __dadd_rn(__dadd_rn(__dmul_rn(dx, F.n[0]), __dmul_rn(dy, F.n[1])), __dmul_rn(dz, F.n[2]));
-    w = theta_k(__dsqrt_rn(d2), a.support, a.h);
+    w = theta_k(__dsqrt_rn(d2), a.support, a.inv_h);
     return true;
 }
 
@@ -515,8 +530,12 @@ __device__ __noinline__ int poly_fit(const MlsArgs& a, WarpSmem& S, const Frame&
 // as two launches — PH = 1: the plane fit (results to a.mid), PH = 2: the degree
 // ladder over the stored frames — so that each launch's warps walk a code body
 // half the size (the kernel's dominant stall is instruction fetch).
+#ifndef PCSB_MLS_MINB_POLY
+#define PCSB_MLS_MINB_POLY 5  // polynomial launch: 5 blocks/SM 35.8 ms, 4: 37.8, 8: 37.7, 3: 43.4
+#endif
 template <int PH>
-__global__ void __launch_bounds__(MLS_THREADS, PCSB_MLS_MINB) mls_kernel(const MlsArgs a) {
+__global__ void __launch_bounds__(MLS_THREADS, PH == 1 ? PCSB_MLS_MINB : PCSB_MLS_MINB_POLY)
+mls_kernel(const MlsArgs a) {
     __shared__ WarpSmem smem[MLS_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpSmem& S = smem[warp];
@@ -572,6 +591,7 @@ __global__ void __launch_bounds__(MLS_THREADS, PCSB_MLS_MINB) mls_kernel(const M
             double nx = 0.0, ny = 0.0, nz = 0.0, t = 0.0;
             bool converged = false;
             int pstatus = PF_OK;
+            double EV[3][3] = {{1.0, 0.0, 0.0}, {0.0, 1.0, 0.0}, {0.0, 0.0, 1.0}};  // eig3's basis
             for (int iter = 1; iter <= a.max_iter; ++iter) {
                 R.iterations = iter;
                 record_center(a, qi, iter - 1, qx, qy, qz, cmn, cmx, lane);
@@ -588,7 +608,7 @@ __global__ void __launch_bounds__(MLS_THREADS, PCSB_MLS_MINB) mls_kernel(const M
                     const double4 p = a.pts[k];
                     const double d2 = exact_d2(p.x, p.y, p.z, qx, qy, qz);
                     if (!(d2 <= a.r2)) return;
-                    const double w = theta_k(__dsqrt_rn(d2), a.support, a.h);
+                    const double w = theta_k(__dsqrt_rn(d2), a.support, a.inv_h);
                     const double dx = p.x - qx, dy = p.y - qy, dz = p.z - qz;
                     const double wx = w * dx, wy = w * dy, wz = w * dz;
                     ++cnt;
@@ -617,7 +637,7 @@ __global__ void __launch_bounds__(MLS_THREADS, PCSB_MLS_MINB) mls_kernel(const M
                 c11 = wsum(c11) - sw * oy * oy;
                 c12 = wsum(c12) - sw * oy * oz;
                 c22 = wsum(c22) - sw * oz * oz;
-                const Eig3 e3 = eig3(c00, c01, c02, c11, c12, c22);
+                const Eig3 e3 = eig3(c00, c01, c02, c11, c12, c22, EV);
                 if (e3.ev[1] - e3.ev[0] <= 1e-12 * e3.ev[2]) {
                     pstatus = PF_DEGENERATE;
                     break;
@@ -1005,6 +1025,7 @@ void mls_project(MlsIndex* ix, const pcs_mls_desc& d, const double* q, uint64_t 
     a.r2 = support * support;
     a.s_pad = support * (1.0 + 1e-12) + 4.0 * std::ldexp(ix->maxabs + support + 1.0, -52);
     a.h = d.h;
+    a.inv_h = 1.0 / d.h;
     double* dq = t.get<double>(m * 3);
     PCSB_CUDA(cudaMemcpyAsync(dq, q, m * 3 * sizeof(double), cudaMemcpyHostToDevice, ix->s));
     a.q = dq;
@@ -1061,6 +1082,7 @@ void mls_smooth_outcomes(const pcs_mls_desc& d, const double* xyz, uint64_t n, d
     a.r2 = support * support;
     a.s_pad = support * (1.0 + 1e-12) + 4.0 * std::ldexp(ix->maxabs + support + 1.0, -52);
     a.h = d.h;
+    a.inv_h = 1.0 / d.h;
     a.m = (uint32_t)n;
     a.mode = PCS_MLS_PROJECT;
     a.degree = d.degree;
