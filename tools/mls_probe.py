@@ -27,7 +27,7 @@ r = O.mls_project(P, P[sub], h, degree=deg)
 tc = time.perf_counter() - t
 err = np.abs(out[sub] - r["projected"]).max()
 same = (res.status[sub] == r["status"]).mean()
-print(f"MLS n={n} h={h} degree={deg}: B200 {tg:.3f} s ({n / tg:.3e} points/s, statuses "
+print(f"MLS n={n} h={h} degree={deg} (mean plane iterations {res.iterations.mean():.2f}): B200 {tg:.3f} s ({n / tg:.3e} points/s, statuses "
       f"{np.bincount(res.status, minlength=4).tolist()}); CPU oracle on {os.cpu_count()} threads "
       f"{sub.size} points in {tc:.2f} s ({sub.size / tc:.3e} points/s); status agreement {same:.4f}, "
       f"max |dev - oracle| {err:.2e}")
