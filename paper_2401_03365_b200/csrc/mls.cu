@@ -1113,13 +1113,13 @@ void mls_smooth(const pcs_mls_desc& d, const double* xyz, uint64_t n, double* ou
                 pcs_mls_result* results) {
     if (n == 0) return;
     if (!xyz || !out_xyz) throw Failure(PCS_ERR_INVALID_PARAM, "null buffer");
-    std::unique_ptr<MlsIndex> ix(mls_index_create(xyz, n, d.device));
-    std::vector<pcs_mls_result> own;
-    pcs_mls_result* R = results;
-    if (!R) {
-        own.resize(n);
-        R = own.data();
+    if (!results) {  // only the cloud is wanted: the two-launch path (same projections)
+        std::vector<pcs_mls_outcome> oc(n);
+        mls_smooth_outcomes(d, xyz, n, out_xyz, oc.data());
+        return;
     }
+    std::unique_ptr<MlsIndex> ix(mls_index_create(xyz, n, d.device));
+    pcs_mls_result* R = results;
     mls_project(ix.get(), d, xyz, n, PCS_MLS_PROJECT, nullptr, R, nullptr);
     for (uint64_t i = 0; i < n; ++i)
         for (int a = 0; a < 3; ++a) out_xyz[3 * i + a] = R[i].projected[a];
