@@ -234,6 +234,72 @@ def self_launch(n: int) -> int:
     return 0  # not reached
 
 
+def bench_mls(args):
+    """SURVEY 8(f) row 1 on one B200: smooth_cloud (proj/src/mls.cpp:75-93) of a
+    noisy sphere (the reference's bench surface, proj/src/bench.cpp:40-87 via the
+    restated generator), h = 0.01.  value = points / device time of the two
+    launches (CUDA events inside the library); e2e = the same call's wall time
+    with host buffers (upload, index build, launches, download).  The CPU
+    baseline is the oracle port of the reference's per-point projection on a
+    20000-point sample with all host threads."""
+    import ctypes as C
+    import paper_2401_03365_b200 as pb
+    from paper_2401_03365_b200 import _lib as L
+    n, deg, h = args.mls_points, args.mls_degree, 0.01
+    P = pb.add_noise(pb.generate_surface("sphere", n, 7), 0.002, 8)
+    prm = pb.MlsParams(kernel=pb.KernelParams(h), degree=deg)
+    pb.smooth_cloud(P[:1000], prm)
+    dev_ms, walls = [], []
+    mon = ClockSampler(0)
+    for i in range(args.warmup + args.steps):
+        if i == args.warmup:
+            mon.start()
+        t = time.perf_counter()
+        out, res = pb.smooth_cloud(P, prm)
+        wall = time.perf_counter() - t
+        a, b = C.c_double(), C.c_double()
+        L.lib().pcs_mls_last_device_ms(C.byref(a), C.byref(b))
+        if i >= args.warmup:
+            dev_ms.append((a.value, b.value))
+            walls.append(wall)
+    clocks = mon.stop()
+    plane = float(np.median([d[0] for d in dev_ms]))
+    poly = float(np.median([d[1] for d in dev_ms]))
+    wall = float(np.median(walls))
+    line = {
+        "metric": "MLS projected points/sec (smooth_cloud)", "value": n / ((plane + poly) * 1e-3),
+        "unit": "points/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": plane + poly, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded host generator)",
+        "config": {"workload": f"MLS smooth_cloud: noisy unit sphere, {n} points, h = {h} "
+                               f"(support {3 * h}), degree {deg}",
+                   "l2": "the cloud (32 MB as double4) fits L2; every step re-uploads and "
+                         "re-indexes it"},
+        "device_ms": {"plane_fit_launch": plane, "polynomial_launch": poly},
+        "mean_plane_iterations": float(res.iterations.mean()),
+        "e2e": {"value": n / wall, "unit": "points/s", "wall_s": wall,
+                "h2d_bytes_per_step": int(P.nbytes), "d2h_bytes_per_step": int(out.nbytes + 8 * n),
+                "api": "pcs_mls_smooth_outcomes (C ABI) with host buffers"},
+        "gpu_launches": 2 * args.steps, "clocks": clocks,
+        "roofline": None,
+        "roofline_note": "instruction-issue bound (ncu: plane launch issue active 71%), see "
+                         "DESIGN.md 5d and profiles/r02_mls_kernel_ncu.json",
+    }
+    if not args.no_cpu:
+        from oracle import oracle as O
+        sub = np.random.default_rng(0).choice(n, min(n, 20000), replace=False)
+        t = time.perf_counter()
+        r = O.mls_project(P, P[sub], h, degree=deg)
+        tc = time.perf_counter() - t
+        line["cpu_baseline"] = {"value": sub.size / tc, "unit": "points/s", "cores": os.cpu_count(),
+                                "kind": "port",
+                                "sample": f"oracle orc_mls_project on {sub.size} seeded points of the "
+                                          f"same cloud, all host threads"}
+        line["max_abs_dev_vs_oracle"] = float(np.abs(out[sub] - r["projected"]).max())
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -244,7 +310,14 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--lanes", type=int, default=0)
+    ap.add_argument("--workload", choices=["lop", "mls"], default="lop",
+                    help="lop: the BASELINE.json metric (default); mls: SURVEY 8(f) row 1, "
+                         "smooth_cloud points/s on a synthetic sphere (one GPU)")
+    ap.add_argument("--mls-points", type=int, default=1_000_000)
+    ap.add_argument("--mls-degree", type=int, default=2)
     args = ap.parse_args()
+    if args.workload == "mls":
+        return bench_mls(args)
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "b200":
         return self_launch(args.gpus)

@@ -313,6 +313,9 @@ typedef struct pcs_mls_outcome {
  * records of pcs_mls_smooth; the queries are the device index's own points. */
 pcs_status pcs_mls_smooth_outcomes(const pcs_mls_desc* d, const double* xyz, uint64_t n,
                                    double* out_xyz, pcs_mls_outcome* outcomes);
+/* Measurement: device time (ms, CUDA events) of the plane-fit and the polynomial
+ * launch of this process's last pcs_mls_smooth_outcomes call (bench.py). */
+pcs_status pcs_mls_last_device_ms(double* plane_ms, double* poly_ms);
 /* partition (proj/src/parallel.cpp:64-127), host only: axis, W-1 cuts, and the
  * worker of every point (counts differ by at most one). */
 pcs_status pcs_mls_partition(const double* xyz, uint64_t n, uint64_t workers, double support,

@@ -352,6 +352,15 @@ pcs_status pcs_mls_smooth_outcomes(const pcs_mls_desc* d, const double* xyz, uin
     return guarded([&] { pcsb::mls_smooth_outcomes(checked_mls(d), xyz, n, out_xyz, outcomes); });
 }
 
+pcs_status pcs_mls_last_device_ms(double* plane_ms, double* poly_ms) {
+    return guarded([&] {
+        double v[2];
+        pcsb::mls_last_device_ms(v);
+        if (plane_ms) *plane_ms = v[0];
+        if (poly_ms) *poly_ms = v[1];
+    });
+}
+
 pcs_status pcs_mls_partition(const double* xyz, uint64_t n, uint64_t workers, double support,
                              int32_t* axis, double* cuts, uint32_t* worker_of) {
     return guarded([&] { pcsb::mls_partition(xyz, n, workers, support, axis, cuts, worker_of); });

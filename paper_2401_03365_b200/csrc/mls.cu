@@ -1058,6 +1058,11 @@ void mls_project(MlsIndex* ix, const pcs_mls_desc& d, const double* q, uint64_t 
     PCSB_CUDA(cudaGetLastError());
 }
 
+namespace {
+std::mutex g_last_mu;
+double g_last_ms[2] = {0.0, 0.0};  // plane / polynomial launch of the last smooth_cloud call
+}  // namespace
+
 // smooth_cloud without the per-point records: the queries are the index's own
 // sorted points (no second upload; consecutive warps work on neighbouring
 // points), 32 bytes per point come back instead of 312.
@@ -1098,15 +1103,35 @@ void mls_smooth_outcomes(const pcs_mls_desc& d, const double* xyz, uint64_t n, d
     const uint64_t want = (n + MLS_WARPS - 1) / MLS_WARPS;
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)sms * 8));
     a.mid = t.get<MlsMid>(n);
+    cudaEvent_t ev[3];
+    for (auto& e : ev) PCSB_CUDA(cudaEventCreate(&e));
+    PCSB_CUDA(cudaEventRecord(ev[0], ix->s));
     mls_kernel<1><<<grid, MLS_THREADS, 0, ix->s>>>(a);
+    PCSB_CUDA(cudaEventRecord(ev[1], ix->s));
     PCSB_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(uint32_t), ix->s));
     mls_kernel<2><<<grid, MLS_THREADS, 0, ix->s>>>(a);
+    PCSB_CUDA(cudaEventRecord(ev[2], ix->s));
     PCSB_CUDA(cudaGetLastError());
     PCSB_CUDA(cudaMemcpyAsync(out_xyz, a.lean_xyz, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, ix->s));
     PCSB_CUDA(cudaMemcpyAsync(outcomes, a.lean_out, n * sizeof(pcs_mls_outcome), cudaMemcpyDeviceToHost,
                               ix->s));
     PCSB_CUDA(cudaStreamSynchronize(ix->s));
     PCSB_CUDA(cudaGetLastError());
+    {   // device time of the two launches (pcs_mls_last_device_ms)
+        float plane = 0.f, poly = 0.f;
+        cudaEventElapsedTime(&plane, ev[0], ev[1]);
+        cudaEventElapsedTime(&poly, ev[1], ev[2]);
+        std::lock_guard<std::mutex> g(g_last_mu);
+        g_last_ms[0] = plane;
+        g_last_ms[1] = poly;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+}
+
+void mls_last_device_ms(double out[2]) {
+    std::lock_guard<std::mutex> g(g_last_mu);
+    out[0] = g_last_ms[0];
+    out[1] = g_last_ms[1];
 }
 
 void mls_smooth(const pcs_mls_desc& d, const double* xyz, uint64_t n, double* out_xyz,

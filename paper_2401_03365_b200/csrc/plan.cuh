@@ -236,6 +236,7 @@ void mls_project(MlsIndex* ix, const pcs_mls_desc& d, const double* q, uint64_t 
                  const double* frames, pcs_mls_result* out, double* centers_out);
 void mls_smooth_outcomes(const pcs_mls_desc& d, const double* xyz, uint64_t n, double* out_xyz,
                          pcs_mls_outcome* outcomes);
+void mls_last_device_ms(double out[2]);
 void mls_smooth(const pcs_mls_desc& d, const double* xyz, uint64_t n, double* out_xyz,
                 pcs_mls_result* results);
 void mls_partition(const double* xyz, uint64_t n, uint64_t workers, double support, int32_t* axis,
