@@ -300,6 +300,100 @@ def bench_mls(args):
     return 0
 
 
+def bench_rows(args):
+    """SURVEY 8(f) rows 2 and 3 on one B200, config-3 clouds, through the C ABI
+    with host buffers (value = e2e: these operators have no device-resident
+    entry point).  deviation: pcs::deviation (proj/src/metrics.cpp:39-53) of
+    1M perturbed projected points against the 10M data points; io: XYZ text of
+    the 10M-point cloud written and parsed back (proj/src/io.cpp).  The CPU
+    baseline is the reference itself (oracle/_ref) on the same inputs
+    (deviation) or on a 30% sample of the cloud (io, its IO is single-threaded)."""
+    import paper_2401_03365_b200 as pb
+    from oracle import oracle as O
+    P, X0 = pb.generate_config(3)
+    mon = ClockSampler(0)
+    if args.workload == "deviation":
+        X = X0 + np.random.default_rng(1).normal(scale=0.002, size=X0.shape)
+        pb.deviation(X[:1000], P[:10000], device=0)
+        walls = []
+        for i in range(args.warmup + args.steps):
+            if i == args.warmup:
+                mon.start()
+            t = time.perf_counter()
+            r = pb.deviation(X, P, keep_distances=True, device=0)
+            if i >= args.warmup:
+                walls.append(time.perf_counter() - t)
+        clocks = mon.stop()
+        wall = float(np.median(walls))
+        line = {"metric": "deviation queries/sec (nearest data point of every projected point)",
+                "value": X.shape[0] / wall, "unit": "queries/s", "ms_per_step": wall * 1e3,
+                "config": {"workload": f"deviation: {X.shape[0]} projected points vs {P.shape[0]} "
+                                       f"data points (config 3 clouds), fp64, bit-exact distances"},
+                "e2e": {"value": X.shape[0] / wall, "unit": "queries/s", "wall_s": wall,
+                        "h2d_bytes_per_step": int(P.nbytes + X.nbytes),
+                        "d2h_bytes_per_step": int(8 * X.shape[0]),
+                        "api": "pcs_deviation (C ABI) with host buffers"},
+                "roofline_note": "latency/divergence bound walk (DESIGN.md 5a); the call is "
+                                 "dominated by the 240 MB host-to-device copy of the data cloud"}
+        if not args.no_cpu and O.ref_available():
+            t = time.perf_counter()
+            rr, rd = O.ref_deviation(X, P)
+            tc = time.perf_counter() - t
+            line["cpu_baseline"] = {"value": X.shape[0] / tc, "unit": "queries/s",
+                                    "cores": os.cpu_count(), "kind": "reference",
+                                    "sample": "pcs::deviation (oracle/_ref) on the same inputs, "
+                                              "kd-tree build included"}
+            line["bit_exact_vs_reference"] = bool(np.array_equal(rd, r.distances))
+    else:
+        pb.format_cloud(P[:1000], device=0)
+        tw, tr = [], []
+        for i in range(args.warmup + args.steps):
+            if i == args.warmup:
+                mon.start()
+            t = time.perf_counter()
+            text = pb.format_cloud(P, "xyz", device=0)
+            t1 = time.perf_counter()
+            back = pb.parse_cloud(text, "xyz", device=0)
+            t2 = time.perf_counter()
+            if i >= args.warmup:
+                tw.append(t1 - t)
+                tr.append(t2 - t1)
+        clocks = mon.stop()
+        w, r_ = float(np.median(tw)), float(np.median(tr))
+        nbytes = len(text)
+        line = {"metric": "cloud text IO bytes/sec (XYZ write + read)",
+                "value": 2 * nbytes / (w + r_), "unit": "bytes/s", "ms_per_step": (w + r_) * 1e3,
+                "config": {"workload": f"XYZ text of the config-3 data cloud: {P.shape[0]} points, "
+                                       f"{nbytes / 1e6:.0f} MB; shortest round-trip digits, "
+                                       f"byte-identical to the reference"},
+                "write_s": w, "read_s": r_,
+                "e2e": {"value": 2 * nbytes / (w + r_), "unit": "bytes/s", "wall_s": w + r_,
+                        "h2d_bytes_per_step": int(P.nbytes + nbytes),
+                        "d2h_bytes_per_step": int(P.nbytes + nbytes),
+                        "api": "pcs_format_cloud + pcs_parse_cloud (C ABI) with host buffers"},
+                "round_trip_bit_exact": bool(np.array_equal(back.view(np.uint64), P.view(np.uint64))),
+                "roofline_note": "host-device staging of the text bound (DESIGN.md 5c): device "
+                                 "kernels are ~7 ms of the call"}
+        if not args.no_cpu and O.ref_available():
+            Ps = P[: int(0.3 * P.shape[0])]
+            t = time.perf_counter()
+            rtext = O.ref_format_cloud(Ps, 0)
+            t1 = time.perf_counter()
+            rback, err = O.ref_parse_cloud(rtext, 0)
+            t2 = time.perf_counter()
+            line["cpu_baseline"] = {"value": 2 * len(rtext) / (t2 - t), "unit": "bytes/s", "cores": 1,
+                                    "kind": "reference",
+                                    "sample": f"write_cloud_stream + read_cloud_stream (oracle/_ref) "
+                                              f"on the first {Ps.shape[0]} points"}
+            line["identical_bytes_on_sample"] = bool(text[: len(rtext)] == rtext) and err is None
+    line.update({"n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+                 "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                 "data": "synthetic (seeded host generator, BASELINE.md §4)", "clocks": clocks,
+                 "roofline": None})
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -310,14 +404,18 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--lanes", type=int, default=0)
-    ap.add_argument("--workload", choices=["lop", "mls"], default="lop",
-                    help="lop: the BASELINE.json metric (default); mls: SURVEY 8(f) row 1, "
-                         "smooth_cloud points/s on a synthetic sphere (one GPU)")
+    ap.add_argument("--workload", choices=["lop", "mls", "deviation", "io"], default="lop",
+                    help="lop: the BASELINE.json metric (default); the others are the SURVEY "
+                         "8(f) rows on one GPU — mls: smooth_cloud points/s on a synthetic "
+                         "sphere; deviation: nearest-neighbour metric of 1M projected vs 10M "
+                         "data points; io: XYZ text write + read of the 10M-point cloud")
     ap.add_argument("--mls-points", type=int, default=1_000_000)
     ap.add_argument("--mls-degree", type=int, default=2)
     args = ap.parse_args()
     if args.workload == "mls":
         return bench_mls(args)
+    if args.workload in ("deviation", "io"):
+        return bench_rows(args)
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "b200":
         return self_launch(args.gpus)
