@@ -134,3 +134,22 @@ def test_smooth_outcomes_equal_full_records(pb, kind, n, seed, sigma, h, deg):
         assert np.array_equal(lean, ro.projected) and ro.coeffs is None
         for k in ("status", "degree_used", "iterations", "plane_status", "poly_status"):
             assert np.array_equal(getattr(ro, k), getattr(rf, k)), k
+
+
+def test_smooth_without_records_buffer(pb):
+    """pcs_mls_smooth with results == NULL (the call INTEGRATION.md shows) takes the
+    two-launch path and returns the same cloud as the record path."""
+    import ctypes as C
+    from paper_2401_03365_b200 import _lib as L
+    from paper_2401_03365_b200 import mls as M
+    P = cloud(pb, "sphere", 3000, 11, 0.01)
+    prm = pb.MlsParams(kernel=pb.KernelParams(0.2), degree=2)
+    full, _ = pb.smooth_cloud(P, prm, full_records=True)
+    out = np.zeros_like(P)
+    d = M._desc(prm, -1)
+    st = L.lib().pcs_mls_smooth(C.byref(d), P.ctypes.data_as(C.POINTER(C.c_double)), P.shape[0],
+                                out.ctypes.data_as(C.POINTER(C.c_double)), None)
+    assert st == 0 and np.array_equal(out, full)
+    a, b = C.c_double(-1.0), C.c_double(-1.0)
+    assert L.lib().pcs_mls_last_device_ms(C.byref(a), C.byref(b)) == 0
+    assert a.value > 0.0 and b.value > 0.0
