@@ -390,7 +390,14 @@ pcs_status pcs_parse_cloud(const pcs_lop_desc* d, const char* text, uint64_t len
         if (len && !text) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null text");
         if (!n_out) throw pcsb::Failure(PCS_ERR_INVALID_PARAM, "null count");
         if (len) pcsb::select_device(desc.device);
-        const std::vector<double> xyz = pcsb::parse_cloud(text, len, format);
+        pcsb::ParseDst dst;  // points go straight to the caller's buffer when they fit
+        dst.ext = xyz_out;
+        dst.cap = xyz_out ? cap : 0;
+        const std::vector<double> xyz = pcsb::parse_cloud(text, len, format, &dst);
+        if (dst.used) {
+            *n_out = dst.n;
+            return;
+        }
         *n_out = xyz.size() / 3;
         if (!xyz_out || cap < *n_out) throw pcsb::Failure(PCS_ERR_CAPACITY, "output buffer too small");
         if (!xyz.empty()) std::memcpy(xyz_out, xyz.data(), xyz.size() * sizeof(double));

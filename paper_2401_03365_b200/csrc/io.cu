@@ -342,15 +342,17 @@ __global__ void line_parse_kernel(const char* __restrict__ t, uint64_t len,
     st[k] = s;
 }
 
-struct DevMem {
+struct DevMem {  // stream-ordered temporaries of one call, from the library's pool
+    cudaStream_t s;
+    int dev = 0;
     std::vector<void*> p;
+    explicit DevMem(cudaStream_t s_) : s(s_) { PCSB_CUDA(cudaGetDevice(&dev)); }
     ~DevMem() {
-        for (void* x : p) cudaFree(x);
+        for (void* x : p) pool_free(x, s);
     }
     template <typename X>
     X* get(size_t count) {
-        void* x = nullptr;
-        PCSB_CUDA(cudaMalloc(&x, std::max<size_t>(count * sizeof(X), 16)));
+        void* x = pool_alloc(dev, std::max<size_t>(count * sizeof(X), 16), s);
         p.push_back(x);
         return (X*)x;
     }
@@ -390,7 +392,7 @@ uint64_t format_cloud(const double* xyz, uint64_t n, int format, char* out, uint
         return head.size();
     }
     IoStream st;
-    DevMem mem;
+    DevMem mem(st.s);
     double* dxyz = mem.get<double>(n * 3);
     uint64_t* len = mem.get<uint64_t>(n + 1);
     uint64_t* off = mem.get<uint64_t>(n + 1);
@@ -421,7 +423,7 @@ uint64_t format_cloud_alloc(const double* xyz, uint64_t n, int format, char** ou
         return head.size();
     }
     IoStream st;
-    DevMem mem;
+    DevMem mem(st.s);
     double* dxyz = mem.get<double>(n * 3);
     uint64_t* len = mem.get<uint64_t>(n + 1);
     uint64_t* off = mem.get<uint64_t>(n + 1);
@@ -471,15 +473,17 @@ __global__ void host_line_kernel(const char* __restrict__ t, uint64_t len,
 struct DevParse {
     uint64_t nlines = 0, ndata = 0;
     std::vector<HostLine> host;
+    double* out = nullptr;  // where the points landed (the caller's buffer or xyz)
 };
 
 DevParse device_parse(const char* t, uint64_t len, bool ply, int ntok, int ix, int iy, int iz,
-                      uint64_t o0, uint64_t cnt, std::vector<double>& xyz) {
+                      uint64_t o0, uint64_t cnt, std::vector<double>& xyz, ParseDst* pdst) {
     DevParse r;
     xyz.clear();
+    if (pdst) pdst->used = false;
     if (len == 0) return r;
     IoStream st;
-    DevMem mem;
+    DevMem mem(st.s);
     char* dt = mem.get<char>(len);
     h2d_staged(dt, t, len, st.s);
     uint8_t* flag = mem.get<uint8_t>(len);
@@ -541,9 +545,16 @@ DevParse device_parse(const char* t, uint64_t len, bool ply, int ntok, int ix, i
     PCSB_CUDA(cudaGetLastError());
     uint64_t nhost = 0;
     PCSB_CUDA(cudaMemcpyAsync(&nhost, nsel + 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, st.s));
-    xyz.resize(npts * 3);
+    if (pdst && pdst->ext && npts <= pdst->cap) {
+        pdst->used = true;
+        pdst->n = npts;
+        r.out = pdst->ext;
+    } else {
+        xyz.resize(npts * 3);
+        r.out = xyz.data();
+    }
     PCSB_CUDA(cudaStreamSynchronize(st.s));
-    if (npts) d2h_staged(xyz.data(), dxyz, npts * 3 * sizeof(double), st.s);
+    if (npts) d2h_staged(r.out, dxyz, npts * 3 * sizeof(double), st.s);
     r.host.resize(nhost);
     if (nhost)
         PCSB_CUDA(cudaMemcpyAsync(r.host.data(), hl, nhost * sizeof(HostLine), cudaMemcpyDeviceToHost, st.s));
@@ -554,16 +565,16 @@ DevParse device_parse(const char* t, uint64_t len, bool ply, int ntok, int ix, i
 
 }  // namespace
 
-std::vector<double> parse_cloud(const char* t, uint64_t len, int format) {
+std::vector<double> parse_cloud(const char* t, uint64_t len, int format, ParseDst* dst) {
     std::vector<double> xyz;
     if (format == PCS_FMT_XYZ) {
-        const DevParse dp = device_parse(t, len, false, 3, 0, 1, 2, 0, ~0ull, xyz);
+        const DevParse dp = device_parse(t, len, false, 3, 0, 1, 2, 0, ~0ull, xyz, dst);
         // lines the device left to the host, in file order (the first error wins)
         for (const HostLine& h : dp.host) {
             const char* b = t + h.b;
             const char* e = t + h.e;
             if (e > b && e[-1] == '\r') --e;
-            xyz_line(b, e, (int64_t)h.k + 1, xyz.data() + 3 * h.ord);
+            xyz_line(b, e, (int64_t)h.k + 1, dp.out + 3 * h.ord);
         }
         return xyz;
     }
@@ -594,10 +605,11 @@ std::vector<double> parse_cloud(const char* t, uint64_t len, int format) {
     if (simple) {
         const uint64_t cnt = (uint64_t)vx->count;
         const DevParse dp = device_parse(t + h.body, len - h.body, true, (int)vx->props.size(), ix, iy,
-                                         iz, off, cnt, xyz);
+                                         iz, off, cnt, xyz, dst);
         if (dp.ndata >= total && dp.host.empty()) return xyz;
     }
     xyz.clear();
+    if (dst) dst->used = false;
     ply_host(t, len, false, xyz, nullptr);
     return xyz;
 }

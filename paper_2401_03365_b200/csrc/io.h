@@ -36,7 +36,16 @@ uint64_t format_cloud(const double* xyz, uint64_t n, int format, char* out, uint
 // Same, one pass, into a malloc'd buffer (*out, freed by the caller with free()).
 uint64_t format_cloud_alloc(const double* xyz, uint64_t n, int format, char** out);
 // read_cloud_stream: xyz of the points; throws ParseFailure.
-std::vector<double> parse_cloud(const char* text, uint64_t len, int format);
+// Caller-side destination of parse_cloud: when the parsed points fit `cap`, they
+// are copied from the device straight into `ext` (used = true, n = points) and
+// the returned vector stays empty — no intermediate host copy.
+struct ParseDst {
+    double* ext = nullptr;
+    uint64_t cap = 0;
+    bool used = false;
+    uint64_t n = 0;
+};
+std::vector<double> parse_cloud(const char* text, uint64_t len, int format, ParseDst* dst = nullptr);
 // read_mesh_stream: 9 doubles per triangle (fan-triangulated faces); throws ParseFailure.
 std::vector<double> parse_mesh(const char* text, uint64_t len);
 
