@@ -154,15 +154,17 @@ nn_kernel(const double4* __restrict__ pts, const uint32_t* __restrict__ order,
     dist_out[qi] = __dsqrt_rn(b.d2);
 }
 
-struct DevBuf {
+struct DevBuf {  // stream-ordered temporaries of one call, from the library's pool
+    cudaStream_t s;
+    int dev = 0;
     std::vector<void*> p;
+    explicit DevBuf(cudaStream_t s_) : s(s_) { PCSB_CUDA(cudaGetDevice(&dev)); }
     ~DevBuf() {
-        for (void* x : p) cudaFree(x);
+        for (void* x : p) pool_free(x, s);
     }
     template <typename X>
     X* get(size_t count) {
-        void* x = nullptr;
-        PCSB_CUDA(cudaMalloc(&x, std::max<size_t>(count * sizeof(X), 16)));
+        void* x = pool_alloc(dev, std::max<size_t>(count * sizeof(X), 16), s);
         p.push_back(x);
         return (X*)x;
     }
@@ -182,7 +184,7 @@ void nearest_device(const double* C, uint64_t n, const double* Qh, uint64_t m, u
                     double* dist, cudaStream_t s) {
     if (n > 0xFFFFFFFEull || m > 0xFFFFFFFEull)
         throw Failure(PCS_ERR_INVALID_PARAM, "nearest: clouds are limited to 2^32-2 points");
-    DevBuf mem;
+    DevBuf mem(s);
     const uint32_t nn = (uint32_t)n, mm = (uint32_t)m;
     double* dC = mem.get<double>(n * 3);
     double* dQ = mem.get<double>(m * 3);
@@ -352,7 +354,7 @@ void deviation_to_mesh(const pcs_lop_desc& d, const double* cloud, uint64_t m, c
     }
     {
         Stream st;
-        DevBuf mem;
+        DevBuf mem(st.s);
         double* dP = mem.get<double>(m * 3);
         double* dT = mem.get<double>(ntri * 9);
         double* dD = mem.get<double>(m);
