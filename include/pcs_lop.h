@@ -313,6 +313,13 @@ typedef struct pcs_mls_outcome {
  * records of pcs_mls_smooth; the queries are the device index's own points. */
 pcs_status pcs_mls_smooth_outcomes(const pcs_mls_desc* d, const double* xyz, uint64_t n,
                                    double* out_xyz, pcs_mls_outcome* outcomes);
+/* The same with, per point, the bounds cmin[3], cmax[3] of the query centres its
+ * projection used (plane iterates and frame origin: what a QueryCoverage guard
+ * sees, proj/src/mls.cpp:28-47) in center_bounds (6n doubles): parallel_smooth
+ * decides each worker point's coverage fallback from them
+ * (proj/src/parallel.cpp:207-301). */
+pcs_status pcs_mls_smooth_bounds(const pcs_mls_desc* d, const double* xyz, uint64_t n, double* out_xyz,
+                                 pcs_mls_outcome* outcomes, double* center_bounds);
 /* Measurement: device time (ms, CUDA events) of the plane-fit and the polynomial
  * launch of this process's last pcs_mls_smooth_outcomes call (bench.py). */
 pcs_status pcs_mls_last_device_ms(double* plane_ms, double* poly_ms);

@@ -45,7 +45,7 @@ EXPORTED = [
     "pcs_format_cloud_alloc", "pcs_free_buffer", "pcs_lop_plan_record_counts",
     "pcs_lop_plan_query_counts", "pcs_trim_device_pool",
     "pcs_mls_desc_default", "pcs_mls_index_create", "pcs_mls_index_destroy", "pcs_mls_index_radius",
-    "pcs_mls_project", "pcs_mls_smooth", "pcs_mls_smooth_outcomes", "pcs_mls_last_device_ms", "pcs_mls_partition", "pcs_lop_plan_set_graphs",
+    "pcs_mls_project", "pcs_mls_smooth", "pcs_mls_smooth_outcomes", "pcs_mls_smooth_bounds", "pcs_mls_last_device_ms", "pcs_mls_partition", "pcs_lop_plan_set_graphs",
     "pcs_lop_plan_graph_launches", "pcs_lop_plan_set_positions",
 ]
 
@@ -211,6 +211,7 @@ def lib():
         L.pcs_mls_smooth.argtypes = [C.POINTER(MlsDesc), _dp, C.c_uint64, _dp,
                                      C.POINTER(MlsResultC)]
         L.pcs_mls_smooth_outcomes.argtypes = [C.POINTER(MlsDesc), _dp, C.c_uint64, _dp, C.c_void_p]
+        L.pcs_mls_smooth_bounds.argtypes = [C.POINTER(MlsDesc), _dp, C.c_uint64, _dp, C.c_void_p, _dp]
         L.pcs_mls_last_device_ms.argtypes = [_dp, _dp]
         L.pcs_mls_partition.argtypes = [_dp, C.c_uint64, C.c_uint64, C.c_double,
                                         C.POINTER(C.c_int32), _dp, _u32p]

@@ -349,7 +349,14 @@ pcs_status pcs_mls_smooth(const pcs_mls_desc* d, const double* xyz, uint64_t n, 
 
 pcs_status pcs_mls_smooth_outcomes(const pcs_mls_desc* d, const double* xyz, uint64_t n,
                                    double* out_xyz, pcs_mls_outcome* outcomes) {
-    return guarded([&] { pcsb::mls_smooth_outcomes(checked_mls(d), xyz, n, out_xyz, outcomes); });
+    return guarded([&] { pcsb::mls_smooth_outcomes(checked_mls(d), xyz, n, out_xyz, outcomes, nullptr); });
+}
+
+pcs_status pcs_mls_smooth_bounds(const pcs_mls_desc* d, const double* xyz, uint64_t n, double* out_xyz,
+                                 pcs_mls_outcome* outcomes, double* center_bounds) {
+    return guarded([&] {
+        pcsb::mls_smooth_outcomes(checked_mls(d), xyz, n, out_xyz, outcomes, center_bounds);
+    });
 }
 
 pcs_status pcs_mls_last_device_ms(double* plane_ms, double* poly_ms) {

@@ -80,12 +80,14 @@ struct MlsArgs {
     const uint32_t* order;
     double* lean_xyz;
     pcs_mls_outcome* lean_out;
+    double* lean_bounds;     // optional: per point cmin[3], cmax[3] of the query centres used
     struct MlsMid* mid;      // plane-fit results between the two launches of the lean path
 };
 
 // What the polynomial launch of the lean path needs from the plane launch.
 struct MlsMid {
     double o[3], n[3], u[3], v[3];
+    double cmn[3], cmx[3];   // bounds of the plane iterates (the coverage guard's centres)
     int32_t iterations, plane_status, have_frame, pad;
 };
 
@@ -573,6 +575,10 @@ mls_kernel(const MlsArgs a) {
                 F.u[i] = M.u[i];
                 F.v[i] = M.v[i];
             }
+            for (int i = 0; i < 3; ++i) {
+                cmn[i] = M.cmn[i];
+                cmx[i] = M.cmx[i];
+            }
             R.iterations = M.iterations;
             R.plane_status = M.plane_status;
             have_frame = M.have_frame != 0;
@@ -703,6 +709,8 @@ mls_kernel(const MlsArgs a) {
                     M.n[i] = have_frame ? F.n[i] : 0.0;
                     M.u[i] = have_frame ? F.u[i] : 0.0;
                     M.v[i] = have_frame ? F.v[i] : 0.0;
+                    M.cmn[i] = cmn[i];
+                    M.cmx[i] = cmx[i];
                 }
                 M.iterations = R.iterations;
                 M.plane_status = R.plane_status;
@@ -775,6 +783,12 @@ mls_kernel(const MlsArgs a) {
                 o.poly_status = (int8_t)R.poly_status;
                 o.iterations = R.iterations;
                 a.lean_out[oi] = o;
+                if (a.lean_bounds) {
+                    for (int i = 0; i < 3; ++i) {
+                        a.lean_bounds[6 * oi + i] = cmn[i];
+                        a.lean_bounds[6 * oi + 3 + i] = cmx[i];
+                    }
+                }
             } else {
                 a.out[qi] = R;
             }
@@ -1067,7 +1081,7 @@ double g_last_ms[2] = {0.0, 0.0};  // plane / polynomial launch of the last smoo
 // sorted points (no second upload; consecutive warps work on neighbouring
 // points), 32 bytes per point come back instead of 312.
 void mls_smooth_outcomes(const pcs_mls_desc& d, const double* xyz, uint64_t n, double* out_xyz,
-                         pcs_mls_outcome* outcomes) {
+                         pcs_mls_outcome* outcomes, double* center_bounds) {
     if (n == 0) return;
     if (!xyz || !out_xyz || !outcomes) throw Failure(PCS_ERR_INVALID_PARAM, "null buffer");
     // parameter checks of mls_project (same messages): a zero-query call validates only
@@ -1096,6 +1110,7 @@ void mls_smooth_outcomes(const pcs_mls_desc& d, const double* xyz, uint64_t n, d
     a.order = ix->order;
     a.lean_xyz = t.get<double>(n * 3);
     a.lean_out = t.get<pcs_mls_outcome>(n);
+    a.lean_bounds = center_bounds ? t.get<double>(n * 6) : nullptr;
     a.counter = t.get<uint32_t>(1);
     PCSB_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(uint32_t), ix->s));
     int sms = 148;
@@ -1115,6 +1130,9 @@ void mls_smooth_outcomes(const pcs_mls_desc& d, const double* xyz, uint64_t n, d
     PCSB_CUDA(cudaMemcpyAsync(out_xyz, a.lean_xyz, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, ix->s));
     PCSB_CUDA(cudaMemcpyAsync(outcomes, a.lean_out, n * sizeof(pcs_mls_outcome), cudaMemcpyDeviceToHost,
                               ix->s));
+    if (center_bounds)
+        PCSB_CUDA(cudaMemcpyAsync(center_bounds, a.lean_bounds, n * 6 * sizeof(double),
+                                  cudaMemcpyDeviceToHost, ix->s));
     PCSB_CUDA(cudaStreamSynchronize(ix->s));
     PCSB_CUDA(cudaGetLastError());
     {   // device time of the two launches (pcs_mls_last_device_ms)
@@ -1140,7 +1158,7 @@ void mls_smooth(const pcs_mls_desc& d, const double* xyz, uint64_t n, double* ou
     if (!xyz || !out_xyz) throw Failure(PCS_ERR_INVALID_PARAM, "null buffer");
     if (!results) {  // only the cloud is wanted: the two-launch path (same projections)
         std::vector<pcs_mls_outcome> oc(n);
-        mls_smooth_outcomes(d, xyz, n, out_xyz, oc.data());
+        mls_smooth_outcomes(d, xyz, n, out_xyz, oc.data(), nullptr);
         return;
     }
     std::unique_ptr<MlsIndex> ix(mls_index_create(xyz, n, d.device));

@@ -262,17 +262,6 @@ ProjectionOutcome project_point(const SpatialIndex& index, Point3 r, const MlsPa
     return *project_point_guarded(index, r, params, nullptr);
 }
 
-namespace {
-std::vector<pcs_mls_result> smooth_device(const PointCloud& cloud, const MlsParams& params,
-                                          PointCloud& out) {
-    const pcs_mls_desc d = mls_desc(params.kernel, params.degree, params.plane_tol, params.plane_max_iter);
-    std::vector<pcs_mls_result> res(cloud.size());
-    out.points.resize(cloud.size());
-    check(pcs_mls_smooth(&d, xyz_of(cloud), cloud.size(), &out.points[0].x, res.data()));
-    return res;
-}
-}  // namespace
-
 std::pair<PointCloud, SmoothingSummary> smooth_cloud(const PointCloud& cloud,
                                                      const MlsParams& params) {
     params.validate();
@@ -365,15 +354,27 @@ std::pair<PointCloud, SmoothingSummary> parallel_smooth(const PointCloud& cloud,
     SmoothingSummary summary;
     if (cloud.empty()) return {out, summary};
     const auto [layout, parts] = partition(cloud, workers, params.kernel.support());
-    const std::vector<pcs_mls_result> res = smooth_device(cloud, params, out);
+    // the projections, each point's outcome and the bounds of the centres it used
+    const pcs_mls_desc d = mls_desc(params.kernel, params.degree, params.plane_tol, params.plane_max_iter);
+    std::vector<pcs_mls_outcome> oc(cloud.size());
+    std::vector<double> bounds(cloud.size() * 6);
+    out.points.resize(cloud.size());
+    check(pcs_mls_smooth_bounds(&d, xyz_of(cloud), cloud.size(), &out.points[0].x, oc.data(),
+                                bounds.data()));
     std::size_t escaped = 0;
     for (std::size_t u = 0; u < workers; ++u) {
         const double lo = layout.lo(u), hi = layout.hi(u);
         for (std::uint32_t i : parts[u].original) {
-            const pcs_mls_result& R = res[i];
-            const double cmin = R.cmin[layout.axis], cmax = R.cmax[layout.axis];
+            const double cmin = bounds[6 * (std::size_t)i + layout.axis];
+            const double cmax = bounds[6 * (std::size_t)i + 3 + layout.axis];
             if (!(cmin >= lo && cmax <= hi)) ++escaped;
-            summary.add(outcome_of(R));
+            ProjectionOutcome o;
+            o.projected = out.points[i];
+            o.status = projection_status_of(oc[i].status);
+            o.degree_used = oc[i].degree_used;
+            o.iterations_used = oc[i].iterations;
+            o.plane_status = plane_status_of(oc[i].plane_status);
+            summary.add(o);
         }
     }
     summary.coverage_fallbacks = escaped;

@@ -235,7 +235,7 @@ void mls_index_radius(MlsIndex* ix, const double* centers, uint64_t m, double r,
 void mls_project(MlsIndex* ix, const pcs_mls_desc& d, const double* q, uint64_t m, int mode,
                  const double* frames, pcs_mls_result* out, double* centers_out);
 void mls_smooth_outcomes(const pcs_mls_desc& d, const double* xyz, uint64_t n, double* out_xyz,
-                         pcs_mls_outcome* outcomes);
+                         pcs_mls_outcome* outcomes, double* center_bounds);
 void mls_last_device_ms(double out[2]);
 void mls_smooth(const pcs_mls_desc& d, const double* xyz, uint64_t n, double* out_xyz,
                 pcs_mls_result* results);

@@ -182,15 +182,17 @@ OUTCOME_DTYPE = np.dtype([("status", "i1"), ("degree_used", "i1"), ("plane_statu
 assert OUTCOME_DTYPE.itemsize == 8
 
 
-def smooth_cloud(cloud, params: MlsParams, device: int = -1,
-                 full_records: bool = False) -> Tuple[np.ndarray, MlsResults]:
+def smooth_cloud(cloud, params: MlsParams, device: int = -1, full_records: bool = False,
+                 center_bounds: bool = False) -> Tuple[np.ndarray, MlsResults]:
     """smooth_cloud (proj/src/mls.cpp:75-93): every point projected against the
     untouched input cloud, one device launch; output order = input order.
 
     As the reference, the call returns the projected cloud and the per-point
     outcome (status, degree used, plane-fit iterations and status); the frames,
     coefficients and centre bounds of ``MlsResults`` are filled only with
-    ``full_records=True`` (312 instead of 32 bytes per point cross PCIe)."""
+    ``full_records=True`` (312 instead of 32 bytes per point cross PCIe);
+    ``center_bounds=True`` adds ``cmin`` / ``cmax`` (the bounds of the query
+    centres each projection used: what parallel_smooth's coverage test reads)."""
     params.validate()
     P = _cloud(cloud)
     n = P.shape[0]
@@ -203,14 +205,20 @@ def smooth_cloud(cloud, params: MlsParams, device: int = -1,
         return out, _results(res[:n])
     oc = np.zeros(max(n, 1), dtype=OUTCOME_DTYPE)
     oc["status"] = 3  # Skipped
+    cb = np.zeros((max(n, 1), 6), dtype=np.float64) if center_bounds else None
     if n:
         d = _desc(params, device)
-        _check(L.lib().pcs_mls_smooth_outcomes(C.byref(d), _ptr(P), n, _ptr(out),
-                                               oc.ctypes.data_as(C.c_void_p)))
+        if center_bounds:
+            _check(L.lib().pcs_mls_smooth_bounds(C.byref(d), _ptr(P), n, _ptr(out),
+                                                 oc.ctypes.data_as(C.c_void_p), _ptr(cb)))
+        else:
+            _check(L.lib().pcs_mls_smooth_outcomes(C.byref(d), _ptr(P), n, _ptr(out),
+                                                   oc.ctypes.data_as(C.c_void_p)))
     oc = oc[:n]
     i4 = lambda k: oc[k].astype(np.int32)  # noqa: E731
     return out, MlsResults(projected=out, origin=None, normal=None, u=None, v=None, coeffs=None,
-                           cmin=None, cmax=None, status=i4("status"),
+                           cmin=cb[:n, :3].copy() if center_bounds else None,
+                           cmax=cb[:n, 3:].copy() if center_bounds else None, status=i4("status"),
                            degree_used=i4("degree_used"), iterations=i4("iterations"),
                            plane_status=i4("plane_status"), poly_status=i4("poly_status"))
 

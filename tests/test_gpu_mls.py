@@ -153,3 +153,16 @@ def test_smooth_without_records_buffer(pb):
     a, b = C.c_double(-1.0), C.c_double(-1.0)
     assert L.lib().pcs_mls_last_device_ms(C.byref(a), C.byref(b)) == 0
     assert a.value > 0.0 and b.value > 0.0
+
+
+def test_center_bounds_equal_full_records(pb):
+    """pcs_mls_smooth_bounds: the bounds of the query centres (plane iterates and
+    frame origin) equal the full records' cmin / cmax bit for bit, on a dense and
+    on a sparse cloud (skipped points keep their single centre)."""
+    for P, h in ((cloud(pb, "torus", 3000, 5, 0.01), 0.1),
+                 (np.random.default_rng(3).uniform(-1.0, 1.0, (300, 3)), 0.05)):
+        prm = pb.MlsParams(kernel=pb.KernelParams(h), degree=2)
+        lean, rb = pb.smooth_cloud(P, prm, center_bounds=True)
+        full, rf = pb.smooth_cloud(P, prm, full_records=True)
+        assert np.array_equal(lean, full)
+        assert np.array_equal(rb.cmin, rf.cmin) and np.array_equal(rb.cmax, rf.cmax)
