@@ -11,6 +11,7 @@
 #include <fstream>
 #include <iterator>
 #include <sstream>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -240,16 +241,20 @@ PointCloud read_cloud_stream(std::istream& in, CloudFormat format, const std::st
     const std::string text = slurp(in);
     pcs_lop_desc d;
     pcs_lop_desc_default(&d);
-    // every point needs at least 6 bytes ("0 0 0\n"): an upper bound, no second pass
-    std::vector<double> xyz(3 * (text.size() / 6 + 1));
+    // every point needs at least 6 bytes ("0 0 0\n"): an upper bound, no second pass.
+    // The landing buffer is left uninitialised (only the pages the n parsed points
+    // reach are ever touched; a value-initialised vector of the bound would zero
+    // 24 bytes per 6 bytes of text)
+    const size_t cap = text.size() / 6 + 1;
+    std::unique_ptr<double[]> xyz(new double[3 * cap]);
     uint64_t n = 0;
     pcs_parse_error err{};
-    const pcs_status st = pcs_parse_cloud(&d, text.data(), text.size(), fmt_code(format), xyz.data(),
-                                          xyz.size() / 3, &n, &err);
+    const pcs_status st = pcs_parse_cloud(&d, text.data(), text.size(), fmt_code(format), xyz.get(),
+                                          cap, &n, &err);
     if (st != PCS_OK) raise_parse(st, err, name);
     PointCloud cloud;
     cloud.points.resize((size_t)n);
-    if (n) std::memcpy(&cloud.points[0].x, xyz.data(), (size_t)n * 3 * sizeof(double));
+    if (n) std::memcpy(&cloud.points[0].x, xyz.get(), (size_t)n * 3 * sizeof(double));
     return cloud;
 }
 
